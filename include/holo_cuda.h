@@ -1,0 +1,230 @@
+/* holo_cuda.h — C-ABI of libholo_cuda.so, the B200 (sm_100a) forward hologram renderer.
+ *
+ * This is the drop-in boundary for the reference's render path
+ * (/root/reference/proj/include/holo/*.hpp).  Every entry point names the
+ * reference interface it replaces.  Plain C: POD structs, raw pointers and
+ * sizes, int status codes, no C++ or torch types.  A context owns one CUDA
+ * stream plus its scratch; calls enqueue on that stream.  A context is
+ * single-threaded; distinct contexts are independent (reference: value
+ * functions, reentrant across threads).
+ *
+ * Errors: every int-returning call returns HOLO_OK or an error code; the
+ * message is in holo_last_error() (thread-local).  Codes 1-4 are the
+ * reference's HoloError kinds (proj/include/holo/common.hpp:76-79):
+ * config, io, usage, numeric.
+ *
+ * Device field layout: the reference's planar [C][H][W] (field.hpp:9-21) with
+ * complex samples as interleaved (re, im) pairs; per-plane stacks are
+ * [L][C][H][W].  HOLO_F32 = float pairs (complex64), HOLO_F64 = double pairs.
+ */
+#ifndef HOLO_CUDA_H
+#define HOLO_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HOLO_CUDA_ABI_VERSION 1
+
+enum holo_status {
+    HOLO_OK = 0,
+    HOLO_ERR_CONFIG = 1,  /* HoloError("config") */
+    HOLO_ERR_IO = 2,      /* HoloError("io") */
+    HOLO_ERR_USAGE = 3,   /* HoloError("usage") */
+    HOLO_ERR_NUMERIC = 4, /* HoloError("numeric") */
+    HOLO_ERR_CUDA = 5,    /* CUDA runtime failure */
+    HOLO_ERR_OOM = 6,     /* device allocation failed */
+    HOLO_ERR_NCCL = 7     /* collective failure (multi-GPU helpers) */
+};
+
+enum holo_dtype { HOLO_F32 = 0, HOLO_F64 = 1 };
+
+#define HOLO_MAX_CHANNELS 16
+
+/* holo::WaveConfig, proj/include/holo/wave_config.hpp:11-23 */
+typedef struct {
+    int nx, ny;
+    double pitch;
+    int channels;
+    double wavelengths[HOLO_MAX_CHANNELS];
+    double distance;
+    double volume_depth;
+    int num_planes;
+} holo_wave;
+
+/* holo::CameraView, proj/include/holo/camera.hpp:14-30 (pose = x, y, z, rx, ry, rz) */
+typedef struct {
+    double pose[6];
+    double focal_px;
+    double cx, cy;
+    int width, height;
+} holo_camera;
+
+/* holo::RenderSettings, proj/include/holo/rasterizer.hpp:12-28 */
+typedef struct {
+    double near_clip, dilation, plane_eps, term_eps, alpha_floor, alpha_clamp, radius_form_cap, ste_tau;
+    int soft_assignment;
+    double soft_tau;
+    int tile;
+} holo_raster_settings;
+
+/* holo::PropagationOptions, proj/include/holo/propagation.hpp:10-13 */
+typedef struct {
+    int pad2x;
+    int local_band_limit;
+} holo_prop_options;
+
+/* holo::GaussianScene, proj/include/holo/scene.hpp:18-37: SoA f64, N Gaussians,
+ * 3 amplitude/phase channels, num_planes plane logits per Gaussian. */
+typedef struct {
+    size_t n;
+    int num_planes;
+    const double* positions;      /* n*3 */
+    const double* rotations;      /* n*4 (w, x, y, z) */
+    const double* log_scales;     /* n*3 */
+    const double* amplitudes;     /* n*3 */
+    const double* opacity_logits; /* n */
+    const double* phases;         /* n*3 */
+    const double* plane_logits;   /* n*num_planes */
+} holo_scene_arrays;
+
+/* Outputs of a render (which buffers holo_render fills). */
+enum holo_output {
+    HOLO_OUT_LAYERS = 1u << 0,    /* RasterForward::layers   [L][C][H][W] complex64 */
+    HOLO_OUT_HOLOGRAM = 1u << 1,  /* PipelineForward::hologram [C][H][W] complex64 */
+    HOLO_OUT_REPLAYED = 1u << 2,  /* PipelineForward::replayed [L][C][H][W] complex64 */
+    HOLO_OUT_INTENSITY = 1u << 3, /* PipelineForward::intensities [L][C][H][W] float32 */
+    HOLO_OUT_AUX = 1u << 4,       /* RasterForward::t_final (f32) and n_contrib (i32), [L][H][W] */
+    HOLO_OUT_LISTS = 1u << 5,     /* RasterForward::entries / bucket_start */
+    HOLO_OUT_PROJECTED = 1u << 6  /* RasterForward::projected (holo_projected, f64) */
+};
+
+/* Buffer ids for holo_frame_buffer(). */
+enum holo_buffer {
+    HOLO_BUF_LAYERS = 0,       /* float2 [L][C][H][W] */
+    HOLO_BUF_HOLOGRAM = 1,     /* float2 [C][H][W] */
+    HOLO_BUF_REPLAYED = 2,     /* float2 [L][C][H][W] */
+    HOLO_BUF_INTENSITY = 3,    /* float [L][C][H][W] */
+    HOLO_BUF_T_FINAL = 4,      /* float [L][H][W] */
+    HOLO_BUF_N_CONTRIB = 5,    /* int32 [L][H][W] */
+    HOLO_BUF_ENTRY_GIDX = 6,   /* int32 [E], bucket-major, depth-sorted (Entry::gidx) */
+    HOLO_BUF_ENTRY_DEPTH = 7,  /* double [E] (Entry::depth = camera-space z) */
+    HOLO_BUF_BUCKET_START = 8, /* uint32 [B+1] */
+    HOLO_BUF_PROJECTED = 9,    /* holo_projected [N] */
+    HOLO_BUF_RHO = 10,         /* float [N][L] plane weights used */
+    HOLO_BUF_TOUCHED = 11,     /* uint8 [N] */
+    HOLO_BUF_SPECTRUM = 12,    /* float2 [C][H][W]: S = sum_l H_{Z_l} FFT2(U_l) (unnormalised) */
+    HOLO_BUF_COUNT = 13
+};
+
+/* detail::Projected, proj/include/holo/rasterizer.hpp:34-45 */
+typedef struct {
+    int32_t valid;
+    int32_t n;
+    double mu_x, mu_y;
+    double inv00, inv01, inv11;
+    double radius;
+    double xc, yc, zc;
+    double alpha_sig;
+    double amp[3];
+    double phase[3];
+    int32_t plane;
+    int32_t pad_;
+} holo_projected;
+
+/* Per-frame facts reported back to the host. */
+typedef struct {
+    uint64_t num_entries; /* E: (bucket, Gaussian) work items */
+    int32_t tiles_x, tiles_y;
+    int32_t num_buckets;  /* L * tiles */
+    int32_t max_bucket;   /* largest bucket (entries) */
+    int32_t num_valid;    /* Gaussians that passed projection culling */
+    int32_t pad_;
+} holo_frame_info;
+
+typedef struct holo_ctx holo_ctx;
+
+/* ---- context ---- */
+const char* holo_last_error(void);
+int holo_abi_version(void);
+int holo_ctx_create(int device, holo_ctx** out);
+int holo_ctx_destroy(holo_ctx* ctx);
+/* Enqueue on a caller stream (cudaStream_t cast to void*); NULL is the legacy
+ * default stream (what torch.cuda.current_stream() reports as 0). */
+int holo_ctx_set_stream(holo_ctx* ctx, void* stream);
+/* Back to the context's own non-blocking stream. */
+int holo_ctx_use_own_stream(holo_ctx* ctx);
+void* holo_ctx_get_stream(holo_ctx* ctx);
+int holo_ctx_synchronize(holo_ctx* ctx);
+/* Optional per-stage CUDA-event timing (ms), accumulated over renders until reset.
+ * Stage ids: 0 preprocess, 1 binning, 2 composite, 3 row FFT, 4 column forward,
+ * 5 column inverse, 6 row inverse + epilogue. */
+int holo_ctx_enable_timing(holo_ctx* ctx, int enable);
+int holo_ctx_stage_times(holo_ctx* ctx, double* ms_out, int* launches_out, int max_stages);
+int holo_ctx_reset_timing(holo_ctx* ctx);
+/* Kernel launches issued by this context since creation. */
+uint64_t holo_ctx_launch_count(holo_ctx* ctx);
+
+/* ---- scene (GaussianScene, scene.hpp:18-37; validated like GaussianScene::validate, scene.cpp:19-32) ---- */
+/* Copies host arrays to the device (H2D on the context stream). */
+int holo_scene_upload(holo_ctx* ctx, const holo_scene_arrays* host);
+/* Copies from device arrays already resident in HBM (D2D). */
+int holo_scene_upload_device(holo_ctx* ctx, const holo_scene_arrays* dev);
+
+/* ---- render ----
+ * holo_render replaces holo::pipeline_forward (pipeline.cpp:20-29) and, with only
+ * raster outputs requested, holo::raster_forward (rasterizer.cpp:139-263).
+ * Raster layers carry wave->channels channels: channels [0, C) of the scene's three
+ * (C = 3 is the reference; C < 3 is the documented single-wavelength adapter).
+ * Outputs live in context-owned device buffers until the next render; fetch them
+ * with holo_frame_buffer / holo_frame_download. */
+int holo_render(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave, const holo_raster_settings* settings,
+                const holo_prop_options* prop, unsigned outputs, holo_frame_info* info);
+
+/* Plane-sharded halves of holo_render (one process per GPU).  begin: rasterise
+ * planes [plane_begin, plane_end) and write their partial spectrum
+ * S_g = sum_{l in g} H_{Z_l} FFT2(U_l) (float2 [C][H][W]) to spectrum_out
+ * (device pointer; NULL = context buffer).  The caller sums S_g over shards
+ * (one allreduce) and calls end with the full spectrum to produce the hologram
+ * (if HOLO_OUT_HOLOGRAM) and the replayed fields / intensities of planes
+ * [plane_begin, plane_end).  Valid only without pad2x. */
+int holo_render_begin(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave,
+                      const holo_raster_settings* settings, const holo_prop_options* prop, int plane_begin,
+                      int plane_end, void* spectrum_out, unsigned outputs, holo_frame_info* info);
+int holo_render_end(holo_ctx* ctx, const holo_wave* wave, const holo_prop_options* prop, int plane_begin,
+                    int plane_end, const void* spectrum, unsigned outputs);
+
+/* Device pointer and size of one output buffer of the last render. */
+int holo_frame_buffer(holo_ctx* ctx, int buffer, void** dev_ptr, size_t* bytes);
+/* Synchronous device-to-host copy of one output buffer (bytes must match). */
+int holo_frame_download(holo_ctx* ctx, int buffer, void* host, size_t bytes);
+
+/* ---- operators on device fields (propagation.hpp:27-40, fft.hpp:11-12, field.hpp:45) ---- */
+/* fft2 / ifft2 (fft.cpp:33-44): in place, batch fields of h x w; inverse carries 1/(w h). */
+int holo_fft2(holo_ctx* ctx, void* data, int w, int h, int batch, int inverse, int dtype);
+/* transfer_function (propagation.cpp:86-91): out [C][h'][w'] (doubled when pad2x). */
+int holo_transfer_function(holo_ctx* ctx, const holo_wave* wave, double z, const holo_prop_options* prop,
+                           void* out, int dtype);
+/* propagate (propagation.cpp:93-101): in/out [C][H][W]; c must equal wave->channels. */
+int holo_propagate(holo_ctx* ctx, const void* in, void* out, int w, int h, int c, const holo_wave* wave, double z,
+                   const holo_prop_options* prop, int dtype);
+/* forward_record (propagation.cpp:103-114): layers [L][C][H][W] -> hologram [C][H][W]. */
+int holo_forward_record(holo_ctx* ctx, const void* layers, int num_layers, void* hologram, const holo_wave* wave,
+                        const holo_prop_options* prop, int dtype);
+/* inverse_propagate (propagation.cpp:116-123): hologram [C][H][W] -> replayed [L][C][H][W]. */
+int holo_inverse_propagate(holo_ctx* ctx, const void* hologram, void* replayed, const holo_wave* wave,
+                           const holo_prop_options* prop, int dtype);
+/* intensity (field.cpp:5-14): |u|^2 per sample; out is float for F32, double for F64. */
+int holo_intensity(holo_ctx* ctx, const void* field, void* out, size_t samples, int dtype);
+
+/* Supported FFT lengths: every n whose prime factors are <= 31. */
+int holo_fft_supported(int n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

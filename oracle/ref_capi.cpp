@@ -1,0 +1,300 @@
+// ref_capi — extern "C" entry points into the reference library built from
+// /root/reference/proj/src by oracle/Makefile (oracle/_ref/libholoref.so).
+//
+// TEST INFRASTRUCTURE: lets the Python tests and bench.py's reference arm call
+// the reference's own C++ functions (holo::pipeline_forward and the operators
+// under it) with the plain structs of oracle/holo_oracle.h.  Nothing here
+// re-implements the algorithm; it only marshals arguments.
+#include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "holo_oracle.h"
+#include "holo/fft.hpp"
+#include "holo/pipeline.hpp"
+#include "holo/propagation.hpp"
+#include "holo/rasterizer.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+int code_for(const holo::HoloError& e) {
+    if (e.kind == "config") return HO_ERR_CONFIG;
+    if (e.kind == "io") return HO_ERR_IO;
+    if (e.kind == "usage") return HO_ERR_USAGE;
+    return HO_ERR_NUMERIC;
+}
+
+holo::WaveConfig to_wave(const ho_wave* w) {
+    holo::WaveConfig c;
+    c.nx = w->nx;
+    c.ny = w->ny;
+    c.pitch = w->pitch;
+    c.wavelengths.assign(w->wavelengths, w->wavelengths + w->channels);
+    c.distance = w->distance;
+    c.volume_depth = w->volume_depth;
+    c.num_planes = w->num_planes;
+    return c;
+}
+
+holo::CameraView to_camera(const ho_camera* c) {
+    holo::CameraView v;
+    for (int i = 0; i < 6; ++i) v.pose[i] = c->pose[i];
+    v.focal_px = c->focal_px;
+    v.cx = c->cx;
+    v.cy = c->cy;
+    v.width = c->width;
+    v.height = c->height;
+    return v;
+}
+
+holo::RenderSettings to_settings(const ho_settings* s) {
+    holo::RenderSettings r;
+    r.near_clip = s->near_clip;
+    r.dilation = s->dilation;
+    r.plane_eps = s->plane_eps;
+    r.term_eps = s->term_eps;
+    r.alpha_floor = s->alpha_floor;
+    r.alpha_clamp = s->alpha_clamp;
+    r.radius_form_cap = s->radius_form_cap;
+    r.ste_tau = s->ste_tau;
+    r.soft_assignment = s->soft_assignment != 0;
+    r.soft_tau = s->soft_tau;
+    r.tile = s->tile;
+    return r;
+}
+
+holo::PropagationOptions to_prop(const ho_prop* p) {
+    holo::PropagationOptions o;
+    if (p) {
+        o.pad2x = p->pad2x != 0;
+        o.local_band_limit = p->local_band_limit != 0;
+    }
+    return o;
+}
+
+holo::GaussianScene to_scene(const ho_scene* s) {
+    holo::GaussianScene g;
+    g.num_planes = s->num_planes;
+    const size_t n = s->n;
+    g.positions.assign(s->positions, s->positions + 3 * n);
+    g.rotations.assign(s->rotations, s->rotations + 4 * n);
+    g.log_scales.assign(s->log_scales, s->log_scales + 3 * n);
+    g.amplitudes.assign(s->amplitudes, s->amplitudes + 3 * n);
+    g.opacity_logits.assign(s->opacity_logits, s->opacity_logits + n);
+    g.phases.assign(s->phases, s->phases + 3 * n);
+    g.plane_logits.assign(s->plane_logits, s->plane_logits + n * static_cast<size_t>(s->num_planes));
+    return g;
+}
+
+holo::ComplexField to_field(const double* d, int w, int h, int c, double pitch) {
+    holo::ComplexField f(w, h, c, pitch);
+    std::memcpy(f.data.data(), d, sizeof(double) * 2 * f.data.size());
+    return f;
+}
+
+void copy_raster(const holo::RasterForward& r, int L, int w, int h, ho_raster* o) {
+    std::memset(o, 0, sizeof *o);
+    const size_t P = static_cast<size_t>(w) * h, N = r.projected.size(), E = r.entries.size();
+    o->L = L;
+    o->w = w;
+    o->h = h;
+    o->tiles_x = r.tiles_x;
+    o->tiles_y = r.tiles_y;
+    o->num_entries = E;
+    o->layers = static_cast<double*>(std::malloc(sizeof(double) * 2 * 3 * P * L));
+    for (int l = 0; l < L; ++l) std::memcpy(o->layers + 2 * 3 * P * l, r.layers[l].data.data(), sizeof(double) * 2 * 3 * P);
+    o->t_final = static_cast<double*>(std::malloc(sizeof(double) * r.t_final.size()));
+    std::memcpy(o->t_final, r.t_final.data(), sizeof(double) * r.t_final.size());
+    o->n_contrib = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * r.n_contrib.size()));
+    std::memcpy(o->n_contrib, r.n_contrib.data(), sizeof(int32_t) * r.n_contrib.size());
+    o->projected = static_cast<ho_projected*>(std::calloc(N ? N : 1, sizeof(ho_projected)));
+    for (size_t i = 0; i < N; ++i) {
+        const auto& p = r.projected[i];
+        ho_projected& q = o->projected[i];
+        q.valid = p.valid;
+        q.n = p.n;
+        q.mu_x = p.mu_x;
+        q.mu_y = p.mu_y;
+        q.inv00 = p.inv00;
+        q.inv01 = p.inv01;
+        q.inv11 = p.inv11;
+        q.radius = p.radius;
+        q.xc = p.xc;
+        q.yc = p.yc;
+        q.zc = p.zc;
+        q.alpha_sig = p.alpha_sig;
+        for (int c = 0; c < 3; ++c) {
+            q.amp[c] = p.amp[c];
+            q.phase[c] = p.phase[c];
+        }
+        q.plane = p.plane;
+    }
+    o->rho = static_cast<double*>(std::malloc(sizeof(double) * (r.rho.size() + 1)));
+    std::memcpy(o->rho, r.rho.data(), sizeof(double) * r.rho.size());
+    o->touched = static_cast<uint8_t*>(std::malloc(N + 1));
+    std::memcpy(o->touched, r.touched.data(), N);
+    o->entry_bucket = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * (E + 1)));
+    o->entry_gidx = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * (E + 1)));
+    o->entry_depth = static_cast<double*>(std::malloc(sizeof(double) * (E + 1)));
+    for (size_t e = 0; e < E; ++e) {
+        o->entry_bucket[e] = r.entries[e].bucket;
+        o->entry_gidx[e] = r.entries[e].gidx;
+        o->entry_depth[e] = r.entries[e].depth;
+    }
+    o->bucket_start = static_cast<uint32_t*>(std::malloc(sizeof(uint32_t) * r.bucket_start.size()));
+    std::memcpy(o->bucket_start, r.bucket_start.data(), sizeof(uint32_t) * r.bucket_start.size());
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return HO_OK;
+    } catch (const holo::HoloError& e) {
+        g_err = e.what();
+        return code_for(e);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return HO_ERR_NUMERIC;
+    }
+}
+
+double secs(std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double>(b - a).count();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+void ref_raster_free(ho_raster* r) {
+    if (!r) return;
+    std::free(r->layers);
+    std::free(r->t_final);
+    std::free(r->n_contrib);
+    std::free(r->projected);
+    std::free(r->rho);
+    std::free(r->touched);
+    std::free(r->entry_bucket);
+    std::free(r->entry_gidx);
+    std::free(r->entry_depth);
+    std::free(r->bucket_start);
+    std::memset(r, 0, sizeof *r);
+}
+
+int ref_raster_forward(const ho_scene* s, const ho_camera* cam, const ho_wave* cfg, const ho_settings* st,
+                       ho_raster* out) {
+    return guarded([&] {
+        const holo::RasterForward r = holo::raster_forward(to_scene(s), to_camera(cam), to_wave(cfg), to_settings(st));
+        copy_raster(r, cfg->num_planes, cfg->nx, cfg->ny, out);
+    });
+}
+
+int ref_brute_force_forward(const ho_scene* s, const ho_camera* cam, const ho_wave* cfg, const ho_settings* st,
+                            double* layers) {
+    return guarded([&] {
+        const auto ls = holo::brute_force_forward(to_scene(s), to_camera(cam), to_wave(cfg), to_settings(st));
+        const size_t n = ls.empty() ? 0 : ls[0].data.size();
+        for (size_t l = 0; l < ls.size(); ++l) std::memcpy(layers + 2 * n * l, ls[l].data.data(), sizeof(double) * 2 * n);
+    });
+}
+
+int ref_fft2(double* data, int w, int h, int inverse) {
+    return guarded([&] {
+        if (inverse)
+            holo::ifft2(reinterpret_cast<holo::c64*>(data), w, h);
+        else
+            holo::fft2(reinterpret_cast<holo::c64*>(data), w, h);
+    });
+}
+
+int ref_transfer_function(const ho_wave* cfg, double z, const ho_prop* opt, double* out) {
+    return guarded([&] {
+        const holo::TransferFunction tf = holo::transfer_function(to_wave(cfg), z, to_prop(opt));
+        std::memcpy(out, tf.hz.data(), sizeof(double) * 2 * tf.hz.size());
+    });
+}
+
+int ref_propagate(const double* in, int w, int h, int c, const ho_wave* cfg, double z, const ho_prop* opt,
+                  double* out) {
+    return guarded([&] {
+        const holo::ComplexField r = holo::propagate(to_field(in, w, h, c, cfg->pitch), to_wave(cfg), z, to_prop(opt));
+        std::memcpy(out, r.data.data(), sizeof(double) * 2 * r.data.size());
+    });
+}
+
+int ref_forward_record(const double* layers, int L, int c, const ho_wave* cfg, const ho_prop* opt, double* holo_out) {
+    return guarded([&] {
+        std::vector<holo::ComplexField> ls;
+        const size_t n = static_cast<size_t>(cfg->nx) * cfg->ny * c;
+        for (int l = 0; l < L; ++l) ls.push_back(to_field(layers + 2 * n * l, cfg->nx, cfg->ny, c, cfg->pitch));
+        const holo::ComplexField r = holo::forward_record(ls, to_wave(cfg), to_prop(opt));
+        std::memcpy(holo_out, r.data.data(), sizeof(double) * 2 * r.data.size());
+    });
+}
+
+int ref_inverse_propagate(const double* holo_in, int c, const ho_wave* cfg, const ho_prop* opt, double* replayed) {
+    return guarded([&] {
+        const auto rs = holo::inverse_propagate(to_field(holo_in, cfg->nx, cfg->ny, c, cfg->pitch), to_wave(cfg),
+                                                to_prop(opt));
+        const size_t n = rs.empty() ? 0 : rs[0].data.size();
+        for (size_t l = 0; l < rs.size(); ++l) std::memcpy(replayed + 2 * n * l, rs[l].data.data(), sizeof(double) * 2 * n);
+    });
+}
+
+// holo::pipeline_forward (pipeline.cpp:20-29), stage by stage so each stage is
+// timed; for cfg->channels == 3 this is exactly the reference composition.  For
+// fewer channels it is the SURVEY.md 8c adapter: the reference rasteriser always
+// emits 3 channels, channels [0, C) are recorded and replayed.
+int ref_pipeline_forward(const ho_scene* s, const ho_camera* cam, const ho_wave* cfg, const ho_settings* st,
+                         const ho_prop* opt, ho_raster* raster_out, double* hologram, double* replayed,
+                         double* intensities, double* stage_seconds) {
+    return guarded([&] {
+        const holo::WaveConfig wc = to_wave(cfg);
+        const holo::PropagationOptions po = to_prop(opt);
+        const holo::GaussianScene scene = to_scene(s);
+        const auto t0 = std::chrono::steady_clock::now();
+        holo::RasterForward r = holo::raster_forward(scene, to_camera(cam), wc, to_settings(st));
+        const auto t1 = std::chrono::steady_clock::now();
+        std::vector<holo::ComplexField> layers;
+        if (wc.channels() == holo::GaussianScene::kChannels) {
+            layers = r.layers;
+        } else {
+            const size_t n = static_cast<size_t>(wc.nx) * wc.ny * wc.channels();
+            for (const auto& f : r.layers) {
+                holo::ComplexField g(wc.nx, wc.ny, wc.channels(), wc.pitch);
+                std::memcpy(g.data.data(), f.data.data(), sizeof(double) * 2 * n);
+                layers.push_back(std::move(g));
+            }
+        }
+        const auto t1b = std::chrono::steady_clock::now();
+        const holo::ComplexField holo_f = holo::forward_record(layers, wc, po);
+        const auto t2 = std::chrono::steady_clock::now();
+        const auto rep = holo::inverse_propagate(holo_f, wc, po);
+        const auto t3 = std::chrono::steady_clock::now();
+        std::vector<holo::IntensityImage> ints;
+        ints.reserve(rep.size());
+        for (const auto& v : rep) ints.push_back(holo::intensity(v));
+        const auto t4 = std::chrono::steady_clock::now();
+        const size_t n = holo_f.data.size();
+        if (hologram) std::memcpy(hologram, holo_f.data.data(), sizeof(double) * 2 * n);
+        for (size_t l = 0; l < rep.size(); ++l) {
+            if (replayed) std::memcpy(replayed + 2 * n * l, rep[l].data.data(), sizeof(double) * 2 * n);
+            if (intensities) std::memcpy(intensities + n * l, ints[l].data.data(), sizeof(double) * n);
+        }
+        if (raster_out) copy_raster(r, cfg->num_planes, cfg->nx, cfg->ny, raster_out);
+        if (stage_seconds) {
+            stage_seconds[0] = secs(t0, t1);
+            stage_seconds[1] = secs(t1b, t2);
+            stage_seconds[2] = secs(t2, t3);
+            stage_seconds[3] = secs(t3, t4);
+        }
+    });
+}
+
+}  // extern "C"

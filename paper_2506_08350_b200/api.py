@@ -1,0 +1,404 @@
+"""Host-side mirror of the reference render/propagate API over libholo_cuda.
+
+Function names, arguments and errors follow proj/include/holo/*.hpp:
+
+* raster_forward(scene, cam, cfg, settings)      rasterizer.hpp:75-76
+* pipeline_forward(scene, cam, cfg, opt)         pipeline.hpp:41-42
+* propagate(u, cfg, z, opt)                      propagation.hpp:31
+* forward_record(layers, cfg, opt)               propagation.hpp:35-36
+* inverse_propagate(hologram, cfg, opt)          propagation.hpp:39-40
+* transfer_function(cfg, z, opt)                 propagation.hpp:27
+* fft2 / ifft2                                   fft.hpp:11-12
+* intensity(u)                                   field.hpp:45
+
+Host data is numpy (complex128 fields [C, H, W], like the reference's f64
+ComplexField); every call runs on the GPU through the C-ABI.  The render path
+computes in fp32 (complex64) as the north star specifies; the propagation
+operators take ``precision="f64"`` (default, reference precision) or "f32".
+
+``Context`` is the device-resident interface used by bench.py and the sharded
+renderer: scene stays in HBM, outputs stay in context buffers and are exposed
+as zero-copy torch views.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Iterable, List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import HoloError
+from .holotypes import (CameraView, GaussianScene, PipelineForward, PipelineOptions, PropagationOptions,
+                        RasterForward, RenderSettings, WaveConfig, plane_positions)
+
+_NP = {"f32": (L.F32, np.complex64, np.float32), "f64": (L.F64, np.complex128, np.float64)}
+
+
+def _wave(cfg: WaveConfig) -> L.Wave:
+    w = L.Wave()
+    w.nx, w.ny = int(cfg.nx), int(cfg.ny)
+    w.pitch = float(cfg.pitch)
+    wl = list(cfg.wavelengths)
+    if len(wl) > L.MAX_CH:
+        raise HoloError("config", "too many wavelength channels")
+    w.channels = len(wl)
+    for i, v in enumerate(wl):
+        w.wavelengths[i] = float(v)
+    w.distance = float(cfg.distance)
+    w.volume_depth = float(cfg.volume_depth)
+    w.num_planes = int(cfg.num_planes)
+    return w
+
+
+def _camera(cam: CameraView) -> L.Camera:
+    c = L.Camera()
+    for i in range(6):
+        c.pose[i] = float(cam.pose[i])
+    c.focal_px = float(cam.focal_px)
+    c.cx, c.cy = float(cam.cx), float(cam.cy)
+    c.width, c.height = int(cam.width), int(cam.height)
+    return c
+
+
+def _settings(st: Optional[RenderSettings]) -> L.RasterSettings:
+    st = st or RenderSettings()
+    s = L.RasterSettings()
+    for k in ("near_clip", "dilation", "plane_eps", "term_eps", "alpha_floor", "alpha_clamp", "radius_form_cap",
+              "ste_tau", "soft_tau"):
+        setattr(s, k, float(getattr(st, k)))
+    s.soft_assignment = int(bool(st.soft_assignment))
+    s.tile = int(st.tile)
+    return s
+
+
+def _prop(opt: Optional[PropagationOptions]) -> L.PropOptions:
+    opt = opt or PropagationOptions()
+    p = L.PropOptions()
+    p.pad2x = int(bool(opt.pad2x))
+    p.local_band_limit = int(bool(opt.local_band_limit))
+    return p
+
+
+class _CudaArray:
+    """Zero-copy __cuda_array_interface__ view of a library-owned device buffer."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def _torch():
+    import torch  # plumbing only: device memory, streams, collectives
+
+    if not torch.cuda.is_available():
+        raise HoloError("usage", "no CUDA device visible; libholo_cuda has no CPU fallback")
+    return torch
+
+
+class Context:
+    """One holo_ctx: a CUDA stream (torch's current stream by default), the resident
+    scene and the last frame's outputs."""
+
+    def __init__(self, device: int = 0, use_torch_stream: bool = True):
+        torch = _torch()
+        self.device = device
+        self.lib = L.lib()
+        h = C.c_void_p()
+        L.check(self.lib.holo_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.info = L.FrameInfo()
+        self._keep = []
+        if use_torch_stream:
+            with torch.cuda.device(device):
+                self.set_stream(torch.cuda.current_stream().cuda_stream)
+
+    def close(self):
+        if getattr(self, "h", None):
+            L.check(self.lib.holo_ctx_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------- plumbing
+    def set_stream(self, stream: int) -> None:
+        """Enqueue on this CUDA stream handle (0 = the legacy default stream)."""
+        L.check(self.lib.holo_ctx_set_stream(self.h, C.c_void_p(stream or None)))
+
+    def use_own_stream(self) -> None:
+        L.check(self.lib.holo_ctx_use_own_stream(self.h))
+
+    def stream(self) -> int:
+        return int(self.lib.holo_ctx_get_stream(self.h) or 0)
+
+    def synchronize(self) -> None:
+        L.check(self.lib.holo_ctx_synchronize(self.h))
+
+    def launch_count(self) -> int:
+        return int(self.lib.holo_ctx_launch_count(self.h))
+
+    def enable_timing(self, on: bool = True) -> None:
+        L.check(self.lib.holo_ctx_enable_timing(self.h, int(on)))
+
+    def reset_timing(self) -> None:
+        L.check(self.lib.holo_ctx_reset_timing(self.h))
+
+    def stage_times(self) -> dict:
+        ms = (C.c_double * 8)()
+        n = (C.c_int * 8)()
+        L.check(self.lib.holo_ctx_stage_times(self.h, ms, n, 8))
+        return {name: (ms[i], n[i]) for i, name in enumerate(L.STAGES)}
+
+    # ---------------------------------------------------------------- scene
+    def upload_scene(self, scene: GaussianScene) -> None:
+        """Host f64 arrays -> HBM (validated on the device at render time, scene.cpp:19-32)."""
+        n = scene.size()
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in
+                (scene.positions, scene.rotations, scene.log_scales, scene.amplitudes, scene.opacity_logits,
+                 scene.phases, scene.plane_logits)]
+        sizes = [a.size for a in arrs]
+        if sizes != [3 * n, 4 * n, 3 * n, 3 * n, n, 3 * n, n * scene.num_planes]:
+            raise HoloError("config", "scene arrays have inconsistent sizes")
+        s = L.SceneArrays()
+        s.n, s.num_planes = n, int(scene.num_planes)
+        for name, a in zip(("positions", "rotations", "log_scales", "amplitudes", "opacity_logits", "phases",
+                            "plane_logits"), arrs):
+            setattr(s, name, a.ctypes.data)
+        L.check(self.lib.holo_scene_upload(self.h, C.byref(s)))
+        # pageable host memory: the copy has completed when the call returns; keep
+        # the arrays alive until the stream drains anyway
+        self._keep = arrs
+
+    def upload_scene_pointers(self, n: int, num_planes: int, ptrs: Sequence[int], device: bool) -> None:
+        """Scene arrays given as raw pointers (pinned host or device), in reference order."""
+        s = L.SceneArrays()
+        s.n, s.num_planes = int(n), int(num_planes)
+        for name, p in zip(("positions", "rotations", "log_scales", "amplitudes", "opacity_logits", "phases",
+                            "plane_logits"), ptrs):
+            setattr(s, name, int(p))
+        fn = self.lib.holo_scene_upload_device if device else self.lib.holo_scene_upload
+        L.check(fn(self.h, C.byref(s)))
+
+    # --------------------------------------------------------------- render
+    def render(self, cam: CameraView, cfg: WaveConfig, settings: Optional[RenderSettings] = None,
+               prop: Optional[PropagationOptions] = None,
+               outputs: int = L.OUT_HOLOGRAM | L.OUT_INTENSITY) -> L.FrameInfo:
+        L.check(self.lib.holo_render(self.h, C.byref(_camera(cam)), C.byref(_wave(cfg)),
+                                     C.byref(_settings(settings)), C.byref(_prop(prop)), int(outputs),
+                                     C.byref(self.info)))
+        return self.info
+
+    def render_begin(self, cam, cfg, settings, prop, plane_begin, plane_end, spectrum_ptr: int, outputs: int):
+        L.check(self.lib.holo_render_begin(self.h, C.byref(_camera(cam)), C.byref(_wave(cfg)),
+                                           C.byref(_settings(settings)), C.byref(_prop(prop)), int(plane_begin),
+                                           int(plane_end), C.c_void_p(spectrum_ptr or None), int(outputs),
+                                           C.byref(self.info)))
+        return self.info
+
+    def render_end(self, cfg, prop, plane_begin, plane_end, spectrum_ptr: int, outputs: int):
+        L.check(self.lib.holo_render_end(self.h, C.byref(_wave(cfg)), C.byref(_prop(prop)), int(plane_begin),
+                                         int(plane_end), C.c_void_p(spectrum_ptr or None), int(outputs)))
+
+    def buffer(self, which: int):
+        p = C.c_void_p()
+        n = C.c_size_t()
+        L.check(self.lib.holo_frame_buffer(self.h, int(which), C.byref(p), C.byref(n)))
+        return int(p.value or 0), int(n.value)
+
+    def download(self, which: int, dtype, shape) -> np.ndarray:
+        out = np.empty(shape, dtype=dtype)
+        L.check(self.lib.holo_frame_download(self.h, int(which), out.ctypes.data, out.nbytes))
+        return out
+
+    def download_into(self, which: int, host_ptr: int, nbytes: int) -> None:
+        L.check(self.lib.holo_frame_download(self.h, int(which), C.c_void_p(host_ptr), int(nbytes)))
+
+    def tensor(self, which: int, dtype: str, shape):
+        """Zero-copy torch view of an output buffer (valid until the next render)."""
+        torch = _torch()
+        ptr, nbytes = self.buffer(which)
+        typestr = {"c8": "<c8", "f4": "<f4", "i4": "<i4", "u4": "<u4", "f8": "<f8", "u1": "|u1"}[dtype]
+        return torch.as_tensor(_CudaArray(ptr, shape, typestr), device=f"cuda:{self.device}")
+
+    # ------------------------------------------------------------ operators
+    def _dev(self, arr: np.ndarray, precision: str):
+        torch = _torch()
+        _, cdt, _ = _NP[precision]
+        a = np.ascontiguousarray(arr, dtype=cdt)
+        return torch.from_numpy(a).to(f"cuda:{self.device}")
+
+    def fft2(self, data: np.ndarray, inverse: bool = False, precision: str = "f64") -> np.ndarray:
+        d = self._dev(data, precision)
+        h, w = d.shape[-2:]
+        batch = int(np.prod(d.shape[:-2])) if d.dim() > 2 else 1
+        L.check(self.lib.holo_fft2(self.h, d.data_ptr(), w, h, batch, int(inverse), _NP[precision][0]))
+        return d.cpu().numpy()
+
+    def transfer_function(self, cfg: WaveConfig, z: float, opt=None, precision: str = "f64") -> np.ndarray:
+        torch = _torch()
+        f = 2 if (opt and opt.pad2x) else 1
+        out = torch.empty((cfg.channels(), cfg.ny * f, cfg.nx * f),
+                          dtype=torch.complex64 if precision == "f32" else torch.complex128,
+                          device=f"cuda:{self.device}")
+        L.check(self.lib.holo_transfer_function(self.h, C.byref(_wave(cfg)), float(z), C.byref(_prop(opt)),
+                                                out.data_ptr(), _NP[precision][0]))
+        return out.cpu().numpy()
+
+    def propagate(self, u: np.ndarray, cfg: WaveConfig, z: float, opt=None, precision: str = "f64") -> np.ndarray:
+        d = self._dev(u, precision)
+        if d.dim() != 3:
+            raise HoloError("config", "propagate: field does not match the configured grid")
+        c, h, w = d.shape
+        out = d.new_empty(d.shape)
+        L.check(self.lib.holo_propagate(self.h, d.data_ptr(), out.data_ptr(), w, h, c, C.byref(_wave(cfg)),
+                                        float(z), C.byref(_prop(opt)), _NP[precision][0]))
+        return out.cpu().numpy()
+
+    def forward_record(self, layers, cfg: WaveConfig, opt=None, precision: str = "f64") -> np.ndarray:
+        d = self._dev(np.stack([np.asarray(x) for x in layers]), precision)
+        out = d.new_empty(d.shape[1:])
+        L.check(self.lib.holo_forward_record(self.h, d.data_ptr(), d.shape[0], out.data_ptr(), C.byref(_wave(cfg)),
+                                             C.byref(_prop(opt)), _NP[precision][0]))
+        return out.cpu().numpy()
+
+    def inverse_propagate(self, hologram: np.ndarray, cfg: WaveConfig, opt=None, precision: str = "f64"):
+        d = self._dev(hologram, precision)
+        out = d.new_empty((cfg.num_planes,) + tuple(d.shape))
+        L.check(self.lib.holo_inverse_propagate(self.h, d.data_ptr(), out.data_ptr(), C.byref(_wave(cfg)),
+                                                C.byref(_prop(opt)), _NP[precision][0]))
+        r = out.cpu().numpy()
+        return [r[l] for l in range(r.shape[0])]
+
+    def intensity(self, u: np.ndarray, precision: str = "f64") -> np.ndarray:
+        d = self._dev(u, precision)
+        torch = _torch()
+        out = torch.empty(d.shape, dtype=torch.float32 if precision == "f32" else torch.float64, device=d.device)
+        L.check(self.lib.holo_intensity(self.h, d.data_ptr(), out.data_ptr(), d.numel(), _NP[precision][0]))
+        return out.cpu().numpy()
+
+
+_DEFAULT: dict = {}
+
+
+def default_context(device: int = 0) -> Context:
+    ctx = _DEFAULT.get(device)
+    if ctx is None:
+        ctx = Context(device)
+        _DEFAULT[device] = ctx
+    return ctx
+
+
+# ------------------------------------------------------------------ reference-shaped functions
+
+def _collect_raster(ctx: Context, scene: GaussianScene, cfg: WaveConfig, C_: int, info: L.FrameInfo,
+                    want_aux: bool = True) -> RasterForward:
+    Ln, H, W = cfg.num_planes, cfg.ny, cfg.nx
+    N = scene.size()
+    layers = ctx.download(L.BUF_LAYERS, np.complex64, (Ln, C_, H, W)).astype(np.complex128)
+    t_final = n_contrib = None
+    if want_aux:
+        t_final = ctx.download(L.BUF_T_FINAL, np.float32, (Ln, H, W)).astype(np.float64)
+        n_contrib = ctx.download(L.BUF_N_CONTRIB, np.int32, (Ln, H, W))
+    E = int(info.num_entries)
+    B = Ln * info.tiles_x * info.tiles_y
+    bucket_start = ctx.download(L.BUF_BUCKET_START, np.uint32, (B + 1,))
+    gidx = ctx.download(L.BUF_ENTRY_GIDX, np.int32, (E,))
+    depth = ctx.download(L.BUF_ENTRY_DEPTH, np.float64, (E,))
+    entries = np.zeros(E, dtype=[("bucket", np.int32), ("gidx", np.int32), ("depth", np.float64)])
+    entries["bucket"] = np.repeat(np.arange(B, dtype=np.int32), np.diff(bucket_start.astype(np.int64)))
+    entries["gidx"] = gidx
+    entries["depth"] = depth
+    proj = ctx.download(L.BUF_PROJECTED, np.uint8, (N * C.sizeof(L.Projected),))
+    pa = np.frombuffer(proj.tobytes(), dtype=np.dtype([(n, "<i4") if t in (C.c_int32,) else
+                                                       (n, "<f8", (3,)) if n in ("amp", "phase") else (n, "<f8")
+                                                       for n, t in L.Projected._fields_]))
+    projected = {k: pa[k].copy() for k in pa.dtype.names if k != "pad_"}
+    rho = ctx.download(L.BUF_RHO, np.float64, (N, Ln))
+    touched = ctx.download(L.BUF_TOUCHED, np.uint8, (N,))
+    return RasterForward(layers=[layers[l] for l in range(Ln)], t_final=t_final, n_contrib=n_contrib,
+                         projected=projected, rho=rho, touched=touched, entries=entries, bucket_start=bucket_start,
+                         tiles_x=int(info.tiles_x), tiles_y=int(info.tiles_y))
+
+
+def _check_shapes(scene: GaussianScene, cam: CameraView, cfg: WaveConfig) -> None:
+    scene.validate()
+    cam.validate()
+    cfg.validate()
+    if scene.num_planes != cfg.num_planes:
+        raise HoloError("config", "scene plane count does not match the wave config")
+    if cam.width != cfg.nx or cam.height != cfg.ny:
+        raise HoloError("config", "camera resolution must match the hologram grid")
+
+
+def raster_forward(scene: GaussianScene, cam: CameraView, cfg: WaveConfig,
+                   settings: Optional[RenderSettings] = None, ctx: Optional[Context] = None) -> RasterForward:
+    """rasterizer.cpp:139-263 on the GPU.  Layers carry cfg.channels() channels when
+    cfg has fewer than 3 wavelengths (C1 adapter), else the reference's 3."""
+    _check_shapes(scene, cam, cfg)
+    ctx = ctx or default_context()
+    ctx.upload_scene(scene)
+    C_ = min(cfg.channels(), 3)
+    cfg3 = cfg if cfg.channels() <= 3 else WaveConfig(cfg.nx, cfg.ny, cfg.pitch, list(cfg.wavelengths)[:3],
+                                                      cfg.distance, cfg.volume_depth, cfg.num_planes)
+    info = ctx.render(cam, cfg3, settings, None,
+                      outputs=L.OUT_LAYERS | L.OUT_AUX | L.OUT_LISTS | L.OUT_PROJECTED)
+    return _collect_raster(ctx, scene, cfg3, C_, info)
+
+
+def pipeline_forward(scene: GaussianScene, cam: CameraView, cfg: WaveConfig,
+                     opt: Optional[PipelineOptions] = None, ctx: Optional[Context] = None,
+                     raster: bool = True, replayed: bool = True) -> PipelineForward:
+    """pipeline.cpp:20-29: raster -> forward_record -> inverse_propagate -> intensity."""
+    _check_shapes(scene, cam, cfg)
+    if cfg.channels() > 3:
+        raise HoloError("config", "propagate: field does not match the configured grid")
+    opt = opt or PipelineOptions()
+    ctx = ctx or default_context()
+    ctx.upload_scene(scene)
+    outs = L.OUT_HOLOGRAM | L.OUT_INTENSITY
+    if replayed:
+        outs |= L.OUT_REPLAYED
+    if raster:
+        outs |= L.OUT_LAYERS | L.OUT_AUX | L.OUT_LISTS | L.OUT_PROJECTED
+    info = ctx.render(cam, cfg, opt.raster, opt.prop, outputs=outs)
+    Cn, Ln, H, W = cfg.channels(), cfg.num_planes, cfg.ny, cfg.nx
+    holo = ctx.download(L.BUF_HOLOGRAM, np.complex64, (Cn, H, W)).astype(np.complex128)
+    ints = ctx.download(L.BUF_INTENSITY, np.float32, (Ln, Cn, H, W)).astype(np.float64)
+    rep = None
+    if replayed:
+        r = ctx.download(L.BUF_REPLAYED, np.complex64, (Ln, Cn, H, W)).astype(np.complex128)
+        rep = [r[l] for l in range(Ln)]
+    ras = _collect_raster(ctx, scene, cfg, Cn, info) if raster else None
+    return PipelineForward(raster=ras, hologram=holo, replayed=rep, intensities=[ints[l] for l in range(Ln)])
+
+
+def propagate(u, cfg: WaveConfig, z: float, opt: Optional[PropagationOptions] = None, precision: str = "f64"):
+    return default_context().propagate(u, cfg, z, opt, precision)
+
+
+def forward_record(layers, cfg: WaveConfig, opt: Optional[PropagationOptions] = None, precision: str = "f64"):
+    return default_context().forward_record(layers, cfg, opt, precision)
+
+
+def inverse_propagate(hologram, cfg: WaveConfig, opt: Optional[PropagationOptions] = None, precision: str = "f64"):
+    return default_context().inverse_propagate(hologram, cfg, opt, precision)
+
+
+def transfer_function(cfg: WaveConfig, z: float, opt: Optional[PropagationOptions] = None, precision: str = "f64"):
+    return default_context().transfer_function(cfg, z, opt, precision)
+
+
+def fft2(data, precision: str = "f64"):
+    return default_context().fft2(data, False, precision)
+
+
+def ifft2(data, precision: str = "f64"):
+    return default_context().fft2(data, True, precision)
+
+
+def intensity(u, precision: str = "f64"):
+    return default_context().intensity(u, precision)

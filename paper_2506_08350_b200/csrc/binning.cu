@@ -1,0 +1,265 @@
+// Tile binning on sm_100a: (plane, tile) bucket histogram, exclusive scan into
+// bucket_start, and emission of (depth key, Gaussian) work items.
+//
+// Replaces the serial emission / counting sort / per-bucket std::sort of
+// raster_forward (proj/src/rasterizer.cpp:172-225).  Emission order inside a
+// bucket is arbitrary here (atomic cursors); the compositing kernel restores the
+// reference order by sorting each bucket on the total order (zc, gidx)
+// (rasterizer.cpp:221-224), so the final lists are deterministic and equal the
+// reference's.  Buckets above kSortCap entries are sorted here instead, by a
+// single-CTA bitonic network per bucket.
+#include "kernels.cuh"
+
+namespace holo_cuda {
+
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ unsigned warp_incl_scan(unsigned v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned u = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += u;
+    }
+    return v;
+}
+
+// Exclusive block scan of one value per thread; returns the exclusive prefix, total in *total.
+__device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* total) {
+    __shared__ unsigned warp_sums[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const unsigned inc = warp_incl_scan(v);
+    if (lane == 31) warp_sums[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        unsigned s = lane < nw ? warp_sums[lane] : 0u;
+        s = warp_incl_scan(s);
+        if (lane < nw) warp_sums[lane] = s;
+    }
+    __syncthreads();
+    const unsigned warp_prefix = wid > 0 ? warp_sums[wid - 1] : 0u;
+    *total = warp_sums[nw - 1];
+    __syncthreads();
+    return warp_prefix + inc - v;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_partials(const unsigned* __restrict__ in, long long n,
+                                                                unsigned* __restrict__ partials,
+                                                                unsigned* __restrict__ dmax) {
+    const long long base = static_cast<long long>(blockIdx.x) * kScanTile;
+    unsigned s = 0, m = 0;
+    for (int k = 0; k < kScanItems; ++k) {
+        const long long i = base + static_cast<long long>(k) * kScanThreads + threadIdx.x;
+        if (i < n) {
+            const unsigned v = in[i];
+            s += v;
+            m = v > m ? v : m;
+        }
+    }
+    unsigned total;
+    block_excl_scan(s, &total);
+    if (threadIdx.x == 0) partials[blockIdx.x] = total;
+    // block max
+    for (int d = 16; d > 0; d >>= 1) {
+        const unsigned o = __shfl_down_sync(0xffffffffu, m, d);
+        m = o > m ? o : m;
+    }
+    if ((threadIdx.x & 31) == 0 && dmax) atomicMax(dmax, m);
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_top(unsigned* __restrict__ partials, int nblocks) {
+    unsigned carry = 0;
+    for (int base = 0; base < nblocks; base += kScanThreads) {
+        const int i = base + threadIdx.x;
+        const unsigned v = i < nblocks ? partials[i] : 0u;
+        unsigned total;
+        const unsigned ex = block_excl_scan(v, &total);
+        if (i < nblocks) partials[i] = carry + ex;
+        carry += total;
+    }
+    if (threadIdx.x == 0) partials[nblocks] = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_final(const unsigned* __restrict__ in, long long n,
+                                                             const unsigned* __restrict__ partials,
+                                                             unsigned* __restrict__ out, int nblocks) {
+    // each thread owns kScanItems consecutive elements
+    const long long base = static_cast<long long>(blockIdx.x) * kScanTile + static_cast<long long>(threadIdx.x) * kScanItems;
+    unsigned v[kScanItems];
+    unsigned s = 0;
+    for (int k = 0; k < kScanItems; ++k) {
+        const long long i = base + k;
+        v[k] = i < n ? in[i] : 0u;
+        s += v[k];
+    }
+    unsigned total;
+    unsigned run = block_excl_scan(s, &total) + partials[blockIdx.x];
+    for (int k = 0; k < kScanItems; ++k) {
+        const long long i = base + k;
+        if (i < n) out[i] = run;
+        run += v[k];
+    }
+    if (blockIdx.x == nblocks - 1 && threadIdx.x == 0) out[n] = partials[nblocks];
+}
+
+// Loop over the (plane, tile) buckets of Gaussian i restricted to planes [pb, pe).
+template <class F>
+__device__ __forceinline__ void for_each_bucket(const PreOut& pre, size_t i, int L, int pb, int pe, int tiles_x,
+                                                int num_tiles, int soft, F f) {
+    if (pre.count[i] == 0) return;
+    const int4 r = pre.rect[i];
+    if (soft) {
+        const unsigned long long mask = pre.pmask[i];
+        for (int l = pb; l < pe && l < 64; ++l) {
+            if (!((mask >> l) & 1ull)) continue;
+            for (int ty = r.z; ty < r.w; ++ty)
+                for (int tx = r.x; tx < r.y; ++tx) f((l - pb) * num_tiles + ty * tiles_x + tx);
+        }
+    } else {
+        const int l = pre.plane[i];
+        if (l < pb || l >= pe) return;
+        for (int ty = r.z; ty < r.w; ++ty)
+            for (int tx = r.x; tx < r.y; ++tx) f((l - pb) * num_tiles + ty * tiles_x + tx);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_bucket_count(PreOut pre, size_t N, int L, int pb, int pe, int tiles_x,
+                                                      int num_tiles, int soft, unsigned* __restrict__ bcount) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= N) return;
+    for_each_bucket(pre, i, L, pb, pe, tiles_x, num_tiles, soft, [&](int b) { atomicAdd(bcount + b, 1u); });
+}
+
+__global__ void __launch_bounds__(256) k_bucket_emit(PreOut pre, size_t N, int L, int pb, int pe, int tiles_x,
+                                                     int num_tiles, int soft, const unsigned* __restrict__ bstart,
+                                                     unsigned* __restrict__ cursor,
+                                                     unsigned long long* __restrict__ ekey, int* __restrict__ egidx) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= N) return;
+    const unsigned long long key = static_cast<unsigned long long>(__double_as_longlong(pre.zc[i]));
+    for_each_bucket(pre, i, L, pb, pe, tiles_x, num_tiles, soft, [&](int b) {
+        const unsigned e = bstart[b] + atomicAdd(cursor + b, 1u);
+        ekey[e] = key;
+        egidx[e] = static_cast<int>(i);
+    });
+}
+
+// (key, gidx) lexicographic order; zc > near > 0, so the IEEE bits of zc order like zc.
+__device__ __forceinline__ bool less_kg(unsigned long long ka, int ga, unsigned long long kb, int gb) {
+    return ka < kb || (ka == kb && ga < gb);
+}
+
+// One CTA per large bucket: bitonic sort over the padded power of two in scratch.
+__global__ void __launch_bounds__(1024) k_sort_large(const int* __restrict__ ids, const unsigned* __restrict__ starts,
+                                                     const unsigned* __restrict__ counts, int pow2,
+                                                     unsigned long long* __restrict__ ekey, int* __restrict__ egidx,
+                                                     unsigned long long* __restrict__ tkey, int* __restrict__ tg) {
+    const unsigned s = starts[blockIdx.x], n = counts[blockIdx.x];
+    unsigned long long* K = tkey + static_cast<size_t>(blockIdx.x) * pow2;
+    int* G = tg + static_cast<size_t>(blockIdx.x) * pow2;
+    unsigned P = 1;
+    while (P < n) P <<= 1;
+    for (unsigned t = threadIdx.x; t < P; t += blockDim.x) {
+        K[t] = t < n ? ekey[s + t] : ~0ull;
+        G[t] = t < n ? egidx[s + t] : 0x7fffffff;
+    }
+    __syncthreads();
+    for (unsigned k = 2; k <= P; k <<= 1) {
+        for (unsigned j = k >> 1; j > 0; j >>= 1) {
+            for (unsigned t = threadIdx.x; t < P; t += blockDim.x) {
+                const unsigned u = t ^ j;
+                if (u > t) {
+                    const bool up = (t & k) == 0;
+                    const unsigned long long ka = K[t], kb = K[u];
+                    const int ga = G[t], gb = G[u];
+                    const bool swap = up ? less_kg(kb, gb, ka, ga) : less_kg(ka, ga, kb, gb);
+                    if (swap) {
+                        K[t] = kb;
+                        K[u] = ka;
+                        G[t] = gb;
+                        G[u] = ga;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (unsigned t = threadIdx.x; t < n; t += blockDim.x) {
+        ekey[s + t] = K[t];
+        egidx[s + t] = G[t];
+    }
+}
+
+__global__ void k_entry_depths(const int* __restrict__ egidx, const double* __restrict__ zc,
+                               double* __restrict__ edepth, size_t E) {
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < E;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x)
+        edepth[e] = zc[egidx[e]];
+}
+
+}  // namespace
+
+void exclusive_scan_u32(holo_ctx* ctx, const unsigned* in, unsigned* out, long long n, unsigned* d_max) {
+    const int nblocks = static_cast<int>((n + kScanTile - 1) / kScanTile);
+    const int nb = nblocks > 0 ? nblocks : 1;
+    unsigned* partials = static_cast<unsigned*>(ctx->buffer("scan_partials", sizeof(unsigned) * (nb + 1)));
+    k_scan_partials<<<nb, kScanThreads, 0, ctx->stream>>>(in, n, partials, d_max);
+    HC_LAUNCHED(ctx);
+    k_scan_top<<<1, kScanThreads, 0, ctx->stream>>>(partials, nb);
+    HC_LAUNCHED(ctx);
+    k_scan_final<<<nb, kScanThreads, 0, ctx->stream>>>(in, n, partials, out, nb);
+    HC_LAUNCHED(ctx);
+}
+
+void bucket_count(holo_ctx* ctx, const PreOut& pre, size_t N, int L, int pb, int pe, int tiles_x, int num_tiles,
+                  int soft, unsigned* bcount) {
+    if (N == 0) return;
+    k_bucket_count<<<static_cast<unsigned>((N + 255) / 256), 256, 0, ctx->stream>>>(pre, N, L, pb, pe, tiles_x,
+                                                                                    num_tiles, soft, bcount);
+    HC_LAUNCHED(ctx);
+}
+
+void bucket_emit(holo_ctx* ctx, const PreOut& pre, size_t N, int L, int pb, int pe, int tiles_x, int num_tiles,
+                 int soft, const unsigned* bstart, unsigned* cursor, unsigned long long* ekey, int* egidx) {
+    if (N == 0) return;
+    k_bucket_emit<<<static_cast<unsigned>((N + 255) / 256), 256, 0, ctx->stream>>>(
+        pre, N, L, pb, pe, tiles_x, num_tiles, soft, bstart, cursor, ekey, egidx);
+    HC_LAUNCHED(ctx);
+}
+
+void sort_large_buckets(holo_ctx* ctx, const std::vector<int>& ids, const std::vector<unsigned>& starts,
+                        const std::vector<unsigned>& counts, unsigned long long* ekey, int* egidx) {
+    const int nl = static_cast<int>(ids.size());
+    if (nl == 0) return;
+    unsigned maxn = 0;
+    for (unsigned c : counts) maxn = c > maxn ? c : maxn;
+    int pow2 = 1;
+    while (static_cast<unsigned>(pow2) < maxn) pow2 <<= 1;
+    int* d_ids = static_cast<int*>(ctx->buffer("large_ids", sizeof(int) * nl));
+    unsigned* d_starts = static_cast<unsigned*>(ctx->buffer("large_starts", sizeof(unsigned) * nl));
+    unsigned* d_counts = static_cast<unsigned*>(ctx->buffer("large_counts", sizeof(unsigned) * nl));
+    HC_CUDA(cudaMemcpyAsync(d_ids, ids.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, ctx->stream));
+    HC_CUDA(cudaMemcpyAsync(d_starts, starts.data(), sizeof(unsigned) * nl, cudaMemcpyHostToDevice, ctx->stream));
+    HC_CUDA(cudaMemcpyAsync(d_counts, counts.data(), sizeof(unsigned) * nl, cudaMemcpyHostToDevice, ctx->stream));
+    auto* tkey = static_cast<unsigned long long*>(
+        ctx->buffer("large_tkey", sizeof(unsigned long long) * static_cast<size_t>(pow2) * nl));
+    auto* tg = static_cast<int*>(ctx->buffer("large_tg", sizeof(int) * static_cast<size_t>(pow2) * nl));
+    k_sort_large<<<nl, 1024, 0, ctx->stream>>>(d_ids, d_starts, d_counts, pow2, ekey, egidx, tkey, tg);
+    HC_LAUNCHED(ctx);
+    // the host vectors must outlive the async copies
+    HC_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void entry_depths(holo_ctx* ctx, const int* egidx, const double* zc, double* edepth, size_t E) {
+    if (E == 0) return;
+    const size_t blocks = (E + 255) / 256;
+    const unsigned grid = static_cast<unsigned>(blocks < 4096 ? blocks : 4096);
+    k_entry_depths<<<grid, 256, 0, ctx->stream>>>(egidx, zc, edepth, E);
+    HC_LAUNCHED(ctx);
+}
+
+}  // namespace holo_cuda

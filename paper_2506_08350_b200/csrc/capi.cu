@@ -1,0 +1,871 @@
+// libholo_cuda C-ABI: context, scene residency, the render orchestration and the
+// propagation operators (include/holo_cuda.h).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+using namespace holo_cuda;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return HOLO_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return HOLO_ERR_OOM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return HOLO_ERR_NUMERIC;
+    }
+}
+
+void require(bool ok, int code, const char* msg) {
+    if (!ok) throw Error(code, msg);
+}
+
+// WaveConfig::validate (wave_config.cpp:5-16), same messages
+void validate_wave(const holo_wave& w) {
+    if (w.nx <= 0 || w.ny <= 0) config_error("resolution must be positive");
+    if (w.pitch <= 0.0) config_error("pixel pitch must be positive");
+    if (w.channels < 1) config_error("at least one wavelength required");
+    if (w.channels > HOLO_MAX_CHANNELS) config_error("too many wavelength channels");
+    for (int c = 0; c < w.channels; ++c)
+        if (w.wavelengths[c] <= 0.0) config_error("wavelengths must be positive");
+    if (w.distance <= 0.0) config_error("propagation distance must be positive");
+    if (w.volume_depth < 0.0) config_error("volume depth must be non-negative");
+    if (w.num_planes < 1) config_error("need at least one depth plane");
+    if (w.num_planes > 1 && w.volume_depth <= 0.0) config_error("multiple planes need a positive volume depth");
+}
+
+// CameraView::validate (camera.cpp:22-27)
+void validate_camera(const holo_camera& c) {
+    if (c.width <= 0 || c.height <= 0) config_error("camera resolution must be positive");
+    if (c.focal_px <= 0.0) config_error("focal length must be positive");
+    for (double v : c.pose)
+        if (!std::isfinite(v)) config_error("camera pose must be finite");
+}
+
+// plane_positions (wave_config.cpp:18-30)
+std::vector<double> plane_positions(const holo_wave& w) {
+    validate_wave(w);
+    const int L = w.num_planes;
+    std::vector<double> z(L);
+    if (L == 1) {
+        z[0] = w.distance;
+        return z;
+    }
+    const double dz = w.volume_depth / (L - 1);
+    const double z0 = w.distance - 0.5 * (L - 1) * dz;
+    for (int l = 0; l < L; ++l) z[l] = z0 + l * dz;
+    return z;
+}
+
+template <class T>
+T* buf(holo_ctx* ctx, const char* name, size_t count) {
+    return static_cast<T*>(ctx->buffer(name, sizeof(T) * (count ? count : 1)));
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- holo_ctx methods
+
+void* holo_ctx::buffer(const std::string& name, size_t bytes) {
+    DevBuf& b = scratch[name];
+    if (b.bytes < bytes) {
+        if (b.p) {
+            HC_CUDA(cudaStreamSynchronize(stream));
+            HC_CUDA(cudaFree(b.p));
+            b.p = nullptr;
+            b.bytes = 0;
+        }
+        const size_t want = bytes + bytes / 8;  // headroom for frame-to-frame growth
+        HC_CUDA(cudaMalloc(&b.p, want));
+        b.bytes = want;
+    }
+    return b.p;
+}
+
+void* holo_ctx::pinned(size_t bytes) {
+    if (host_pinned_bytes < bytes) {
+        if (host_pinned) {
+            HC_CUDA(cudaStreamSynchronize(stream));
+            HC_CUDA(cudaFreeHost(host_pinned));
+        }
+        HC_CUDA(cudaMallocHost(&host_pinned, bytes));
+        host_pinned_bytes = bytes;
+    }
+    return host_pinned;
+}
+
+template <class T>
+const cx<T>* holo_ctx::twiddle(int n) {
+    const auto key = std::make_pair(n, static_cast<int>(sizeof(T)));
+    auto it = twiddles.find(key);
+    if (it != twiddles.end()) return static_cast<const cx<T>*>(it->second);
+    std::vector<cx<T>> h(n);
+    const double two_pi = 6.283185307179586476925286766559;
+    for (int q = 0; q < n; ++q) {
+        const double a = -two_pi * static_cast<double>(q) / static_cast<double>(n);
+        h[q] = mk<T>(static_cast<T>(std::cos(a)), static_cast<T>(std::sin(a)));
+    }
+    void* d = nullptr;
+    HC_CUDA(cudaMalloc(&d, sizeof(cx<T>) * n));
+    HC_CUDA(cudaMemcpy(d, h.data(), sizeof(cx<T>) * n, cudaMemcpyHostToDevice));
+    twiddles[key] = d;
+    return static_cast<const cx<T>*>(d);
+}
+template const cx<float>* holo_ctx::twiddle<float>(int);
+template const cx<double>* holo_ctx::twiddle<double>(int);
+
+const double* holo_ctx::freq(int n, double pitch) {
+    uint64_t bits;
+    std::memcpy(&bits, &pitch, sizeof bits);
+    const auto key = std::make_pair(n, bits);
+    auto it = freqs.find(key);
+    if (it != freqs.end()) return it->second;
+    std::vector<double> h(n);
+    for (int i = 0; i < n; ++i) {
+        const int k = (i < (n + 1) / 2) ? i : i - n;  // freq_at, propagation.cpp:13-16
+        h[i] = static_cast<double>(k) / (static_cast<double>(n) * pitch);
+    }
+    double* d = nullptr;
+    HC_CUDA(cudaMalloc(&d, sizeof(double) * n));
+    HC_CUDA(cudaMemcpy(d, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+    freqs[key] = d;
+    return d;
+}
+
+namespace {
+
+cudaEvent_t take_event(holo_ctx* ctx) {
+    if (!ctx->event_pool.empty()) {
+        cudaEvent_t e = ctx->event_pool.back();
+        ctx->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    HC_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+// async upload of a small host table via a pinned ring slot (no stream stall)
+void upload_small(holo_ctx* ctx, void* dev, const void* host, size_t bytes) {
+    if (bytes > holo_ctx::kRingSlotBytes) {
+        HC_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        HC_CUDA(cudaStreamSynchronize(ctx->stream));
+        return;
+    }
+    if (!ctx->ring) {
+        HC_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->ring), holo_ctx::kRingSlots * holo_ctx::kRingSlotBytes));
+        for (auto& e : ctx->ring_ev) HC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const int s = ctx->ring_next;
+    ctx->ring_next = (s + 1) % holo_ctx::kRingSlots;
+    if (ctx->ring_used[s]) HC_CUDA(cudaEventSynchronize(ctx->ring_ev[s]));
+    unsigned char* slot = ctx->ring + static_cast<size_t>(s) * holo_ctx::kRingSlotBytes;
+    std::memcpy(slot, host, bytes);
+    HC_CUDA(cudaMemcpyAsync(dev, slot, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    HC_CUDA(cudaEventRecord(ctx->ring_ev[s], ctx->stream));
+    ctx->ring_used[s] = true;
+}
+
+}  // namespace
+
+void holo_ctx::stage_begin() {
+    if (!timing) return;
+    ev_a = take_event(this);
+    HC_CUDA(cudaEventRecord(ev_a, stream));
+}
+
+void holo_ctx::stage_end(int stage) {
+    if (!timing) return;
+    cudaEvent_t b = take_event(this);
+    HC_CUDA(cudaEventRecord(b, stream));
+    pending.push_back({stage, ev_a, b});
+    ++stage_calls[stage];
+}
+
+namespace {
+
+void resolve_timing(holo_ctx* ctx) {
+    if (ctx->pending.empty()) return;
+    HC_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (const holo_ctx::Timed& t : ctx->pending) {
+        float ms = 0.0f;
+        HC_CUDA(cudaEventElapsedTime(&ms, t.a, t.b));
+        ctx->stage_ms[t.stage] += ms;
+        ctx->event_pool.push_back(t.a);
+        ctx->event_pool.push_back(t.b);
+    }
+    ctx->pending.clear();
+}
+
+// ---------------------------------------------------------------- render internals
+
+struct FrameGeom {
+    int W, H, C, L, tile, tiles_x, tiles_y, num_tiles;
+    size_t P;
+};
+
+FrameGeom check_render(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, const holo_raster_settings& st) {
+    validate_camera(cam);
+    validate_wave(wave);
+    if (ctx->scene_planes != wave.num_planes)
+        config_error("scene plane count does not match the wave config");  // rasterizer.cpp:144-145
+    if (cam.width != wave.nx || cam.height != wave.ny)
+        config_error("camera resolution must match the hologram grid");  // rasterizer.cpp:146-147
+    if (wave.channels > 3) config_error("propagate: field does not match the configured grid");
+    if (st.tile != 8 && st.tile != 16 && st.tile != 32) config_error("render supports tile sizes 8, 16 and 32");
+    if (st.soft_assignment && wave.num_planes > 64) config_error("soft plane assignment supports at most 64 planes");
+    FrameGeom g;
+    g.W = wave.nx;
+    g.H = wave.ny;
+    g.C = wave.channels;
+    g.L = wave.num_planes;
+    g.tile = st.tile;
+    g.tiles_x = (g.W + g.tile - 1) / g.tile;
+    g.tiles_y = (g.H + g.tile - 1) / g.tile;
+    g.num_tiles = g.tiles_x * g.tiles_y;
+    g.P = static_cast<size_t>(g.W) * g.H;
+    return g;
+}
+
+// raster stage for planes [pb, pe): preprocess, binning, composite -> "layers"
+void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, const holo_raster_settings& st,
+                   const FrameGeom& g, int pb, int pe, unsigned outputs, holo_frame_info* info) {
+    const size_t N = ctx->n;
+    const int L = g.L;
+    const int nplanes = pe - pb;
+    const long long B = static_cast<long long>(nplanes) * g.num_tiles;
+
+    CameraConsts cc;
+    host_world_to_cam(cam, cc.wc);
+    for (int i = 0; i < 3; ++i) cc.pos[i] = cam.pose[i];
+    cc.focal = cam.focal_px;
+    cc.ppx = cam.cx >= 0.0 ? cam.cx : cam.width / 2.0;   // camera.hpp:26-27
+    cc.ppy = cam.cy >= 0.0 ? cam.cy : cam.height / 2.0;
+    const double near_clip = st.near_clip > 0.0 ? st.near_clip : 0.2 * wave.distance;  // rasterizer.hpp:25-27
+
+    const bool want_proj = (outputs & HOLO_OUT_PROJECTED) != 0;
+    PreOut pre{};
+    pre.rec = buf<GRec>(ctx, "rec", N);
+    pre.rect = buf<int4>(ctx, "rect", N);
+    pre.count = buf<unsigned>(ctx, "count", N);
+    pre.zc = buf<double>(ctx, "zc", N);
+    pre.plane = buf<int>(ctx, "plane", N);
+    pre.pmask = st.soft_assignment ? buf<unsigned long long>(ctx, "pmask", N) : nullptr;
+    pre.rho = (st.soft_assignment || want_proj) ? buf<double>(ctx, "rho", N * L) : nullptr;
+    pre.touched = buf<unsigned char>(ctx, "touched", N);
+    pre.projected = want_proj ? buf<holo_projected>(ctx, "projected", N) : nullptr;
+    unsigned* misc = buf<unsigned>(ctx, "misc", 4);  // flags, num_valid, max bucket
+    pre.flags = misc;
+    pre.num_valid = misc + 1;
+    unsigned* bcount = buf<unsigned>(ctx, "bcount", B + 1);
+    unsigned* bstart = buf<unsigned>(ctx, "bstart", B + 1);
+    HC_CUDA(cudaMemsetAsync(misc, 0, sizeof(unsigned) * 4, ctx->stream));
+    HC_CUDA(cudaMemsetAsync(bcount, 0, sizeof(unsigned) * (B + 1), ctx->stream));
+
+    ctx->stage_begin();
+    preprocess(ctx, cc, st, near_clip, L, g.tiles_x, g.tiles_y, pre);
+    ctx->stage_end(0);
+
+    ctx->stage_begin();
+    bucket_count(ctx, pre, N, L, pb, pe, g.tiles_x, g.num_tiles, st.soft_assignment, bcount);
+    exclusive_scan_u32(ctx, bcount, bstart, B, misc + 2);
+    // one host sync per frame: entry count, largest bucket, validation flags
+    unsigned* hp = static_cast<unsigned*>(ctx->pinned(64));
+    HC_CUDA(cudaMemcpyAsync(hp, misc, sizeof(unsigned) * 3, cudaMemcpyDeviceToHost, ctx->stream));
+    HC_CUDA(cudaMemcpyAsync(hp + 4, bstart + B, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+    HC_CUDA(cudaStreamSynchronize(ctx->stream));
+    const unsigned flags = hp[0], num_valid = hp[1], max_bucket = hp[2];
+    const unsigned E = hp[4];
+    if (flags & 1u) config_error("degenerate quaternion in scene");     // scene.cpp:27
+    if (flags & 2u) config_error("amplitudes must be non-negative");    // scene.cpp:30
+
+    auto* ekey = buf<unsigned long long>(ctx, "ekey", E);
+    int* egidx = buf<int>(ctx, "egidx", E);
+    unsigned* cursor = bcount;  // reuse: zero it and count again during emission
+    HC_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned) * (B + 1), ctx->stream));
+    bucket_emit(ctx, pre, N, L, pb, pe, g.tiles_x, g.num_tiles, st.soft_assignment, bstart, cursor, ekey, egidx);
+    if (max_bucket > static_cast<unsigned>(kSortCap)) {
+        std::vector<unsigned> hs(B + 1);
+        HC_CUDA(cudaMemcpyAsync(hs.data(), bstart, sizeof(unsigned) * (B + 1), cudaMemcpyDeviceToHost, ctx->stream));
+        HC_CUDA(cudaStreamSynchronize(ctx->stream));
+        std::vector<int> ids;
+        std::vector<unsigned> starts, counts;
+        for (long long b = 0; b < B; ++b) {
+            const unsigned c = hs[b + 1] - hs[b];
+            if (c > static_cast<unsigned>(kSortCap)) {
+                ids.push_back(static_cast<int>(b));
+                starts.push_back(hs[b]);
+                counts.push_back(c);
+            }
+        }
+        sort_large_buckets(ctx, ids, starts, counts, ekey, egidx);
+    }
+    ctx->stage_end(1);
+
+    // composite into [nplanes][C][H][W]
+    const bool want_aux = (outputs & HOLO_OUT_AUX) != 0;
+    const bool want_lists = (outputs & HOLO_OUT_LISTS) != 0;
+    CompositeArgs ca{};
+    ca.bstart = bstart;
+    ca.ekey = ekey;
+    ca.egidx = egidx;
+    ca.rec = pre.rec;
+    ca.rho = pre.rho;
+    ca.L = L;
+    ca.C = g.C;
+    ca.W = g.W;
+    ca.H = g.H;
+    ca.tiles_x = g.tiles_x;
+    ca.num_tiles = g.num_tiles;
+    ca.plane_begin = pb;
+    ca.num_buckets = static_cast<int>(B);
+    ca.soft = st.soft_assignment;
+    ca.write_lists = want_lists ? 1 : 0;
+    ca.term_eps = static_cast<float>(st.term_eps);
+    ca.alpha_floor = static_cast<float>(st.alpha_floor);
+    ca.alpha_clamp = static_cast<float>(st.alpha_clamp);
+    ca.floor_positive = st.alpha_floor > 0.0 ? 1 : 0;
+    ca.layers = buf<cx<float>>(ctx, "layers", static_cast<size_t>(nplanes) * g.C * g.P);
+    ca.t_final = want_aux ? buf<float>(ctx, "t_final", static_cast<size_t>(nplanes) * g.P) : nullptr;
+    ca.n_contrib = want_aux ? buf<int>(ctx, "n_contrib", static_cast<size_t>(nplanes) * g.P) : nullptr;
+    ctx->stage_begin();
+    composite(ctx, ca, g.tile);
+    ctx->stage_end(2);
+    if (want_lists) entry_depths(ctx, egidx, pre.zc, buf<double>(ctx, "edepth", E), E);
+
+    ctx->f_E = E;
+    if (info) {
+        info->num_entries = E;
+        info->tiles_x = g.tiles_x;
+        info->tiles_y = g.tiles_y;
+        info->num_buckets = static_cast<int32_t>(B);
+        info->max_bucket = static_cast<int32_t>(max_bucket);
+        info->num_valid = static_cast<int32_t>(num_valid);
+    }
+}
+
+TfChan* upload_tf(holo_ctx* ctx, const char* name, const holo_wave& wave, const std::vector<double>& z, int w, int h,
+                  int local) {
+    const std::vector<TfChan> t = make_tf_consts(wave, z.data(), static_cast<int>(z.size()), w, h, local);
+    TfChan* d = buf<TfChan>(ctx, name, t.size());
+    upload_small(ctx, d, t.data(), sizeof(TfChan) * t.size());
+    return d;
+}
+
+// ---------------------------------------------------------------- generic operators (any precision)
+
+template <class T>
+void op_fft2(holo_ctx* ctx, cx<T>* data, int w, int h, int batch, bool inverse) {
+    const T s = inverse ? static_cast<T>(1.0 / (static_cast<double>(w) * h)) : T(1);
+    rows_fft<T>(ctx, data, data, w, static_cast<long long>(batch) * h, inverse ? +1 : -1, T(1));
+    cols_fft<T>(ctx, data, data, w, h, batch, inverse ? +1 : -1, s);
+}
+
+// Spectrum of L layers [L][C][h][w] (row-transformed in place in `work`), S = sum_l H_{z_l} FFT2(U_l).
+template <class T>
+void spectrum_of_layers(holo_ctx* ctx, const cx<T>* layers, cx<T>* work, cx<T>* spec, int w, int h, int C,
+                        const holo_wave& wave, const std::vector<double>& z, int local) {
+    const int L = static_cast<int>(z.size());
+    rows_fft<T>(ctx, layers, work, w, static_cast<long long>(L) * C * h, -1, T(1));
+    const TfChan* tfc = upload_tf(ctx, sizeof(T) == 4 ? "tf_f32" : "tf_f64", wave, z, w, h, local);
+    col_spectrum<T>(ctx, work, spec, w, h, C, L, tfc, wave.pitch);
+}
+
+// out[o] = IFFT2(M_o S) for outputs o with plane_of[o] (-1: none) -> [O][C][h][w] scaled by 1/(w h)
+template <class T>
+void replay_from_spectrum(holo_ctx* ctx, const cx<T>* spec, cx<T>* out, int w, int h, int C, const holo_wave& wave,
+                          const std::vector<double>& z, const std::vector<int>& plane_of, int local) {
+    const int O = static_cast<int>(plane_of.size());
+    const TfChan* tfc = upload_tf(ctx, sizeof(T) == 4 ? "tfr_f32" : "tfr_f64", wave, z, w, h, local);
+    int* d_plane_of = buf<int>(ctx, sizeof(T) == 4 ? "plane_of_f32" : "plane_of_f64", O);
+    upload_small(ctx, d_plane_of, plane_of.data(), sizeof(int) * O);
+    col_replay<T>(ctx, spec, out, w, h, C, O, d_plane_of, tfc, wave.pitch);
+    rows_fft<T>(ctx, out, out, w, static_cast<long long>(O) * C * h, +1,
+                static_cast<T>(1.0 / (static_cast<double>(w) * h)));
+}
+
+// propagate (propagation.cpp:93-101) on device fields
+template <class T>
+void op_propagate(holo_ctx* ctx, const cx<T>* in, cx<T>* out, int w, int h, int C, const holo_wave& wave, double z,
+                  const holo_prop_options& prop) {
+    validate_wave(wave);
+    const int pw = prop.pad2x ? 2 * w : w, ph = prop.pad2x ? 2 * h : h;
+    const size_t n = static_cast<size_t>(pw) * ph * C;
+    cx<T>* a = buf<cx<T>>(ctx, sizeof(T) == 4 ? "prop_a32" : "prop_a64", n);
+    cx<T>* s = buf<cx<T>>(ctx, sizeof(T) == 4 ? "prop_s32" : "prop_s64", n);
+    const cx<T>* src = in;
+    if (prop.pad2x) {
+        pad_field<T>(ctx, in, a, w, h, C);
+        src = a;
+    }
+    const std::vector<double> zs{z};
+    spectrum_of_layers<T>(ctx, src, a, s, pw, ph, C, wave, zs, prop.local_band_limit);
+    cx<T>* dst = prop.pad2x ? a : out;
+    replay_from_spectrum<T>(ctx, s, dst, pw, ph, C, wave, zs, std::vector<int>{-1}, prop.local_band_limit);
+    if (prop.pad2x) crop_field<T>(ctx, a, out, w, h, C);
+}
+
+// forward_record (propagation.cpp:103-114)
+template <class T>
+void op_forward_record(holo_ctx* ctx, const cx<T>* layers, int L, cx<T>* holo, const holo_wave& wave,
+                       const holo_prop_options& prop) {
+    const std::vector<double> z = plane_positions(wave);
+    if (L != static_cast<int>(z.size())) config_error("forward_record: layer count does not match num_planes");
+    const int w = wave.nx, h = wave.ny, C = wave.channels;
+    if (!prop.pad2x) {
+        const size_t n = static_cast<size_t>(w) * h * C;
+        cx<T>* work = buf<cx<T>>(ctx, sizeof(T) == 4 ? "fr_w32" : "fr_w64", n * L);
+        cx<T>* s = buf<cx<T>>(ctx, sizeof(T) == 4 ? "fr_s32" : "fr_s64", n);
+        spectrum_of_layers<T>(ctx, layers, work, s, w, h, C, wave, z, prop.local_band_limit);
+        replay_from_spectrum<T>(ctx, s, holo, w, h, C, wave, z, std::vector<int>{-1}, prop.local_band_limit);
+        return;
+    }
+    // padded: the crop after every propagate (propagation.cpp:100) keeps the planes separate
+    const size_t n = static_cast<size_t>(w) * h * C;
+    cx<T>* tmp = buf<cx<T>>(ctx, sizeof(T) == 4 ? "fr_t32" : "fr_t64", n);
+    for (int l = 0; l < L; ++l) {
+        op_propagate<T>(ctx, layers + n * l, tmp, w, h, C, wave, z[l], prop);
+        accumulate<T>(ctx, tmp, holo, n, l == 0);
+    }
+}
+
+// inverse_propagate (propagation.cpp:116-123)
+template <class T>
+void op_inverse_propagate(holo_ctx* ctx, const cx<T>* holo, cx<T>* replayed, const holo_wave& wave,
+                          const holo_prop_options& prop) {
+    const std::vector<double> z = plane_positions(wave);
+    const int w = wave.nx, h = wave.ny, C = wave.channels, L = static_cast<int>(z.size());
+    const size_t n = static_cast<size_t>(w) * h * C;
+    if (!prop.pad2x) {
+        cx<T>* s = buf<cx<T>>(ctx, sizeof(T) == 4 ? "ip_s32" : "ip_s64", n);
+        HC_CUDA(cudaMemcpyAsync(s, holo, sizeof(cx<T>) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+        op_fft2<T>(ctx, s, w, h, C, false);
+        std::vector<int> plane_of(L);
+        for (int l = 0; l < L; ++l) plane_of[l] = l;
+        replay_from_spectrum<T>(ctx, s, replayed, w, h, C, wave, z, plane_of, prop.local_band_limit);
+        return;
+    }
+    for (int l = 0; l < L; ++l) op_propagate<T>(ctx, holo, replayed + n * l, w, h, C, wave, -z[l], prop);
+}
+
+void check_dtype(int dtype) {
+    if (dtype != HOLO_F32 && dtype != HOLO_F64) throw Error(HOLO_ERR_USAGE, "dtype must be HOLO_F32 or HOLO_F64");
+}
+
+}  // namespace
+
+// ================================================================== C-ABI
+
+extern "C" {
+
+const char* holo_last_error(void) { return g_last_error.c_str(); }
+int holo_abi_version(void) { return HOLO_CUDA_ABI_VERSION; }
+
+int holo_fft_supported(int n) {
+    FftPlan p;
+    return make_plan(n, &p) ? 1 : 0;
+}
+
+int holo_ctx_create(int device, holo_ctx** out) {
+    return guarded([&] {
+        require(out != nullptr, HOLO_ERR_USAGE, "holo_ctx_create: null output");
+        int count = 0;
+        HC_CUDA(cudaGetDeviceCount(&count));
+        require(device >= 0 && device < count, HOLO_ERR_USAGE, "holo_ctx_create: no such CUDA device");
+        HC_CUDA(cudaSetDevice(device));
+        auto* ctx = new holo_ctx();
+        ctx->device = device;
+        HC_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
+        HC_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+        ctx->stream = ctx->own_stream;
+        *out = ctx;
+    });
+}
+
+int holo_ctx_destroy(holo_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        for (auto& kv : ctx->scratch) cudaFree(kv.second.p);
+        for (auto& kv : ctx->twiddles) cudaFree(kv.second);
+        for (auto& kv : ctx->freqs) cudaFree(kv.second);
+        for (double* p : {ctx->d_positions, ctx->d_rotations, ctx->d_log_scales, ctx->d_amplitudes, ctx->d_opacity,
+                          ctx->d_phases, ctx->d_plane_logits})
+            cudaFree(p);
+        if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
+        for (auto& t : ctx->pending) {
+            cudaEventDestroy(t.a);
+            cudaEventDestroy(t.b);
+        }
+        for (auto e : ctx->event_pool) cudaEventDestroy(e);
+        if (ctx->ring) {
+            cudaFreeHost(ctx->ring);
+            for (auto e : ctx->ring_ev) cudaEventDestroy(e);
+        }
+        cudaStreamDestroy(ctx->own_stream);
+        delete ctx;
+    });
+}
+
+int holo_ctx_set_stream(holo_ctx* ctx, void* stream) {
+    return guarded([&] {
+        require(ctx != nullptr, HOLO_ERR_USAGE, "null context");
+        HC_CUDA(cudaStreamSynchronize(ctx->stream));
+        ctx->stream = static_cast<cudaStream_t>(stream);
+    });
+}
+
+int holo_ctx_use_own_stream(holo_ctx* ctx) {
+    return guarded([&] {
+        require(ctx != nullptr, HOLO_ERR_USAGE, "null context");
+        HC_CUDA(cudaStreamSynchronize(ctx->stream));
+        ctx->stream = ctx->own_stream;
+    });
+}
+
+void* holo_ctx_get_stream(holo_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int holo_ctx_synchronize(holo_ctx* ctx) {
+    return guarded([&] { HC_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int holo_ctx_enable_timing(holo_ctx* ctx, int enable) {
+    return guarded([&] { ctx->timing = enable != 0; });
+}
+
+int holo_ctx_stage_times(holo_ctx* ctx, double* ms_out, int* launches_out, int max_stages) {
+    return guarded([&] {
+        resolve_timing(ctx);
+        for (int s = 0; s < max_stages && s < kNumStages; ++s) {
+            if (ms_out) ms_out[s] = ctx->stage_ms[s];
+            if (launches_out) launches_out[s] = ctx->stage_calls[s];
+        }
+    });
+}
+
+int holo_ctx_reset_timing(holo_ctx* ctx) {
+    return guarded([&] {
+        resolve_timing(ctx);
+        for (int s = 0; s < kNumStages; ++s) {
+            ctx->stage_ms[s] = 0.0;
+            ctx->stage_calls[s] = 0;
+        }
+    });
+}
+
+uint64_t holo_ctx_launch_count(holo_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+static int scene_upload(holo_ctx* ctx, const holo_scene_arrays* s, cudaMemcpyKind kind) {
+    return guarded([&] {
+        require(ctx && s, HOLO_ERR_USAGE, "null argument");
+        if (s->num_planes < 1) config_error("scene needs at least one plane");  // scene.cpp:21
+        const size_t n = s->n;
+        if (n > 0)
+            require(s->positions && s->rotations && s->log_scales && s->amplitudes && s->opacity_logits && s->phases &&
+                        s->plane_logits,
+                    HOLO_ERR_CONFIG, "scene arrays have inconsistent sizes");
+        HC_CUDA(cudaSetDevice(ctx->device));
+        struct A {
+            double** dst;
+            const double* src;
+            size_t count;
+        } arrays[] = {{&ctx->d_positions, s->positions, 3 * n},       {&ctx->d_rotations, s->rotations, 4 * n},
+                      {&ctx->d_log_scales, s->log_scales, 3 * n},     {&ctx->d_amplitudes, s->amplitudes, 3 * n},
+                      {&ctx->d_opacity, s->opacity_logits, n},        {&ctx->d_phases, s->phases, 3 * n},
+                      {&ctx->d_plane_logits, s->plane_logits, n * static_cast<size_t>(s->num_planes)}};
+        const bool grow = n > ctx->n || static_cast<size_t>(s->num_planes) * n >
+                                            static_cast<size_t>(ctx->scene_planes) * ctx->n;
+        if (grow) {
+            HC_CUDA(cudaStreamSynchronize(ctx->stream));
+            for (auto& a : arrays) {
+                cudaFree(*a.dst);
+                *a.dst = nullptr;
+                HC_CUDA(cudaMalloc(a.dst, sizeof(double) * (a.count ? a.count : 1)));
+            }
+        }
+        for (auto& a : arrays)
+            if (a.count) HC_CUDA(cudaMemcpyAsync(*a.dst, a.src, sizeof(double) * a.count, kind, ctx->stream));
+        ctx->n = n;
+        ctx->scene_planes = s->num_planes;
+    });
+}
+
+int holo_scene_upload(holo_ctx* ctx, const holo_scene_arrays* host) {
+    return scene_upload(ctx, host, cudaMemcpyHostToDevice);
+}
+
+int holo_scene_upload_device(holo_ctx* ctx, const holo_scene_arrays* dev) {
+    return scene_upload(ctx, dev, cudaMemcpyDeviceToDevice);
+}
+
+int holo_render_begin(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave,
+                      const holo_raster_settings* settings, const holo_prop_options* prop, int plane_begin,
+                      int plane_end, void* spectrum_out, unsigned outputs, holo_frame_info* info) {
+    return guarded([&] {
+        require(ctx && cam && wave && settings, HOLO_ERR_USAGE, "null argument");
+        HC_CUDA(cudaSetDevice(ctx->device));
+        const FrameGeom g = check_render(ctx, *cam, *wave, *settings);
+        require(plane_begin >= 0 && plane_end <= g.L && plane_begin <= plane_end, HOLO_ERR_USAGE,
+                "plane range outside [0, num_planes]");
+        const holo_prop_options po = prop ? *prop : holo_prop_options{0, 0};
+        require(!po.pad2x || (plane_begin == 0 && plane_end == g.L && spectrum_out == nullptr), HOLO_ERR_CONFIG,
+                "plane-sharded rendering does not support pad2x");
+        ctx->f_L = g.L;
+        ctx->f_C = g.C;
+        ctx->f_W = g.W;
+        ctx->f_H = g.H;
+        ctx->f_tiles = g.num_tiles;
+        ctx->f_outputs = outputs;
+        ctx->f_plane_begin = plane_begin;
+        ctx->f_plane_end = plane_end;
+        raster_planes(ctx, *cam, *wave, *settings, g, plane_begin, plane_end, outputs, info);
+        if (po.pad2x) return;  // holo_render handles the padded path on the spatial layers
+        const int np = plane_end - plane_begin;
+        const bool need_prop = spectrum_out != nullptr ||
+                               (outputs & (HOLO_OUT_HOLOGRAM | HOLO_OUT_REPLAYED | HOLO_OUT_INTENSITY)) != 0;
+        if (!need_prop) return;
+        const std::vector<double> zall = plane_positions(*wave);
+        const std::vector<double> z(zall.begin() + plane_begin, zall.begin() + plane_end);
+        cx<float>* layers = static_cast<cx<float>*>(ctx->buffer("layers", 1));
+        cx<float>* spec = spectrum_out ? static_cast<cx<float>*>(spectrum_out)
+                                       : buf<cx<float>>(ctx, "spectrum", static_cast<size_t>(g.C) * g.P);
+        // row FFT (in place unless the spatial layers are an output), then the spectrum column pass
+        cx<float>* work = (outputs & HOLO_OUT_LAYERS) ? buf<cx<float>>(ctx, "rowwork", static_cast<size_t>(np) * g.C * g.P)
+                                                      : layers;
+        if (np == 0) {
+            HC_CUDA(cudaMemsetAsync(spec, 0, sizeof(cx<float>) * g.C * g.P, ctx->stream));
+            return;
+        }
+        ctx->stage_begin();
+        rows_fft<float>(ctx, layers, work, g.W, static_cast<long long>(np) * g.C * g.H, -1, 1.0f);
+        ctx->stage_end(3);
+        const TfChan* tfc = upload_tf(ctx, "tf_render", *wave, z, g.W, g.H, po.local_band_limit);
+        ctx->stage_begin();
+        col_spectrum<float>(ctx, work, spec, g.W, g.H, g.C, np, tfc, wave->pitch);
+        ctx->stage_end(4);
+    });
+}
+
+int holo_render_end(holo_ctx* ctx, const holo_wave* wave, const holo_prop_options* prop, int plane_begin,
+                    int plane_end, const void* spectrum, unsigned outputs) {
+    return guarded([&] {
+        require(ctx && wave, HOLO_ERR_USAGE, "null argument");
+        HC_CUDA(cudaSetDevice(ctx->device));
+        validate_wave(*wave);
+        const holo_prop_options po = prop ? *prop : holo_prop_options{0, 0};
+        require(!po.pad2x, HOLO_ERR_CONFIG, "plane-sharded rendering does not support pad2x");
+        const int W = wave->nx, H = wave->ny, C = wave->channels;
+        const size_t P = static_cast<size_t>(W) * H;
+        const int np = plane_end - plane_begin;
+        const bool holo = (outputs & HOLO_OUT_HOLOGRAM) != 0;
+        const bool rep = (outputs & HOLO_OUT_REPLAYED) != 0;
+        const bool ints = (outputs & HOLO_OUT_INTENSITY) != 0;
+        std::vector<int> plane_of;
+        if (holo) plane_of.push_back(-1);
+        if (rep || ints)
+            for (int l = 0; l < np; ++l) plane_of.push_back(l);
+        ctx->f_outputs |= outputs;
+        if (plane_of.empty()) return;
+        const std::vector<double> zall = plane_positions(*wave);
+        const std::vector<double> z(zall.begin() + plane_begin, zall.begin() + plane_end);
+        const cx<float>* spec = spectrum ? static_cast<const cx<float>*>(spectrum)
+                                         : static_cast<const cx<float>*>(ctx->buffer("spectrum", 1));
+        const int O = static_cast<int>(plane_of.size());
+        cx<float>* stage = buf<cx<float>>(ctx, "replay_stage", static_cast<size_t>(O) * C * P);
+        const TfChan* tfc = upload_tf(ctx, "tf_replay", *wave, z.empty() ? std::vector<double>{0.0} : z, W, H,
+                                      po.local_band_limit);
+        int* d_plane_of = buf<int>(ctx, "plane_of", O);
+        upload_small(ctx, d_plane_of, plane_of.data(), sizeof(int) * O);
+        ctx->stage_begin();
+        col_replay<float>(ctx, spec, stage, W, H, C, O, d_plane_of, tfc, wave->pitch);
+        ctx->stage_end(5);
+        cx<float>* d_holo = holo ? buf<cx<float>>(ctx, "hologram", static_cast<size_t>(C) * P) : nullptr;
+        cx<float>* d_rep = rep ? buf<cx<float>>(ctx, "replayed", static_cast<size_t>(np) * C * P) : nullptr;
+        float* d_int = ints ? buf<float>(ctx, "intensity", static_cast<size_t>(np) * C * P) : nullptr;
+        ctx->stage_begin();
+        rows_epilogue(ctx, stage, W, H, C, O, holo ? 1 : 0, d_holo, d_rep, d_int);
+        ctx->stage_end(6);
+    });
+}
+
+int holo_render(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave, const holo_raster_settings* settings,
+                const holo_prop_options* prop, unsigned outputs, holo_frame_info* info) {
+    const holo_prop_options po = prop ? *prop : holo_prop_options{0, 0};
+    if (!po.pad2x) {
+        int rc = holo_render_begin(ctx, cam, wave, settings, &po, 0, wave ? wave->num_planes : 0, nullptr, outputs, info);
+        if (rc) return rc;
+        return holo_render_end(ctx, wave, &po, 0, wave->num_planes, nullptr, outputs);
+    }
+    // pad2x: the spectrum shortcut does not hold (the crop after each propagate,
+    // propagation.cpp:100), so run forward_record / inverse_propagate literally.
+    int rc = holo_render_begin(ctx, cam, wave, settings, &po, 0, wave->num_planes, nullptr, outputs, info);
+    if (rc) return rc;
+    return guarded([&] {
+        const int W = wave->nx, H = wave->ny, C = wave->channels, L = wave->num_planes;
+        const size_t P = static_cast<size_t>(W) * H;
+        if (!(outputs & (HOLO_OUT_HOLOGRAM | HOLO_OUT_REPLAYED | HOLO_OUT_INTENSITY))) return;
+        const cx<float>* layers = static_cast<const cx<float>*>(ctx->buffer("layers", 1));
+        cx<float>* d_holo = buf<cx<float>>(ctx, "hologram", static_cast<size_t>(C) * P);
+        op_forward_record<float>(ctx, layers, L, d_holo, *wave, po);
+        if (outputs & (HOLO_OUT_REPLAYED | HOLO_OUT_INTENSITY)) {
+            cx<float>* d_rep = buf<cx<float>>(ctx, "replayed", static_cast<size_t>(L) * C * P);
+            op_inverse_propagate<float>(ctx, d_holo, d_rep, *wave, po);
+            if (outputs & HOLO_OUT_INTENSITY)
+                intensity<float>(ctx, d_rep, buf<float>(ctx, "intensity", static_cast<size_t>(L) * C * P),
+                                 static_cast<size_t>(L) * C * P);
+        }
+    });
+}
+
+int holo_frame_buffer(holo_ctx* ctx, int which, void** dev_ptr, size_t* bytes) {
+    return guarded([&] {
+        require(ctx != nullptr, HOLO_ERR_USAGE, "null context");
+        const size_t P = static_cast<size_t>(ctx->f_W) * ctx->f_H;
+        const size_t np = static_cast<size_t>(ctx->f_plane_end - ctx->f_plane_begin);
+        const size_t C = static_cast<size_t>(ctx->f_C);
+        const size_t B = np * ctx->f_tiles;
+        const char* name = nullptr;
+        size_t sz = 0;
+        switch (which) {
+            case HOLO_BUF_LAYERS: name = "layers"; sz = np * C * P * 8; break;
+            case HOLO_BUF_HOLOGRAM: name = "hologram"; sz = C * P * 8; break;
+            case HOLO_BUF_REPLAYED: name = "replayed"; sz = np * C * P * 8; break;
+            case HOLO_BUF_INTENSITY: name = "intensity"; sz = np * C * P * 4; break;
+            case HOLO_BUF_T_FINAL: name = "t_final"; sz = np * P * 4; break;
+            case HOLO_BUF_N_CONTRIB: name = "n_contrib"; sz = np * P * 4; break;
+            case HOLO_BUF_ENTRY_GIDX: name = "egidx"; sz = ctx->f_E * 4; break;
+            case HOLO_BUF_ENTRY_DEPTH: name = "edepth"; sz = ctx->f_E * 8; break;
+            case HOLO_BUF_BUCKET_START: name = "bstart"; sz = (B + 1) * 4; break;
+            case HOLO_BUF_PROJECTED: name = "projected"; sz = ctx->n * sizeof(holo_projected); break;
+            case HOLO_BUF_RHO: name = "rho"; sz = ctx->n * static_cast<size_t>(ctx->f_L) * 8; break;
+            case HOLO_BUF_TOUCHED: name = "touched"; sz = ctx->n; break;
+            case HOLO_BUF_SPECTRUM: name = "spectrum"; sz = C * P * 8; break;
+            default: throw Error(HOLO_ERR_USAGE, "unknown buffer id");
+        }
+        auto it = ctx->scratch.find(name);
+        if (it == ctx->scratch.end() || it->second.bytes < sz)
+            throw Error(HOLO_ERR_USAGE, std::string("buffer not produced by the last render: ") + name);
+        if (dev_ptr) *dev_ptr = it->second.p;
+        if (bytes) *bytes = sz;
+    });
+}
+
+int holo_frame_download(holo_ctx* ctx, int which, void* host, size_t bytes) {
+    void* d = nullptr;
+    size_t sz = 0;
+    int rc = holo_frame_buffer(ctx, which, &d, &sz);
+    if (rc) return rc;
+    return guarded([&] {
+        require(bytes == sz, HOLO_ERR_USAGE, "holo_frame_download: size mismatch");
+        HC_CUDA(cudaMemcpyAsync(host, d, sz, cudaMemcpyDeviceToHost, ctx->stream));
+        HC_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int holo_fft2(holo_ctx* ctx, void* data, int w, int h, int batch, int inverse, int dtype) {
+    return guarded([&] {
+        require(ctx && data, HOLO_ERR_USAGE, "null argument");
+        check_dtype(dtype);
+        require(w > 0 && h > 0 && batch >= 0, HOLO_ERR_CONFIG, "fft2: dimensions must be positive");
+        if (dtype == HOLO_F32)
+            op_fft2<float>(ctx, static_cast<cx<float>*>(data), w, h, batch, inverse != 0);
+        else
+            op_fft2<double>(ctx, static_cast<cx<double>*>(data), w, h, batch, inverse != 0);
+    });
+}
+
+int holo_transfer_function(holo_ctx* ctx, const holo_wave* wave, double z, const holo_prop_options* prop, void* out,
+                           int dtype) {
+    return guarded([&] {
+        require(ctx && wave && out, HOLO_ERR_USAGE, "null argument");
+        check_dtype(dtype);
+        validate_wave(*wave);
+        const holo_prop_options po = prop ? *prop : holo_prop_options{0, 0};
+        const int w = po.pad2x ? 2 * wave->nx : wave->nx, h = po.pad2x ? 2 * wave->ny : wave->ny;
+        const std::vector<double> zs{z};
+        const TfChan* tfc = upload_tf(ctx, "tf_op", *wave, zs, w, h, po.local_band_limit);
+        if (dtype == HOLO_F32)
+            transfer_function<float>(ctx, static_cast<cx<float>*>(out), w, h, wave->channels, tfc, wave->pitch);
+        else
+            transfer_function<double>(ctx, static_cast<cx<double>*>(out), w, h, wave->channels, tfc, wave->pitch);
+    });
+}
+
+int holo_propagate(holo_ctx* ctx, const void* in, void* out, int w, int h, int c, const holo_wave* wave, double z,
+                   const holo_prop_options* prop, int dtype) {
+    return guarded([&] {
+        require(ctx && in && out && wave, HOLO_ERR_USAGE, "null argument");
+        check_dtype(dtype);
+        if (w != wave->nx || h != wave->ny || c != wave->channels)
+            config_error("propagate: field does not match the configured grid");  // propagation.cpp:94-95
+        const holo_prop_options po = prop ? *prop : holo_prop_options{0, 0};
+        if (dtype == HOLO_F32)
+            op_propagate<float>(ctx, static_cast<const cx<float>*>(in), static_cast<cx<float>*>(out), w, h, c, *wave, z,
+                                po);
+        else
+            op_propagate<double>(ctx, static_cast<const cx<double>*>(in), static_cast<cx<double>*>(out), w, h, c,
+                                 *wave, z, po);
+    });
+}
+
+int holo_forward_record(holo_ctx* ctx, const void* layers, int num_layers, void* hologram, const holo_wave* wave,
+                        const holo_prop_options* prop, int dtype) {
+    return guarded([&] {
+        require(ctx && layers && hologram && wave, HOLO_ERR_USAGE, "null argument");
+        check_dtype(dtype);
+        const holo_prop_options po = prop ? *prop : holo_prop_options{0, 0};
+        if (dtype == HOLO_F32)
+            op_forward_record<float>(ctx, static_cast<const cx<float>*>(layers), num_layers,
+                                     static_cast<cx<float>*>(hologram), *wave, po);
+        else
+            op_forward_record<double>(ctx, static_cast<const cx<double>*>(layers), num_layers,
+                                      static_cast<cx<double>*>(hologram), *wave, po);
+    });
+}
+
+int holo_inverse_propagate(holo_ctx* ctx, const void* hologram, void* replayed, const holo_wave* wave,
+                           const holo_prop_options* prop, int dtype) {
+    return guarded([&] {
+        require(ctx && hologram && replayed && wave, HOLO_ERR_USAGE, "null argument");
+        check_dtype(dtype);
+        const holo_prop_options po = prop ? *prop : holo_prop_options{0, 0};
+        if (dtype == HOLO_F32)
+            op_inverse_propagate<float>(ctx, static_cast<const cx<float>*>(hologram), static_cast<cx<float>*>(replayed),
+                                        *wave, po);
+        else
+            op_inverse_propagate<double>(ctx, static_cast<const cx<double>*>(hologram),
+                                         static_cast<cx<double>*>(replayed), *wave, po);
+    });
+}
+
+int holo_intensity(holo_ctx* ctx, const void* field, void* out, size_t samples, int dtype) {
+    return guarded([&] {
+        require(ctx && field && out, HOLO_ERR_USAGE, "null argument");
+        check_dtype(dtype);
+        if (samples == 0) return;
+        if (dtype == HOLO_F32)
+            intensity<float>(ctx, static_cast<const cx<float>*>(field), static_cast<float*>(out), samples);
+        else
+            intensity<double>(ctx, static_cast<const cx<double>*>(field), static_cast<double*>(out), samples);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,211 @@
+// K7 composite: per-(plane, tile) front-to-back complex alpha compositing (sm_100a).
+//
+// Restates the hot loop of raster_forward (proj/src/rasterizer.cpp:227-261) with
+// evaluate() (:124-135): per pixel centre (px + 0.5, py + 0.5), in bucket order,
+//   stop once T < term_eps (checked before each entry),
+//   a = min(alpha * exp(-form / 2) * rho, alpha_clamp), skip unless a > alpha_floor,
+//   acc_c += a T amp_c e^{i phi_c},  T *= 1 - a,  ++n_contrib.
+// One CTA per bucket, one thread per pixel.  The CTA first restores the
+// reference order of its bucket -- ascending (zc, gidx), rasterizer.cpp:221-224 --
+// by a rank sort (<= 256 entries) or a bitonic sort (<= kSortCap) in shared
+// memory; larger buckets arrive presorted from binning.cu.  Records are staged
+// 256 at a time in shared memory; each warp covers an 8x4 pixel block and skips
+// (warp-uniformly) entries whose support circle (radius, rasterizer.cpp:54-62,
+// beyond which a < alpha_floor) misses the block.  Evaluation is fp32 with the
+// centre offset formed in f64 per entry, so dx, dy keep full fp32 precision.
+#include "kernels.cuh"
+
+namespace holo_cuda {
+
+namespace {
+
+template <int TILE>
+struct TileGeom {
+    static constexpr int kThreads = TILE * TILE;
+    // warp block: 8 wide x 4 tall (TILE >= 8); TILE/8 blocks per row
+    static constexpr int kBlocksX = TILE / 8;
+};
+
+template <int TILE, int C>
+__global__ void __launch_bounds__(TILE * TILE) k_composite(CompositeArgs a) {
+    using G = TileGeom<TILE>;
+    __shared__ unsigned long long s_key[kSortCap];
+    __shared__ int s_gid[kSortCap];
+    __shared__ int s_ord[kSortCap];
+    constexpr int kStage = 256;          // records staged per batch
+    __shared__ float4 s_a[kStage];  // mx, my, ca, cb
+    __shared__ float4 s_b[kStage];  // cc, alpha, ylo, yhi
+    __shared__ float4 s_c[kStage];  // xlo, xhi, col0
+    __shared__ float4 s_d[kStage];  // col1, col2
+
+    const int lb = blockIdx.x;  // local bucket within the rendered planes
+    const int lplane = lb / a.num_tiles;
+    const int tile = lb - lplane * a.num_tiles;
+    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+    const int px0 = tx * TILE, py0 = ty * TILE;
+    const unsigned e0 = a.bstart[lb];
+    const int n = static_cast<int>(a.bstart[lb + 1] - e0);
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int bx = (warp % G::kBlocksX) * 8, by = (warp / G::kBlocksX) * 4;
+    const int lx = bx + (lane & 7), ly = by + (lane >> 3);
+    const int px = px0 + lx, py = py0 + ly;
+    const bool inside = px < a.W && py < a.H;
+
+    // ---- restore the reference order (zc asc, gidx asc) inside the bucket
+    const bool presorted = n > kSortCap;
+    if (!presorted && n > 0) {
+        for (int t = tid; t < n; t += G::kThreads) {
+            s_key[t] = a.ekey[e0 + t];
+            s_gid[t] = a.egidx[e0 + t];
+        }
+        __syncthreads();
+        if (n <= G::kThreads) {
+            if (tid < n) {
+                const unsigned long long k = s_key[tid];
+                const int g = s_gid[tid];
+                int rank = 0;
+                for (int j = 0; j < n; ++j) {
+                    const unsigned long long kj = s_key[j];
+                    rank += (kj < k || (kj == k && s_gid[j] < g)) ? 1 : 0;
+                }
+                s_ord[rank] = g;
+            }
+        } else {
+            int P = 1;
+            while (P < n) P <<= 1;
+            for (int t = n + tid; t < P; t += G::kThreads) {
+                s_key[t] = ~0ull;
+                s_gid[t] = 0x7fffffff;
+            }
+            __syncthreads();
+            for (int k = 2; k <= P; k <<= 1) {
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    for (int t = tid; t < P; t += G::kThreads) {
+                        const int u = t ^ j;
+                        if (u > t) {
+                            const bool up = (t & k) == 0;
+                            const unsigned long long ka = s_key[t], kb = s_key[u];
+                            const int ga = s_gid[t], gb = s_gid[u];
+                            const bool b_less = kb < ka || (kb == ka && gb < ga);
+                            const bool a_less = ka < kb || (ka == kb && ga < gb);
+                            if (up ? b_less : a_less) {
+                                s_key[t] = kb;
+                                s_key[u] = ka;
+                                s_gid[t] = gb;
+                                s_gid[u] = ga;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            for (int t = tid; t < n; t += G::kThreads) s_ord[t] = s_gid[t];
+        }
+        __syncthreads();
+        if (a.write_lists) {
+            for (int t = tid; t < n; t += G::kThreads) a.egidx[e0 + t] = s_ord[t];
+        }
+    }
+
+    // ---- composite
+    float T = 1.0f;
+    int contrib = 0;
+    float acc[2 * C];
+#pragma unroll
+    for (int c = 0; c < 2 * C; ++c) acc[c] = 0.0f;
+    bool done = !inside || !(1.0f >= a.term_eps);  // the reference checks T < term_eps before every entry
+    const float fx = static_cast<float>(lx) + 0.5f, fy = static_cast<float>(ly) + 0.5f;
+    const float bxlo = static_cast<float>(bx) + 0.5f, bxhi = static_cast<float>(bx) + 7.5f;
+    const float bylo = static_cast<float>(by) + 0.5f, byhi = static_cast<float>(by) + 3.5f;
+    const int plane = a.plane_begin + lplane;
+
+    for (int base = 0; base < n; base += kStage) {
+        const int cnt = (n - base) < kStage ? (n - base) : kStage;
+        for (int t = tid; t < cnt; t += G::kThreads) {
+            const int g = presorted ? a.egidx[e0 + base + t] : s_ord[base + t];
+            const GRec r = a.rec[g];
+            const float mx = static_cast<float>(r.mu_x - static_cast<double>(px0));
+            const float my = static_cast<float>(r.mu_y - static_cast<double>(py0));
+            const float rr = r.radius * 1.00001f + 1e-3f;
+            float alpha = r.alpha;
+            if (a.soft) alpha = static_cast<float>(static_cast<double>(r.alpha) * a.rho[static_cast<size_t>(g) * a.L + plane]);
+            s_a[t] = make_float4(mx, my, r.ca, r.cb);
+            s_b[t] = make_float4(r.cc, alpha, my - rr, my + rr);
+            s_c[t] = make_float4(mx - rr, mx + rr, r.col[0], r.col[1]);
+            s_d[t] = make_float4(r.col[2], r.col[3], r.col[4], r.col[5]);
+        }
+        __syncthreads();
+        if (!done) {
+            for (int j = 0; j < cnt; ++j) {
+                const float4 B = s_b[j];
+                const float4 Cc = s_c[j];
+                // warp-uniform support test against this warp's 8x4 block of pixel centres
+                if (Cc.y < bxlo || Cc.x > bxhi || B.w < bylo || B.z > byhi) continue;
+                const float4 A = s_a[j];
+                const float dx = fx - A.x, dy = fy - A.y;
+                const float q = A.z * dx * dx + A.w * dx * dy + B.x * dy * dy;
+                const float g = exp2f(q);
+                float al = B.y * g;
+                al = al > a.alpha_clamp ? a.alpha_clamp : al;
+                const bool accept = a.floor_positive ? (al > a.alpha_floor) : (al > 0.0f);
+                if (!accept) continue;
+                const float w = al * T;
+                acc[0] += w * Cc.z;
+                acc[1] += w * Cc.w;
+                if (C > 1) {
+                    const float4 D = s_d[j];
+                    acc[2 % (2 * C)] += w * D.x;
+                    acc[3 % (2 * C)] += w * D.y;
+                    if (C > 2) {
+                        acc[4 % (2 * C)] += w * D.z;
+                        acc[5 % (2 * C)] += w * D.w;
+                    }
+                }
+                T *= 1.0f - al;
+                ++contrib;
+                if (T < a.term_eps) {
+                    done = true;
+                    break;
+                }
+            }
+        }
+        if (__syncthreads_count(done ? 1 : 0) == G::kThreads) break;
+    }
+
+    if (inside) {
+        const size_t P = static_cast<size_t>(a.W) * a.H;
+        const size_t pix = static_cast<size_t>(py) * a.W + px;
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+            a.layers[(static_cast<size_t>(lplane) * C + c) * P + pix] = mk(acc[2 * c], acc[2 * c + 1]);
+        if (a.t_final) a.t_final[static_cast<size_t>(lplane) * P + pix] = T;
+        if (a.n_contrib) a.n_contrib[static_cast<size_t>(lplane) * P + pix] = contrib;
+    }
+}
+
+template <int TILE>
+void launch_tile(holo_ctx* ctx, const CompositeArgs& a) {
+    if (a.num_buckets <= 0) return;
+    switch (a.C) {
+        case 1: k_composite<TILE, 1><<<a.num_buckets, TILE * TILE, 0, ctx->stream>>>(a); break;
+        case 2: k_composite<TILE, 2><<<a.num_buckets, TILE * TILE, 0, ctx->stream>>>(a); break;
+        case 3: k_composite<TILE, 3><<<a.num_buckets, TILE * TILE, 0, ctx->stream>>>(a); break;
+        default: throw Error(HOLO_ERR_CONFIG, "render supports 1 to 3 wavelength channels");
+    }
+    HC_LAUNCHED(ctx);
+}
+
+}  // namespace
+
+void composite(holo_ctx* ctx, const CompositeArgs& a, int tile) {
+    switch (tile) {
+        case 8: launch_tile<8>(ctx, a); break;
+        case 16: launch_tile<16>(ctx, a); break;
+        case 32: launch_tile<32>(ctx, a); break;
+        default: throw Error(HOLO_ERR_CONFIG, "render supports tile sizes 8, 16 and 32");
+    }
+}
+
+}  // namespace holo_cuda

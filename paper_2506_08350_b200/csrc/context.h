@@ -1,0 +1,97 @@
+// holo_ctx: one CUDA stream, grow-only device scratch, the resident scene and the
+// last frame's outputs.  Internal to libholo_cuda.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+#include "fft.cuh"
+
+namespace holo_cuda {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+// Per-(plane, channel) transfer-function constants, see tf_value() in kernels.cuh.
+struct TfChan {
+    double inv_l2;      // 1 / lambda^2
+    double two_pi_z;    // 2 pi z (f64, as propagation.cpp:51)
+    double fx_lim, fy_lim;
+    float inv_l;        // 1 / lambda
+    float two_pi_z_f;   // 2 pi z
+    float phase0;       // (2 pi z / lambda) mod 2 pi
+    int local;          // local band limit active (opt && z != 0)
+};
+
+constexpr int kNumStages = 8;
+
+}  // namespace holo_cuda
+
+struct holo_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    uint64_t launches = 0;
+
+    // stage timing (CUDA events on the context stream)
+    bool timing = false;
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+    double stage_ms[holo_cuda::kNumStages] = {};
+    int stage_calls[holo_cuda::kNumStages] = {};
+
+    std::map<std::string, holo_cuda::DevBuf> scratch;
+    std::map<std::pair<int, int>, void*> twiddles;      // (n, sizeof(T)) -> exp(-2 pi i q/n)
+    std::map<std::pair<int, uint64_t>, double*> freqs;  // (n, pitch bits) -> freq_at(i, n, pitch)
+    void* host_pinned = nullptr;
+    size_t host_pinned_bytes = 0;
+
+    // resident scene (device, f64 SoA)
+    size_t n = 0;
+    int scene_planes = 0;
+    double* d_positions = nullptr;
+    double* d_rotations = nullptr;
+    double* d_log_scales = nullptr;
+    double* d_amplitudes = nullptr;
+    double* d_opacity = nullptr;
+    double* d_phases = nullptr;
+    double* d_plane_logits = nullptr;
+
+    // last frame
+    int f_L = 0, f_C = 0, f_W = 0, f_H = 0, f_tiles = 0;
+    uint64_t f_E = 0;
+    unsigned f_outputs = 0;
+    int f_plane_begin = 0, f_plane_end = 0;
+
+    // stage-timing event pairs awaiting resolution, and a pool of spare events
+    struct Timed {
+        int stage;
+        cudaEvent_t a, b;
+    };
+    std::vector<Timed> pending;
+    std::vector<cudaEvent_t> event_pool;
+    // pinned ring for small asynchronous table uploads
+    static constexpr int kRingSlots = 64;
+    static constexpr size_t kRingSlotBytes = 64 * 1024;
+    unsigned char* ring = nullptr;
+    cudaEvent_t ring_ev[kRingSlots] = {};
+    bool ring_used[kRingSlots] = {};
+    int ring_next = 0;
+
+    void note_launch() { ++launches; }
+    void* buffer(const std::string& name, size_t bytes);
+    void* pinned(size_t bytes);
+    template <class T>
+    const holo_cuda::cx<T>* twiddle(int n);
+    const double* freq(int n, double pitch);
+    void stage_begin();
+    void stage_end(int stage);
+};

@@ -1,0 +1,138 @@
+// Internal kernel-side declarations shared by the libholo_cuda translation units.
+#pragma once
+
+#include <vector>
+
+#include "context.h"
+
+namespace holo_cuda {
+
+// Transfer function H_z(fx, fy) (propagation.cpp:18-54) for one (plane, channel).
+// The band test is done in f64 with the reference's expression order
+// ((1/l^2 - fx^2) - fy^2 < 0 -> 0; __d*_rn keeps it uncontracted).  The f64
+// variant evaluates the reference phase 2 pi z sqrt(arg) directly; the f32
+// variant uses the cancellation-free split
+//   2 pi z sqrt(1/l^2 - f^2) = 2 pi z / l  -  2 pi z f^2 / (1/l + sqrt(1/l^2 - f^2))
+// with the first term reduced mod 2 pi on the host in f64 (phase0), so only a
+// residual of at most a few hundred radians is formed in fp32.
+template <class T>
+__device__ __forceinline__ cx<T> tf_value(const TfChan& p, double fx, double fy);
+
+template <>
+__device__ __forceinline__ cx<double> tf_value<double>(const TfChan& p, double fx, double fy) {
+    const double arg = __dsub_rn(__dsub_rn(p.inv_l2, __dmul_rn(fx, fx)), __dmul_rn(fy, fy));
+    if (arg < 0.0) return mk(0.0, 0.0);
+    if (p.local && (fabs(fx) > p.fx_lim || fabs(fy) > p.fy_lim)) return mk(0.0, 0.0);
+    const double phase = __dmul_rn(p.two_pi_z, sqrt(arg));
+    double s, c;
+    sincos(phase, &s, &c);
+    return mk(c, s);
+}
+
+template <>
+__device__ __forceinline__ cx<float> tf_value<float>(const TfChan& p, double fx, double fy) {
+    const double fx2 = __dmul_rn(fx, fx), fy2 = __dmul_rn(fy, fy);
+    const double arg = __dsub_rn(__dsub_rn(p.inv_l2, fx2), fy2);
+    if (arg < 0.0) return mk(0.0f, 0.0f);
+    if (p.local && (fabs(fx) > p.fx_lim || fabs(fy) > p.fy_lim)) return mk(0.0f, 0.0f);
+    const float f2 = static_cast<float>(__dadd_rn(fx2, fy2));
+    const float sq = sqrtf(static_cast<float>(arg));
+    const float theta = p.phase0 - p.two_pi_z_f * f2 / (p.inv_l + sq);
+    float s, c;
+    sincosf(theta, &s, &c);
+    return mk(c, s);
+}
+
+// ---- propagation.cu
+FftPlan plan_or_throw(int n);
+std::vector<TfChan> make_tf_consts(const holo_wave& wave, const double* z, int L, int w, int h, int local_limit);
+template <class T>
+void rows_fft(holo_ctx* ctx, const cx<T>* in, cx<T>* out, int n, long long nrows, int dir, T s);
+template <class T>
+void cols_fft(holo_ctx* ctx, const cx<T>* in, cx<T>* out, int w, int h, int batch, int dir, T s);
+template <class T>
+void col_spectrum(holo_ctx* ctx, const cx<T>* layers, cx<T>* spec, int w, int h, int C, int L, const TfChan* d_tfc,
+                  double pitch);
+template <class T>
+void col_replay(holo_ctx* ctx, const cx<T>* spec, cx<T>* out, int w, int h, int C, int nout, const int* d_plane_of,
+                const TfChan* d_tfc, double pitch);
+void rows_epilogue(holo_ctx* ctx, const cx<float>* in, int w, int h, int C, int nout, int has_holo, cx<float>* holo,
+                   cx<float>* replayed, float* intens);
+template <class T>
+void pad_field(holo_ctx* ctx, const cx<T>* in, cx<T>* out, int w, int h, int C);
+template <class T>
+void crop_field(holo_ctx* ctx, const cx<T>* in, cx<T>* out, int w, int h, int C);
+template <class T>
+void accumulate(holo_ctx* ctx, const cx<T>* in, cx<T>* acc, size_t n, bool first);
+template <class T>
+void intensity(holo_ctx* ctx, const cx<T>* f, T* out, size_t n);
+template <class T>
+void transfer_function(holo_ctx* ctx, cx<T>* out, int w, int h, int C, const TfChan* d_tfc, double pitch);
+
+// ---- preprocess.cu (f64, compiled without FMA contraction)
+
+// Per-Gaussian record consumed by the compositing kernel (64 bytes).
+struct alignas(16) GRec {
+    double mu_x, mu_y;        // projected centre, pixels
+    float ca, cb, cc;         // -0.5 log2(e) * (inv00, 2 inv01, inv11): g = 2^(ca dx^2 + cb dx dy + cc dy^2)
+    float alpha;              // sigmoid(opacity logit)
+    float radius;             // support radius, pixels
+    float col[6];             // amp_c * (cos phi_c, sin phi_c), c < 3
+    float pad;
+};
+static_assert(sizeof(GRec) == 64, "GRec must stay 64 bytes");
+
+struct CameraConsts {
+    double wc[9];  // world_to_cam, row-major (camera.cpp:16)
+    double pos[3];
+    double focal, ppx, ppy;
+};
+
+struct PreOut {
+    GRec* rec;
+    int4* rect;              // tile span [x0, x1) x [y0, y1)
+    unsigned* count;         // entries per Gaussian
+    double* zc;              // depth key
+    int* plane;              // hard assignment (argmax)
+    unsigned long long* pmask;  // planes passing the gate (soft mode)
+    double* rho;             // N x L plane weights (may be null in hard mode)
+    unsigned char* touched;  // count > 0
+    holo_projected* projected;  // optional full f64 record
+    unsigned* flags;         // bit0 degenerate quaternion, bit1 negative amplitude
+    unsigned* num_valid;
+};
+
+void host_world_to_cam(const holo_camera& cam, double wc[9]);
+void preprocess(holo_ctx* ctx, const CameraConsts& cc, const holo_raster_settings& st, double near_clip, int L,
+                int tiles_x, int tiles_y, const PreOut& out);
+
+// ---- binning.cu
+void exclusive_scan_u32(holo_ctx* ctx, const unsigned* in, unsigned* out, long long n, unsigned* d_max);
+void bucket_count(holo_ctx* ctx, const PreOut& pre, size_t N, int L, int plane_begin, int plane_end, int tiles_x,
+                  int num_tiles, int soft, unsigned* bcount);
+void bucket_emit(holo_ctx* ctx, const PreOut& pre, size_t N, int L, int plane_begin, int plane_end, int tiles_x,
+                 int num_tiles, int soft, const unsigned* bstart, unsigned* cursor,
+                 unsigned long long* ekey, int* egidx);
+void sort_large_buckets(holo_ctx* ctx, const std::vector<int>& ids, const std::vector<unsigned>& starts,
+                        const std::vector<unsigned>& counts, unsigned long long* ekey, int* egidx);
+void entry_depths(holo_ctx* ctx, const int* egidx, const double* zc, double* edepth, size_t E);
+
+// ---- composite.cu
+constexpr int kSortCap = 1024;
+struct CompositeArgs {
+    const unsigned* bstart;   // bucket_start for the rendered planes, indexed by local bucket
+    unsigned long long* ekey; // depth bits per entry (unsorted for small buckets)
+    int* egidx;               // gidx per entry
+    const GRec* rec;
+    const double* rho;        // soft mode weights or null
+    int L, C, W, H, tiles_x, num_tiles, plane_begin, num_buckets;
+    int soft, write_lists;
+    float term_eps, alpha_floor, alpha_clamp;
+    int floor_positive;
+    cx<float>* layers;        // [planes][C][H][W], plane relative to plane_begin
+    float* t_final;           // optional [planes][H][W]
+    int* n_contrib;           // optional
+};
+void composite(holo_ctx* ctx, const CompositeArgs& a, int tile);
+
+}  // namespace holo_cuda
