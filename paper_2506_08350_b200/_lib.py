@@ -22,7 +22,10 @@ OUT_LAYERS, OUT_HOLOGRAM, OUT_REPLAYED, OUT_INTENSITY, OUT_AUX, OUT_LISTS, OUT_P
 (BUF_LAYERS, BUF_HOLOGRAM, BUF_REPLAYED, BUF_INTENSITY, BUF_T_FINAL, BUF_N_CONTRIB, BUF_ENTRY_GIDX,
  BUF_ENTRY_DEPTH, BUF_BUCKET_START, BUF_PROJECTED, BUF_RHO, BUF_TOUCHED, BUF_SPECTRUM) = range(13)
 
-STAGES = ("preprocess", "binning", "composite", "row_fft", "col_spectrum", "col_replay", "row_epilogue")
+# stage ids of holo_ctx_stage_times (include/holo_cuda.h); the fft passes are, on the
+# compile-time-plan path: column FFT, row pass (spectrum + inverse rows), row replay
+# (sharded only), column IFFT + epilogue
+STAGES = ("preprocess", "binning", "composite", "fft_pass1", "fft_pass2", "fft_pass3", "fft_pass4")
 
 
 class HoloError(RuntimeError):

@@ -616,51 +616,157 @@ int holo_scene_upload_device(holo_ctx* ctx, const holo_scene_arrays* dev) {
     return scene_upload(ctx, dev, cudaMemcpyDeviceToDevice);
 }
 
+}  // extern "C"
+
+namespace {
+
+std::vector<int> output_planes(unsigned outputs, int np) {
+    std::vector<int> plane_of;
+    if (outputs & HOLO_OUT_HOLOGRAM) plane_of.push_back(-1);
+    if (outputs & (HOLO_OUT_REPLAYED | HOLO_OUT_INTENSITY))
+        for (int l = 0; l < np; ++l) plane_of.push_back(l);
+    return plane_of;
+}
+
+struct OutBufs {
+    cx<float>* holo = nullptr;
+    cx<float>* rep = nullptr;
+    float* ints = nullptr;
+};
+
+OutBufs output_buffers(holo_ctx* ctx, unsigned outputs, int np, int C, size_t P) {
+    OutBufs o;
+    if (outputs & HOLO_OUT_HOLOGRAM) o.holo = buf<cx<float>>(ctx, "hologram", static_cast<size_t>(C) * P);
+    if (outputs & HOLO_OUT_REPLAYED) o.rep = buf<cx<float>>(ctx, "replayed", static_cast<size_t>(np) * C * P);
+    if (outputs & HOLO_OUT_INTENSITY) o.ints = buf<float>(ctx, "intensity", static_cast<size_t>(np) * C * P);
+    return o;
+}
+
+// Second half of the propagation: the hologram and the replayed planes [pb, pe)
+// from the spectrum S (forward_record's sum, propagation.cpp:103-114; the replay of
+// inverse_propagate, :116-123, reuses S = FFT2(hologram)).
+void render_back(holo_ctx* ctx, const holo_wave& wave, const holo_prop_options& po, int pb, int pe,
+                 const cx<float>* spec, unsigned outputs) {
+    const int W = wave.nx, H = wave.ny, C = wave.channels;
+    const size_t P = static_cast<size_t>(W) * H;
+    const int np = pe - pb;
+    const std::vector<int> plane_of = output_planes(outputs, np);
+    ctx->f_outputs |= outputs;
+    if (plane_of.empty()) return;
+    const std::vector<double> zall = plane_positions(wave);
+    std::vector<double> z(zall.begin() + pb, zall.begin() + pe);
+    if (z.empty()) z.push_back(0.0);
+    const int O = static_cast<int>(plane_of.size());
+    const TfChan* tfc = upload_tf(ctx, "tf_replay", wave, z, W, H, po.local_band_limit);
+    int* d_plane_of = buf<int>(ctx, "plane_of_replay", O);
+    upload_small(ctx, d_plane_of, plane_of.data(), sizeof(int) * O);
+    cx<float>* stage = buf<cx<float>>(ctx, "replay_stage", static_cast<size_t>(O) * C * P);
+    const OutBufs ob = output_buffers(ctx, outputs, np, C, P);
+    const int has_holo = (outputs & HOLO_OUT_HOLOGRAM) ? 1 : 0;
+    if (static_render_supported(W, H)) {
+        ctx->stage_begin();
+        static_row(ctx, kModeReplay, nullptr, const_cast<cx<float>*>(spec), stage, W, H, C, np, O, d_plane_of, tfc,
+                   wave.pitch);
+        ctx->stage_end(5);
+        ctx->stage_begin();
+        static_col_inv(ctx, stage, W, H, C, O, has_holo, ob.holo, ob.rep, ob.ints);
+        ctx->stage_end(6);
+        return;
+    }
+    ctx->stage_begin();
+    col_replay<float>(ctx, spec, stage, W, H, C, O, d_plane_of, tfc, wave.pitch);
+    ctx->stage_end(5);
+    ctx->stage_begin();
+    rows_epilogue(ctx, stage, W, H, C, O, has_holo, ob.holo, ob.rep, ob.ints);
+    ctx->stage_end(6);
+}
+
+// Raster planes [pb, pe) and run the forward half of the propagation.  full: go on
+// to the outputs (one GPU owns every plane); otherwise leave the partial spectrum
+// S_g in spectrum_out for the caller's all-reduce.
+void render_front(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, const holo_raster_settings& st,
+                  const holo_prop_options& po, int pb, int pe, void* spectrum_out, unsigned outputs,
+                  holo_frame_info* info, bool full) {
+    const FrameGeom g = check_render(ctx, cam, wave, st);
+    require(pb >= 0 && pe <= g.L && pb <= pe, HOLO_ERR_USAGE, "plane range outside [0, num_planes]");
+    require(!po.pad2x || full, HOLO_ERR_CONFIG, "plane-sharded rendering does not support pad2x");
+    ctx->f_L = g.L;
+    ctx->f_C = g.C;
+    ctx->f_W = g.W;
+    ctx->f_H = g.H;
+    ctx->f_tiles = g.num_tiles;
+    ctx->f_outputs = outputs;
+    ctx->f_plane_begin = pb;
+    ctx->f_plane_end = pe;
+    raster_planes(ctx, cam, wave, st, g, pb, pe, outputs, info);
+    if (po.pad2x) return;  // holo_render runs the padded operators on the spatial layers
+    const int np = pe - pb;
+    const std::vector<int> plane_of = output_planes(outputs, np);
+    if (full && plane_of.empty()) return;
+    cx<float>* spec = (!full && spectrum_out) ? static_cast<cx<float>*>(spectrum_out)
+                                              : buf<cx<float>>(ctx, "spectrum", static_cast<size_t>(g.C) * g.P);
+    if (np == 0) {
+        HC_CUDA(cudaMemsetAsync(spec, 0, sizeof(cx<float>) * g.C * g.P, ctx->stream));
+        if (full) render_back(ctx, wave, po, pb, pe, spec, outputs);
+        return;
+    }
+    const std::vector<double> zall = plane_positions(wave);
+    const std::vector<double> z(zall.begin() + pb, zall.begin() + pe);
+    const TfChan* tfc = upload_tf(ctx, "tf_render", wave, z, g.W, g.H, po.local_band_limit);
+    cx<float>* layers = static_cast<cx<float>*>(ctx->buffer("layers", 1));
+    const size_t nlay = static_cast<size_t>(np) * g.C * g.P;
+    if (static_render_supported(g.W, g.H)) {
+        cx<float>* work = layers;
+        if (outputs & HOLO_OUT_LAYERS) {  // keep the spatial layers: transform a copy
+            work = buf<cx<float>>(ctx, "colwork", nlay);
+            HC_CUDA(cudaMemcpyAsync(work, layers, sizeof(cx<float>) * nlay, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+        ctx->stage_begin();
+        static_col_fwd(ctx, work, g.W, g.H, np * g.C);
+        ctx->stage_end(3);
+        if (!full) {
+            ctx->stage_begin();
+            static_row(ctx, kModeSpec, work, spec, nullptr, g.W, g.H, g.C, np, 0, nullptr, tfc, wave.pitch);
+            ctx->stage_end(4);
+            return;
+        }
+        const int O = static_cast<int>(plane_of.size());
+        int* d_plane_of = buf<int>(ctx, "plane_of_render", O);
+        upload_small(ctx, d_plane_of, plane_of.data(), sizeof(int) * O);
+        cx<float>* stage = buf<cx<float>>(ctx, "replay_stage", static_cast<size_t>(O) * g.C * g.P);
+        const OutBufs ob = output_buffers(ctx, outputs, np, g.C, g.P);
+        ctx->stage_begin();
+        static_row(ctx, kModeFull, work, nullptr, stage, g.W, g.H, g.C, np, O, d_plane_of, tfc, wave.pitch);
+        ctx->stage_end(4);
+        ctx->stage_begin();
+        static_col_inv(ctx, stage, g.W, g.H, g.C, O, (outputs & HOLO_OUT_HOLOGRAM) ? 1 : 0, ob.holo, ob.rep,
+                       ob.ints);
+        ctx->stage_end(6);
+        return;
+    }
+    // generic sizes: runtime-planned passes (rows, then the spectrum column pass)
+    cx<float>* work = (outputs & HOLO_OUT_LAYERS) ? buf<cx<float>>(ctx, "rowwork", nlay) : layers;
+    ctx->stage_begin();
+    rows_fft<float>(ctx, layers, work, g.W, static_cast<long long>(np) * g.C * g.H, -1, 1.0f);
+    ctx->stage_end(3);
+    ctx->stage_begin();
+    col_spectrum<float>(ctx, work, spec, g.W, g.H, g.C, np, tfc, wave.pitch);
+    ctx->stage_end(4);
+    if (full) render_back(ctx, wave, po, pb, pe, spec, outputs);
+}
+
+}  // namespace
+
+extern "C" {
+
 int holo_render_begin(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave,
                       const holo_raster_settings* settings, const holo_prop_options* prop, int plane_begin,
                       int plane_end, void* spectrum_out, unsigned outputs, holo_frame_info* info) {
     return guarded([&] {
         require(ctx && cam && wave && settings, HOLO_ERR_USAGE, "null argument");
         HC_CUDA(cudaSetDevice(ctx->device));
-        const FrameGeom g = check_render(ctx, *cam, *wave, *settings);
-        require(plane_begin >= 0 && plane_end <= g.L && plane_begin <= plane_end, HOLO_ERR_USAGE,
-                "plane range outside [0, num_planes]");
         const holo_prop_options po = prop ? *prop : holo_prop_options{0, 0};
-        require(!po.pad2x || (plane_begin == 0 && plane_end == g.L && spectrum_out == nullptr), HOLO_ERR_CONFIG,
-                "plane-sharded rendering does not support pad2x");
-        ctx->f_L = g.L;
-        ctx->f_C = g.C;
-        ctx->f_W = g.W;
-        ctx->f_H = g.H;
-        ctx->f_tiles = g.num_tiles;
-        ctx->f_outputs = outputs;
-        ctx->f_plane_begin = plane_begin;
-        ctx->f_plane_end = plane_end;
-        raster_planes(ctx, *cam, *wave, *settings, g, plane_begin, plane_end, outputs, info);
-        if (po.pad2x) return;  // holo_render handles the padded path on the spatial layers
-        const int np = plane_end - plane_begin;
-        const bool need_prop = spectrum_out != nullptr ||
-                               (outputs & (HOLO_OUT_HOLOGRAM | HOLO_OUT_REPLAYED | HOLO_OUT_INTENSITY)) != 0;
-        if (!need_prop) return;
-        const std::vector<double> zall = plane_positions(*wave);
-        const std::vector<double> z(zall.begin() + plane_begin, zall.begin() + plane_end);
-        cx<float>* layers = static_cast<cx<float>*>(ctx->buffer("layers", 1));
-        cx<float>* spec = spectrum_out ? static_cast<cx<float>*>(spectrum_out)
-                                       : buf<cx<float>>(ctx, "spectrum", static_cast<size_t>(g.C) * g.P);
-        // row FFT (in place unless the spatial layers are an output), then the spectrum column pass
-        cx<float>* work = (outputs & HOLO_OUT_LAYERS) ? buf<cx<float>>(ctx, "rowwork", static_cast<size_t>(np) * g.C * g.P)
-                                                      : layers;
-        if (np == 0) {
-            HC_CUDA(cudaMemsetAsync(spec, 0, sizeof(cx<float>) * g.C * g.P, ctx->stream));
-            return;
-        }
-        ctx->stage_begin();
-        rows_fft<float>(ctx, layers, work, g.W, static_cast<long long>(np) * g.C * g.H, -1, 1.0f);
-        ctx->stage_end(3);
-        const TfChan* tfc = upload_tf(ctx, "tf_render", *wave, z, g.W, g.H, po.local_band_limit);
-        ctx->stage_begin();
-        col_spectrum<float>(ctx, work, spec, g.W, g.H, g.C, np, tfc, wave->pitch);
-        ctx->stage_end(4);
+        render_front(ctx, *cam, *wave, *settings, po, plane_begin, plane_end, spectrum_out, outputs, info, false);
     });
 }
 
@@ -672,53 +778,24 @@ int holo_render_end(holo_ctx* ctx, const holo_wave* wave, const holo_prop_option
         validate_wave(*wave);
         const holo_prop_options po = prop ? *prop : holo_prop_options{0, 0};
         require(!po.pad2x, HOLO_ERR_CONFIG, "plane-sharded rendering does not support pad2x");
-        const int W = wave->nx, H = wave->ny, C = wave->channels;
-        const size_t P = static_cast<size_t>(W) * H;
-        const int np = plane_end - plane_begin;
-        const bool holo = (outputs & HOLO_OUT_HOLOGRAM) != 0;
-        const bool rep = (outputs & HOLO_OUT_REPLAYED) != 0;
-        const bool ints = (outputs & HOLO_OUT_INTENSITY) != 0;
-        std::vector<int> plane_of;
-        if (holo) plane_of.push_back(-1);
-        if (rep || ints)
-            for (int l = 0; l < np; ++l) plane_of.push_back(l);
-        ctx->f_outputs |= outputs;
-        if (plane_of.empty()) return;
-        const std::vector<double> zall = plane_positions(*wave);
-        const std::vector<double> z(zall.begin() + plane_begin, zall.begin() + plane_end);
+        require(plane_begin >= 0 && plane_end <= wave->num_planes && plane_begin <= plane_end, HOLO_ERR_USAGE,
+                "plane range outside [0, num_planes]");
         const cx<float>* spec = spectrum ? static_cast<const cx<float>*>(spectrum)
                                          : static_cast<const cx<float>*>(ctx->buffer("spectrum", 1));
-        const int O = static_cast<int>(plane_of.size());
-        cx<float>* stage = buf<cx<float>>(ctx, "replay_stage", static_cast<size_t>(O) * C * P);
-        const TfChan* tfc = upload_tf(ctx, "tf_replay", *wave, z.empty() ? std::vector<double>{0.0} : z, W, H,
-                                      po.local_band_limit);
-        int* d_plane_of = buf<int>(ctx, "plane_of", O);
-        upload_small(ctx, d_plane_of, plane_of.data(), sizeof(int) * O);
-        ctx->stage_begin();
-        col_replay<float>(ctx, spec, stage, W, H, C, O, d_plane_of, tfc, wave->pitch);
-        ctx->stage_end(5);
-        cx<float>* d_holo = holo ? buf<cx<float>>(ctx, "hologram", static_cast<size_t>(C) * P) : nullptr;
-        cx<float>* d_rep = rep ? buf<cx<float>>(ctx, "replayed", static_cast<size_t>(np) * C * P) : nullptr;
-        float* d_int = ints ? buf<float>(ctx, "intensity", static_cast<size_t>(np) * C * P) : nullptr;
-        ctx->stage_begin();
-        rows_epilogue(ctx, stage, W, H, C, O, holo ? 1 : 0, d_holo, d_rep, d_int);
-        ctx->stage_end(6);
+        render_back(ctx, *wave, po, plane_begin, plane_end, spec, outputs);
     });
 }
 
 int holo_render(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave, const holo_raster_settings* settings,
                 const holo_prop_options* prop, unsigned outputs, holo_frame_info* info) {
-    const holo_prop_options po = prop ? *prop : holo_prop_options{0, 0};
-    if (!po.pad2x) {
-        int rc = holo_render_begin(ctx, cam, wave, settings, &po, 0, wave ? wave->num_planes : 0, nullptr, outputs, info);
-        if (rc) return rc;
-        return holo_render_end(ctx, wave, &po, 0, wave->num_planes, nullptr, outputs);
-    }
-    // pad2x: the spectrum shortcut does not hold (the crop after each propagate,
-    // propagation.cpp:100), so run forward_record / inverse_propagate literally.
-    int rc = holo_render_begin(ctx, cam, wave, settings, &po, 0, wave->num_planes, nullptr, outputs, info);
-    if (rc) return rc;
     return guarded([&] {
+        require(ctx && cam && wave && settings, HOLO_ERR_USAGE, "null argument");
+        HC_CUDA(cudaSetDevice(ctx->device));
+        const holo_prop_options po = prop ? *prop : holo_prop_options{0, 0};
+        render_front(ctx, *cam, *wave, *settings, po, 0, wave->num_planes, nullptr, outputs, info, true);
+        if (!po.pad2x) return;
+        // pad2x: the spectrum shortcut does not hold (the crop after each propagate,
+        // propagation.cpp:100), so run forward_record / inverse_propagate literally.
         const int W = wave->nx, H = wave->ny, C = wave->channels, L = wave->num_planes;
         const size_t P = static_cast<size_t>(W) * H;
         if (!(outputs & (HOLO_OUT_HOLOGRAM | HOLO_OUT_REPLAYED | HOLO_OUT_INTENSITY))) return;

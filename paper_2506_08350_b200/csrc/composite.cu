@@ -19,6 +19,13 @@ namespace holo_cuda {
 
 namespace {
 
+// 2^x on the MUFU pipe (max rel. error 2^-22.5); x <= 0 here, results below 2^-126 flush to 0.
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 template <int TILE>
 struct TileGeom {
     static constexpr int kThreads = TILE * TILE;
@@ -137,38 +144,48 @@ __global__ void __launch_bounds__(TILE * TILE) k_composite(CompositeArgs a) {
             s_d[t] = make_float4(r.col[2], r.col[3], r.col[4], r.col[5]);
         }
         __syncthreads();
-        if (!done) {
-            for (int j = 0; j < cnt; ++j) {
-                const float4 B = s_b[j];
-                const float4 Cc = s_c[j];
-                // warp-uniform support test against this warp's 8x4 block of pixel centres
-                if (Cc.y < bxlo || Cc.x > bxhi || B.w < bylo || B.z > byhi) continue;
-                const float4 A = s_a[j];
-                const float dx = fx - A.x, dy = fy - A.y;
-                const float q = A.z * dx * dx + A.w * dx * dy + B.x * dy * dy;
-                const float g = exp2f(q);
-                float al = B.y * g;
-                al = al > a.alpha_clamp ? a.alpha_clamp : al;
-                const bool accept = a.floor_positive ? (al > a.alpha_floor) : (al > 0.0f);
-                if (!accept) continue;
-                const float w = al * T;
-                acc[0] += w * Cc.z;
-                acc[1] += w * Cc.w;
-                if (C > 1) {
-                    const float4 D = s_d[j];
-                    acc[2 % (2 * C)] += w * D.x;
-                    acc[3 % (2 * C)] += w * D.y;
-                    if (C > 2) {
-                        acc[4 % (2 * C)] += w * D.z;
-                        acc[5 % (2 * C)] += w * D.w;
+        if (!__all_sync(0xffffffffu, done)) {
+            // 32 entries at a time: each lane tests one entry's support box against
+            // this warp's 8x4 block of pixel centres, the ballot lists the hits and
+            // the warp walks them in order (bucket order is preserved).
+            for (int c0 = 0; c0 < cnt; c0 += 32) {
+                bool hit = false;
+                if (c0 + lane < cnt) {
+                    const float4 Bb = s_b[c0 + lane];
+                    const float4 Cb = s_c[c0 + lane];
+                    hit = !(Cb.y < bxlo || Cb.x > bxhi || Bb.w < bylo || Bb.z > byhi);
+                }
+                unsigned mask = __ballot_sync(0xffffffffu, hit);
+                while (mask) {
+                    const int j = c0 + __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    if (done) continue;
+                    const float4 A = s_a[j];
+                    const float4 B = s_b[j];
+                    const float dx = fx - A.x, dy = fy - A.y;
+                    const float q = dx * fmaf(A.z, dx, A.w * dy) + B.x * dy * dy;
+                    float al = B.y * ex2_approx(q);
+                    al = al > a.alpha_clamp ? a.alpha_clamp : al;
+                    const bool accept = a.floor_positive ? (al > a.alpha_floor) : (al > 0.0f);
+                    if (!accept) continue;
+                    const float w = al * T;
+                    const float4 Cc = s_c[j];
+                    acc[0] = fmaf(w, Cc.z, acc[0]);
+                    acc[1] = fmaf(w, Cc.w, acc[1]);
+                    if (C > 1) {
+                        const float4 D = s_d[j];
+                        acc[2 % (2 * C)] = fmaf(w, D.x, acc[2 % (2 * C)]);
+                        acc[3 % (2 * C)] = fmaf(w, D.y, acc[3 % (2 * C)]);
+                        if (C > 2) {
+                            acc[4 % (2 * C)] = fmaf(w, D.z, acc[4 % (2 * C)]);
+                            acc[5 % (2 * C)] = fmaf(w, D.w, acc[5 % (2 * C)]);
+                        }
                     }
+                    T -= w;  // T (1 - a)
+                    ++contrib;
+                    if (T < a.term_eps) done = true;
                 }
-                T *= 1.0f - al;
-                ++contrib;
-                if (T < a.term_eps) {
-                    done = true;
-                    break;
-                }
+                if (__all_sync(0xffffffffu, done)) break;
             }
         }
         if (__syncthreads_count(done ? 1 : 0) == G::kThreads) break;

@@ -117,6 +117,15 @@ void sort_large_buckets(holo_ctx* ctx, const std::vector<int>& ids, const std::v
                         const std::vector<unsigned>& counts, unsigned long long* ekey, int* egidx);
 void entry_depths(holo_ctx* ctx, const int* egidx, const double* zc, double* edepth, size_t E);
 
+// ---- render_static.cu (compile-time FFT plans for the common grid sizes)
+enum { kModeFull = 0, kModeSpec = 1, kModeReplay = 2 };
+bool static_render_supported(int W, int H);
+void static_col_fwd(holo_ctx* ctx, cx<float>* data, int W, int H, int nfields);
+void static_col_inv(holo_ctx* ctx, const cx<float>* in, int W, int H, int C, int nout, int has_holo,
+                    cx<float>* holo, cx<float>* rep, float* intens);
+void static_row(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spec, cx<float>* out, int W, int H,
+                int C, int Lloc, int nout, const int* plane_of, const TfChan* tfc, double pitch);
+
 // ---- composite.cu
 constexpr int kSortCap = 1024;
 struct CompositeArgs {

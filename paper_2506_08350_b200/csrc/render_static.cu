@@ -1,0 +1,362 @@
+// Render-path propagation with compile-time FFT plans (sm_100a, fp32).
+//
+// pipeline_forward's propagation (forward_record + inverse_propagate,
+// proj/src/propagation.cpp:103-123) as three passes over HBM:
+//   1. k_col_fwd      column FFT of every raster layer, in place
+//   2. k_row_fused    per row (c, y): row FFT of each plane, times H_{Z_l}, summed
+//                     into the spectrum S held in registers; then for every output
+//                     (the hologram and each replayed plane) S . M_o -> row IFFT
+//                     with M_o = 1 or conj(H_{Z_l}) = H_{-Z_l}
+//   3. k_col_inv_epi  column IFFT of each output with the epilogue: hologram
+//                     x 1/(w h); intensity |v / (w h)|^2; optional replayed field
+// S never exists as a full field unless the planes are sharded across GPUs
+// (modes SPEC / REPLAY of k_row_fused bracket the all-reduce of S).  The
+// identity FFT2(hologram) = S (the hologram is IFFT2(S)) removes the forward
+// transform of inverse_propagate.
+#include "fft_static.cuh"
+#include "kernels.cuh"
+
+namespace holo_cuda {
+
+namespace {
+
+template <int N>
+struct PlanOf;
+template <> struct PlanOf<48> { using type = Radices<16, 3>; };
+template <> struct PlanOf<64> { using type = Radices<16, 4>; };
+template <> struct PlanOf<128> { using type = Radices<16, 8>; };
+template <> struct PlanOf<256> { using type = Radices<16, 16>; };
+template <> struct PlanOf<512> { using type = Radices<8, 8, 8>; };
+template <> struct PlanOf<1024> { using type = Radices<16, 16, 4>; };
+template <> struct PlanOf<1080> { using type = Radices<8, 9, 15>; };
+template <> struct PlanOf<1920> { using type = Radices<16, 8, 15>; };
+template <> struct PlanOf<2048> { using type = Radices<16, 16, 8>; };
+template <> struct PlanOf<2160> { using type = Radices<16, 9, 15>; };
+template <> struct PlanOf<3840> { using type = Radices<16, 16, 15>; };
+
+// column passes: strips of 8 columns (64-byte row segments)
+template <int H>
+struct ColCfg {
+    static constexpr int NB = 8;
+    static constexpr int NT = H >= 1024 ? 512 : 256;
+    static constexpr int kMinBlocks = H <= 1280 ? 2 : 1;  // 2 CTAs per SM while 64 registers suffice
+    using B = Batch<H, NB, NT>;
+    static constexpr size_t kSmem = sizeof(cx<float>) * H * NB;
+};
+
+// row pass: NBR rows of one channel per CTA
+template <int W>
+struct RowCfg {
+    static constexpr int NBR = W <= 512 ? 4 : (W <= 2048 ? 2 : 1);
+    static constexpr int NT = W >= 1024 ? 256 : 128;
+    using B = Batch<W, NBR, NT>;
+    static constexpr size_t kSmem = sizeof(cx<float>) * W * NBR;
+};
+
+__device__ __forceinline__ cx<float> czf() { return mk(0.0f, 0.0f); }
+
+// e^{i theta} for |theta| up to a few thousand rad: two-constant reduction into
+// [-pi, pi] then the MUFU sin/cos (abs. error <= 2^-21.4 there).
+__device__ __forceinline__ cx<float> phasor_reduced(float theta) {
+    const float k = rintf(theta * 0.159154943091895336f);
+    float red = fmaf(-k, 6.28318548202514648f, theta);  // 2 pi rounded to float
+    red = fmaf(-k, -1.74845553e-07f, red);              // minus (2 pi - that)
+    float s, c;
+    __sincosf(red, &s, &c);
+    return mk(c, s);
+}
+
+// ---------------------------------------------------------------- 1. column FFT (forward, in place)
+
+template <int H>
+__global__ void __launch_bounds__(ColCfg<H>::NT, ColCfg<H>::kMinBlocks) k_col_fwd(cx<float>* __restrict__ data, int W,
+                                                           const cx<float>* __restrict__ tw) {
+    using Cfg = ColCfg<H>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cx<float>* sm = reinterpret_cast<cx<float>*>(smem_raw);
+    const int x0 = blockIdx.x * Cfg::NB;
+    cx<float>* base = data + static_cast<size_t>(blockIdx.y) * H * W;
+    auto load = [&](int, int, int b, int i) -> cx<float> {
+        const int x = x0 + b;
+        return x < W ? base[static_cast<size_t>(i) * W + x] : czf();
+    };
+    auto store = [&](int, int, int b, int i, cx<float> v) {
+        const int x = x0 + b;
+        if (x < W) base[static_cast<size_t>(i) * W + x] = v;
+    };
+    fft_static<float, -1, typename Cfg::B, typename PlanOf<H>::type>(sm, tw, load, store);
+}
+
+// ---------------------------------------------------------------- 2. row pass with the spectrum in registers
+
+template <int W, int MODE>
+__global__ void __launch_bounds__(RowCfg<W>::NT, 2) k_row_fused(
+    const cx<float>* __restrict__ layers,  // [Lloc][C][H][W], column-transformed (FULL, SPEC)
+    cx<float>* __restrict__ spec,          // [C][H][W]: written (SPEC) or read (REPLAY)
+    cx<float>* __restrict__ out,           // [O][C][H][W] row-inverse-transformed outputs (FULL, REPLAY)
+    int H, int C, int Lloc, int nout, const int* __restrict__ plane_of, const TfChan* __restrict__ tfc,
+    const double* __restrict__ fx, const double* __restrict__ fy, const cx<float>* __restrict__ tw) {
+    using Cfg = RowCfg<W>;
+    using B = typename Cfg::B;
+    using P = typename PlanOf<W>::type;
+    using Pinv = typename RevPlan<P>::type;
+    using LS = LastStage<B, P>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cx<float>* sm = reinterpret_cast<cx<float>*>(smem_raw);
+
+    const int row0 = blockIdx.x * Cfg::NBR;  // row = c * H + y; a CTA never spans two channels
+    const int c = row0 / H;
+    const size_t plane_stride = static_cast<size_t>(C) * H * W;
+
+    // (q, r) <-> (b, i) of the last forward stage = first inverse stage
+    auto owner = [&](int q, int r, int& b, int& i) -> bool {
+        constexpr int M = W / LS::kR;
+        const int t = threadIdx.x + q * B::kNT;
+        b = t % B::kNB;
+        i = t / B::kNB + r * M;
+        return t < M * B::kNB;
+    };
+
+    cx<float> S[LS::kBPT][LS::kR];
+    // Plane-independent part of the transfer-function phase for each owned spectral
+    // sample: g = f^2 / (1/l + sqrt(1/l^2 - f^2)), or -1 outside the propagating
+    // band (band test in f64, reference order).  Per plane the phase is then
+    // phase0 - 2 pi z g (see tf_value<float>).
+    float G[LS::kBPT][LS::kR];
+    {
+        const TfChan p0 = tfc[c];  // 1/l^2, 1/l depend on the channel only
+#pragma unroll
+        for (int q = 0; q < LS::kBPT; ++q)
+#pragma unroll
+            for (int r = 0; r < LS::kR; ++r) {
+                S[q][r] = czf();
+                G[q][r] = -1.0f;
+                int b, i;
+                if (owner(q, r, b, i)) {
+                    const double fxv = fx[i], fyv = fy[(row0 + b) - c * H];
+                    const double fx2 = __dmul_rn(fxv, fxv), fy2 = __dmul_rn(fyv, fyv);
+                    const double arg = __dsub_rn(__dsub_rn(p0.inv_l2, fx2), fy2);
+                    if (!(arg < 0.0))
+                        G[q][r] = static_cast<float>(__dadd_rn(fx2, fy2)) / (p0.inv_l + sqrtf(static_cast<float>(arg)));
+                }
+            }
+    }
+    auto tf = [&](const TfChan& p, int q, int r, int b, int i) -> cx<float> {
+        if (p.local) return tf_value<float>(p, fx[i], fy[(row0 + b) - c * H]);
+        const float g = G[q][r];
+        if (g < 0.0f) return czf();
+        return phasor_reduced(p.phase0 - p.two_pi_z_f * g);
+    };
+
+    if constexpr (MODE != kModeReplay) {
+        for (int l = 0; l < Lloc; ++l) {
+            const TfChan p = tfc[l * C + c];
+            const cx<float>* src = layers + l * plane_stride + static_cast<size_t>(row0) * W;
+            auto load = [&](int, int, int b, int i) -> cx<float> { return src[static_cast<size_t>(b) * W + i]; };
+            auto store = [&](int q, int r, int b, int i, cx<float> v) { S[q][r] = S[q][r] + v * tf(p, q, r, b, i); };
+            fft_static<float, -1, B, P>(sm, tw, load, store);
+        }
+    }
+    if constexpr (MODE == kModeSpec) {
+        cx<float>* dst = spec + static_cast<size_t>(row0) * W;
+#pragma unroll
+        for (int q = 0; q < LS::kBPT; ++q)
+#pragma unroll
+            for (int r = 0; r < LS::kR; ++r) {
+                int b, i;
+                if (owner(q, r, b, i)) dst[static_cast<size_t>(b) * W + i] = S[q][r];
+            }
+        return;
+    }
+    if constexpr (MODE == kModeReplay) {
+        const cx<float>* srcs = spec + static_cast<size_t>(row0) * W;
+#pragma unroll
+        for (int q = 0; q < LS::kBPT; ++q)
+#pragma unroll
+            for (int r = 0; r < LS::kR; ++r) {
+                int b, i;
+                if (owner(q, r, b, i)) S[q][r] = srcs[static_cast<size_t>(b) * W + i];
+            }
+    }
+    for (int o = 0; o < nout; ++o) {
+        const int l = plane_of[o];
+        TfChan p;
+        if (l >= 0) p = tfc[l * C + c];
+        cx<float>* dst = out + (static_cast<size_t>(o) * C * H + row0) * W;
+        auto load = [&](int q, int r, int b, int i) -> cx<float> {
+            if (l < 0) return S[q][r];
+            return S[q][r] * conj(tf(p, q, r, b, i));
+        };
+        auto store = [&](int, int, int b, int i, cx<float> v) { dst[static_cast<size_t>(b) * W + i] = v; };
+        fft_static<float, +1, B, Pinv>(sm, tw, load, store);
+    }
+}
+
+// ---------------------------------------------------------------- 3. column IFFT + epilogue
+
+template <int H>
+__global__ void __launch_bounds__(ColCfg<H>::NT, ColCfg<H>::kMinBlocks) k_col_inv_epi(const cx<float>* __restrict__ in, int W, int C,
+                                                               int has_holo, float s, const cx<float>* __restrict__ tw,
+                                                               cx<float>* __restrict__ holo,
+                                                               cx<float>* __restrict__ replayed,
+                                                               float* __restrict__ intens) {
+    using Cfg = ColCfg<H>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cx<float>* sm = reinterpret_cast<cx<float>*>(smem_raw);
+    const int x0 = blockIdx.x * Cfg::NB;
+    const int c = blockIdx.y, o = blockIdx.z;
+    const size_t P = static_cast<size_t>(H) * W;
+    const cx<float>* src = in + (static_cast<size_t>(o) * C + c) * P;
+    const bool is_holo = has_holo && o == 0;
+    const size_t obase = is_holo ? static_cast<size_t>(c) * P : (static_cast<size_t>(o - has_holo) * C + c) * P;
+    auto load = [&](int, int, int b, int i) -> cx<float> {
+        const int x = x0 + b;
+        return x < W ? src[static_cast<size_t>(i) * W + x] : czf();
+    };
+    auto store = [&](int, int, int b, int i, cx<float> v) {
+        const int x = x0 + b;
+        if (x >= W) return;
+        const size_t at = obase + static_cast<size_t>(i) * W + x;
+        v = scale(v, s);
+        if (is_holo) {
+            holo[at] = v;
+        } else {
+            if (replayed) replayed[at] = v;
+            if (intens) intens[at] = v.x * v.x + v.y * v.y;
+        }
+    };
+    using Pinv = typename RevPlan<typename PlanOf<H>::type>::type;
+    fft_static<float, +1, typename Cfg::B, Pinv>(sm, tw, load, store);
+}
+
+template <class K>
+void smem_attr(K kernel, size_t bytes) {
+    if (bytes > 48 * 1024)
+        HC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+}
+
+template <int H>
+void launch_col_fwd(holo_ctx* ctx, cx<float>* data, int W, int nfields) {
+    using Cfg = ColCfg<H>;
+    smem_attr(k_col_fwd<H>, Cfg::kSmem);
+    const dim3 grid((W + Cfg::NB - 1) / Cfg::NB, nfields);
+    k_col_fwd<H><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(data, W, ctx->twiddle<float>(H));
+    HC_LAUNCHED(ctx);
+}
+
+template <int H>
+void launch_col_inv(holo_ctx* ctx, const cx<float>* in, int W, int C, int nout, int has_holo, cx<float>* holo,
+                    cx<float>* rep, float* intens) {
+    using Cfg = ColCfg<H>;
+    smem_attr(k_col_inv_epi<H>, Cfg::kSmem);
+    const dim3 grid((W + Cfg::NB - 1) / Cfg::NB, C, nout);
+    const float s = static_cast<float>(1.0 / (static_cast<double>(W) * H));
+    k_col_inv_epi<H><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(in, W, C, has_holo, s, ctx->twiddle<float>(H),
+                                                                 holo, rep, intens);
+    HC_LAUNCHED(ctx);
+}
+
+template <int W>
+void launch_row(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spec, cx<float>* out, int H, int C,
+                int Lloc, int nout, const int* plane_of, const TfChan* tfc, const double* fx, const double* fy) {
+    using Cfg = RowCfg<W>;
+    const int rows = C * H;
+    const dim3 grid(rows / Cfg::NBR);
+    const cx<float>* tw = ctx->twiddle<float>(W);
+    switch (mode) {
+        case kModeFull:
+            smem_attr(k_row_fused<W, kModeFull>, Cfg::kSmem);
+            k_row_fused<W, kModeFull><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(layers, spec, out, H, C, Lloc, nout,
+                                                                                  plane_of, tfc, fx, fy, tw);
+            break;
+        case kModeSpec:
+            smem_attr(k_row_fused<W, kModeSpec>, Cfg::kSmem);
+            k_row_fused<W, kModeSpec><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(layers, spec, out, H, C, Lloc, nout,
+                                                                                  plane_of, tfc, fx, fy, tw);
+            break;
+        default:
+            smem_attr(k_row_fused<W, kModeReplay>, Cfg::kSmem);
+            k_row_fused<W, kModeReplay><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(
+                layers, spec, out, H, C, Lloc, nout, plane_of, tfc, fx, fy, tw);
+            break;
+    }
+    HC_LAUNCHED(ctx);
+}
+
+#define HC_SIZES(X) X(48) X(64) X(128) X(256) X(512) X(1024) X(1080) X(1920) X(2048) X(2160) X(3840)
+
+bool size_listed(int n) {
+#define HC_CASE(N) case N:
+    switch (n) {
+        HC_SIZES(HC_CASE)
+        return true;
+        default:
+            return false;
+    }
+#undef HC_CASE
+}
+
+int row_nbr(int W) {
+#define HC_CASE(N) \
+    case N:        \
+        return RowCfg<N>::NBR;
+    switch (W) {
+        HC_SIZES(HC_CASE)
+        default:
+            return 1;
+    }
+#undef HC_CASE
+}
+
+}  // namespace
+
+bool static_render_supported(int W, int H) {
+    return size_listed(W) && size_listed(H) && H % row_nbr(W) == 0;
+}
+
+void static_col_fwd(holo_ctx* ctx, cx<float>* data, int W, int H, int nfields) {
+    if (nfields <= 0) return;
+#define HC_CASE(N)                                    \
+    case N:                                           \
+        launch_col_fwd<N>(ctx, data, W, nfields);     \
+        return;
+    switch (H) {
+        HC_SIZES(HC_CASE)
+        default:
+            throw Error(HOLO_ERR_CONFIG, "no static column plan");
+    }
+#undef HC_CASE
+}
+
+void static_col_inv(holo_ctx* ctx, const cx<float>* in, int W, int H, int C, int nout, int has_holo,
+                    cx<float>* holo, cx<float>* rep, float* intens) {
+    if (nout <= 0) return;
+#define HC_CASE(N)                                                          \
+    case N:                                                                 \
+        launch_col_inv<N>(ctx, in, W, C, nout, has_holo, holo, rep, intens); \
+        return;
+    switch (H) {
+        HC_SIZES(HC_CASE)
+        default:
+            throw Error(HOLO_ERR_CONFIG, "no static column plan");
+    }
+#undef HC_CASE
+}
+
+void static_row(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spec, cx<float>* out, int W, int H,
+                int C, int Lloc, int nout, const int* plane_of, const TfChan* tfc, double pitch) {
+    const double* fx = ctx->freq(W, pitch);
+    const double* fy = ctx->freq(H, pitch);
+#define HC_CASE(N)                                                                               \
+    case N:                                                                                      \
+        launch_row<N>(ctx, mode, layers, spec, out, H, C, Lloc, nout, plane_of, tfc, fx, fy); \
+        return;
+    switch (W) {
+        HC_SIZES(HC_CASE)
+        default:
+            throw Error(HOLO_ERR_CONFIG, "no static row plan");
+    }
+#undef HC_CASE
+}
+
+}  // namespace holo_cuda
