@@ -189,8 +189,8 @@ class Oracle:
         self.lib = C.CDLL(path)
         self.pre = pre
         L = self.lib
-        L[pre + "last_error"].restype = C.c_char_p
-        self._free = L[pre + "raster_free"]
+        getattr(L, pre + "last_error").restype = C.c_char_p
+        self._free = getattr(L, pre + "raster_free")
 
     @staticmethod
     def available(kind: str) -> bool:
@@ -198,11 +198,30 @@ class Oracle:
         return os.path.exists(os.path.join(HERE, *sub))
 
     def _fn(self, name):
-        return self.lib[self.pre + name]
+        return getattr(self.lib, self.pre + name)
 
     def _check(self, rc):
         if rc != 0:
             raise OracleError(rc, self._fn("last_error")().decode())
+
+    # ----------------------------------------------------------- small pieces
+    def covariance_3d(self, quat, log_scales):
+        """covariance_3d (scene.cpp:125-130), restatement only; returns 3x3."""
+        q = np.ascontiguousarray(quat, dtype=np.float64)
+        s = np.ascontiguousarray(log_scales, dtype=np.float64)
+        out = np.zeros(9)
+        self.lib.ho_covariance_3d(_ptr(q), _ptr(s), _ptr(out))
+        return out.reshape(3, 3)
+
+    def ste_argmax(self, logits):
+        a = np.ascontiguousarray(logits, dtype=np.float64)
+        return int(self.lib.ho_ste_argmax(_ptr(a), C.c_int(a.size)))
+
+    def plane_positions(self, wave):
+        wv = _wave(wave)
+        z = np.zeros(wv.num_planes)
+        self._check(self.lib.ho_plane_positions(C.byref(wv), _ptr(z)))
+        return z
 
     # ---------------------------------------------------------------- raster
     def _unpack_raster(self, r: _Raster, N: int):
@@ -217,7 +236,7 @@ class Oracle:
             return np.ctypeslib.as_array(ptr, shape=(n,)).astype(dt, copy=True)
 
         layers = arr(r.layers, L * 3 * P * 2, np.float64).view(np.complex128).reshape(L, 3, h, w)
-        projected = None
+        projected = {name: np.zeros(0) for name, _ in _Projected._fields_}
         if N:
             proj = np.ctypeslib.as_array(r.projected, shape=(N,))
             projected = {k: np.array(proj[k], copy=True) for k in proj.dtype.names}

@@ -135,7 +135,10 @@ __global__ void __launch_bounds__(TILE * TILE) k_composite(CompositeArgs a) {
             const GRec r = a.rec[g];
             const float mx = static_cast<float>(r.mu_x - static_cast<double>(px0));
             const float my = static_cast<float>(r.mu_y - static_cast<double>(py0));
-            const float rr = r.radius * 1.00001f + 1e-3f;
+            // Beyond the support radius a < alpha_floor (rasterizer.cpp:54-62), so the
+            // warp cull is exact only for a positive floor; without one every pixel
+            // of the tile is evaluated, as the reference does.
+            const float rr = a.floor_positive ? r.radius * 1.00001f + 1e-3f : INFINITY;
             float alpha = r.alpha;
             if (a.soft) alpha = static_cast<float>(static_cast<double>(r.alpha) * a.rho[static_cast<size_t>(g) * a.L + plane]);
             s_a[t] = make_float4(mx, my, r.ca, r.cb);

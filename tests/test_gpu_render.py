@@ -1,0 +1,267 @@
+"""GPU parity of the forward render (holo_render = pipeline_forward /
+raster_forward, pipeline.cpp:20-29, rasterizer.cpp:139-263) against the C
+restatement of the reference, on identical synthetic scenes.
+
+Bars (north star): complex fields rel-L2 <= 1e-4 (fp32 vs f64), intensity PSNR
+within 0.01 dB, per-tile work lists (entries, bucket_start) bit-exact, f64
+projections of centres and depths bit-exact."""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import desk_config, front_camera, mild_posed_camera, overlapping_scene, random_scene, rel_l2, \
+    single_scene
+from oracle.oracle import psnr
+from paper_2506_08350_b200 import _lib as L
+from paper_2506_08350_b200 import api
+from paper_2506_08350_b200._lib import HoloError
+from paper_2506_08350_b200.holotypes import PipelineOptions, PropagationOptions, RenderSettings, WaveConfig
+from paper_2506_08350_b200.scenes import CONFIGS, synthetic_scene
+from paper_2506_08350_b200.scenes import front_camera as wide_camera
+
+pytestmark = pytest.mark.gpu
+RGB = (639e-9, 532e-9, 473e-9)
+
+
+def check_pipeline(ctx, oracle, scene, cam, cfg, st=None, prop=None, tol=1e-4, lists=True):
+    st = st or RenderSettings()
+    prop = prop or PropagationOptions()
+    g = api.pipeline_forward(scene, cam, cfg, PipelineOptions(raster=st, prop=prop), ctx=ctx)
+    r = oracle.pipeline_forward(scene, cam, cfg, st, prop)
+    C = cfg.channels()
+    errs = {"layers": rel_l2(np.stack(g.raster.layers), r.raster.layers[:, :C]),
+            "hologram": rel_l2(g.hologram, r.hologram),
+            "replayed": rel_l2(np.stack(g.replayed), r.replayed),
+            "intensity": rel_l2(np.stack(g.intensities), r.intensities)}
+    for k, v in errs.items():
+        assert v <= tol, (k, v)
+    ints = np.stack(g.intensities)
+    for l in range(cfg.num_planes):
+        t = 0.9025 * r.intensities[l]  # target: the same scene with amplitudes x 0.95
+        assert abs(psnr(ints[l], t) - psnr(r.intensities[l], t)) <= 0.01
+    if lists:
+        assert np.array_equal(g.raster.bucket_start, r.raster.bucket_start)
+        assert np.array_equal(g.raster.entries["gidx"], r.raster.entry_gidx)
+        assert np.array_equal(g.raster.entries["bucket"], r.raster.entry_bucket)
+        assert np.array_equal(g.raster.entries["depth"], r.raster.entry_depth)
+        for k in ("valid", "plane", "mu_x", "mu_y", "zc", "xc", "yc"):
+            assert np.array_equal(g.raster.projected[k], r.raster.projected[k]), k
+        for k in ("inv00", "inv01", "inv11", "radius", "alpha_sig"):
+            # CUDA's f64 exp/log may differ from glibc's by an ulp; inv01 carries
+            # cancellation, so scale the bound by the conic's magnitude
+            ref = r.raster.projected[k]
+            scale = np.abs(ref).max() if ref.size else 0.0
+            assert np.allclose(g.raster.projected[k], ref, rtol=1e-12, atol=1e-12 * scale), k
+        assert np.array_equal(g.raster.touched, r.raster.touched)
+        assert np.array_equal(g.raster.rho, r.raster.rho)
+    # Contribution counts and final transmittance: an fp32 alpha within an ulp of
+    # alpha_floor (or of term_eps for T) can flip one accept decision, which moves T
+    # of that pixel by a factor (1 - 1/255).  Such pixels must stay rare.  With no
+    # floor (alpha_floor <= 0) the reference also counts contributions below fp32's
+    # normal range, so only the fields are compared.
+    if st.alpha_floor > 0:
+        mism = np.count_nonzero(g.raster.n_contrib != r.raster.n_contrib)
+        assert mism <= max(3, 2e-4 * g.raster.n_contrib.size), mism
+        dT = np.abs(g.raster.t_final - r.raster.t_final)
+        assert np.count_nonzero(dT > 1e-4) <= max(3, 2e-4 * dT.size)
+        assert dT.max() < 0.01
+    return g, r, errs
+
+
+@pytest.mark.parametrize("n,W,H,L,wl,seed", [
+    (300, 64, 48, 3, RGB, 1),
+    (3000, 256, 256, 3, (515e-9,), 2),        # C1-like, single wavelength adapter
+    (20000, 512, 384, 4, (638e-9, 520e-9, 450e-9), 3),
+    (800, 96, 80, 2, RGB, 4),                 # generic (runtime-planned) FFT sizes
+    (500, 30, 42, 5, RGB, 5),                 # ragged tiles, odd grid
+    (0, 64, 64, 2, RGB, 6),                   # empty scene
+    (1, 64, 64, 1, RGB, 7),                   # one Gaussian, one plane
+])
+def test_pipeline_parity(gpu_ctx, oracle, n, W, H, L, wl, seed):
+    cfg = WaveConfig(nx=W, ny=H, wavelengths=wl, num_planes=L)
+    check_pipeline(gpu_ctx, oracle, synthetic_scene(n, cfg, seed), wide_camera(cfg), cfg)
+
+
+@pytest.mark.parametrize("tile", [8, 16, 32])
+def test_tile_sizes(gpu_ctx, oracle, tile):
+    cfg = WaveConfig(nx=96, ny=64, wavelengths=RGB, num_planes=3)
+    check_pipeline(gpu_ctx, oracle, synthetic_scene(1500, cfg, 10 + tile), wide_camera(cfg), cfg,
+                   RenderSettings(tile=tile))
+
+
+def test_soft_assignment(gpu_ctx, oracle):
+    cfg = WaveConfig(nx=64, ny=64, wavelengths=RGB, num_planes=3)
+    st = RenderSettings(soft_assignment=True, soft_tau=1.0)
+    check_pipeline(gpu_ctx, oracle, synthetic_scene(400, cfg, 21), wide_camera(cfg), cfg, st)
+
+
+def test_gradcheck_settings(gpu_ctx, oracle):
+    # helpers.hpp:105-111: no floor, no termination, wide cutoff
+    cfg = WaveConfig(nx=48, ny=48, wavelengths=RGB, num_planes=2)
+    st = RenderSettings(alpha_floor=0.0, term_eps=0.0, radius_form_cap=80.0)
+    check_pipeline(gpu_ctx, oracle, random_scene(40, cfg, 22), front_camera(cfg), cfg, st)
+
+
+def test_posed_camera_and_reference_helpers(gpu_ctx, oracle):
+    cfg = WaveConfig(nx=48, ny=48, num_planes=2)
+    check_pipeline(gpu_ctx, oracle, random_scene(60, cfg, 23), mild_posed_camera(cfg), cfg)
+    check_pipeline(gpu_ctx, oracle, overlapping_scene(40, cfg, 24), front_camera(cfg), cfg)
+
+
+def test_pad2x_pipeline(gpu_ctx, oracle):
+    cfg = WaveConfig(nx=48, ny=32, wavelengths=RGB, num_planes=2)
+    check_pipeline(gpu_ctx, oracle, synthetic_scene(200, cfg, 25), wide_camera(cfg), cfg,
+                   prop=PropagationOptions(pad2x=True))
+
+
+def test_large_buckets_sorted_globally(gpu_ctx, oracle):
+    # the reference's own bench scene packs thousands of splats into a few tiles
+    # (holo_main.cpp:53-81): exercises buckets above the in-CTA sort capacity
+    cfg = WaveConfig(nx=64, ny=64, wavelengths=RGB, num_planes=2)
+    s = synthetic_scene(6000, cfg, 26)
+    s.positions[:, :2] *= 0.05
+    g, r, _ = check_pipeline(gpu_ctx, oracle, s, wide_camera(cfg), cfg)
+    assert int(np.diff(r.raster.bucket_start.astype(np.int64)).max()) > 1024
+
+
+def test_render_is_deterministic(gpu_ctx):
+    cfg = WaveConfig(nx=256, ny=192, wavelengths=RGB, num_planes=4)
+    s = synthetic_scene(30000, cfg, 27)
+    a = api.pipeline_forward(s, wide_camera(cfg), cfg, ctx=gpu_ctx)
+    b = api.pipeline_forward(s, wide_camera(cfg), cfg, ctx=gpu_ctx)
+    assert np.array_equal(a.hologram, b.hologram)
+    assert np.array_equal(np.stack(a.intensities), np.stack(b.intensities))
+    assert np.array_equal(a.raster.entries, b.raster.entries)
+
+
+# ---------------------------------------------------------------- rasterizer KATs (test_rasterizer.cpp) on the GPU
+
+def centred(n, logits, phases=None):
+    cfg = desk_config(32, 1)
+    cam = front_camera(cfg)
+    z = 0.3
+    off = 0.5 * z / cam.focal_px
+    s = single_scene(n, 1)
+    s.positions = np.tile([off, off, z], (n, 1))
+    s.log_scales = np.full((n, 3), np.log(0.004))
+    s.amplitudes = np.ones((n, 3))
+    s.opacity_logits = np.array(logits, dtype=float)
+    if phases is not None:
+        s.phases = np.array(phases, dtype=float)
+    return cfg, cam, s
+
+
+def test_blending_kats(gpu_ctx):
+    # test_rasterizer.cpp:117-157, fp32 tolerance
+    cfg, cam, s = centred(1, [math.log(0.8 / 0.2)])
+    r = api.raster_forward(s, cam, cfg, ctx=gpu_ctx)
+    assert abs(r.layers[0][0, 16, 16] - 0.8) < 1e-6 and abs(r.t_final[0, 16, 16] - 0.2) < 1e-6
+    cfg, cam, s = centred(1, [math.log(0.8 / 0.2)], [[math.pi / 2] * 3])
+    assert abs(api.raster_forward(s, cam, cfg, ctx=gpu_ctx).layers[0][0, 16, 16] - 0.8j) < 1e-6
+    cfg, cam, s = centred(2, [0.0, 0.0], [[0, 0, 0], [math.pi] * 3])
+    r = api.raster_forward(s, cam, cfg, ctx=gpu_ctx)
+    assert abs(r.layers[0][0, 16, 16] - 0.25) < 1e-6 and abs(r.t_final[0, 16, 16] - 0.25) < 1e-6
+
+
+def test_equal_depth_tie_by_index(gpu_ctx):
+    cfg = desk_config(32, 1)
+    s = single_scene(2, 1)
+    s.positions = np.array([[0.0, 0.0, 0.3], [0.0, 0.0, 0.3]])
+    s.log_scales = np.full((2, 3), np.log(0.005))
+    s.amplitudes = np.ones((2, 3))
+    s.phases = np.array([[0.0] * 3, [math.pi / 2] * 3])
+    r = api.raster_forward(s, front_camera(cfg), cfg, ctx=gpu_ctx)
+    first_bucket = r.entries["bucket"][0]
+    assert list(r.entries["gidx"][r.entries["bucket"] == first_bucket]) == [0, 1]
+
+
+def test_culling_and_clamp(gpu_ctx):
+    cfg = desk_config(32, 1)
+    s = single_scene(2, 1)
+    s.positions = np.array([[0.0, 0.0, 1e-4], [0.0, 0.0, -0.5]])
+    s.log_scales = np.full((2, 3), np.log(0.005))
+    s.amplitudes = np.ones((2, 3))
+    s.opacity_logits = np.array([2.0, 2.0])
+    r = api.raster_forward(s, front_camera(cfg), cfg, ctx=gpu_ctx)
+    assert list(r.projected["valid"]) == [0, 0] and not np.any(np.stack(r.layers))
+    s = single_scene(1, 1)
+    s.positions = np.array([[0.0, 0.0, 0.3]])
+    s.log_scales = np.full((1, 3), np.log(0.05))
+    s.amplitudes = np.ones((1, 3))
+    s.opacity_logits = np.array([40.0])
+    r = api.raster_forward(s, front_camera(cfg), cfg, ctx=gpu_ctx)
+    assert r.t_final[0, 16, 16] >= 1.0 - 0.999 - 1e-7
+    assert np.abs(np.stack(r.layers)).max() <= 0.999 + 1e-6
+
+
+def test_rejects_bad_inputs(gpu_ctx):
+    cfg = desk_config(32, 2)
+    s = random_scene(3, cfg, 1)
+    bad = front_camera(cfg)
+    bad.width = 16
+    with pytest.raises(HoloError):
+        api.raster_forward(s, bad, cfg, ctx=gpu_ctx)
+    s.rotations[1] = 0.0  # degenerate quaternion: validated on the device (scene.cpp:27)
+    gpu_ctx.upload_scene(s)
+    with pytest.raises(HoloError) as e:
+        gpu_ctx.render(front_camera(cfg), cfg)
+    assert e.value.kind == "config" and "quaternion" in str(e.value)
+    s = random_scene(3, cfg, 1)
+    s.amplitudes[0, 0] = -1.0
+    gpu_ctx.upload_scene(s)
+    with pytest.raises(HoloError):
+        gpu_ctx.render(front_camera(cfg), cfg)
+
+
+# ---------------------------------------------------------------- plane sharding (begin / all-reduce / end) on one GPU
+
+def test_plane_sharded_halves_equal_full_render(gpu_ctx):
+    import torch
+
+    cfg = WaveConfig(nx=256, ny=256, wavelengths=RGB, num_planes=4)
+    s = synthetic_scene(20000, cfg, 31)
+    cam = wide_camera(cfg)
+    full = api.pipeline_forward(s, cam, cfg, ctx=gpu_ctx, raster=False)
+    gpu_ctx.upload_scene(s)
+    C, H, W = 3, 256, 256
+    spec = torch.zeros((C, H, W, 2), dtype=torch.float32, device="cuda")
+    parts = []
+    for pb, pe in [(0, 2), (2, 4)]:  # two "ranks" emulated in sequence; the all-reduce is a sum
+        part = torch.empty_like(spec)
+        gpu_ctx.render_begin(cam, cfg, None, None, pb, pe, part.data_ptr(), 0)
+        torch.cuda.synchronize()
+        parts.append(part)
+    spec = parts[0] + parts[1]
+    torch.cuda.synchronize()
+    ints = []
+    for pb, pe in [(0, 2), (2, 4)]:
+        outs = L.OUT_INTENSITY | (L.OUT_HOLOGRAM if pb == 0 else 0)
+        gpu_ctx.render_end(cfg, None, pb, pe, spec.data_ptr(), outs)
+        ints.append(gpu_ctx.download(L.BUF_INTENSITY, np.float32, (pe - pb, C, H, W)))
+        if pb == 0:
+            holo = gpu_ctx.download(L.BUF_HOLOGRAM, np.complex64, (C, H, W))
+    assert rel_l2(holo, full.hologram) < 1e-5
+    assert rel_l2(np.concatenate(ints), np.stack(full.intensities)) < 1e-5
+
+
+# ---------------------------------------------------------------- BASELINE configurations at full size
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_baseline_config_parity(gpu_ctx, oracle, name):
+    c = CONFIGS[name]
+    cfg = c.wave()
+    scene = synthetic_scene(c.n, cfg, c.seed)
+    cam = c.cameras()[0]
+    g = api.pipeline_forward(scene, cam, cfg, ctx=gpu_ctx, replayed=False)
+    r = oracle.pipeline_forward(scene, cam, cfg, replayed=False)
+    assert rel_l2(np.stack(g.raster.layers), r.raster.layers[:, :cfg.channels()]) <= 1e-4
+    assert rel_l2(g.hologram, r.hologram) <= 1e-4
+    ints = np.stack(g.intensities)
+    assert rel_l2(ints, r.intensities) <= 1e-4
+    for l in range(cfg.num_planes):
+        t = 0.9025 * r.intensities[l]
+        assert abs(psnr(ints[l], t) - psnr(r.intensities[l], t)) <= 0.01
+    assert np.array_equal(g.raster.bucket_start, r.raster.bucket_start)
+    assert np.array_equal(g.raster.entries["gidx"], r.raster.entry_gidx)

@@ -1,6 +1,6 @@
 """Quick GPU bring-up script (not a pytest module): prints parity numbers per stage."""
 import sys, os, time, traceback
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))  # repo root
 import numpy as np
 from oracle.oracle import Oracle, rel_l2
 from paper_2506_08350_b200 import api
