@@ -7,11 +7,11 @@
 //   acc_c += a T amp_c e^{i phi_c},  T *= 1 - a,  ++n_contrib.
 // One CTA per bucket, one thread per pixel.  The CTA first restores the
 // reference order of its bucket -- ascending (zc, gidx), rasterizer.cpp:221-224 --
-// by a rank sort (<= 256 entries) or a bitonic sort (<= kSortCap) in shared
-// memory; larger buckets arrive presorted from binning.cu.  Records are staged
-// 256 at a time in shared memory; each warp covers an 8x4 pixel block and skips
-// (warp-uniformly) entries whose support circle (radius, rasterizer.cpp:54-62,
-// beyond which a < alpha_floor) misses the block.  Evaluation is fp32 with the
+// by a warp-shuffle bitonic sort (<= 128 entries), a rank sort (<= 256) or a
+// shared-memory bitonic sort (<= kSortCap); larger buckets arrive presorted from
+// binning.cu.  Records are staged 256 at a time in shared memory; each warp
+// covers an 8x4 pixel block and, 32 entries per ballot, skips entries whose
+// accept ellipse (a > alpha_floor) has a bounding box missing the block.  Evaluation is fp32 with the
 // centre offset formed in f64 per entry, so dx, dy keep full fp32 precision.
 #include "kernels.cuh"
 
@@ -33,6 +33,73 @@ struct TileGeom {
     static constexpr int kBlocksX = TILE / 8;
 };
 
+struct KeyG {
+    unsigned long long k;  // IEEE bits of zc (> 0, so they order like zc)
+    int g;                 // Gaussian index: the tie-break
+};
+
+__device__ __forceinline__ bool kg_less(const KeyG& a, const KeyG& b) {
+    return a.k < b.k || (a.k == b.k && a.g < b.g);
+}
+
+// Bitonic sort of 32 * NE (key, gidx) pairs held by one warp, element i in lane
+// i % 32, slot i / 32; ascending on (zc, gidx) -- rasterizer.cpp:221-224.
+template <int NE>
+__device__ __forceinline__ void warp_bitonic(KeyG (&v)[NE], int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32 * NE; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+#pragma unroll
+                for (int s = 0; s < NE; ++s) {
+                    const int s2 = s ^ (j >> 5);
+                    if (s2 > s) {
+                        const bool up = ((lane + 32 * s) & k) == 0;
+                        const bool swap = up ? kg_less(v[s2], v[s]) : kg_less(v[s], v[s2]);
+                        if (swap) {
+                            const KeyG t = v[s];
+                            v[s] = v[s2];
+                            v[s2] = t;
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int s = 0; s < NE; ++s) {
+                    KeyG o;
+                    o.k = __shfl_xor_sync(0xffffffffu, v[s].k, j);
+                    o.g = __shfl_xor_sync(0xffffffffu, v[s].g, j);
+                    const bool lower = (lane & j) == 0;
+                    const bool up = ((lane + 32 * s) & k) == 0;
+                    const bool take_min = lower == up;
+                    const bool o_less = kg_less(o, v[s]);
+                    if (take_min ? o_less : !o_less) v[s] = o;
+                }
+            }
+        }
+    }
+}
+
+template <int NE>
+__device__ __forceinline__ void warp_sort_bucket(const unsigned long long* __restrict__ ekey,
+                                                 const int* __restrict__ egidx, unsigned e0, int n, int lane,
+                                                 int* __restrict__ s_ord) {
+    KeyG v[NE];
+#pragma unroll
+    for (int s = 0; s < NE; ++s) {
+        const int i = lane + 32 * s;
+        v[s].k = i < n ? ekey[e0 + i] : ~0ull;
+        v[s].g = i < n ? egidx[e0 + i] : 0x7fffffff;
+    }
+    warp_bitonic<NE>(v, lane);
+#pragma unroll
+    for (int s = 0; s < NE; ++s) {
+        const int i = lane + 32 * s;
+        if (i < n) s_ord[i] = v[s].g;
+    }
+}
+
 template <int TILE, int C>
 __global__ void __launch_bounds__(TILE * TILE) k_composite(CompositeArgs a) {
     using G = TileGeom<TILE>;
@@ -45,10 +112,8 @@ __global__ void __launch_bounds__(TILE * TILE) k_composite(CompositeArgs a) {
     __shared__ float4 s_c[kStage];  // xlo, xhi, col0
     __shared__ float4 s_d[kStage];  // col1, col2
 
-    const int lb = blockIdx.x;  // local bucket within the rendered planes
-    const int lplane = lb / a.num_tiles;
-    const int tile = lb - lplane * a.num_tiles;
-    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+    const int tx = blockIdx.x, ty = blockIdx.y, lplane = blockIdx.z;  // grid = (tiles_x, tiles_y, planes)
+    const int lb = (lplane * gridDim.y + ty) * gridDim.x + tx;        // local bucket
     const int px0 = tx * TILE, py0 = ty * TILE;
     const unsigned e0 = a.bstart[lb];
     const int n = static_cast<int>(a.bstart[lb + 1] - e0);
@@ -63,52 +128,64 @@ __global__ void __launch_bounds__(TILE * TILE) k_composite(CompositeArgs a) {
     // ---- restore the reference order (zc asc, gidx asc) inside the bucket
     const bool presorted = n > kSortCap;
     if (!presorted && n > 0) {
-        for (int t = tid; t < n; t += G::kThreads) {
-            s_key[t] = a.ekey[e0 + t];
-            s_gid[t] = a.egidx[e0 + t];
-        }
-        __syncthreads();
-        if (n <= G::kThreads) {
-            if (tid < n) {
-                const unsigned long long k = s_key[tid];
-                const int g = s_gid[tid];
-                int rank = 0;
-                for (int j = 0; j < n; ++j) {
-                    const unsigned long long kj = s_key[j];
-                    rank += (kj < k || (kj == k && s_gid[j] < g)) ? 1 : 0;
-                }
-                s_ord[rank] = g;
+        if (n <= 128) {
+            // one warp, registers and shuffles
+            if (warp == 0) {
+                if (n <= 32)
+                    warp_sort_bucket<1>(a.ekey, a.egidx, e0, n, lane, s_ord);
+                else if (n <= 64)
+                    warp_sort_bucket<2>(a.ekey, a.egidx, e0, n, lane, s_ord);
+                else
+                    warp_sort_bucket<4>(a.ekey, a.egidx, e0, n, lane, s_ord);
             }
         } else {
-            int P = 1;
-            while (P < n) P <<= 1;
-            for (int t = n + tid; t < P; t += G::kThreads) {
-                s_key[t] = ~0ull;
-                s_gid[t] = 0x7fffffff;
+            for (int t = tid; t < n; t += G::kThreads) {
+                s_key[t] = a.ekey[e0 + t];
+                s_gid[t] = a.egidx[e0 + t];
             }
             __syncthreads();
-            for (int k = 2; k <= P; k <<= 1) {
-                for (int j = k >> 1; j > 0; j >>= 1) {
-                    for (int t = tid; t < P; t += G::kThreads) {
-                        const int u = t ^ j;
-                        if (u > t) {
-                            const bool up = (t & k) == 0;
-                            const unsigned long long ka = s_key[t], kb = s_key[u];
-                            const int ga = s_gid[t], gb = s_gid[u];
-                            const bool b_less = kb < ka || (kb == ka && gb < ga);
-                            const bool a_less = ka < kb || (ka == kb && ga < gb);
-                            if (up ? b_less : a_less) {
-                                s_key[t] = kb;
-                                s_key[u] = ka;
-                                s_gid[t] = gb;
-                                s_gid[u] = ga;
+            if (n <= G::kThreads) {
+                if (tid < n) {
+                    const unsigned long long k = s_key[tid];
+                    const int g = s_gid[tid];
+                    int rank = 0;
+                    for (int j = 0; j < n; ++j) {
+                        const unsigned long long kj = s_key[j];
+                        rank += (kj < k || (kj == k && s_gid[j] < g)) ? 1 : 0;
+                    }
+                    s_ord[rank] = g;
+                }
+            } else {
+                int P = 1;
+                while (P < n) P <<= 1;
+                for (int t = n + tid; t < P; t += G::kThreads) {
+                    s_key[t] = ~0ull;
+                    s_gid[t] = 0x7fffffff;
+                }
+                __syncthreads();
+                for (int k = 2; k <= P; k <<= 1) {
+                    for (int j = k >> 1; j > 0; j >>= 1) {
+                        for (int t = tid; t < P; t += G::kThreads) {
+                            const int u = t ^ j;
+                            if (u > t) {
+                                const bool up = (t & k) == 0;
+                                const unsigned long long ka = s_key[t], kb = s_key[u];
+                                const int ga = s_gid[t], gb = s_gid[u];
+                                const bool b_less = kb < ka || (kb == ka && gb < ga);
+                                const bool a_less = ka < kb || (ka == kb && ga < gb);
+                                if (up ? b_less : a_less) {
+                                    s_key[t] = kb;
+                                    s_key[u] = ka;
+                                    s_gid[t] = gb;
+                                    s_gid[u] = ga;
+                                }
                             }
                         }
+                        __syncthreads();
                     }
-                    __syncthreads();
                 }
+                for (int t = tid; t < n; t += G::kThreads) s_ord[t] = s_gid[t];
             }
-            for (int t = tid; t < n; t += G::kThreads) s_ord[t] = s_gid[t];
         }
         __syncthreads();
         if (a.write_lists) {
@@ -135,15 +212,13 @@ __global__ void __launch_bounds__(TILE * TILE) k_composite(CompositeArgs a) {
             const GRec r = a.rec[g];
             const float mx = static_cast<float>(r.mu_x - static_cast<double>(px0));
             const float my = static_cast<float>(r.mu_y - static_cast<double>(py0));
-            // Beyond the support radius a < alpha_floor (rasterizer.cpp:54-62), so the
-            // warp cull is exact only for a positive floor; without one every pixel
-            // of the tile is evaluated, as the reference does.
-            const float rr = a.floor_positive ? r.radius * 1.00001f + 1e-3f : INFINITY;
+            // Box of the accept ellipse (GRec::hx, hy; infinite without a positive
+            // alpha floor, where the reference evaluates every pixel of the tile).
             float alpha = r.alpha;
             if (a.soft) alpha = static_cast<float>(static_cast<double>(r.alpha) * a.rho[static_cast<size_t>(g) * a.L + plane]);
             s_a[t] = make_float4(mx, my, r.ca, r.cb);
-            s_b[t] = make_float4(r.cc, alpha, my - rr, my + rr);
-            s_c[t] = make_float4(mx - rr, mx + rr, r.col[0], r.col[1]);
+            s_b[t] = make_float4(r.cc, alpha, my - r.hy, my + r.hy);
+            s_c[t] = make_float4(mx - r.hx, mx + r.hx, r.col[0], r.col[1]);
             s_d[t] = make_float4(r.col[2], r.col[3], r.col[4], r.col[5]);
         }
         __syncthreads();
@@ -208,10 +283,12 @@ __global__ void __launch_bounds__(TILE * TILE) k_composite(CompositeArgs a) {
 template <int TILE>
 void launch_tile(holo_ctx* ctx, const CompositeArgs& a) {
     if (a.num_buckets <= 0) return;
+    const int tiles_y = a.num_tiles / a.tiles_x;
+    const dim3 grid(a.tiles_x, tiles_y, a.num_buckets / a.num_tiles);
     switch (a.C) {
-        case 1: k_composite<TILE, 1><<<a.num_buckets, TILE * TILE, 0, ctx->stream>>>(a); break;
-        case 2: k_composite<TILE, 2><<<a.num_buckets, TILE * TILE, 0, ctx->stream>>>(a); break;
-        case 3: k_composite<TILE, 3><<<a.num_buckets, TILE * TILE, 0, ctx->stream>>>(a); break;
+        case 1: k_composite<TILE, 1><<<grid, TILE * TILE, 0, ctx->stream>>>(a); break;
+        case 2: k_composite<TILE, 2><<<grid, TILE * TILE, 0, ctx->stream>>>(a); break;
+        case 3: k_composite<TILE, 3><<<grid, TILE * TILE, 0, ctx->stream>>>(a); break;
         default: throw Error(HOLO_ERR_CONFIG, "render supports 1 to 3 wavelength channels");
     }
     HC_LAUNCHED(ctx);

@@ -51,7 +51,13 @@ struct RevPlan<Radices<R, Rs...>> {
 template <int N, int NB, int NT>
 struct Batch {
     static constexpr int kN = N, kNB = NB, kNT = NT;
-    static __device__ __forceinline__ int at(int b, int i) { return i * NB + b; }
+    // one pad slot per 32 complex values: the stride-R writes of early Stockham
+    // stages (i = R j + r) would otherwise land 32 lanes on one bank pair
+    static constexpr int kSmemElems = N * NB + (N * NB) / 32 + 1;
+    static __device__ __forceinline__ int at(int b, int i) {
+        const int c = i * NB + b;
+        return c + (c >> 5);
+    }
 };
 
 // One stage: radix R, ns = product of the earlier radices; FIRST/LAST select the

@@ -76,9 +76,9 @@ struct alignas(16) GRec {
     double mu_x, mu_y;        // projected centre, pixels
     float ca, cb, cc;         // -0.5 log2(e) * (inv00, 2 inv01, inv11): g = 2^(ca dx^2 + cb dx dy + cc dy^2)
     float alpha;              // sigmoid(opacity logit)
-    float radius;             // support radius, pixels
+    float hx;                 // half-extents of the box holding every pixel with a > alpha_floor:
     float col[6];             // amp_c * (cos phi_c, sin phi_c), c < 3
-    float pad;
+    float hy;                 //   sqrt(F cov_xx), sqrt(F cov_yy), F = 2 ln(alpha / floor); +inf without a floor
 };
 static_assert(sizeof(GRec) == 64, "GRec must stay 64 bytes");
 

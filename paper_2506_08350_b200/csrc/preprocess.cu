@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(256) k_preprocess(PreArgs a, PreOut o) {
     bool valid = false;
     double alpha = 0.0, radius = 0.0;
     double inv00 = 0.0, inv01 = 0.0, inv11 = 0.0;
+    double cov00_out = 0.0, cov11_out = 0.0;
     if (xc2 > a.near_clip) {
         p.xc = xc0;
         p.yc = xc1;
@@ -172,6 +173,8 @@ __global__ void __launch_bounds__(256) k_preprocess(PreArgs a, PreOut o) {
         double cov11 = (T[3] * M[3] + T[4] * M[4]) + T[5] * M[5];
         cov00 += a.dilation;
         cov11 += a.dilation;
+        cov00_out = cov00;
+        cov11_out = cov11;
         const double det = cov00 * cov11 - cov01 * cov01;
         if (det > 0.0 && isfinite(det)) {
             const double idet = 1.0 / det;
@@ -216,8 +219,15 @@ __global__ void __launch_bounds__(256) k_preprocess(PreArgs a, PreOut o) {
     r.cb = static_cast<float>(k * 2.0 * inv01);
     r.cc = static_cast<float>(k * inv11);
     r.alpha = static_cast<float>(alpha);
-    r.radius = static_cast<float>(radius);
-    r.pad = 0.0f;
+    // Accept region a = alpha g > floor is the ellipse d^T cov^-1 d < F, F = 2 ln(alpha/floor);
+    // its bounding box has half-widths sqrt(F cov_xx), sqrt(F cov_yy).  Slightly
+    // widened so fp32 evaluation at the boundary is never culled.
+    r.hx = r.hy = INFINITY;
+    if (valid && a.alpha_floor > 0.0) {
+        const double F = 2.0 * log(alpha / a.alpha_floor);
+        r.hx = static_cast<float>(sqrt(F * cov00_out) * 1.0001 + 1e-3);
+        r.hy = static_cast<float>(sqrt(F * cov11_out) * 1.0001 + 1e-3);
+    }
     for (int c = 0; c < 6; ++c) r.col[c] = 0.0f;
     if (valid) {
         for (int c = 0; c < 3; ++c) {

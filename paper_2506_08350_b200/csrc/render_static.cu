@@ -41,7 +41,7 @@ struct ColCfg {
     static constexpr int NT = H >= 1024 ? 512 : 256;
     static constexpr int kMinBlocks = H <= 1280 ? 2 : 1;  // 2 CTAs per SM while 64 registers suffice
     using B = Batch<H, NB, NT>;
-    static constexpr size_t kSmem = sizeof(cx<float>) * H * NB;
+    static constexpr size_t kSmem = sizeof(cx<float>) * B::kSmemElems;
 };
 
 // row pass: NBR rows of one channel per CTA
@@ -50,7 +50,7 @@ struct RowCfg {
     static constexpr int NBR = W <= 512 ? 4 : (W <= 2048 ? 2 : 1);
     static constexpr int NT = W >= 1024 ? 256 : 128;
     using B = Batch<W, NBR, NT>;
-    static constexpr size_t kSmem = sizeof(cx<float>) * W * NBR;
+    static constexpr size_t kSmem = sizeof(cx<float>) * B::kSmemElems;
 };
 
 __device__ __forceinline__ cx<float> czf() { return mk(0.0f, 0.0f); }
