@@ -338,6 +338,7 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     ca.num_buckets = static_cast<int>(B);
     ca.soft = st.soft_assignment;
     ca.write_lists = want_lists ? 1 : 0;
+    ca.pack_ok = N < (size_t{1} << 24) ? 1 : 0;
     ca.term_eps = static_cast<float>(st.term_eps);
     ca.alpha_floor = static_cast<float>(st.alpha_floor);
     ca.alpha_clamp = static_cast<float>(st.alpha_clamp);

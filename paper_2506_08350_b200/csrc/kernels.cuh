@@ -136,6 +136,7 @@ struct CompositeArgs {
     const double* rho;        // soft mode weights or null
     int L, C, W, H, tiles_x, num_tiles, plane_begin, num_buckets;
     int soft, write_lists;
+    int pack_ok;              // N < 2^24: a bucket slot fits under gidx in a 31-bit tie-break key
     float term_eps, alpha_floor, alpha_clamp;
     int floor_positive;
     cx<float>* layers;        // [planes][C][H][W], plane relative to plane_begin
