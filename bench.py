@@ -67,6 +67,26 @@ def stage_bytes(N, L, C, P, E, planes_local, sharded, has_holo):
     }
 
 
+STAGE_KERNEL = {"preprocess": "k_preprocess", "composite": "k_composite", "fft_pass1": "k_col_fwd",
+                "fft_pass2": "k_row_fused", "fft_pass3": "k_row_fused", "fft_pass4": "k_col_inv_epi"}
+
+
+def ncu_traffic(stage):
+    """dram read + write bytes per launch of the stage's kernel from the newest
+    committed ncu --set full summary (profiles/r*_kernels.csv), or None."""
+    import csv
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_kernels.csv")))
+    prefix = STAGE_KERNEL.get(stage)
+    if not files or not prefix:
+        return None
+    for row in csv.DictReader(open(files[-1])):
+        if row["kernel"].startswith(prefix):
+            return float(row["dram__bytes_read.sum"]) + float(row["dram__bytes_write.sum"])
+    return None
+
+
 # ------------------------------------------------------------------ clocks
 
 class ClockSampler:
@@ -273,7 +293,7 @@ def main():
     dom = max(stages, key=lambda k: stages[k]["ms"])
     d = stages[dom]
     roofline = {"bound": "hbm", "kernel": dom, "achieved": d["GBps"], "peak": hbm_peak, "unit": "GB/s",
-                "frac": d["GBps"] / hbm_peak, "traffic": None, "peak_kind": peak_kind,
+                "frac": d["GBps"] / hbm_peak, "traffic": ncu_traffic(dom), "traffic_source": "profiles (ncu --set full, per launch)", "peak_kind": peak_kind,
                 "frame_bytes": sum(sb.values()), "frame_frac": sum(sb.values()) / (ms_per_step * 1e-3) / 1e9 /
                 (hbm_peak * world)}
 

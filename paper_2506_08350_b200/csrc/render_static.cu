@@ -13,6 +13,8 @@
 // (modes SPEC / REPLAY of k_row_fused bracket the all-reduce of S).  The
 // identity FFT2(hologram) = S (the hologram is IFFT2(S)) removes the forward
 // transform of inverse_propagate.
+#include <cstdlib>
+
 #include "fft_static.cuh"
 #include "kernels.cuh"
 
@@ -34,24 +36,32 @@ template <> struct PlanOf<2048> { using type = Radices<16, 16, 8>; };
 template <> struct PlanOf<2160> { using type = Radices<16, 9, 15>; };
 template <> struct PlanOf<3840> { using type = Radices<16, 16, 15>; };
 
-// column passes: strips of 8 columns (64-byte row segments)
-template <int H>
-struct ColCfg {
-    static constexpr int NB = 8;
-    static constexpr int NT = H >= 1024 ? 512 : 256;
-    static constexpr int kMinBlocks = H <= 1280 ? 2 : 1;  // 2 CTAs per SM while 64 registers suffice
+// column passes: strips of NB columns, NT threads, MINB CTAs per SM (register cap)
+template <int H_, int NB_, int NT_, int MINB_>
+struct ColCfgT {
+    static constexpr int H = H_, NB = NB_, NT = NT_, kMinBlocks = MINB_;
     using B = Batch<H, NB, NT>;
     static constexpr size_t kSmem = sizeof(cx<float>) * B::kSmemElems;
 };
+// default: 8-column strips (64-byte row segments); 2 CTAs per SM while 64 registers suffice
+template <int H>
+using ColCfg = ColCfgT<H, 8, (H >= 1024 ? 512 : 256), (H <= 1280 ? 2 : 1)>;
 
 // row pass: NBR rows of one channel per CTA
-template <int W>
-struct RowCfg {
-    static constexpr int NBR = W <= 512 ? 4 : (W <= 2048 ? 2 : 1);
-    static constexpr int NT = W >= 1024 ? 256 : 128;
+template <int W_, int NBR_, int NT_, int MINB_>
+struct RowCfgT {
+    static constexpr int W = W_, NBR = NBR_, NT = NT_, kMinBlocks = MINB_;
     using B = Batch<W, NBR, NT>;
     static constexpr size_t kSmem = sizeof(cx<float>) * B::kSmemElems;
 };
+template <int W>
+using RowCfg = RowCfgT<W, (W <= 512 ? 4 : (W <= 2048 ? 2 : 1)), (W >= 1024 ? 256 : 128), 2>;
+
+// Shape variants for tuning at the C3 sizes (HOLO_COL_VARIANT / HOLO_ROW_VARIANT).
+int env_variant(const char* name) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : 0;
+}
 
 __device__ __forceinline__ cx<float> czf() { return mk(0.0f, 0.0f); }
 
@@ -68,10 +78,10 @@ __device__ __forceinline__ cx<float> phasor_reduced(float theta) {
 
 // ---------------------------------------------------------------- 1. column FFT (forward, in place)
 
-template <int H>
-__global__ void __launch_bounds__(ColCfg<H>::NT, ColCfg<H>::kMinBlocks) k_col_fwd(cx<float>* __restrict__ data, int W,
-                                                           const cx<float>* __restrict__ tw) {
-    using Cfg = ColCfg<H>;
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_col_fwd(cx<float>* __restrict__ data, int W,
+                                                                      const cx<float>* __restrict__ tw) {
+    constexpr int H = Cfg::H;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<float>* sm = reinterpret_cast<cx<float>*>(smem_raw);
     const int x0 = blockIdx.x * Cfg::NB;
@@ -89,14 +99,14 @@ __global__ void __launch_bounds__(ColCfg<H>::NT, ColCfg<H>::kMinBlocks) k_col_fw
 
 // ---------------------------------------------------------------- 2. row pass with the spectrum in registers
 
-template <int W, int MODE>
-__global__ void __launch_bounds__(RowCfg<W>::NT, 2) k_row_fused(
+template <class Cfg, int MODE>
+__global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
     const cx<float>* __restrict__ layers,  // [Lloc][C][H][W], column-transformed (FULL, SPEC)
     cx<float>* __restrict__ spec,          // [C][H][W]: written (SPEC) or read (REPLAY)
     cx<float>* __restrict__ out,           // [O][C][H][W] row-inverse-transformed outputs (FULL, REPLAY)
     int H, int C, int Lloc, int nout, const int* __restrict__ plane_of, const TfChan* __restrict__ tfc,
     const double* __restrict__ fx, const double* __restrict__ fy, const cx<float>* __restrict__ tw) {
-    using Cfg = RowCfg<W>;
+    constexpr int W = Cfg::W;
     using B = typename Cfg::B;
     using P = typename PlanOf<W>::type;
     using Pinv = typename RevPlan<P>::type;
@@ -194,13 +204,14 @@ __global__ void __launch_bounds__(RowCfg<W>::NT, 2) k_row_fused(
 
 // ---------------------------------------------------------------- 3. column IFFT + epilogue
 
-template <int H>
-__global__ void __launch_bounds__(ColCfg<H>::NT, ColCfg<H>::kMinBlocks) k_col_inv_epi(const cx<float>* __restrict__ in, int W, int C,
-                                                               int has_holo, float s, const cx<float>* __restrict__ tw,
-                                                               cx<float>* __restrict__ holo,
-                                                               cx<float>* __restrict__ replayed,
-                                                               float* __restrict__ intens) {
-    using Cfg = ColCfg<H>;
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_col_inv_epi(const cx<float>* __restrict__ in, int W,
+                                                                          int C, int has_holo, float s,
+                                                                          const cx<float>* __restrict__ tw,
+                                                                          cx<float>* __restrict__ holo,
+                                                                          cx<float>* __restrict__ replayed,
+                                                                          float* __restrict__ intens) {
+    constexpr int H = Cfg::H;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<float>* sm = reinterpret_cast<cx<float>*>(smem_raw);
     const int x0 = blockIdx.x * Cfg::NB;
@@ -235,52 +246,90 @@ void smem_attr(K kernel, size_t bytes) {
         HC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
 }
 
+template <class Cfg>
+void launch_col_fwd_cfg(holo_ctx* ctx, cx<float>* data, int W, int nfields) {
+    smem_attr(k_col_fwd<Cfg>, Cfg::kSmem);
+    const dim3 grid((W + Cfg::NB - 1) / Cfg::NB, nfields);
+    k_col_fwd<Cfg><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(data, W, ctx->twiddle<float>(Cfg::H));
+    HC_LAUNCHED(ctx);
+}
+
+template <class Cfg>
+void launch_col_inv_cfg(holo_ctx* ctx, const cx<float>* in, int W, int C, int nout, int has_holo, cx<float>* holo,
+                        cx<float>* rep, float* intens) {
+    smem_attr(k_col_inv_epi<Cfg>, Cfg::kSmem);
+    const dim3 grid((W + Cfg::NB - 1) / Cfg::NB, C, nout);
+    const float s = static_cast<float>(1.0 / (static_cast<double>(W) * Cfg::H));
+    k_col_inv_epi<Cfg><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(in, W, C, has_holo, s,
+                                                                   ctx->twiddle<float>(Cfg::H), holo, rep, intens);
+    HC_LAUNCHED(ctx);
+}
+
+template <class Cfg>
+void launch_row_cfg(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spec, cx<float>* out, int H, int C,
+                    int Lloc, int nout, const int* plane_of, const TfChan* tfc, const double* fx, const double* fy) {
+    const int rows = C * H;
+    const dim3 grid(rows / Cfg::NBR);
+    const cx<float>* tw = ctx->twiddle<float>(Cfg::W);
+    switch (mode) {
+        case kModeFull:
+            smem_attr(k_row_fused<Cfg, kModeFull>, Cfg::kSmem);
+            k_row_fused<Cfg, kModeFull><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(
+                layers, spec, out, H, C, Lloc, nout, plane_of, tfc, fx, fy, tw);
+            break;
+        case kModeSpec:
+            smem_attr(k_row_fused<Cfg, kModeSpec>, Cfg::kSmem);
+            k_row_fused<Cfg, kModeSpec><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(
+                layers, spec, out, H, C, Lloc, nout, plane_of, tfc, fx, fy, tw);
+            break;
+        default:
+            smem_attr(k_row_fused<Cfg, kModeReplay>, Cfg::kSmem);
+            k_row_fused<Cfg, kModeReplay><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(
+                layers, spec, out, H, C, Lloc, nout, plane_of, tfc, fx, fy, tw);
+            break;
+    }
+    HC_LAUNCHED(ctx);
+}
+
 template <int H>
 void launch_col_fwd(holo_ctx* ctx, cx<float>* data, int W, int nfields) {
-    using Cfg = ColCfg<H>;
-    smem_attr(k_col_fwd<H>, Cfg::kSmem);
-    const dim3 grid((W + Cfg::NB - 1) / Cfg::NB, nfields);
-    k_col_fwd<H><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(data, W, ctx->twiddle<float>(H));
-    HC_LAUNCHED(ctx);
+    if constexpr (H == 1080) {
+        switch (env_variant("HOLO_COL_VARIANT")) {
+            case 1: return launch_col_fwd_cfg<ColCfgT<H, 4, 256, 4>>(ctx, data, W, nfields);
+            case 2: return launch_col_fwd_cfg<ColCfgT<H, 16, 512, 1>>(ctx, data, W, nfields);
+            case 3: return launch_col_fwd_cfg<ColCfgT<H, 8, 256, 3>>(ctx, data, W, nfields);
+            default: break;
+        }
+    }
+    launch_col_fwd_cfg<ColCfg<H>>(ctx, data, W, nfields);
 }
 
 template <int H>
 void launch_col_inv(holo_ctx* ctx, const cx<float>* in, int W, int C, int nout, int has_holo, cx<float>* holo,
                     cx<float>* rep, float* intens) {
-    using Cfg = ColCfg<H>;
-    smem_attr(k_col_inv_epi<H>, Cfg::kSmem);
-    const dim3 grid((W + Cfg::NB - 1) / Cfg::NB, C, nout);
-    const float s = static_cast<float>(1.0 / (static_cast<double>(W) * H));
-    k_col_inv_epi<H><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(in, W, C, has_holo, s, ctx->twiddle<float>(H),
-                                                                 holo, rep, intens);
-    HC_LAUNCHED(ctx);
+    if constexpr (H == 1080) {
+        switch (env_variant("HOLO_COL_VARIANT")) {
+            case 1: return launch_col_inv_cfg<ColCfgT<H, 4, 256, 4>>(ctx, in, W, C, nout, has_holo, holo, rep, intens);
+            case 2: return launch_col_inv_cfg<ColCfgT<H, 16, 512, 1>>(ctx, in, W, C, nout, has_holo, holo, rep, intens);
+            case 3: return launch_col_inv_cfg<ColCfgT<H, 8, 256, 3>>(ctx, in, W, C, nout, has_holo, holo, rep, intens);
+            default: break;
+        }
+    }
+    launch_col_inv_cfg<ColCfg<H>>(ctx, in, W, C, nout, has_holo, holo, rep, intens);
 }
 
 template <int W>
 void launch_row(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spec, cx<float>* out, int H, int C,
                 int Lloc, int nout, const int* plane_of, const TfChan* tfc, const double* fx, const double* fy) {
-    using Cfg = RowCfg<W>;
-    const int rows = C * H;
-    const dim3 grid(rows / Cfg::NBR);
-    const cx<float>* tw = ctx->twiddle<float>(W);
-    switch (mode) {
-        case kModeFull:
-            smem_attr(k_row_fused<W, kModeFull>, Cfg::kSmem);
-            k_row_fused<W, kModeFull><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(layers, spec, out, H, C, Lloc, nout,
-                                                                                  plane_of, tfc, fx, fy, tw);
-            break;
-        case kModeSpec:
-            smem_attr(k_row_fused<W, kModeSpec>, Cfg::kSmem);
-            k_row_fused<W, kModeSpec><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(layers, spec, out, H, C, Lloc, nout,
-                                                                                  plane_of, tfc, fx, fy, tw);
-            break;
-        default:
-            smem_attr(k_row_fused<W, kModeReplay>, Cfg::kSmem);
-            k_row_fused<W, kModeReplay><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(
-                layers, spec, out, H, C, Lloc, nout, plane_of, tfc, fx, fy, tw);
-            break;
+    if constexpr (W == 1920) {
+        switch (env_variant("HOLO_ROW_VARIANT")) {
+            case 1: return launch_row_cfg<RowCfgT<W, 1, 128, 4>>(ctx, mode, layers, spec, out, H, C, Lloc, nout, plane_of, tfc, fx, fy);
+            case 2: return launch_row_cfg<RowCfgT<W, 4, 512, 1>>(ctx, mode, layers, spec, out, H, C, Lloc, nout, plane_of, tfc, fx, fy);
+            case 3: return launch_row_cfg<RowCfgT<W, 2, 256, 1>>(ctx, mode, layers, spec, out, H, C, Lloc, nout, plane_of, tfc, fx, fy);
+            default: break;
+        }
     }
-    HC_LAUNCHED(ctx);
+    launch_row_cfg<RowCfg<W>>(ctx, mode, layers, spec, out, H, C, Lloc, nout, plane_of, tfc, fx, fy);
 }
 
 #define HC_SIZES(X) X(48) X(64) X(128) X(256) X(512) X(1024) X(1080) X(1920) X(2048) X(2160) X(3840)
