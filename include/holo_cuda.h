@@ -1,7 +1,7 @@
 /* holo_cuda.h — C-ABI of libholo_cuda.so, the B200 (sm_100a) forward hologram renderer.
  *
  * This is the drop-in boundary for the reference's render path
- * (/root/reference/proj/include/holo/*.hpp).  Every entry point names the
+ * (the headers under /root/reference/proj/include/holo).  Every entry point names the
  * reference interface it replaces.  Plain C: POD structs, raw pointers and
  * sizes, int status codes, no C++ or torch types.  A context owns one CUDA
  * stream plus its scratch; calls enqueue on that stream.  A context is

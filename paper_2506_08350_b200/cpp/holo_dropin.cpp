@@ -1,0 +1,659 @@
+// libholo.so — the reference's render-path C++ API (proj/include/holo/*.hpp)
+// implemented over libholo_cuda's C-ABI (include/holo_cuda.h).
+//
+// Host-side pieces that are not compute (configuration, validation, camera
+// rotation, scene bookkeeping, HOLOFIELD I/O, the energy / dot_real reductions
+// the reference uses as test metrics, the analytic point-source field) are
+// plain C++ here; every transform, propagation, rasterisation and the render
+// itself run on the GPU.  There is no CPU fallback: without a CUDA device the
+// calls throw HoloError("cuda", ...).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <bit>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+
+#include "holo/camera.hpp"
+#include "holo/device.hpp"
+#include "holo/fft.hpp"
+#include "holo/field.hpp"
+#include "holo/field_io.hpp"
+#include "holo/pipeline.hpp"
+#include "holo/propagation.hpp"
+#include "holo/rasterizer.hpp"
+#include "holo/scene.hpp"
+#include "holo/wave_config.hpp"
+#include "holo_cuda.h"
+
+namespace holo {
+
+// ------------------------------------------------------------------ device plumbing
+
+namespace {
+
+thread_local int t_device = 0;
+thread_local bool t_f64 = true;
+
+void check(int rc) {
+    if (rc == HOLO_OK) return;
+    static const char* kinds[] = {"", "config", "io", "usage", "numeric", "cuda", "oom", "nccl"};
+    throw HoloError(rc > 0 && rc < 8 ? kinds[rc] : "numeric", holo_last_error());
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw HoloError("cuda", std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct CtxHolder {
+    holo_ctx* h = nullptr;
+    ~CtxHolder() {
+        if (h) holo_ctx_destroy(h);
+    }
+};
+
+holo_ctx* ctx() {
+    thread_local CtxHolder c;
+    if (!c.h) check(holo_ctx_create(t_device, &c.h));
+    return c.h;
+}
+
+cudaStream_t stream() { return static_cast<cudaStream_t>(holo_ctx_get_stream(ctx())); }
+
+struct DevMem {
+    void* p = nullptr;
+    explicit DevMem(size_t bytes) { cuda_check(cudaMalloc(&p, bytes ? bytes : 1), "cudaMalloc"); }
+    ~DevMem() { cudaFree(p); }
+    DevMem(const DevMem&) = delete;
+    DevMem& operator=(const DevMem&) = delete;
+};
+
+void h2d(void* d, const void* h, size_t n) {
+    cuda_check(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, stream()), "cudaMemcpyAsync H2D");
+}
+void d2h(void* h, const void* d, size_t n) {
+    cuda_check(cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, stream()), "cudaMemcpyAsync D2H");
+    cuda_check(cudaStreamSynchronize(stream()), "cudaStreamSynchronize");
+}
+
+holo_wave to_c(const WaveConfig& w) {
+    holo_wave c{};
+    c.nx = w.nx;
+    c.ny = w.ny;
+    c.pitch = w.pitch;
+    if (w.channels() > HOLO_MAX_CHANNELS) throw HoloError("config", "too many wavelength channels");
+    c.channels = w.channels();
+    for (int i = 0; i < c.channels; ++i) c.wavelengths[i] = w.wavelengths[i];
+    c.distance = w.distance;
+    c.volume_depth = w.volume_depth;
+    c.num_planes = w.num_planes;
+    return c;
+}
+
+holo_camera to_c(const CameraView& v) {
+    holo_camera c{};
+    for (int i = 0; i < 6; ++i) c.pose[i] = v.pose[i];
+    c.focal_px = v.focal_px;
+    c.cx = v.cx;
+    c.cy = v.cy;
+    c.width = v.width;
+    c.height = v.height;
+    return c;
+}
+
+holo_raster_settings to_c(const RenderSettings& s) {
+    return {s.near_clip, s.dilation,  s.plane_eps, s.term_eps, s.alpha_floor, s.alpha_clamp, s.radius_form_cap,
+            s.ste_tau,   s.soft_assignment ? 1 : 0, s.soft_tau, s.tile};
+}
+
+holo_prop_options to_c(const PropagationOptions& o) { return {o.pad2x ? 1 : 0, o.local_band_limit ? 1 : 0}; }
+
+int dtype() { return t_f64 ? HOLO_F64 : HOLO_F32; }
+
+// Upload a host complex<double> array in the operator precision.
+void upload_field(void* d, const c64* h, size_t n) {
+    if (t_f64) {
+        h2d(d, h, sizeof(c64) * n);
+        return;
+    }
+    std::vector<std::complex<float>> tmp(n);
+    for (size_t i = 0; i < n; ++i) tmp[i] = std::complex<float>(static_cast<float>(h[i].real()), static_cast<float>(h[i].imag()));
+    h2d(d, tmp.data(), sizeof(std::complex<float>) * n);
+    cuda_check(cudaStreamSynchronize(stream()), "cudaStreamSynchronize");
+}
+
+void download_field(c64* h, const void* d, size_t n) {
+    if (t_f64) {
+        d2h(h, d, sizeof(c64) * n);
+        return;
+    }
+    std::vector<std::complex<float>> tmp(n);
+    d2h(tmp.data(), d, sizeof(std::complex<float>) * n);
+    for (size_t i = 0; i < n; ++i) h[i] = c64(tmp[i].real(), tmp[i].imag());
+}
+
+size_t elem() { return t_f64 ? sizeof(c64) : sizeof(std::complex<float>); }
+
+}  // namespace
+
+namespace device {
+void set_device(int d) { t_device = d; }
+void set_operator_precision(bool use_f64) { t_f64 = use_f64; }
+bool operator_precision_f64() { return t_f64; }
+}  // namespace device
+
+// ------------------------------------------------------------------ wave_config (wave_config.cpp:5-30)
+
+void WaveConfig::validate() const {
+    if (nx <= 0 || ny <= 0) throw HoloError("config", "resolution must be positive");
+    if (pitch <= 0.0) throw HoloError("config", "pixel pitch must be positive");
+    if (wavelengths.empty()) throw HoloError("config", "at least one wavelength required");
+    if (std::any_of(wavelengths.begin(), wavelengths.end(), [](double l) { return l <= 0.0; }))
+        throw HoloError("config", "wavelengths must be positive");
+    if (distance <= 0.0) throw HoloError("config", "propagation distance must be positive");
+    if (volume_depth < 0.0) throw HoloError("config", "volume depth must be non-negative");
+    if (num_planes < 1) throw HoloError("config", "need at least one depth plane");
+    if (num_planes > 1 && volume_depth <= 0.0) throw HoloError("config", "multiple planes need a positive volume depth");
+}
+
+std::vector<double> plane_positions(const WaveConfig& cfg) {
+    cfg.validate();
+    const int L = cfg.num_planes;
+    if (L == 1) return {cfg.distance};
+    const double dz = cfg.volume_depth / (L - 1);
+    const double z0 = cfg.distance - 0.5 * (L - 1) * dz;
+    std::vector<double> z(L);
+    for (int l = 0; l < L; ++l) z[l] = z0 + l * dz;
+    return z;
+}
+
+// ------------------------------------------------------------------ field (field.cpp)
+
+IntensityImage intensity(const ComplexField& u) {
+    IntensityImage out(u.w, u.h, u.c);
+    const size_t n = u.data.size();
+    if (n == 0) return out;
+    DevMem din(sizeof(c64) * n), dout(sizeof(double) * n);
+    h2d(din.p, u.data.data(), sizeof(c64) * n);
+    check(holo_intensity(ctx(), din.p, dout.p, n, HOLO_F64));
+    d2h(out.data.data(), dout.p, sizeof(double) * n);
+    return out;
+}
+
+double energy_channel(const ComplexField& u, int ch) {
+    std::vector<double> rows(u.h, 0.0);
+    const c64* base = u.channel(ch);
+    for (int y = 0; y < u.h; ++y) {
+        double s = 0.0;
+        for (int x = 0; x < u.w; ++x) {
+            const c64 v = base[static_cast<size_t>(y) * u.w + x];
+            s += v.real() * v.real() + v.imag() * v.imag();
+        }
+        rows[y] = s;
+    }
+    return fold_partials(rows);
+}
+
+double energy(const ComplexField& u) {
+    double s = 0.0;
+    for (int ch = 0; ch < u.c; ++ch) s += energy_channel(u, ch);
+    return s;
+}
+
+double dot_real(const ComplexField& a, const ComplexField& b) {
+    if (!a.same_shape(b)) throw HoloError("numeric", "dot_real: shape mismatch");
+    std::vector<double> rows(static_cast<size_t>(a.h) * a.c, 0.0);
+    for (int ch = 0; ch < a.c; ++ch)
+        for (int y = 0; y < a.h; ++y) {
+            double s = 0.0;
+            const c64* ra = a.channel(ch) + static_cast<size_t>(y) * a.w;
+            const c64* rb = b.channel(ch) + static_cast<size_t>(y) * a.w;
+            for (int x = 0; x < a.w; ++x) s += ra[x].real() * rb[x].real() + ra[x].imag() * rb[x].imag();
+            rows[static_cast<size_t>(ch) * a.h + y] = s;
+        }
+    return fold_partials(rows);
+}
+
+// ------------------------------------------------------------------ fft (fft.cpp:33-44)
+
+static void fft2_dir(c64* data, int w, int h, int inverse) {
+    if (w <= 0 || h <= 0) throw HoloError("numeric", "fft2: dimensions must be positive");
+    const size_t n = static_cast<size_t>(w) * h;
+    DevMem d(sizeof(c64) * n);
+    h2d(d.p, data, sizeof(c64) * n);
+    check(holo_fft2(ctx(), d.p, w, h, 1, inverse, HOLO_F64));
+    d2h(data, d.p, sizeof(c64) * n);
+}
+
+void fft2(c64* data, int w, int h) { fft2_dir(data, w, h, 0); }
+void ifft2(c64* data, int w, int h) { fft2_dir(data, w, h, 1); }
+
+// ------------------------------------------------------------------ propagation (propagation.cpp:86-167)
+
+TransferFunction transfer_function(const WaveConfig& cfg, double z, const PropagationOptions& opt) {
+    cfg.validate();
+    TransferFunction tf;
+    tf.w = opt.pad2x ? 2 * cfg.nx : cfg.nx;
+    tf.h = opt.pad2x ? 2 * cfg.ny : cfg.ny;
+    tf.c = cfg.channels();
+    tf.z = z;
+    tf.hz.resize(static_cast<size_t>(tf.w) * tf.h * tf.c);
+    DevMem d(sizeof(c64) * tf.hz.size());
+    const holo_wave w = to_c(cfg);
+    const holo_prop_options po = to_c(opt);
+    check(holo_transfer_function(ctx(), &w, z, &po, d.p, HOLO_F64));
+    d2h(tf.hz.data(), d.p, sizeof(c64) * tf.hz.size());
+    return tf;
+}
+
+ComplexField propagate(const ComplexField& u, const WaveConfig& cfg, double z, const PropagationOptions& opt) {
+    if (u.w != cfg.nx || u.h != cfg.ny || u.c != cfg.channels())
+        throw HoloError("config", "propagate: field does not match the configured grid");
+    ComplexField out(u.w, u.h, u.c, u.pitch);
+    const size_t n = u.data.size();
+    DevMem din(elem() * n), dout(elem() * n);
+    upload_field(din.p, u.data.data(), n);
+    const holo_wave w = to_c(cfg);
+    const holo_prop_options po = to_c(opt);
+    check(holo_propagate(ctx(), din.p, dout.p, u.w, u.h, u.c, &w, z, &po, dtype()));
+    download_field(out.data.data(), dout.p, n);
+    return out;
+}
+
+ComplexField forward_record(const std::vector<ComplexField>& layers, const WaveConfig& cfg,
+                            const PropagationOptions& opt) {
+    const std::vector<double> zs = plane_positions(cfg);
+    if (layers.size() != zs.size())
+        throw HoloError("config", "forward_record: layer count does not match num_planes");
+    for (const ComplexField& l : layers)
+        if (l.w != cfg.nx || l.h != cfg.ny || l.c != cfg.channels())
+            throw HoloError("config", "propagate: field does not match the configured grid");
+    const size_t n = static_cast<size_t>(cfg.nx) * cfg.ny * cfg.channels();
+    DevMem dl(elem() * n * layers.size()), dh(elem() * n);
+    for (size_t l = 0; l < layers.size(); ++l)
+        upload_field(static_cast<char*>(dl.p) + elem() * n * l, layers[l].data.data(), n);
+    const holo_wave w = to_c(cfg);
+    const holo_prop_options po = to_c(opt);
+    check(holo_forward_record(ctx(), dl.p, static_cast<int>(layers.size()), dh.p, &w, &po, dtype()));
+    ComplexField out(cfg.nx, cfg.ny, cfg.channels(), cfg.pitch);
+    download_field(out.data.data(), dh.p, n);
+    return out;
+}
+
+std::vector<ComplexField> inverse_propagate(const ComplexField& hologram, const WaveConfig& cfg,
+                                            const PropagationOptions& opt) {
+    const std::vector<double> zs = plane_positions(cfg);
+    if (hologram.w != cfg.nx || hologram.h != cfg.ny || hologram.c != cfg.channels())
+        throw HoloError("config", "propagate: field does not match the configured grid");
+    const size_t n = hologram.data.size();
+    DevMem dh(elem() * n), dr(elem() * n * zs.size());
+    upload_field(dh.p, hologram.data.data(), n);
+    const holo_wave w = to_c(cfg);
+    const holo_prop_options po = to_c(opt);
+    check(holo_inverse_propagate(ctx(), dh.p, dr.p, &w, &po, dtype()));
+    std::vector<ComplexField> out;
+    out.reserve(zs.size());
+    for (size_t l = 0; l < zs.size(); ++l) {
+        ComplexField f(cfg.nx, cfg.ny, cfg.channels(), cfg.pitch);
+        download_field(f.data.data(), static_cast<const char*>(dr.p) + elem() * n * l, n);
+        out.push_back(std::move(f));
+    }
+    return out;
+}
+
+double point_phase_exact(double lambda, double dx, double dy, double z) {
+    return wrap_phase(kTwoPi * std::sqrt(dx * dx + dy * dy + z * z) / lambda);
+}
+
+double point_phase_paraxial(double lambda, double dx, double dy, double z) {
+    return wrap_phase(kTwoPi * (z + (dx * dx + dy * dy) / (2.0 * z)) / lambda);
+}
+
+// Analytic spherical-wave field on the hologram grid (propagation.cpp:135-167); a
+// validation oracle in the reference, evaluated directly here.
+ComplexField point_source_field(const WaveConfig& cfg, const std::vector<PointSource>& sources,
+                                const PointSourceOptions& opt) {
+    cfg.validate();
+    for (const PointSource& s : sources) {
+        if (s.z <= 0.0) throw HoloError("config", "point sources must sit in front of the hologram plane");
+        if (s.amps.size() != 1 && s.amps.size() != static_cast<size_t>(cfg.channels()))
+            throw HoloError("config", "point source amplitude count must be 1 or match the channels");
+    }
+    const double ox = opt.cx >= 0.0 ? opt.cx : cfg.nx / 2.0;
+    const double oy = opt.cy >= 0.0 ? opt.cy : cfg.ny / 2.0;
+    ComplexField out(cfg.nx, cfg.ny, cfg.channels(), cfg.pitch);
+    for (int ch = 0; ch < cfg.channels(); ++ch) {
+        const double lambda = cfg.wavelengths[ch];
+        for (const PointSource& s : sources) {
+            const double amp = s.amps.size() == 1 ? s.amps[0] : s.amps[ch];
+            for (int y = 0; y < cfg.ny; ++y) {
+                const double py = ((y + 0.5) - oy) * cfg.pitch - s.y;
+                for (int x = 0; x < cfg.nx; ++x) {
+                    const double px = ((x + 0.5) - ox) * cfg.pitch - s.x;
+                    const double phi = s.phase0 + (opt.paraxial ? point_phase_paraxial(lambda, px, py, s.z)
+                                                                : point_phase_exact(lambda, px, py, s.z));
+                    const double a = opt.inverse_r ? amp / std::sqrt(px * px + py * py + s.z * s.z) : amp;
+                    out.at(ch, y, x) += c64(a * std::cos(phi), a * std::sin(phi));
+                }
+            }
+        }
+    }
+    return out;
+}
+
+// ------------------------------------------------------------------ camera (camera.cpp)
+
+Mat3 Mat3::transpose() const {
+    Mat3 t;
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) t(c, r) = (*this)(r, c);
+    return t;
+}
+
+Mat3 Mat3::operator*(const Mat3& o) const {
+    Mat3 t;
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) t(r, c) = ((*this)(r, 0) * o(0, c) + (*this)(r, 1) * o(1, c)) + (*this)(r, 2) * o(2, c);
+    return t;
+}
+
+Vec3 Mat3::operator*(const Vec3& x) const {
+    Vec3 y;
+    for (int r = 0; r < 3; ++r) y[r] = ((*this)(r, 0) * x[0] + (*this)(r, 1) * x[1]) + (*this)(r, 2) * x[2];
+    return y;
+}
+
+Mat3 CameraView::rot_cam_to_world() const {
+    const double ca = std::cos(pose[3]), sa = std::sin(pose[3]);
+    const double cb = std::cos(pose[4]), sb = std::sin(pose[4]);
+    const double cg = std::cos(pose[5]), sg = std::sin(pose[5]);
+    Mat3 rx, ry, rz;
+    rx.m[0] = 1; rx.m[4] = ca; rx.m[5] = -sa; rx.m[7] = sa; rx.m[8] = ca;
+    ry.m[0] = cb; ry.m[2] = sb; ry.m[4] = 1; ry.m[6] = -sb; ry.m[8] = cb;
+    rz.m[0] = cg; rz.m[1] = -sg; rz.m[3] = sg; rz.m[4] = cg; rz.m[8] = 1;
+    return (rz * ry) * rx;
+}
+
+Mat3 CameraView::rot_world_to_cam() const { return rot_cam_to_world().transpose(); }
+
+Vec3 CameraView::world_to_camera(const Vec3& p) const {
+    return rot_world_to_cam() * Vec3(p[0] - pose[0], p[1] - pose[1], p[2] - pose[2]);
+}
+
+void CameraView::validate() const {
+    if (width <= 0 || height <= 0) throw HoloError("config", "camera resolution must be positive");
+    if (focal_px <= 0.0) throw HoloError("config", "focal length must be positive");
+    for (double v : pose)
+        if (!std::isfinite(v)) throw HoloError("config", "camera pose must be finite");
+}
+
+// ------------------------------------------------------------------ scene (scene.cpp)
+
+void GaussianScene::resize(size_t n) {
+    positions.assign(n * 3, 0.0);
+    rotations.assign(n * 4, 0.0);
+    for (size_t i = 0; i < n; ++i) rotations[i * 4] = 1.0;
+    log_scales.assign(n * 3, 0.0);
+    amplitudes.assign(n * 3, 0.0);
+    opacity_logits.assign(n, 0.0);
+    phases.assign(n * 3, 0.0);
+    plane_logits.assign(n * static_cast<size_t>(num_planes), 0.0);
+}
+
+static double quat_norm(const double* q) { return std::sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]); }
+
+void GaussianScene::validate() const {
+    const size_t n = size();
+    if (num_planes < 1) throw HoloError("config", "scene needs at least one plane");
+    if (positions.size() != n * 3 || rotations.size() != n * 4 || log_scales.size() != n * 3 ||
+        amplitudes.size() != n * 3 || phases.size() != n * 3 || plane_logits.size() != n * static_cast<size_t>(num_planes))
+        throw HoloError("config", "scene arrays have inconsistent sizes");
+    for (size_t i = 0; i < n; ++i)
+        if (!(quat_norm(&rotations[i * 4]) > 1e-8)) throw HoloError("config", "degenerate quaternion in scene");
+    for (double a : amplitudes)
+        if (a < 0.0) throw HoloError("config", "amplitudes must be non-negative");
+}
+
+void GaussianScene::renormalize() {
+    for (size_t i = 0; i < size(); ++i) {
+        double* q = &rotations[i * 4];
+        const double nq = quat_norm(q);
+        if (nq > 1e-12) {
+            for (int k = 0; k < 4; ++k) q[k] /= nq;
+        } else {
+            q[0] = 1.0;
+            q[1] = q[2] = q[3] = 0.0;
+        }
+    }
+    for (double& a : amplitudes) a = std::max(a, 0.0);
+}
+
+namespace detail {
+Mat3 quat_to_rot(const double* q) {
+    const double n = quat_norm(q);
+    const double w = q[0] / n, x = q[1] / n, y = q[2] / n, z = q[3] / n;
+    Mat3 r;
+    r.m[0] = 1 - 2 * (y * y + z * z); r.m[1] = 2 * (x * y - w * z);     r.m[2] = 2 * (x * z + w * y);
+    r.m[3] = 2 * (x * y + w * z);     r.m[4] = 1 - 2 * (x * x + z * z); r.m[5] = 2 * (y * z - w * x);
+    r.m[6] = 2 * (x * z - w * y);     r.m[7] = 2 * (y * z + w * x);     r.m[8] = 1 - 2 * (x * x + y * y);
+    return r;
+}
+}  // namespace detail
+
+Mat3 covariance_3d(const double* quat, const double* log_scales) {
+    const Mat3 R = detail::quat_to_rot(quat);
+    Mat3 M = R;
+    for (int k = 0; k < 3; ++k) {
+        const double e = std::exp(log_scales[k]);
+        for (int r = 0; r < 3; ++r) M(r, k) = R(r, k) * e;
+    }
+    return M * M.transpose();
+}
+
+SteAssign ste_assign(const double* logits, int L, double tau) {
+    if (L < 1) throw HoloError("config", "ste_assign needs at least one plane");
+    if (tau <= 0.0) throw HoloError("config", "ste temperature must be positive");
+    SteAssign a;
+    a.onehot.assign(L, 0.0);
+    a.backward_weights.assign(L, 0.0);
+    for (int l = 1; l < L; ++l)
+        if (logits[l] > logits[a.index]) a.index = l;
+    a.onehot[a.index] = 1.0;
+    double denom = 0.0;
+    for (int l = 0; l < L; ++l) denom += (a.backward_weights[l] = std::exp((logits[l] - logits[a.index]) / tau));
+    for (double& v : a.backward_weights) v /= denom;
+    return a;
+}
+
+// ------------------------------------------------------------------ rasterizer + pipeline (GPU)
+
+namespace {
+
+holo_scene_arrays scene_arrays(const GaussianScene& s) {
+    return {s.size(),          s.num_planes,          s.positions.data(), s.rotations.data(),
+            s.log_scales.data(), s.amplitudes.data(), s.opacity_logits.data(), s.phases.data(),
+            s.plane_logits.data()};
+}
+
+void check_raster_inputs(const GaussianScene& scene, const CameraView& cam, const WaveConfig& cfg) {
+    scene.validate();
+    cam.validate();
+    cfg.validate();
+    if (scene.num_planes != cfg.num_planes) throw HoloError("config", "scene plane count does not match the wave config");
+    if (cam.width != cfg.nx || cam.height != cfg.ny)
+        throw HoloError("config", "camera resolution must match the hologram grid");
+}
+
+template <class T>
+std::vector<T> download_buf(int which) {
+    void* d = nullptr;
+    size_t bytes = 0;
+    check(holo_frame_buffer(ctx(), which, &d, &bytes));
+    std::vector<T> h(bytes / sizeof(T));
+    if (bytes) d2h(h.data(), d, bytes);
+    return h;
+}
+
+RasterForward collect_raster(const GaussianScene& scene, const WaveConfig& cfg, int C, const holo_frame_info& info) {
+    RasterForward r;
+    const int L = cfg.num_planes, W = cfg.nx, H = cfg.ny;
+    const size_t P = static_cast<size_t>(W) * H, N = scene.size();
+    r.tiles_x = info.tiles_x;
+    r.tiles_y = info.tiles_y;
+    const std::vector<std::complex<float>> lay = download_buf<std::complex<float>>(HOLO_BUF_LAYERS);
+    for (int l = 0; l < L; ++l) {
+        ComplexField f(W, H, GaussianScene::kChannels, cfg.pitch);
+        for (int c = 0; c < C; ++c)
+            for (size_t i = 0; i < P; ++i) {
+                const std::complex<float> v = lay[(static_cast<size_t>(l) * C + c) * P + i];
+                f.data[static_cast<size_t>(c) * P + i] = c64(v.real(), v.imag());
+            }
+        r.layers.push_back(std::move(f));
+    }
+    const std::vector<float> tf = download_buf<float>(HOLO_BUF_T_FINAL);
+    r.t_final.assign(tf.begin(), tf.begin() + static_cast<long>(L * P));
+    r.n_contrib = download_buf<std::int32_t>(HOLO_BUF_N_CONTRIB);
+    r.n_contrib.resize(L * P);
+    const std::vector<holo_projected> proj = download_buf<holo_projected>(HOLO_BUF_PROJECTED);
+    r.projected.resize(N);
+    for (size_t i = 0; i < N; ++i) {
+        const holo_projected& q = proj[i];
+        detail::Projected& p = r.projected[i];
+        p.valid = q.valid != 0;
+        p.n = q.n;
+        p.mu_x = q.mu_x;
+        p.mu_y = q.mu_y;
+        p.inv00 = q.inv00;
+        p.inv01 = q.inv01;
+        p.inv11 = q.inv11;
+        p.radius = q.radius;
+        p.xc = q.xc;
+        p.yc = q.yc;
+        p.zc = q.zc;
+        p.alpha_sig = q.alpha_sig;
+        for (int c = 0; c < 3; ++c) {
+            p.amp[c] = q.amp[c];
+            p.phase[c] = q.phase[c];
+        }
+        p.plane = q.plane;
+    }
+    r.rho = download_buf<double>(HOLO_BUF_RHO);
+    r.rho.resize(N * L);
+    r.touched = download_buf<std::uint8_t>(HOLO_BUF_TOUCHED);
+    r.touched.resize(N);
+    r.bucket_start = download_buf<std::uint32_t>(HOLO_BUF_BUCKET_START);
+    const size_t B = static_cast<size_t>(L) * info.tiles_x * info.tiles_y;
+    r.bucket_start.resize(B + 1);
+    const size_t E = info.num_entries;
+    std::vector<std::int32_t> gidx = download_buf<std::int32_t>(HOLO_BUF_ENTRY_GIDX);
+    std::vector<double> depth = download_buf<double>(HOLO_BUF_ENTRY_DEPTH);
+    r.entries.resize(E);
+    for (size_t b = 0; b < B; ++b)
+        for (std::uint32_t e = r.bucket_start[b]; e < r.bucket_start[b + 1]; ++e)
+            r.entries[e] = detail::Entry{static_cast<std::int32_t>(b), gidx[e], depth[e]};
+    return r;
+}
+
+constexpr unsigned kRasterOutputs = HOLO_OUT_LAYERS | HOLO_OUT_AUX | HOLO_OUT_LISTS | HOLO_OUT_PROJECTED;
+
+}  // namespace
+
+// rasterizer.cpp:139-263: always 3 channels of layers, like the reference
+RasterForward raster_forward(const GaussianScene& scene, const CameraView& cam, const WaveConfig& cfg,
+                             const RenderSettings& settings) {
+    check_raster_inputs(scene, cam, cfg);
+    const holo_scene_arrays sa = scene_arrays(scene);
+    check(holo_scene_upload(ctx(), &sa));
+    holo_wave w = to_c(cfg);
+    w.channels = GaussianScene::kChannels;  // the rasteriser ignores wavelengths; it emits every scene channel
+    for (int c = cfg.channels(); c < w.channels; ++c) w.wavelengths[c] = cfg.wavelengths.back();
+    const holo_camera c = to_c(cam);
+    const holo_raster_settings st = to_c(settings);
+    const holo_prop_options po{0, 0};
+    holo_frame_info info{};
+    check(holo_render(ctx(), &c, &w, &st, &po, kRasterOutputs, &info));
+    return collect_raster(scene, cfg, GaussianScene::kChannels, info);
+}
+
+// pipeline.cpp:20-29
+PipelineForward pipeline_forward(const GaussianScene& scene, const CameraView& cam, const WaveConfig& cfg,
+                                 const PipelineOptions& opt) {
+    check_raster_inputs(scene, cam, cfg);
+    if (cfg.channels() != GaussianScene::kChannels)  // propagate's channel check (propagation.cpp:94-95)
+        throw HoloError("config", "propagate: field does not match the configured grid");
+    const holo_scene_arrays sa = scene_arrays(scene);
+    check(holo_scene_upload(ctx(), &sa));
+    const holo_wave w = to_c(cfg);
+    const holo_camera c = to_c(cam);
+    const holo_raster_settings st = to_c(opt.raster);
+    const holo_prop_options po = to_c(opt.prop);
+    holo_frame_info info{};
+    check(holo_render(ctx(), &c, &w, &st, &po,
+                      kRasterOutputs | HOLO_OUT_HOLOGRAM | HOLO_OUT_REPLAYED | HOLO_OUT_INTENSITY, &info));
+    PipelineForward f;
+    const int L = cfg.num_planes, C = cfg.channels();
+    const size_t n = static_cast<size_t>(cfg.nx) * cfg.ny * C;
+    f.raster = collect_raster(scene, cfg, C, info);
+    const std::vector<std::complex<float>> holo = download_buf<std::complex<float>>(HOLO_BUF_HOLOGRAM);
+    const std::vector<std::complex<float>> rep = download_buf<std::complex<float>>(HOLO_BUF_REPLAYED);
+    const std::vector<float> ints = download_buf<float>(HOLO_BUF_INTENSITY);
+    f.hologram = ComplexField(cfg.nx, cfg.ny, C, cfg.pitch);
+    for (size_t i = 0; i < n; ++i) f.hologram.data[i] = c64(holo[i].real(), holo[i].imag());
+    for (int l = 0; l < L; ++l) {
+        ComplexField r(cfg.nx, cfg.ny, C, cfg.pitch);
+        IntensityImage im(cfg.nx, cfg.ny, C);
+        for (size_t i = 0; i < n; ++i) {
+            const std::complex<float> v = rep[static_cast<size_t>(l) * n + i];
+            r.data[i] = c64(v.real(), v.imag());
+            im.data[i] = ints[static_cast<size_t>(l) * n + i];
+        }
+        f.replayed.push_back(std::move(r));
+        f.intensities.push_back(std::move(im));
+    }
+    return f;
+}
+
+// ------------------------------------------------------------------ HOLOFIELD I/O (field_io.cpp)
+
+namespace {
+constexpr char kFieldMagic[16] = {'H', 'O', 'L', 'O', 'F', 'I', 'E', 'L', 'D', 0, 0, 0, 0, 0, 0, 0};
+struct FileCloser {
+    void operator()(std::FILE* f) const {
+        if (f) std::fclose(f);
+    }
+};
+using File = std::unique_ptr<std::FILE, FileCloser>;
+static_assert(std::endian::native == std::endian::little, "HOLOFIELD is little endian");
+}  // namespace
+
+void write_field(const std::string& path, const ComplexField& f) {
+    if (f.w <= 0 || f.h <= 0 || f.c <= 0) throw HoloError("io", "write_field: empty field");
+    File fp(std::fopen(path.c_str(), "wb"));
+    if (!fp) throw HoloError("io", "cannot open for writing: " + path);
+    const std::uint32_t dims[3] = {static_cast<std::uint32_t>(f.w), static_cast<std::uint32_t>(f.h),
+                                   static_cast<std::uint32_t>(f.c)};
+    if (std::fwrite(kFieldMagic, 1, 16, fp.get()) != 16 || std::fwrite(dims, 4, 3, fp.get()) != 3 ||
+        std::fwrite(f.data.data(), sizeof(c64), f.data.size(), fp.get()) != f.data.size() ||
+        std::fflush(fp.get()) != 0)
+        throw HoloError("io", "short write: " + path);
+}
+
+ComplexField read_field(const std::string& path, double pitch) {
+    File fp(std::fopen(path.c_str(), "rb"));
+    if (!fp) throw HoloError("io", "cannot open: " + path);
+    char magic[16];
+    if (std::fread(magic, 1, 16, fp.get()) != 16) throw HoloError("io", "truncated header: " + path);
+    if (std::memcmp(magic, kFieldMagic, 16) != 0) throw HoloError("io", "bad magic, not a HOLOFIELD file: " + path);
+    std::uint32_t dims[3];
+    if (std::fread(dims, 4, 3, fp.get()) != 3) throw HoloError("io", "truncated header: " + path);
+    if (dims[0] == 0 || dims[1] == 0 || dims[2] == 0 || dims[2] > 64)
+        throw HoloError("io", "implausible dimensions in " + path);
+    const size_t n = static_cast<size_t>(dims[0]) * dims[1] * dims[2];
+    if (n > (1ull << 28)) throw HoloError("io", "field too large in " + path);
+    ComplexField f(static_cast<int>(dims[0]), static_cast<int>(dims[1]), static_cast<int>(dims[2]), pitch);
+    if (std::fread(f.data.data(), sizeof(c64), n, fp.get()) != n) throw HoloError("io", "truncated payload: " + path);
+    return f;
+}
+
+}  // namespace holo

@@ -1,0 +1,37 @@
+"""The C++ drop-in (include/holo/*.hpp -> libholo.so -> libholo_cuda.so).
+
+GPU: runs tests/cpp/test_dropin.cpp and -- compiled against the drop-in headers
+by paper_2506_08350_b200/cpp/Makefile where /root/reference exists -- the
+reference's OWN unit tests test_field.cpp and test_propagation.cpp, unmodified,
+at the reference's tolerances (f64 operators on the GPU).
+CPU: libholo.so exports the reference API symbols."""
+import os
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+LIB = os.path.join(ROOT, "paper_2506_08350_b200", "lib")
+
+
+def test_libholo_exports_reference_api():
+    so = os.path.join(LIB, "libholo.so")
+    assert os.path.exists(so), "build with __graft_entry__.build()"
+    syms = subprocess.run(["nm", "-DC", "--defined-only", so], capture_output=True, text=True).stdout
+    for name in ("holo::pipeline_forward(", "holo::raster_forward(", "holo::propagate(", "holo::forward_record(",
+                 "holo::inverse_propagate(", "holo::transfer_function(", "holo::fft2(", "holo::ifft2(",
+                 "holo::intensity(", "holo::plane_positions(", "holo::read_field(", "holo::write_field("):
+        assert name in syms, name
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("binary", ["test_dropin", "ref_test_field", "ref_test_propagation"])
+def test_cpp_suite(binary, tmp_path):
+    path = os.path.join(LIB, binary)
+    if not os.path.exists(path):
+        pytest.skip(f"{binary} not built (needs /root/reference at build time)")
+    r = subprocess.run([path], capture_output=True, text=True, cwd=tmp_path, timeout=600)
+    print(r.stdout[-2000:], r.stderr[-4000:])
+    assert r.returncode == 0, r.stderr[-4000:]
+    assert "failed: 0;" in r.stdout
