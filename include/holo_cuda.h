@@ -167,6 +167,19 @@ int holo_ctx_stage_times(holo_ctx* ctx, double* ms_out, int* launches_out, int m
 int holo_ctx_reset_timing(holo_ctx* ctx);
 /* Kernel launches issued by this context since creation. */
 uint64_t holo_ctx_launch_count(holo_ctx* ctx);
+/* Asynchronous frames.  By default a render makes one host round trip (entry
+ * count + scene validation) and returns with its outputs complete, like the
+ * reference.  With async enabled a render only enqueues work: the entry buffers
+ * hold the reserved capacity (holo_ctx_reserve_entries, or 1.25x the largest
+ * synchronous frame so far), the frame info is filled by holo_ctx_frame_status,
+ * and validation failures / capacity overflow are reported there (HOLO_ERR_CONFIG /
+ * HOLO_ERR_NUMERIC) for every frame since the previous status call.  Renders on
+ * one context are stream-ordered; several contexts on separate streams overlap. */
+int holo_ctx_set_async(holo_ctx* ctx, int enable);
+int holo_ctx_reserve_entries(holo_ctx* ctx, uint64_t entries);
+/* Waits for the context's frames, reports the last frame's info and any error
+ * flag raised since the previous call (then clears the flags). */
+int holo_ctx_frame_status(holo_ctx* ctx, holo_frame_info* info);
 
 /* ---- scene (GaussianScene, scene.hpp:18-37; validated like GaussianScene::validate, scene.cpp:19-32) ---- */
 /* Copies host arrays to the device (H2D on the context stream). */

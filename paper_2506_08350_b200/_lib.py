@@ -107,6 +107,9 @@ def lib() -> C.CDLL:
         "holo_ctx_stage_times": (i, [vp, P(d), P(i), i]),
         "holo_ctx_reset_timing": (i, [vp]),
         "holo_ctx_launch_count": (C.c_uint64, [vp]),
+        "holo_ctx_set_async": (i, [vp, i]),
+        "holo_ctx_reserve_entries": (i, [vp, C.c_uint64]),
+        "holo_ctx_frame_status": (i, [vp, P(FrameInfo)]),
         "holo_scene_upload": (i, [vp, P(SceneArrays)]),
         "holo_scene_upload_device": (i, [vp, P(SceneArrays)]),
         "holo_render": (i, [vp, P(Camera), P(Wave), P(RasterSettings), P(PropOptions), u, P(FrameInfo)]),

@@ -141,6 +141,18 @@ class Context:
     def launch_count(self) -> int:
         return int(self.lib.holo_ctx_launch_count(self.h))
 
+    def set_async(self, on: bool = True) -> None:
+        """Asynchronous frames: render() only enqueues; frame_status() reports (holo_cuda.h)."""
+        L.check(self.lib.holo_ctx_set_async(self.h, int(on)))
+
+    def reserve_entries(self, n: int) -> None:
+        L.check(self.lib.holo_ctx_reserve_entries(self.h, int(n)))
+
+    def frame_status(self) -> L.FrameInfo:
+        """Wait for this context's frames; raise on flags raised since the last call."""
+        L.check(self.lib.holo_ctx_frame_status(self.h, C.byref(self.info)))
+        return self.info
+
     def enable_timing(self, on: bool = True) -> None:
         L.check(self.lib.holo_ctx_enable_timing(self.h, int(on)))
 

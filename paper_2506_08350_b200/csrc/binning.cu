@@ -127,6 +127,11 @@ __device__ __forceinline__ void for_each_bucket(const PreOut& pre, size_t i, int
     }
 }
 
+// (key, gidx) lexicographic order; zc > near > 0, so the IEEE bits of zc order like zc.
+__device__ __forceinline__ bool less_kg(unsigned long long ka, int ga, unsigned long long kb, int gb) {
+    return ka < kb || (ka == kb && ga < gb);
+}
+
 __global__ void __launch_bounds__(256) k_bucket_count(PreOut pre, size_t N, int L, int pb, int pe, int tiles_x,
                                                       int num_tiles, int soft, unsigned* __restrict__ bcount) {
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
@@ -137,65 +142,88 @@ __global__ void __launch_bounds__(256) k_bucket_count(PreOut pre, size_t N, int 
 __global__ void __launch_bounds__(256) k_bucket_emit(PreOut pre, size_t N, int L, int pb, int pe, int tiles_x,
                                                      int num_tiles, int soft, const unsigned* __restrict__ bstart,
                                                      unsigned* __restrict__ cursor,
-                                                     unsigned long long* __restrict__ ekey, int* __restrict__ egidx) {
+                                                     unsigned long long* __restrict__ ekey, int* __restrict__ egidx,
+                                                     unsigned capacity, unsigned* __restrict__ flags) {
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     if (i >= N) return;
     const unsigned long long key = static_cast<unsigned long long>(__double_as_longlong(pre.zc[i]));
+    bool over = false;
     for_each_bucket(pre, i, L, pb, pe, tiles_x, num_tiles, soft, [&](int b) {
         const unsigned e = bstart[b] + atomicAdd(cursor + b, 1u);
+        if (e >= capacity) {  // asynchronous frames: entries beyond the reserved capacity are dropped
+            over = true;
+            return;
+        }
         ekey[e] = key;
         egidx[e] = static_cast<int>(i);
     });
+    if (over) atomicOr(flags, kFlagOverflow);
 }
 
-// (key, gidx) lexicographic order; zc > near > 0, so the IEEE bits of zc order like zc.
-__device__ __forceinline__ bool less_kg(unsigned long long ka, int ga, unsigned long long kb, int gb) {
-    return ka < kb || (ka == kb && ga < gb);
+// Buckets above the in-CTA sort capacity, compacted into a device list.
+__global__ void k_find_large(const unsigned* __restrict__ bstart, long long B, int cap, int* __restrict__ list,
+                             unsigned* __restrict__ nlist) {
+    for (long long b = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; b < B;
+         b += static_cast<long long>(gridDim.x) * blockDim.x)
+        if (bstart[b + 1] - bstart[b] > static_cast<unsigned>(cap)) list[atomicAdd(nlist, 1u)] = static_cast<int>(b);
 }
 
-// One CTA per large bucket: bitonic sort over the padded power of two in scratch.
-__global__ void __launch_bounds__(1024) k_sort_large(const int* __restrict__ ids, const unsigned* __restrict__ starts,
-                                                     const unsigned* __restrict__ counts, int pow2,
-                                                     unsigned long long* __restrict__ ekey, int* __restrict__ egidx,
-                                                     unsigned long long* __restrict__ tkey, int* __restrict__ tg) {
-    const unsigned s = starts[blockIdx.x], n = counts[blockIdx.x];
-    unsigned long long* K = tkey + static_cast<size_t>(blockIdx.x) * pow2;
-    int* G = tg + static_cast<size_t>(blockIdx.x) * pow2;
-    unsigned P = 1;
-    while (P < n) P <<= 1;
-    for (unsigned t = threadIdx.x; t < P; t += blockDim.x) {
-        K[t] = t < n ? ekey[s + t] : ~0ull;
-        G[t] = t < n ? egidx[s + t] : 0x7fffffff;
-    }
-    __syncthreads();
-    for (unsigned k = 2; k <= P; k <<= 1) {
-        for (unsigned j = k >> 1; j > 0; j >>= 1) {
-            for (unsigned t = threadIdx.x; t < P; t += blockDim.x) {
-                const unsigned u = t ^ j;
-                if (u > t) {
-                    const bool up = (t & k) == 0;
-                    const unsigned long long ka = K[t], kb = K[u];
-                    const int ga = G[t], gb = G[u];
-                    const bool swap = up ? less_kg(kb, gb, ka, ga) : less_kg(ka, ga, kb, gb);
-                    if (swap) {
-                        K[t] = kb;
-                        K[u] = ka;
-                        G[t] = gb;
-                        G[u] = ga;
+// Persistent CTAs sort the listed buckets by (zc, gidx) with a bitonic network in
+// global scratch; bucket b uses the scratch range [2 bstart[b], 2 bstart[b] + pow2(n)),
+// which never overlaps another bucket's since pow2(n) < 2 n.
+__global__ void __launch_bounds__(1024) k_sort_large_dev(const int* __restrict__ list,
+                                                         const unsigned* __restrict__ nlist,
+                                                         const unsigned* __restrict__ bstart, unsigned capacity,
+                                                         unsigned long long* __restrict__ ekey, int* __restrict__ egidx,
+                                                         unsigned long long* __restrict__ tkey, int* __restrict__ tg) {
+    const unsigned count = *nlist;
+    for (unsigned w = blockIdx.x; w < count; w += gridDim.x) {
+        const int bk = list[w];
+        const unsigned s = bstart[bk];
+        unsigned n = bstart[bk + 1] - s;
+        if (s >= capacity) continue;
+        if (n > capacity - s) n = capacity - s;
+        unsigned P = 1;
+        while (P < n) P <<= 1;
+        unsigned long long* K = tkey + 2 * static_cast<size_t>(s);
+        int* G = tg + 2 * static_cast<size_t>(s);
+        for (unsigned t = threadIdx.x; t < P; t += blockDim.x) {
+            K[t] = t < n ? ekey[s + t] : ~0ull;
+            G[t] = t < n ? egidx[s + t] : 0x7fffffff;
+        }
+        __syncthreads();
+        for (unsigned k = 2; k <= P; k <<= 1) {
+            for (unsigned j = k >> 1; j > 0; j >>= 1) {
+                for (unsigned t = threadIdx.x; t < P; t += blockDim.x) {
+                    const unsigned u = t ^ j;
+                    if (u > t) {
+                        const bool up = (t & k) == 0;
+                        const unsigned long long ka = K[t], kb = K[u];
+                        const int ga = G[t], gb = G[u];
+                        const bool swap = up ? less_kg(kb, gb, ka, ga) : less_kg(ka, ga, kb, gb);
+                        if (swap) {
+                            K[t] = kb;
+                            K[u] = ka;
+                            G[t] = gb;
+                            G[u] = ga;
+                        }
                     }
                 }
+                __syncthreads();
             }
-            __syncthreads();
         }
-    }
-    for (unsigned t = threadIdx.x; t < n; t += blockDim.x) {
-        ekey[s + t] = K[t];
-        egidx[s + t] = G[t];
+        for (unsigned t = threadIdx.x; t < n; t += blockDim.x) {
+            ekey[s + t] = K[t];
+            egidx[s + t] = G[t];
+        }
+        __syncthreads();
     }
 }
 
+// Entry::depth = zc[gidx] for e < min(E, capacity), E read on the device.
 __global__ void k_entry_depths(const int* __restrict__ egidx, const double* __restrict__ zc,
-                               double* __restrict__ edepth, size_t E) {
+                               double* __restrict__ edepth, const unsigned* __restrict__ d_E, unsigned capacity) {
+    const unsigned E = *d_E < capacity ? *d_E : capacity;
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < E;
          e += static_cast<size_t>(gridDim.x) * blockDim.x)
         edepth[e] = zc[egidx[e]];
@@ -224,41 +252,35 @@ void bucket_count(holo_ctx* ctx, const PreOut& pre, size_t N, int L, int pb, int
 }
 
 void bucket_emit(holo_ctx* ctx, const PreOut& pre, size_t N, int L, int pb, int pe, int tiles_x, int num_tiles,
-                 int soft, const unsigned* bstart, unsigned* cursor, unsigned long long* ekey, int* egidx) {
+                 int soft, const unsigned* bstart, unsigned* cursor, unsigned long long* ekey, int* egidx,
+                 unsigned capacity, unsigned* flags) {
     if (N == 0) return;
     k_bucket_emit<<<static_cast<unsigned>((N + 255) / 256), 256, 0, ctx->stream>>>(
-        pre, N, L, pb, pe, tiles_x, num_tiles, soft, bstart, cursor, ekey, egidx);
+        pre, N, L, pb, pe, tiles_x, num_tiles, soft, bstart, cursor, ekey, egidx, capacity, flags);
     HC_LAUNCHED(ctx);
 }
 
-void sort_large_buckets(holo_ctx* ctx, const std::vector<int>& ids, const std::vector<unsigned>& starts,
-                        const std::vector<unsigned>& counts, unsigned long long* ekey, int* egidx) {
-    const int nl = static_cast<int>(ids.size());
-    if (nl == 0) return;
-    unsigned maxn = 0;
-    for (unsigned c : counts) maxn = c > maxn ? c : maxn;
-    int pow2 = 1;
-    while (static_cast<unsigned>(pow2) < maxn) pow2 <<= 1;
-    int* d_ids = static_cast<int*>(ctx->buffer("large_ids", sizeof(int) * nl));
-    unsigned* d_starts = static_cast<unsigned*>(ctx->buffer("large_starts", sizeof(unsigned) * nl));
-    unsigned* d_counts = static_cast<unsigned*>(ctx->buffer("large_counts", sizeof(unsigned) * nl));
-    HC_CUDA(cudaMemcpyAsync(d_ids, ids.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, ctx->stream));
-    HC_CUDA(cudaMemcpyAsync(d_starts, starts.data(), sizeof(unsigned) * nl, cudaMemcpyHostToDevice, ctx->stream));
-    HC_CUDA(cudaMemcpyAsync(d_counts, counts.data(), sizeof(unsigned) * nl, cudaMemcpyHostToDevice, ctx->stream));
-    auto* tkey = static_cast<unsigned long long*>(
-        ctx->buffer("large_tkey", sizeof(unsigned long long) * static_cast<size_t>(pow2) * nl));
-    auto* tg = static_cast<int*>(ctx->buffer("large_tg", sizeof(int) * static_cast<size_t>(pow2) * nl));
-    k_sort_large<<<nl, 1024, 0, ctx->stream>>>(d_ids, d_starts, d_counts, pow2, ekey, egidx, tkey, tg);
+void sort_large_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsigned capacity,
+                        unsigned long long* ekey, int* egidx, unsigned* d_nlist) {
+    // list buffer sized for the worst case: at most capacity / (kSortCap + 1) buckets can exceed the cap
+    const size_t max_list = capacity / (kSortCap + 1) + 1;
+    int* list = static_cast<int*>(ctx->buffer("large_list", sizeof(int) * max_list));
+    auto* tkey = static_cast<unsigned long long*>(ctx->buffer("large_tkey", sizeof(unsigned long long) * 2 * (capacity + 1)));
+    auto* tg = static_cast<int*>(ctx->buffer("large_tg", sizeof(int) * 2 * (capacity + 1)));
+    const long long blocks = (B + 255) / 256;
+    k_find_large<<<static_cast<unsigned>(blocks < 4096 ? (blocks > 0 ? blocks : 1) : 4096), 256, 0, ctx->stream>>>(
+        bstart, B, kSortCap, list, d_nlist);
     HC_LAUNCHED(ctx);
-    // the host vectors must outlive the async copies
-    HC_CUDA(cudaStreamSynchronize(ctx->stream));
+    k_sort_large_dev<<<ctx->sm_count, 1024, 0, ctx->stream>>>(list, d_nlist, bstart, capacity, ekey, egidx, tkey, tg);
+    HC_LAUNCHED(ctx);
 }
 
-void entry_depths(holo_ctx* ctx, const int* egidx, const double* zc, double* edepth, size_t E) {
-    if (E == 0) return;
-    const size_t blocks = (E + 255) / 256;
+void entry_depths(holo_ctx* ctx, const int* egidx, const double* zc, double* edepth, const unsigned* d_E,
+                  unsigned capacity) {
+    if (capacity == 0) return;
+    const size_t blocks = (static_cast<size_t>(capacity) + 255) / 256;
     const unsigned grid = static_cast<unsigned>(blocks < 4096 ? blocks : 4096);
-    k_entry_depths<<<grid, 256, 0, ctx->stream>>>(egidx, zc, edepth, E);
+    k_entry_depths<<<grid, 256, 0, ctx->stream>>>(egidx, zc, edepth, d_E, capacity);
     HC_LAUNCHED(ctx);
 }
 

@@ -214,6 +214,43 @@ void resolve_timing(holo_ctx* ctx) {
     ctx->pending.clear();
 }
 
+// Fold the status words of finished asynchronous frames into the context, oldest
+// first.  wait_all: block until every pending frame is done; otherwise take the
+// finished ones and block only while the ring is full.
+void consume_status(holo_ctx* ctx, bool wait_all) {
+    while (ctx->status_pending_n > 0) {
+        const int slot = ctx->status_order[0];
+        const cudaEvent_t ev = ctx->status_events[slot];
+        if (wait_all || ctx->status_pending_n == holo_ctx::kStatusSlots) {
+            HC_CUDA(cudaEventSynchronize(ev));
+        } else {
+            const cudaError_t q = cudaEventQuery(ev);
+            if (q == cudaErrorNotReady) {
+                (void)cudaGetLastError();
+                break;
+            }
+            HC_CUDA(q);
+        }
+        const unsigned* h = ctx->host_status + slot * holo_ctx::kStatusWords;
+        ctx->sticky_flags |= h[0];
+        ctx->f_num_valid = h[1];
+        ctx->f_max_bucket = h[2];
+        ctx->f_E = h[4];
+        for (int i = 1; i < ctx->status_pending_n; ++i) ctx->status_order[i - 1] = ctx->status_order[i];
+        --ctx->status_pending_n;
+    }
+}
+
+void fill_info(const holo_ctx* ctx, holo_frame_info* info) {
+    *info = holo_frame_info{};
+    info->num_entries = ctx->f_E;
+    info->tiles_x = ctx->f_tiles_x;
+    info->tiles_y = ctx->f_tiles_y;
+    info->num_buckets = static_cast<int32_t>(ctx->f_buckets);
+    info->max_bucket = static_cast<int32_t>(ctx->f_max_bucket);
+    info->num_valid = static_cast<int32_t>(ctx->f_num_valid);
+}
+
 // ---------------------------------------------------------------- render internals
 
 struct FrameGeom {
@@ -286,37 +323,32 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     ctx->stage_begin();
     bucket_count(ctx, pre, N, L, pb, pe, g.tiles_x, g.num_tiles, st.soft_assignment, bcount);
     exclusive_scan_u32(ctx, bcount, bstart, B, misc + 2);
-    // one host sync per frame: entry count, largest bucket, validation flags
-    unsigned* hp = static_cast<unsigned*>(ctx->pinned(64));
-    HC_CUDA(cudaMemcpyAsync(hp, misc, sizeof(unsigned) * 3, cudaMemcpyDeviceToHost, ctx->stream));
-    HC_CUDA(cudaMemcpyAsync(hp + 4, bstart + B, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
-    HC_CUDA(cudaStreamSynchronize(ctx->stream));
-    const unsigned flags = hp[0], num_valid = hp[1], max_bucket = hp[2];
-    const unsigned E = hp[4];
-    if (flags & 1u) config_error("degenerate quaternion in scene");     // scene.cpp:27
-    if (flags & 2u) config_error("amplitudes must be non-negative");    // scene.cpp:30
-
-    auto* ekey = buf<unsigned long long>(ctx, "ekey", E);
-    int* egidx = buf<int>(ctx, "egidx", E);
+    // pinned status words: flags, num_valid, max bucket, -, E
+    unsigned* hp = ctx->host_status + holo_ctx::kStatusSlots * holo_ctx::kStatusWords;
+    unsigned capacity;
+    if (!ctx->async) {
+        // synchronous frame: one host round trip for the entry count and the
+        // validation flags, so errors surface from this call like the reference's
+        HC_CUDA(cudaMemcpyAsync(hp, misc, sizeof(unsigned) * 3, cudaMemcpyDeviceToHost, ctx->stream));
+        HC_CUDA(cudaMemcpyAsync(hp + 4, bstart + B, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+        HC_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (hp[0] & kFlagDegenerateQuat) config_error("degenerate quaternion in scene");  // scene.cpp:27
+        if (hp[0] & kFlagNegativeAmp) config_error("amplitudes must be non-negative");    // scene.cpp:30
+        capacity = hp[4];
+        ctx->e_cap = std::max<size_t>(ctx->e_cap, capacity + capacity / 4);  // headroom for later async frames
+    } else {
+        // asynchronous frame: entries beyond the reserved capacity are dropped and
+        // flagged; holo_ctx_frame_status reports it (and the validation flags)
+        if (ctx->e_cap == 0) config_error("asynchronous rendering needs holo_ctx_reserve_entries or a synchronous frame first");
+        capacity = static_cast<unsigned>(std::min<size_t>(ctx->e_cap, 0xffffffffu));
+    }
+    auto* ekey = buf<unsigned long long>(ctx, "ekey", capacity);
+    int* egidx = buf<int>(ctx, "egidx", capacity);
     unsigned* cursor = bcount;  // reuse: zero it and count again during emission
     HC_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned) * (B + 1), ctx->stream));
-    bucket_emit(ctx, pre, N, L, pb, pe, g.tiles_x, g.num_tiles, st.soft_assignment, bstart, cursor, ekey, egidx);
-    if (max_bucket > static_cast<unsigned>(kSortCap)) {
-        std::vector<unsigned> hs(B + 1);
-        HC_CUDA(cudaMemcpyAsync(hs.data(), bstart, sizeof(unsigned) * (B + 1), cudaMemcpyDeviceToHost, ctx->stream));
-        HC_CUDA(cudaStreamSynchronize(ctx->stream));
-        std::vector<int> ids;
-        std::vector<unsigned> starts, counts;
-        for (long long b = 0; b < B; ++b) {
-            const unsigned c = hs[b + 1] - hs[b];
-            if (c > static_cast<unsigned>(kSortCap)) {
-                ids.push_back(static_cast<int>(b));
-                starts.push_back(hs[b]);
-                counts.push_back(c);
-            }
-        }
-        sort_large_buckets(ctx, ids, starts, counts, ekey, egidx);
-    }
+    bucket_emit(ctx, pre, N, L, pb, pe, g.tiles_x, g.num_tiles, st.soft_assignment, bstart, cursor, ekey, egidx,
+                capacity, misc);
+    sort_large_buckets(ctx, bstart, B, capacity, ekey, egidx, misc + 3);
     ctx->stage_end(1);
 
     // composite into [nplanes][C][H][W]
@@ -339,6 +371,7 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     ca.soft = st.soft_assignment;
     ca.write_lists = want_lists ? 1 : 0;
     ca.pack_ok = N < (size_t{1} << 24) ? 1 : 0;
+    ca.capacity = capacity;
     ca.term_eps = static_cast<float>(st.term_eps);
     ca.alpha_floor = static_cast<float>(st.alpha_floor);
     ca.alpha_clamp = static_cast<float>(st.alpha_clamp);
@@ -349,17 +382,32 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     ctx->stage_begin();
     composite(ctx, ca, g.tile);
     ctx->stage_end(2);
-    if (want_lists) entry_depths(ctx, egidx, pre.zc, buf<double>(ctx, "edepth", E), E);
+    if (want_lists) entry_depths(ctx, egidx, pre.zc, buf<double>(ctx, "edepth", capacity), bstart + B, capacity);
 
-    ctx->f_E = E;
-    if (info) {
-        info->num_entries = E;
-        info->tiles_x = g.tiles_x;
-        info->tiles_y = g.tiles_y;
-        info->num_buckets = static_cast<int32_t>(B);
-        info->max_bucket = static_cast<int32_t>(max_bucket);
-        info->num_valid = static_cast<int32_t>(num_valid);
+    ctx->f_tiles_x = g.tiles_x;
+    ctx->f_tiles_y = g.tiles_y;
+    ctx->f_buckets = B;
+    ctx->f_cap = capacity;
+    if (!ctx->async) {
+        // flags / counters after the whole raster (overflow cannot happen here)
+        HC_CUDA(cudaMemcpyAsync(hp, misc, sizeof(unsigned) * 3, cudaMemcpyDeviceToHost, ctx->stream));
+        HC_CUDA(cudaStreamSynchronize(ctx->stream));
+        ctx->f_E = hp[4];
+        ctx->f_num_valid = hp[1];
+        ctx->f_max_bucket = hp[2];
+        if (info) fill_info(ctx, info);
+        return;
     }
+    // ring slot for this frame's status (waits for the oldest frame when all are in flight)
+    consume_status(ctx, false);
+    const int slot = ctx->status_next;
+    ctx->status_next = (slot + 1) % holo_ctx::kStatusSlots;
+    hp = ctx->host_status + slot * holo_ctx::kStatusWords;
+    HC_CUDA(cudaMemcpyAsync(hp, misc, sizeof(unsigned) * 3, cudaMemcpyDeviceToHost, ctx->stream));
+    HC_CUDA(cudaMemcpyAsync(hp + 4, bstart + B, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+    HC_CUDA(cudaEventRecord(ctx->status_events[slot], ctx->stream));
+    ctx->status_order[ctx->status_pending_n++] = slot;
+    if (info) *info = holo_frame_info{};  // known after holo_ctx_frame_status
 }
 
 TfChan* upload_tf(holo_ctx* ctx, const char* name, const holo_wave& wave, const std::vector<double>& z, int w, int h,
@@ -496,6 +544,10 @@ int holo_ctx_create(int device, holo_ctx** out) {
         HC_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
         HC_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
         ctx->stream = ctx->own_stream;
+        HC_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->host_status),
+                               sizeof(unsigned) * (holo_ctx::kStatusSlots + 1) * holo_ctx::kStatusWords));
+        std::memset(ctx->host_status, 0, sizeof(unsigned) * (holo_ctx::kStatusSlots + 1) * holo_ctx::kStatusWords);
+        for (auto& e : ctx->status_events) HC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         *out = ctx;
     });
 }
@@ -512,6 +564,9 @@ int holo_ctx_destroy(holo_ctx* ctx) {
                           ctx->d_phases, ctx->d_plane_logits})
             cudaFree(p);
         if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
+        if (ctx->host_status) cudaFreeHost(ctx->host_status);
+        for (auto e : ctx->status_events)
+            if (e) cudaEventDestroy(e);
         for (auto& t : ctx->pending) {
             cudaEventDestroy(t.a);
             cudaEventDestroy(t.b);
@@ -545,7 +600,46 @@ int holo_ctx_use_own_stream(holo_ctx* ctx) {
 void* holo_ctx_get_stream(holo_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 
 int holo_ctx_synchronize(holo_ctx* ctx) {
-    return guarded([&] { HC_CUDA(cudaStreamSynchronize(ctx->stream)); });
+    return guarded([&] {
+        require(ctx != nullptr, HOLO_ERR_USAGE, "null context");
+        HC_CUDA(cudaStreamSynchronize(ctx->stream));
+        consume_status(ctx, true);
+    });
+}
+
+int holo_ctx_set_async(holo_ctx* ctx, int enable) {
+    return guarded([&] {
+        require(ctx != nullptr, HOLO_ERR_USAGE, "null context");
+        if (!enable) consume_status(ctx, true);
+        ctx->async = enable != 0;
+    });
+}
+
+int holo_ctx_reserve_entries(holo_ctx* ctx, uint64_t entries) {
+    return guarded([&] {
+        require(ctx != nullptr, HOLO_ERR_USAGE, "null context");
+        require(entries < 0xffffffffull, HOLO_ERR_USAGE, "holo_ctx_reserve_entries: at most 2^32 - 2 entries");
+        ctx->e_cap = std::max<size_t>(ctx->e_cap, static_cast<size_t>(entries));
+    });
+}
+
+int holo_ctx_frame_status(holo_ctx* ctx, holo_frame_info* info) {
+    return guarded([&] {
+        require(ctx != nullptr, HOLO_ERR_USAGE, "null context");
+        consume_status(ctx, true);
+        if (info) fill_info(ctx, info);
+        const unsigned f = ctx->sticky_flags;
+        ctx->sticky_flags = 0;
+        if (f & kFlagDegenerateQuat) config_error("degenerate quaternion in scene");  // scene.cpp:27
+        if (f & kFlagNegativeAmp) config_error("amplitudes must be non-negative");    // scene.cpp:30
+        if (f & kFlagOverflow) {
+            const std::string m = "asynchronous frame needed " + std::to_string(ctx->f_E) +
+                                  " entries but only " + std::to_string(ctx->e_cap) +
+                                  " are reserved (holo_ctx_reserve_entries); its outputs are incomplete";
+            ctx->e_cap = std::max<size_t>(ctx->e_cap, ctx->f_E + ctx->f_E / 4);
+            throw Error(HOLO_ERR_NUMERIC, m);
+        }
+    });
 }
 
 int holo_ctx_enable_timing(holo_ctx* ctx, int enable) {
@@ -822,6 +916,9 @@ int holo_frame_buffer(holo_ctx* ctx, int which, void** dev_ptr, size_t* bytes) {
         const size_t B = np * ctx->f_tiles;
         const char* name = nullptr;
         size_t sz = 0;
+        if (which == HOLO_BUF_ENTRY_GIDX || which == HOLO_BUF_ENTRY_DEPTH)
+            consume_status(ctx, true);  // E of an asynchronous frame
+        const size_t E = std::min<uint64_t>(ctx->f_E, ctx->f_cap);
         switch (which) {
             case HOLO_BUF_LAYERS: name = "layers"; sz = np * C * P * 8; break;
             case HOLO_BUF_HOLOGRAM: name = "hologram"; sz = C * P * 8; break;
@@ -829,8 +926,8 @@ int holo_frame_buffer(holo_ctx* ctx, int which, void** dev_ptr, size_t* bytes) {
             case HOLO_BUF_INTENSITY: name = "intensity"; sz = np * C * P * 4; break;
             case HOLO_BUF_T_FINAL: name = "t_final"; sz = np * P * 4; break;
             case HOLO_BUF_N_CONTRIB: name = "n_contrib"; sz = np * P * 4; break;
-            case HOLO_BUF_ENTRY_GIDX: name = "egidx"; sz = ctx->f_E * 4; break;
-            case HOLO_BUF_ENTRY_DEPTH: name = "edepth"; sz = ctx->f_E * 8; break;
+            case HOLO_BUF_ENTRY_GIDX: name = "egidx"; sz = E * 4; break;
+            case HOLO_BUF_ENTRY_DEPTH: name = "edepth"; sz = E * 8; break;
             case HOLO_BUF_BUCKET_START: name = "bstart"; sz = (B + 1) * 4; break;
             case HOLO_BUF_PROJECTED: name = "projected"; sz = ctx->n * sizeof(holo_projected); break;
             case HOLO_BUF_RHO: name = "rho"; sz = ctx->n * static_cast<size_t>(ctx->f_L) * 8; break;

@@ -133,8 +133,8 @@ __global__ void __launch_bounds__(TILE * TILE) k_composite(CompositeArgs a) {
     const int tx = blockIdx.x, ty = blockIdx.y, lplane = blockIdx.z;  // grid = (tiles_x, tiles_y, planes)
     const int lb = (lplane * gridDim.y + ty) * gridDim.x + tx;        // local bucket
     const int px0 = tx * TILE, py0 = ty * TILE;
-    const unsigned e0 = a.bstart[lb];
-    const int n = static_cast<int>(a.bstart[lb + 1] - e0);
+    const unsigned e0 = min(a.bstart[lb], a.capacity);
+    const int n = static_cast<int>(min(a.bstart[lb + 1], a.capacity) - e0);
     const int plane = a.plane_begin + lplane;
 
     const int tid = threadIdx.x;

@@ -67,9 +67,26 @@ struct holo_ctx {
 
     // last frame
     int f_L = 0, f_C = 0, f_W = 0, f_H = 0, f_tiles = 0;
+    int f_tiles_x = 0, f_tiles_y = 0;
+    long long f_buckets = 0;
     uint64_t f_E = 0;
+    unsigned f_num_valid = 0, f_max_bucket = 0;
     unsigned f_outputs = 0;
     int f_plane_begin = 0, f_plane_end = 0;
+
+    // asynchronous frames (holo_ctx_set_async): no host round trip inside a frame;
+    // the entry buffers hold e_cap entries and each frame's status words
+    // (flags, num_valid, max bucket, -, E) land in a pinned ring, consumed in order
+    bool async = false;
+    size_t e_cap = 0;
+    unsigned f_cap = 0;               // entry-buffer capacity of the last frame
+    static constexpr int kStatusSlots = 8;
+    static constexpr int kStatusWords = 8;
+    unsigned* host_status = nullptr;  // pinned, (kStatusSlots + 1) x kStatusWords; the last slot serves synchronous frames
+    cudaEvent_t status_events[kStatusSlots] = {};
+    int status_order[kStatusSlots] = {};  // pending slots, oldest first
+    int status_pending_n = 0, status_next = 0;
+    unsigned sticky_flags = 0;        // validation / overflow flags of consumed asynchronous frames
 
     // stage-timing event pairs awaiting resolution, and a pool of spare events
     struct Timed {

@@ -53,7 +53,7 @@ struct Batch {
     static constexpr int kN = N, kNB = NB, kNT = NT;
     // one pad slot per 32 complex values: the stride-R writes of early Stockham
     // stages (i = R j + r) would otherwise land 32 lanes on one bank pair
-    static constexpr int kSmemElems = N * NB + (N * NB) / 32 + 1;
+    static constexpr int kSmemElems = ((N * NB + (N * NB) / 32 + 1) + 1) & ~1;  // even: 16-byte multiple
     static __device__ __forceinline__ int at(int b, int i) {
         const int c = i * NB + b;
         return c + (c >> 5);
@@ -174,6 +174,17 @@ struct Stages<T, DIR, B, NS, FIRST, Radices<R, R2, Rs...>> {
 template <class T, int DIR, class B, class P, class Load, class Store>
 __device__ __forceinline__ void fft_static(cx<T>* sm, const cx<T>* __restrict__ tw, Load load, Store store) {
     Stages<T, DIR, B, 1, true, P>::run(sm, tw, load, store);
+}
+
+// Asynchronous 16-byte global -> shared copies (LDGSTS), grouped by commit.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
 // Last-stage geometry of plan P (for register arrays living across transforms).

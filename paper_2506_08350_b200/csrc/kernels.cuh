@@ -106,16 +106,22 @@ void host_world_to_cam(const holo_camera& cam, double wc[9]);
 void preprocess(holo_ctx* ctx, const CameraConsts& cc, const holo_raster_settings& st, double near_clip, int L,
                 int tiles_x, int tiles_y, const PreOut& out);
 
+constexpr int kSortCap = 1024;  // largest bucket the compositing CTA sorts in shared memory
+
 // ---- binning.cu
 void exclusive_scan_u32(holo_ctx* ctx, const unsigned* in, unsigned* out, long long n, unsigned* d_max);
 void bucket_count(holo_ctx* ctx, const PreOut& pre, size_t N, int L, int plane_begin, int plane_end, int tiles_x,
                   int num_tiles, int soft, unsigned* bcount);
+// validation / status flags written by the frame's kernels (misc[0])
+constexpr unsigned kFlagDegenerateQuat = 1u, kFlagNegativeAmp = 2u, kFlagOverflow = 4u;
 void bucket_emit(holo_ctx* ctx, const PreOut& pre, size_t N, int L, int plane_begin, int plane_end, int tiles_x,
                  int num_tiles, int soft, const unsigned* bstart, unsigned* cursor,
-                 unsigned long long* ekey, int* egidx);
-void sort_large_buckets(holo_ctx* ctx, const std::vector<int>& ids, const std::vector<unsigned>& starts,
-                        const std::vector<unsigned>& counts, unsigned long long* ekey, int* egidx);
-void entry_depths(holo_ctx* ctx, const int* egidx, const double* zc, double* edepth, size_t E);
+                 unsigned long long* ekey, int* egidx, unsigned capacity, unsigned* flags);
+// device-driven: buckets above kSortCap are found and sorted without a host round trip
+void sort_large_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsigned capacity,
+                        unsigned long long* ekey, int* egidx, unsigned* d_nlist);
+void entry_depths(holo_ctx* ctx, const int* egidx, const double* zc, double* edepth, const unsigned* d_E,
+                  unsigned capacity);
 
 // ---- render_static.cu (compile-time FFT plans for the common grid sizes)
 enum { kModeFull = 0, kModeSpec = 1, kModeReplay = 2 };
@@ -127,7 +133,6 @@ void static_row(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spe
                 int C, int Lloc, int nout, const int* plane_of, const TfChan* tfc, double pitch);
 
 // ---- composite.cu
-constexpr int kSortCap = 1024;
 struct CompositeArgs {
     const unsigned* bstart;   // bucket_start for the rendered planes, indexed by local bucket
     unsigned long long* ekey; // depth bits per entry (unsorted for small buckets)
@@ -137,6 +142,7 @@ struct CompositeArgs {
     int L, C, W, H, tiles_x, num_tiles, plane_begin, num_buckets;
     int soft, write_lists;
     int pack_ok;              // N < 2^24: a bucket slot fits under gidx in a 31-bit tie-break key
+    unsigned capacity;        // entry-buffer size: bucket ranges are clamped to it (overflowed async frames)
     float term_eps, alpha_floor, alpha_clamp;
     int floor_positive;
     cx<float>* layers;        // [planes][C][H][W], plane relative to plane_begin

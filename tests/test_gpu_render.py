@@ -214,6 +214,98 @@ def test_rejects_bad_inputs(gpu_ctx):
         gpu_ctx.render(front_camera(cfg), cfg)
 
 
+# ---------------------------------------------------------------- asynchronous frames (holo_ctx_set_async)
+
+def _frame(ctx, C, H, W, L_):
+    holo = ctx.download(L.BUF_HOLOGRAM, np.complex64, (C, H, W))
+    ints = ctx.download(L.BUF_INTENSITY, np.float32, (L_, C, H, W))
+    return holo, ints
+
+
+def test_async_frames_equal_sync_frames():
+    cfg = WaveConfig(nx=256, ny=192, wavelengths=RGB, num_planes=4)
+    scenes = [synthetic_scene(20000, cfg, 40 + i) for i in range(3)]
+    cam = wide_camera(cfg)
+    ctx = api.Context(0, use_torch_stream=False)
+    want, infos = [], []
+    for s in scenes:
+        ctx.upload_scene(s)
+        infos.append((ctx.render(cam, cfg).num_entries, ctx.info.max_bucket, ctx.info.num_valid))
+        want.append(_frame(ctx, 3, 192, 256, 4))
+    ctx.set_async(True)
+    for s, w, inf in zip(scenes, want, infos):
+        ctx.upload_scene(s)
+        assert ctx.render(cam, cfg).num_entries == 0  # not known until frame_status
+        st = ctx.frame_status()
+        assert (st.num_entries, st.max_bucket, st.num_valid) == inf
+        got = _frame(ctx, 3, 192, 256, 4)
+        assert np.array_equal(got[0], w[0]) and np.array_equal(got[1], w[1])
+    # lists of an asynchronous frame (E read back lazily)
+    ctx.render(cam, cfg, outputs=L.OUT_HOLOGRAM | L.OUT_LISTS)
+    p, nbytes = ctx.buffer(L.BUF_ENTRY_GIDX)
+    assert nbytes == 4 * infos[-1][0]
+    ctx.close()
+
+
+def test_async_capacity_and_validation_reported_by_frame_status():
+    cfg = WaveConfig(nx=128, ny=128, wavelengths=RGB, num_planes=2)
+    s = synthetic_scene(5000, cfg, 44)
+    cam = wide_camera(cfg)
+    ctx = api.Context(0, use_torch_stream=False)
+    ctx.set_async(True)
+    ctx.upload_scene(s)
+    with pytest.raises(HoloError) as e:  # nothing reserved and no synchronous frame yet
+        ctx.render(cam, cfg)
+    assert e.value.kind == "config"
+    ctx.reserve_entries(100)
+    ctx.render(cam, cfg)  # overflows: dropped entries, no out-of-bounds access
+    with pytest.raises(HoloError) as e:
+        ctx.frame_status()
+    assert e.value.kind == "numeric" and "reserve" in str(e.value)
+    ctx.render(cam, cfg)  # the failed status grew the reservation
+    E = ctx.frame_status().num_entries
+    ctx.set_async(False)
+    assert ctx.render(cam, cfg).num_entries == E
+    ref = _frame(ctx, 3, 128, 128, 2)
+    ctx.set_async(True)
+    ctx.render(cam, cfg)
+    ctx.frame_status()
+    got = _frame(ctx, 3, 128, 128, 2)
+    assert np.array_equal(got[0], ref[0])
+    bad = random_scene(3, cfg, 1)
+    bad.amplitudes[0, 0] = -1.0
+    ctx.upload_scene(bad)
+    ctx.render(cam, cfg)
+    with pytest.raises(HoloError) as e:
+        ctx.frame_status()
+    assert e.value.kind == "config" and "non-negative" in str(e.value)
+    ctx.frame_status()  # flags cleared
+    ctx.close()
+
+
+def test_two_async_contexts_overlap_and_agree():
+    import torch
+
+    cfg = WaveConfig(nx=256, ny=256, wavelengths=RGB, num_planes=4)
+    s = synthetic_scene(30000, cfg, 45)
+    cam = wide_camera(cfg)
+    ctxs = [api.Context(0, use_torch_stream=False) for _ in range(2)]
+    for c in ctxs:
+        c.upload_scene(s)
+        c.render(cam, cfg)
+        c.set_async(True)
+    ref = _frame(ctxs[0], 3, 256, 256, 4)
+    for _ in range(4):
+        for c in ctxs:
+            c.render(cam, cfg)
+    for c in ctxs:
+        c.frame_status()
+        got = _frame(c, 3, 256, 256, 4)
+        assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
+        c.close()
+    torch.cuda.synchronize()
+
+
 # ---------------------------------------------------------------- plane sharding (begin / all-reduce / end) on one GPU
 
 def test_plane_sharded_halves_equal_full_render(gpu_ctx):
