@@ -349,6 +349,7 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     bucket_emit(ctx, pre, N, L, pb, pe, g.tiles_x, g.num_tiles, st.soft_assignment, bstart, cursor, ekey, egidx,
                 capacity, misc);
     sort_large_buckets(ctx, bstart, B, capacity, ekey, egidx, misc + 3);
+    sort_small_buckets(ctx, bstart, B, capacity, ekey, egidx);
     ctx->stage_end(1);
 
     // composite into [nplanes][C][H][W]
@@ -370,7 +371,6 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     ca.num_buckets = static_cast<int>(B);
     ca.soft = st.soft_assignment;
     ca.write_lists = want_lists ? 1 : 0;
-    ca.pack_ok = N < (size_t{1} << 24) ? 1 : 0;
     ca.capacity = capacity;
     ca.term_eps = static_cast<float>(st.term_eps);
     ca.alpha_floor = static_cast<float>(st.alpha_floor);

@@ -5,14 +5,17 @@
 //   stop once T < term_eps (checked before each entry),
 //   a = min(alpha * exp(-form / 2) * rho, alpha_clamp), skip unless a > alpha_floor,
 //   acc_c += a T amp_c e^{i phi_c},  T *= 1 - a,  ++n_contrib.
-// One CTA per bucket, one thread per pixel.  The CTA first restores the
-// reference order of its bucket -- ascending (zc, gidx), rasterizer.cpp:221-224 --
-// by a warp-shuffle bitonic sort (<= 128 entries), a rank sort (<= 256) or a
-// shared-memory bitonic sort (<= kSortCap); larger buckets arrive presorted from
-// binning.cu.  Records are staged 256 at a time in shared memory; each warp
-// covers an 8x4 pixel block and, 32 entries per ballot, skips entries whose
-// accept ellipse (a > alpha_floor) has a bounding box missing the block.  Evaluation is fp32 with the
-// centre offset formed in f64 per entry, so dx, dy keep full fp32 precision.
+// Bucket order -- ascending (zc, gidx), rasterizer.cpp:221-224 -- is restored
+// before compositing: buckets of up to kWarpSortCap entries by k_sort_small (one
+// warp per bucket, shuffle bitonic), buckets above kSortCap by binning.cu, and the
+// ones in between by the compositing CTA itself in shared memory.
+// Compositing: one CTA per bucket, one thread per pixel.  Records are staged 256
+// at a time in shared memory; each warp covers an 8x4 pixel block and, 32
+// entries per ballot, skips entries whose accept ellipse (a > alpha_floor) misses
+// the block's bounding box, then walks the hits two at a time (the two
+// evaluations are independent; only the blend is serial).  Evaluation is fp32
+// with the centre offset formed in f64 per entry, so dx, dy keep full fp32
+// precision, and alpha folded into the exponent: a = 2^(q + log2 alpha).
 #include "kernels.cuh"
 
 namespace holo_cuda {
@@ -81,54 +84,104 @@ __device__ __forceinline__ void warp_bitonic(KeyG (&v)[NE], int lane) {
     }
 }
 
-// Sort one bucket (n <= 32 NE entries) in a warp.  PACK: the tie-break key carries
-// the emission slot in its low 7 bits ((gidx << 7) | slot, n <= 128, gidx < 2^24),
-// which orders exactly like gidx, and s_ord receives slots instead of indices.
-template <int NE, bool PACK>
-__device__ __forceinline__ void warp_sort_bucket(const unsigned long long* __restrict__ ekey,
-                                                 const int* __restrict__ egidx, unsigned e0, int n, int lane,
-                                                 int* __restrict__ s_ord) {
+// Sort one bucket (n <= 32 NE entries) in a warp and write its gidx back in order.
+template <int NE>
+__device__ __forceinline__ void warp_sort_bucket(const unsigned long long* __restrict__ ekey, int* __restrict__ egidx,
+                                                 unsigned e0, int n, int lane) {
     KeyG v[NE];
 #pragma unroll
     for (int s = 0; s < NE; ++s) {
         const int i = lane + 32 * s;
         v[s].k = i < n ? ekey[e0 + i] : ~0ull;
-        v[s].g = i < n ? (PACK ? ((egidx[e0 + i] << 7) | i) : egidx[e0 + i]) : 0x7fffffff;
+        v[s].g = i < n ? egidx[e0 + i] : 0x7fffffff;
     }
     warp_bitonic<NE>(v, lane);
 #pragma unroll
     for (int s = 0; s < NE; ++s) {
         const int i = lane + 32 * s;
-        if (i < n) s_ord[i] = PACK ? (v[s].g & 127) : v[s].g;
+        if (i < n) egidx[e0 + i] = v[s].g;
     }
 }
 
-template <int NE, bool PACK>
-__device__ __forceinline__ void warp_sort_any(const CompositeArgs& a, unsigned e0, int n, int lane, int* s_ord) {
+// One warp per bucket of 2..kWarpSortCap entries.
+__global__ void __launch_bounds__(256) k_sort_small(const unsigned* __restrict__ bstart, long long B,
+                                                    unsigned capacity, const unsigned long long* __restrict__ ekey,
+                                                    int* __restrict__ egidx) {
+    const long long b = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (b >= B) return;
+    const int lane = threadIdx.x & 31;
+    const unsigned e0 = min(bstart[b], capacity);
+    const int n = static_cast<int>(min(bstart[b + 1], capacity) - e0);
+    if (n < 2 || n > kWarpSortCap) return;  // warp-uniform
     if (n <= 32)
-        warp_sort_bucket<1, PACK>(a.ekey, a.egidx, e0, n, lane, s_ord);
+        warp_sort_bucket<1>(ekey, egidx, e0, n, lane);
     else if (n <= 64)
-        warp_sort_bucket<2, PACK>(a.ekey, a.egidx, e0, n, lane, s_ord);
+        warp_sort_bucket<2>(ekey, egidx, e0, n, lane);
     else
-        warp_sort_bucket<4, PACK>(a.ekey, a.egidx, e0, n, lane, s_ord);
+        warp_sort_bucket<4>(ekey, egidx, e0, n, lane);
 }
 
-// One staged entry: 64 bytes, read with four 16-byte shared loads from one base.
+// One staged entry: 48 bytes, read with three 16-byte shared loads from one base;
+// its accept box lives in a separate array read only by the ballot test.
 struct alignas(16) Staged {
     float4 a;  // mx, my, ca, cb   (centre relative to the tile origin; conic, log2-scaled)
-    float4 b;  // cc, alpha, ylo, yhi
-    float4 c;  // xlo, xhi, col0 re, col0 im
-    float4 d;  // col1 re, col1 im, col2 re, col2 im
+    float4 b;  // cc, log2(alpha), col0 re, col0 im
+    float4 c;  // col1 re, col1 im, col2 re, col2 im
 };
 
+#ifdef HOLO_COUNT
+__device__ unsigned long long g_counts[4];
+#endif
+
+__device__ __forceinline__ float eval_alpha(const Staged* e, float fx, float fy, float clamp, float4& B) {
+    const float4 A = e->a;
+    B = e->b;
+    const float dx = fx - A.x, dy = fy - A.y;
+    const float t = fmaf(A.w, dy, A.z * dx);
+    const float u = fmaf(dx, t, B.y);
+    const float q = fmaf(B.x * dy, dy, u);
+    return fminf(ex2_approx(q), clamp);
+}
+
+template <int C>
+__device__ __forceinline__ void blend(const Staged* e, const float4& B, float w, float (&acc)[2 * C]) {
+    acc[0] = fmaf(w, B.z, acc[0]);
+    acc[1] = fmaf(w, B.w, acc[1]);
+    if constexpr (C > 1) {
+        const float4 Cc = e->c;
+        acc[2 % (2 * C)] = fmaf(w, Cc.x, acc[2 % (2 * C)]);
+        acc[3 % (2 * C)] = fmaf(w, Cc.y, acc[3 % (2 * C)]);
+        if constexpr (C > 2) {
+            acc[4 % (2 * C)] = fmaf(w, Cc.z, acc[4 % (2 * C)]);
+            acc[5 % (2 * C)] = fmaf(w, Cc.w, acc[5 % (2 * C)]);
+        }
+    }
+}
+
+// 16x16 tiles: 6 CTAs (48 warps) per SM, 40 registers -- measured faster than 5
+// (48 registers) and 8 (32 registers, spills)
+#ifndef HOLO_COMP_MINB
+#define HOLO_COMP_MINB 6
+#endif
+
 template <int TILE, int C>
-__global__ void __launch_bounds__(TILE * TILE) k_composite(CompositeArgs a) {
+__global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) k_composite(CompositeArgs a) {
     using G = TileGeom<TILE>;
-    __shared__ unsigned long long s_key[kSortCap];
-    __shared__ int s_gid[kSortCap];
-    __shared__ int s_ord[kSortCap];
     constexpr int kStage = 256;  // records staged per batch
-    __shared__ Staged s_rec[kStage];
+    // the mid-size sort's arrays share storage with the staging arrays (the sort
+    // finishes, behind a barrier, before the first staging write)
+    union Smem {
+        struct {
+            unsigned long long key[kSortCap];
+            int gid[kSortCap];
+        } sort;
+        struct {
+            Staged rec[kStage];
+            float4 box[kStage];  // xlo, xhi, ylo, yhi of the accept ellipse, tile-relative
+        } st;
+    };
+    __shared__ Smem sm;
+    __shared__ int s_ord[kSortCap];
 
     const int tx = blockIdx.x, ty = blockIdx.y, lplane = blockIdx.z;  // grid = (tiles_x, tiles_y, planes)
     const int lb = (lplane * gridDim.y + ty) * gridDim.x + tx;        // local bucket
@@ -143,70 +196,66 @@ __global__ void __launch_bounds__(TILE * TILE) k_composite(CompositeArgs a) {
     const int lx = bx + (lane & 7), ly = by + (lane >> 3);
     const int px = px0 + lx, py = py0 + ly;
     const bool inside = px < a.W && py < a.H;
+    const float eps = a.term_eps;
 
     float T = 1.0f;
     int contrib = 0;
     float acc[2 * C];
 #pragma unroll
     for (int c = 0; c < 2 * C; ++c) acc[c] = 0.0f;
-    bool done = !inside || !(1.0f >= a.term_eps);  // the reference checks T < term_eps before every entry
+    // the reference checks T < term_eps before every entry; T never increases, so
+    // "stopped" is exactly !(T >= eps) (outside pixels are parked as stopped)
+    bool done = !inside || !(1.0f >= eps);
 
     if (n > 0) {
-        // ---- restore the reference order (zc asc, gidx asc): warp-shuffle bitonic
-        // for <= 128 entries, rank / shared bitonic sorts up to kSortCap, presorted
-        // by binning.cu beyond
-        const bool presorted = n > kSortCap;
+        const bool presorted = n <= kWarpSortCap || n > kSortCap;
         if (!presorted) {
-            if (n <= 128) {
-                if (warp == 0) warp_sort_any<4, false>(a, e0, n, lane, s_ord);
+            for (int t = tid; t < n; t += G::kThreads) {
+                sm.sort.key[t] = a.ekey[e0 + t];
+                sm.sort.gid[t] = a.egidx[e0 + t];
+            }
+            __syncthreads();
+            if (n <= G::kThreads) {
+                if (tid < n) {
+                    const unsigned long long k = sm.sort.key[tid];
+                    const int g = sm.sort.gid[tid];
+                    int rank = 0;
+                    for (int j = 0; j < n; ++j) {
+                        const unsigned long long kj = sm.sort.key[j];
+                        rank += (kj < k || (kj == k && sm.sort.gid[j] < g)) ? 1 : 0;
+                    }
+                    s_ord[rank] = g;
+                }
             } else {
-                for (int t = tid; t < n; t += G::kThreads) {
-                    s_key[t] = a.ekey[e0 + t];
-                    s_gid[t] = a.egidx[e0 + t];
+                int P = 1;
+                while (P < n) P <<= 1;
+                for (int t = n + tid; t < P; t += G::kThreads) {
+                    sm.sort.key[t] = ~0ull;
+                    sm.sort.gid[t] = 0x7fffffff;
                 }
                 __syncthreads();
-                if (n <= G::kThreads) {
-                    if (tid < n) {
-                        const unsigned long long k = s_key[tid];
-                        const int g = s_gid[tid];
-                        int rank = 0;
-                        for (int j = 0; j < n; ++j) {
-                            const unsigned long long kj = s_key[j];
-                            rank += (kj < k || (kj == k && s_gid[j] < g)) ? 1 : 0;
-                        }
-                        s_ord[rank] = g;
-                    }
-                } else {
-                    int P = 1;
-                    while (P < n) P <<= 1;
-                    for (int t = n + tid; t < P; t += G::kThreads) {
-                        s_key[t] = ~0ull;
-                        s_gid[t] = 0x7fffffff;
-                    }
-                    __syncthreads();
-                    for (int k = 2; k <= P; k <<= 1) {
-                        for (int j = k >> 1; j > 0; j >>= 1) {
-                            for (int t = tid; t < P; t += G::kThreads) {
-                                const int u = t ^ j;
-                                if (u > t) {
-                                    const bool up = (t & k) == 0;
-                                    const unsigned long long ka = s_key[t], kb = s_key[u];
-                                    const int ga = s_gid[t], gb = s_gid[u];
-                                    const bool b_less = kb < ka || (kb == ka && gb < ga);
-                                    const bool a_less = ka < kb || (ka == kb && ga < gb);
-                                    if (up ? b_less : a_less) {
-                                        s_key[t] = kb;
-                                        s_key[u] = ka;
-                                        s_gid[t] = gb;
-                                        s_gid[u] = ga;
-                                    }
+                for (int k = 2; k <= P; k <<= 1) {
+                    for (int j = k >> 1; j > 0; j >>= 1) {
+                        for (int t = tid; t < P; t += G::kThreads) {
+                            const int u = t ^ j;
+                            if (u > t) {
+                                const bool up = (t & k) == 0;
+                                const unsigned long long ka = sm.sort.key[t], kb = sm.sort.key[u];
+                                const int ga = sm.sort.gid[t], gb = sm.sort.gid[u];
+                                const bool b_less = kb < ka || (kb == ka && gb < ga);
+                                const bool a_less = ka < kb || (ka == kb && ga < gb);
+                                if (up ? b_less : a_less) {
+                                    sm.sort.key[t] = kb;
+                                    sm.sort.key[u] = ka;
+                                    sm.sort.gid[t] = gb;
+                                    sm.sort.gid[u] = ga;
                                 }
                             }
-                            __syncthreads();
                         }
+                        __syncthreads();
                     }
-                    for (int t = tid; t < n; t += G::kThreads) s_ord[t] = s_gid[t];
                 }
+                for (int t = tid; t < n; t += G::kThreads) s_ord[t] = sm.sort.gid[t];
             }
             __syncthreads();
             if (a.write_lists)
@@ -218,11 +267,12 @@ __global__ void __launch_bounds__(TILE * TILE) k_composite(CompositeArgs a) {
         const float bylo = static_cast<float>(by) + 0.5f, byhi = static_cast<float>(by) + 3.5f;
         // accept = a > alpha_floor, or a > 0 without a positive floor (rasterizer.cpp:133)
         const float thr = a.floor_positive ? a.alpha_floor : 0.0f;
+        const float clamp = a.alpha_clamp;
 
         for (int base = 0; base < n; base += kStage) {
             const int cnt = (n - base) < kStage ? (n - base) : kStage;
-            // stage sorted records: tile-relative centre (formed in f64), conic, alpha
-            // (times rho in soft mode), accept-ellipse box, channel phasors
+            // stage sorted records: tile-relative centre (formed in f64), conic,
+            // log2(alpha) (times rho in soft mode), channel phasors, accept box
             for (int t = tid; t < cnt; t += G::kThreads) {
                 const int g = presorted ? a.egidx[e0 + base + t] : s_ord[base + t];
                 const GRec r = a.rec[g];
@@ -233,50 +283,60 @@ __global__ void __launch_bounds__(TILE * TILE) k_composite(CompositeArgs a) {
                     alpha = static_cast<float>(static_cast<double>(r.alpha) * a.rho[static_cast<size_t>(g) * a.L + plane]);
                 Staged st;
                 st.a = make_float4(mx, my, r.ca, r.cb);
-                st.b = make_float4(r.cc, alpha, my - r.hy, my + r.hy);
-                st.c = make_float4(mx - r.hx, mx + r.hx, r.col[0], r.col[1]);
-                st.d = make_float4(r.col[2], r.col[3], r.col[4], r.col[5]);
-                s_rec[t] = st;
+                st.b = make_float4(r.cc, log2f(alpha), r.col[0], r.col[1]);
+                st.c = make_float4(r.col[2], r.col[3], r.col[4], r.col[5]);
+                sm.st.rec[t] = st;
+                sm.st.box[t] = make_float4(mx - r.hx, mx + r.hx, my - r.hy, my + r.hy);
             }
             __syncthreads();
             if (!__all_sync(0xffffffffu, done)) {
                 // 32 entries at a time: each lane tests one entry's accept box against
                 // this warp's 8x4 block of pixel centres; the warp walks the hits in
-                // order, branch-free per lane (predicated accept).
+                // order, two per step, branch-free per lane (predicated accept).
                 for (int c0 = 0; c0 < cnt; c0 += 32) {
                     bool hit = false;
                     if (c0 + lane < cnt) {
-                        const float4 Bb = s_rec[c0 + lane].b;
-                        const float4 Cb = s_rec[c0 + lane].c;
-                        hit = !(Cb.y < bxlo || Cb.x > bxhi || Bb.w < bylo || Bb.z > byhi);
+                        const float4 bb = sm.st.box[c0 + lane];
+                        hit = !(bb.y < bxlo || bb.x > bxhi || bb.w < bylo || bb.z > byhi);
                     }
                     unsigned mask = __ballot_sync(0xffffffffu, hit);
+#ifdef HOLO_COUNT
+                    unsigned long long n_eval = 0, n_any = 0, n_acc = 0;
+#endif
                     while (mask) {
-                        const Staged* e = &s_rec[c0 + __ffs(mask) - 1];
+                        const Staged* e0p = &sm.st.rec[c0 + __ffs(mask) - 1];
                         mask &= mask - 1;
-                        const float4 A = e->a;
-                        const float4 B = e->b;
-                        const float dx = fx - A.x, dy = fy - A.y;
-                        const float q = dx * fmaf(A.z, dx, A.w * dy) + B.x * dy * dy;
-                        const float al = fminf(B.y * ex2_approx(q), a.alpha_clamp);
-                        const bool accept = (al > thr) && !done;
-                        const float w = accept ? al * T : 0.0f;
-                        const float4 Cc = e->c;
-                        acc[0] = fmaf(w, Cc.z, acc[0]);
-                        acc[1] = fmaf(w, Cc.w, acc[1]);
-                        if (C > 1) {
-                            const float4 D = e->d;
-                            acc[2 % (2 * C)] = fmaf(w, D.x, acc[2 % (2 * C)]);
-                            acc[3 % (2 * C)] = fmaf(w, D.y, acc[3 % (2 * C)]);
-                            if (C > 2) {
-                                acc[4 % (2 * C)] = fmaf(w, D.z, acc[4 % (2 * C)]);
-                                acc[5 % (2 * C)] = fmaf(w, D.w, acc[5 % (2 * C)]);
-                            }
-                        }
-                        T -= w;  // T (1 - a)
-                        contrib += accept ? 1 : 0;
-                        done = done || (T < a.term_eps);
+                        const bool two = mask != 0;
+                        const Staged* e1p = &sm.st.rec[c0 + (two ? __ffs(mask) - 1 : 0)];
+                        mask &= mask - 1;
+                        float4 B0, B1;
+                        const float al0 = eval_alpha(e0p, fx, fy, clamp, B0);
+                        const float al1 = eval_alpha(e1p, fx, fy, clamp, B1);
+                        const bool acc0 = (al0 > thr) && (T >= eps);
+                        const float w0 = acc0 ? al0 * T : 0.0f;
+                        blend<C>(e0p, B0, w0, acc);
+                        T -= w0;  // T (1 - a)
+                        contrib += acc0 ? 1 : 0;
+                        const bool acc1 = two && (al1 > thr) && (T >= eps);
+                        const float w1 = acc1 ? al1 * T : 0.0f;
+                        blend<C>(e1p, B1, w1, acc);
+                        T -= w1;
+                        contrib += acc1 ? 1 : 0;
+#ifdef HOLO_COUNT
+                        n_eval += two ? 2 : 1;
+                        n_any += (__ballot_sync(0xffffffffu, acc0) ? 1 : 0) + (__ballot_sync(0xffffffffu, acc1) ? 1 : 0);
+                        n_acc += __popc(__ballot_sync(0xffffffffu, acc0)) + __popc(__ballot_sync(0xffffffffu, acc1));
+#endif
                     }
+#ifdef HOLO_COUNT
+                    if (lane == 0) {
+                        atomicAdd(&g_counts[0], n_eval);
+                        atomicAdd(&g_counts[1], n_any);
+                        atomicAdd(&g_counts[2], n_acc);
+                        atomicAdd(&g_counts[3], 1ull);
+                    }
+#endif
+                    done = !inside || !(T >= eps);
                     if (__all_sync(0xffffffffu, done)) break;
                 }
             }
@@ -296,6 +356,14 @@ __global__ void __launch_bounds__(TILE * TILE) k_composite(CompositeArgs a) {
     }
 }
 
+#ifdef HOLO_COUNT
+__global__ void k_print_counts() {
+    printf("composite counts: warp-evals %llu, with any accept %llu, accepted lanes %llu, chunks %llu\n",
+           g_counts[0], g_counts[1], g_counts[2], g_counts[3]);
+    for (int i = 0; i < 4; ++i) g_counts[i] = 0;
+}
+#endif
+
 template <int TILE>
 void launch_tile(holo_ctx* ctx, const CompositeArgs& a) {
     if (a.num_buckets <= 0) return;
@@ -308,9 +376,19 @@ void launch_tile(holo_ctx* ctx, const CompositeArgs& a) {
         default: throw Error(HOLO_ERR_CONFIG, "render supports 1 to 3 wavelength channels");
     }
     HC_LAUNCHED(ctx);
+#ifdef HOLO_COUNT
+    k_print_counts<<<1, 1, 0, ctx->stream>>>();
+#endif
 }
 
 }  // namespace
+
+void sort_small_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsigned capacity,
+                        const unsigned long long* ekey, int* egidx) {
+    if (B <= 0) return;
+    k_sort_small<<<static_cast<unsigned>((B + 7) / 8), 256, 0, ctx->stream>>>(bstart, B, capacity, ekey, egidx);
+    HC_LAUNCHED(ctx);
+}
 
 void composite(holo_ctx* ctx, const CompositeArgs& a, int tile) {
     switch (tile) {

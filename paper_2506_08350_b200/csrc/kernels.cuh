@@ -106,7 +106,8 @@ void host_world_to_cam(const holo_camera& cam, double wc[9]);
 void preprocess(holo_ctx* ctx, const CameraConsts& cc, const holo_raster_settings& st, double near_clip, int L,
                 int tiles_x, int tiles_y, const PreOut& out);
 
-constexpr int kSortCap = 1024;  // largest bucket the compositing CTA sorts in shared memory
+constexpr int kSortCap = 1024;     // largest bucket the compositing CTA sorts in shared memory
+constexpr int kWarpSortCap = 128;  // buckets up to this size are sorted one warp each (k_sort_small)
 
 // ---- binning.cu
 void exclusive_scan_u32(holo_ctx* ctx, const unsigned* in, unsigned* out, long long n, unsigned* d_max);
@@ -141,7 +142,6 @@ struct CompositeArgs {
     const double* rho;        // soft mode weights or null
     int L, C, W, H, tiles_x, num_tiles, plane_begin, num_buckets;
     int soft, write_lists;
-    int pack_ok;              // N < 2^24: a bucket slot fits under gidx in a 31-bit tie-break key
     unsigned capacity;        // entry-buffer size: bucket ranges are clamped to it (overflowed async frames)
     float term_eps, alpha_floor, alpha_clamp;
     int floor_positive;
@@ -150,5 +150,8 @@ struct CompositeArgs {
     int* n_contrib;           // optional
 };
 void composite(holo_ctx* ctx, const CompositeArgs& a, int tile);
+// (zc, gidx) order for buckets of 2..kWarpSortCap entries, written back to egidx
+void sort_small_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsigned capacity,
+                        const unsigned long long* ekey, int* egidx);
 
 }  // namespace holo_cuda

@@ -1,0 +1,11 @@
+#!/bin/bash
+# Build libholo_cuda with extra -D flags in a scratch copy and print the bench stage times.
+# usage: tools/variant_bench.sh "<EXTRA_NVFLAGS>" <label>
+set -e
+src=$(pwd)
+dst=/tmp/variant_$2
+rm -rf $dst && cp -a $src $dst && cd $dst
+touch paper_2506_08350_b200/csrc/${3:-composite}.cu
+make -C paper_2506_08350_b200/csrc -j16 EXTRA_NVFLAGS="$1" > /dev/null
+python bench.py --steps 30 --warmup 5 --no-cpu-baseline --inflight 1 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.readline()); print('$2', round(d['ms_per_step'],4), {k: round(v['ms'],4) for k,v in d['stages'].items()})"
