@@ -760,8 +760,8 @@ void render_back(holo_ctx* ctx, const holo_wave& wave, const holo_prop_options& 
     const int has_holo = (outputs & HOLO_OUT_HOLOGRAM) ? 1 : 0;
     if (static_render_supported(W, H)) {
         ctx->stage_begin();
-        static_row(ctx, kModeReplay, nullptr, const_cast<cx<float>*>(spec), stage, W, H, C, np, O, d_plane_of, tfc,
-                   wave.pitch);
+        static_row(ctx, kModeReplay, nullptr, const_cast<cx<float>*>(spec), stage, W, H, C, np, has_holo,
+                   O - has_holo, tfc, wave.pitch, po.local_band_limit != 0);
         ctx->stage_end(5);
         ctx->stage_begin();
         static_col_inv(ctx, stage, W, H, C, O, has_holo, ob.holo, ob.rep, ob.ints);
@@ -821,17 +821,18 @@ void render_front(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, 
         ctx->stage_end(3);
         if (!full) {
             ctx->stage_begin();
-            static_row(ctx, kModeSpec, work, spec, nullptr, g.W, g.H, g.C, np, 0, nullptr, tfc, wave.pitch);
+            static_row(ctx, kModeSpec, work, spec, nullptr, g.W, g.H, g.C, np, 0, 0, tfc, wave.pitch,
+                       po.local_band_limit != 0);
             ctx->stage_end(4);
             return;
         }
         const int O = static_cast<int>(plane_of.size());
-        int* d_plane_of = buf<int>(ctx, "plane_of_render", O);
-        upload_small(ctx, d_plane_of, plane_of.data(), sizeof(int) * O);
+        const int has_holo = (outputs & HOLO_OUT_HOLOGRAM) ? 1 : 0;
         cx<float>* stage = buf<cx<float>>(ctx, "replay_stage", static_cast<size_t>(O) * g.C * g.P);
         const OutBufs ob = output_buffers(ctx, outputs, np, g.C, g.P);
         ctx->stage_begin();
-        static_row(ctx, kModeFull, work, nullptr, stage, g.W, g.H, g.C, np, O, d_plane_of, tfc, wave.pitch);
+        static_row(ctx, kModeFull, work, nullptr, stage, g.W, g.H, g.C, np, has_holo, O - has_holo, tfc, wave.pitch,
+                   po.local_band_limit != 0);
         ctx->stage_end(4);
         ctx->stage_begin();
         static_col_inv(ctx, stage, g.W, g.H, g.C, O, (outputs & HOLO_OUT_HOLOGRAM) ? 1 : 0, ob.holo, ob.rep,

@@ -183,6 +183,38 @@ struct DftCT {
     }
 };
 
+// R = A * B with gcd(A, B) = 1 by Good-Thomas (prime-factor) indexing: no internal
+// twiddles.  n = (B a + A b) mod R, k = (B <B^-1>_A k1 + A <A^-1>_B k2) mod R, so
+// exp(2 pi i n k / R) = exp(2 pi i a k1 / A) exp(2 pi i b k2 / B).
+template <int A, int B, int DIR, class T>
+struct DftPFA {
+    static constexpr int inv_mod(int x, int m) {
+        int r = 1;
+        while ((x * r) % m != 1) ++r;
+        return r;
+    }
+    static __host__ __device__ __forceinline__ void run(cx<T>* v) {
+        constexpr int R = A * B;
+        constexpr int CA = B * inv_mod(B % A, A), CB = A * inv_mod(A % B, B);
+        cx<T> y[R];  // y[k1 * B + b]
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            cx<T> u[A];
+#pragma unroll
+            for (int a = 0; a < A; ++a) u[a] = v[(B * a + A * b) % R];
+            Dft<A, DIR, T>::run(u);
+#pragma unroll
+            for (int k1 = 0; k1 < A; ++k1) y[k1 * B + b] = u[k1];
+        }
+#pragma unroll
+        for (int k1 = 0; k1 < A; ++k1) {
+            Dft<B, DIR, T>::run(y + k1 * B);
+#pragma unroll
+            for (int k2 = 0; k2 < B; ++k2) v[(CA * k1 + CB * k2) % R] = y[k1 * B + k2];
+        }
+    }
+};
+
 // direct DFT for the odd primes 7..31
 template <int R, int DIR, class T>
 struct DftDirect {
@@ -200,13 +232,13 @@ struct DftDirect {
     }
 };
 
-template <int DIR, class T> struct Dft<6, DIR, T> : DftCT<2, 3, DIR, T> {};
+template <int DIR, class T> struct Dft<6, DIR, T> : DftPFA<2, 3, DIR, T> {};
 template <int DIR, class T> struct Dft<8, DIR, T> : DftCT<2, 4, DIR, T> {};
 template <int DIR, class T> struct Dft<9, DIR, T> : DftCT<3, 3, DIR, T> {};
-template <int DIR, class T> struct Dft<10, DIR, T> : DftCT<2, 5, DIR, T> {};
-template <int DIR, class T> struct Dft<12, DIR, T> : DftCT<3, 4, DIR, T> {};
-template <int DIR, class T> struct Dft<14, DIR, T> : DftCT<2, 7, DIR, T> {};
-template <int DIR, class T> struct Dft<15, DIR, T> : DftCT<3, 5, DIR, T> {};
+template <int DIR, class T> struct Dft<10, DIR, T> : DftPFA<2, 5, DIR, T> {};
+template <int DIR, class T> struct Dft<12, DIR, T> : DftPFA<3, 4, DIR, T> {};
+template <int DIR, class T> struct Dft<14, DIR, T> : DftPFA<2, 7, DIR, T> {};
+template <int DIR, class T> struct Dft<15, DIR, T> : DftPFA<3, 5, DIR, T> {};
 template <int DIR, class T> struct Dft<16, DIR, T> : DftCT<4, 4, DIR, T> {};
 template <int DIR, class T> struct Dft<7, DIR, T> : DftDirect<7, DIR, T> {};
 template <int DIR, class T> struct Dft<11, DIR, T> : DftDirect<11, DIR, T> {};

@@ -130,8 +130,9 @@ bool static_render_supported(int W, int H);
 void static_col_fwd(holo_ctx* ctx, cx<float>* data, int W, int H, int nfields);
 void static_col_inv(holo_ctx* ctx, const cx<float>* in, int W, int H, int C, int nout, int has_holo,
                     cx<float>* holo, cx<float>* rep, float* intens);
+// outputs of modes FULL / REPLAY: [hologram if has_holo] then planes 0..nrep-1
 void static_row(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spec, cx<float>* out, int W, int H,
-                int C, int Lloc, int nout, const int* plane_of, const TfChan* tfc, double pitch);
+                int C, int Lloc, int has_holo, int nrep, const TfChan* tfc, double pitch, bool local);
 
 // ---- composite.cu
 struct CompositeArgs {

@@ -52,7 +52,6 @@ template <int W_, int NBR_, int NT_, int MINB_>
 struct RowCfgT {
     static constexpr int W = W_, NBR = NBR_, NT = NT_, kMinBlocks = MINB_;
     using B = Batch<W, NBR, NT>;
-    static constexpr size_t kSmem = sizeof(cx<float>) * B::kSmemElems;
 };
 template <int W>
 using RowCfg = RowCfgT<W, (W <= 512 ? 4 : (W <= 2048 ? 2 : 1)), (W >= 1024 ? 256 : 128), 2>;
@@ -99,24 +98,99 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_col_fwd(cx<float>*
 
 // ---------------------------------------------------------------- 2. row pass with the spectrum in registers
 
+// Bulk (TMA) copies global -> shared completing on an mbarrier.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+// Row-pass shared memory: FFT work area, two prefetch buffers of NBR rows (each
+// row padded by 8 complex = 16 banks, FULL / SPEC), per-plane TF constants.
 template <class Cfg, int MODE>
+struct RowSmem {
+    static constexpr int kRowPad = Cfg::W + 8;
+    static constexpr size_t kWork = sizeof(cx<float>) * Cfg::B::kSmemElems;
+    static constexpr size_t kPre = MODE == kModeReplay ? 0 : sizeof(cx<float>) * 2 * Cfg::NBR * kRowPad;
+    static size_t bytes(int Lloc) { return kWork + kPre + sizeof(float2) * (Lloc > 0 ? Lloc : 1); }
+};
+
+template <class Cfg, int MODE, bool LOCAL>
 __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
     const cx<float>* __restrict__ layers,  // [Lloc][C][H][W], column-transformed (FULL, SPEC)
     cx<float>* __restrict__ spec,          // [C][H][W]: written (SPEC) or read (REPLAY)
     cx<float>* __restrict__ out,           // [O][C][H][W] row-inverse-transformed outputs (FULL, REPLAY)
-    int H, int C, int Lloc, int nout, const int* __restrict__ plane_of, const TfChan* __restrict__ tfc,
+    int H, int C, int Lloc, int has_holo, int nrep, const TfChan* __restrict__ tfc,
     const double* __restrict__ fx, const double* __restrict__ fy, const cx<float>* __restrict__ tw) {
     constexpr int W = Cfg::W;
+    constexpr int NBR = Cfg::NBR;
     using B = typename Cfg::B;
     using P = typename PlanOf<W>::type;
     using Pinv = typename RevPlan<P>::type;
     using LS = LastStage<B, P>;
+    using SM = RowSmem<Cfg, MODE>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<float>* sm = reinterpret_cast<cx<float>*>(smem_raw);
+    cx<float>* pre = reinterpret_cast<cx<float>*>(smem_raw + SM::kWork);
+    float2* s_tf = reinterpret_cast<float2*>(smem_raw + SM::kWork + SM::kPre);  // (phase0, 2 pi z) per plane
+    __shared__ unsigned long long s_bar[2];
 
-    const int row0 = blockIdx.x * Cfg::NBR;  // row = c * H + y; a CTA never spans two channels
+    const int row0 = blockIdx.x * NBR;  // row = c * H + y; a CTA never spans two channels
     const int c = row0 / H;
     const size_t plane_stride = static_cast<size_t>(C) * H * W;
+    const int nplanes = MODE == kModeReplay ? nrep : Lloc;
+    for (int l = threadIdx.x; l < nplanes; l += Cfg::NT) s_tf[l] = make_float2(tfc[l * C + c].phase0, tfc[l * C + c].two_pi_z_f);
+
+    // prefetch of plane l's NBR rows into buffer l & 1 (one thread issues)
+    auto issue = [&](int l) {
+        const int bsel = l & 1;
+        const cx<float>* src = layers + l * plane_stride + static_cast<size_t>(row0) * W;
+        fence_proxy_async_smem();  // the buffer's previous generic reads precede the async writes
+        mbar_expect_tx(&s_bar[bsel], NBR * W * static_cast<unsigned>(sizeof(cx<float>)));
+#pragma unroll
+        for (int b = 0; b < NBR; ++b)
+            bulk_g2s(pre + (bsel * NBR + b) * SM::kRowPad, src + static_cast<size_t>(b) * W,
+                     W * static_cast<unsigned>(sizeof(cx<float>)), &s_bar[bsel]);
+    };
+    if constexpr (MODE != kModeReplay) {
+        if (threadIdx.x == 0) {
+            mbar_init(&s_bar[0], 1);
+            mbar_init(&s_bar[1], 1);
+            mbar_init_fence();
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && Lloc > 0) issue(0);
+    } else {
+        __syncthreads();
+    }
 
     // (q, r) <-> (b, i) of the last forward stage = first inverse stage
     auto owner = [&](int q, int r, int& b, int& i) -> bool {
@@ -151,19 +225,28 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
                 }
             }
     }
-    auto tf = [&](const TfChan& p, int q, int r, int b, int i) -> cx<float> {
-        if (p.local) return tf_value<float>(p, fx[i], fy[(row0 + b) - c * H]);
+    // H_{Z_l} at owned sample (q, r): the plane-independent part G and the plane's
+    // (phase0, 2 pi z); local band limits (rare) take the full f64 path
+    auto tf = [&](int l, int q, int r, int b, int i) -> cx<float> {
+        if constexpr (LOCAL) {
+            const TfChan p = tfc[l * C + c];
+            if (p.local) return tf_value<float>(p, fx[i], fy[(row0 + b) - c * H]);
+        }
         const float g = G[q][r];
         if (g < 0.0f) return czf();
-        return phasor_reduced(p.phase0 - p.two_pi_z_f * g);
+        const float2 t = s_tf[l];
+        return phasor_reduced(t.x - t.y * g);
     };
 
     if constexpr (MODE != kModeReplay) {
         for (int l = 0; l < Lloc; ++l) {
-            const TfChan p = tfc[l * C + c];
-            const cx<float>* src = layers + l * plane_stride + static_cast<size_t>(row0) * W;
-            auto load = [&](int, int, int b, int i) -> cx<float> { return src[static_cast<size_t>(b) * W + i]; };
-            auto store = [&](int q, int r, int b, int i, cx<float> v) { S[q][r] = S[q][r] + v * tf(p, q, r, b, i); };
+            // buffer (l + 1) & 1 was last read by plane l - 1's first stage, which
+            // ended with a barrier
+            if (threadIdx.x == 0 && l + 1 < Lloc) issue(l + 1);
+            mbar_wait(&s_bar[l & 1], (l >> 1) & 1);
+            const cx<float>* src = pre + (l & 1) * NBR * SM::kRowPad;
+            auto load = [&](int, int, int b, int i) -> cx<float> { return src[b * SM::kRowPad + i]; };
+            auto store = [&](int q, int r, int b, int i, cx<float> v) { S[q][r] = S[q][r] + v * tf(l, q, r, b, i); };
             fft_static<float, -1, B, P>(sm, tw, load, store);
         }
     }
@@ -188,15 +271,16 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
                 if (owner(q, r, b, i)) S[q][r] = srcs[static_cast<size_t>(b) * W + i];
             }
     }
-    for (int o = 0; o < nout; ++o) {
-        const int l = plane_of[o];
-        TfChan p;
-        if (l >= 0) p = tfc[l * C + c];
-        cx<float>* dst = out + (static_cast<size_t>(o) * C * H + row0) * W;
-        auto load = [&](int q, int r, int b, int i) -> cx<float> {
-            if (l < 0) return S[q][r];
-            return S[q][r] * conj(tf(p, q, r, b, i));
-        };
+    // outputs: [hologram] then planes 0..nrep-1 (output_planes in capi.cu)
+    if (has_holo) {
+        cx<float>* dst = out + static_cast<size_t>(row0) * W;
+        auto load = [&](int q, int r, int, int) -> cx<float> { return S[q][r]; };
+        auto store = [&](int, int, int b, int i, cx<float> v) { dst[static_cast<size_t>(b) * W + i] = v; };
+        fft_static<float, +1, B, Pinv>(sm, tw, load, store);
+    }
+    for (int l = 0; l < nrep; ++l) {
+        cx<float>* dst = out + (static_cast<size_t>(l + has_holo) * C * H + row0) * W;
+        auto load = [&](int q, int r, int b, int i) -> cx<float> { return S[q][r] * conj(tf(l, q, r, b, i)); };
         auto store = [&](int, int, int b, int i, cx<float> v) { dst[static_cast<size_t>(b) * W + i] = v; };
         fft_static<float, +1, B, Pinv>(sm, tw, load, store);
     }
@@ -265,30 +349,32 @@ void launch_col_inv_cfg(holo_ctx* ctx, const cx<float>* in, int W, int C, int no
     HC_LAUNCHED(ctx);
 }
 
+template <class Cfg, int MODE, bool LOCAL>
+void launch_row_mode(holo_ctx* ctx, const cx<float>* layers, cx<float>* spec, cx<float>* out, int H, int C, int Lloc,
+                     int has_holo, int nrep, const TfChan* tfc, const double* fx, const double* fy) {
+    const dim3 grid(C * H / Cfg::NBR);
+    const int nplanes = MODE == kModeReplay ? nrep : Lloc;
+    const size_t smem = RowSmem<Cfg, MODE>::bytes(nplanes);
+    HC_CUDA(cudaFuncSetAttribute(k_row_fused<Cfg, MODE, LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    k_row_fused<Cfg, MODE, LOCAL><<<grid, Cfg::NT, smem, ctx->stream>>>(
+        layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, ctx->twiddle<float>(Cfg::W));
+    HC_LAUNCHED(ctx);
+}
+
 template <class Cfg>
 void launch_row_cfg(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spec, cx<float>* out, int H, int C,
-                    int Lloc, int nout, const int* plane_of, const TfChan* tfc, const double* fx, const double* fy) {
-    const int rows = C * H;
-    const dim3 grid(rows / Cfg::NBR);
-    const cx<float>* tw = ctx->twiddle<float>(Cfg::W);
+                    int Lloc, int has_holo, int nrep, const TfChan* tfc, const double* fx, const double* fy,
+                    bool local) {
+#define HC_ROW_MODE(M)                                                                                      \
+    (local ? launch_row_mode<Cfg, M, true>(ctx, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy) \
+           : launch_row_mode<Cfg, M, false>(ctx, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy))
     switch (mode) {
-        case kModeFull:
-            smem_attr(k_row_fused<Cfg, kModeFull>, Cfg::kSmem);
-            k_row_fused<Cfg, kModeFull><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(
-                layers, spec, out, H, C, Lloc, nout, plane_of, tfc, fx, fy, tw);
-            break;
-        case kModeSpec:
-            smem_attr(k_row_fused<Cfg, kModeSpec>, Cfg::kSmem);
-            k_row_fused<Cfg, kModeSpec><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(
-                layers, spec, out, H, C, Lloc, nout, plane_of, tfc, fx, fy, tw);
-            break;
-        default:
-            smem_attr(k_row_fused<Cfg, kModeReplay>, Cfg::kSmem);
-            k_row_fused<Cfg, kModeReplay><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(
-                layers, spec, out, H, C, Lloc, nout, plane_of, tfc, fx, fy, tw);
-            break;
+        case kModeFull: HC_ROW_MODE(kModeFull); break;
+        case kModeSpec: HC_ROW_MODE(kModeSpec); break;
+        default: HC_ROW_MODE(kModeReplay); break;
     }
-    HC_LAUNCHED(ctx);
+#undef HC_ROW_MODE
 }
 
 template <int H>
@@ -320,16 +406,8 @@ void launch_col_inv(holo_ctx* ctx, const cx<float>* in, int W, int C, int nout, 
 
 template <int W>
 void launch_row(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spec, cx<float>* out, int H, int C,
-                int Lloc, int nout, const int* plane_of, const TfChan* tfc, const double* fx, const double* fy) {
-    if constexpr (W == 1920) {
-        switch (env_variant("HOLO_ROW_VARIANT")) {
-            case 1: return launch_row_cfg<RowCfgT<W, 1, 128, 4>>(ctx, mode, layers, spec, out, H, C, Lloc, nout, plane_of, tfc, fx, fy);
-            case 2: return launch_row_cfg<RowCfgT<W, 4, 512, 1>>(ctx, mode, layers, spec, out, H, C, Lloc, nout, plane_of, tfc, fx, fy);
-            case 3: return launch_row_cfg<RowCfgT<W, 2, 256, 1>>(ctx, mode, layers, spec, out, H, C, Lloc, nout, plane_of, tfc, fx, fy);
-            default: break;
-        }
-    }
-    launch_row_cfg<RowCfg<W>>(ctx, mode, layers, spec, out, H, C, Lloc, nout, plane_of, tfc, fx, fy);
+                int Lloc, int has_holo, int nrep, const TfChan* tfc, const double* fx, const double* fy, bool local) {
+    launch_row_cfg<RowCfg<W>>(ctx, mode, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, local);
 }
 
 #define HC_SIZES(X) X(48) X(64) X(128) X(256) X(512) X(1024) X(1080) X(1920) X(2048) X(2160) X(3840)
@@ -393,12 +471,12 @@ void static_col_inv(holo_ctx* ctx, const cx<float>* in, int W, int H, int C, int
 }
 
 void static_row(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spec, cx<float>* out, int W, int H,
-                int C, int Lloc, int nout, const int* plane_of, const TfChan* tfc, double pitch) {
+                int C, int Lloc, int has_holo, int nrep, const TfChan* tfc, double pitch, bool local) {
     const double* fx = ctx->freq(W, pitch);
     const double* fy = ctx->freq(H, pitch);
 #define HC_CASE(N)                                                                               \
     case N:                                                                                      \
-        launch_row<N>(ctx, mode, layers, spec, out, H, C, Lloc, nout, plane_of, tfc, fx, fy); \
+        launch_row<N>(ctx, mode, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, local); \
         return;
     switch (W) {
         HC_SIZES(HC_CASE)
