@@ -201,6 +201,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
     ap.add_argument("--inflight", type=int, default=2, help="frames in flight (contexts / streams) at N=1")
+    ap.add_argument("--e2e-inflight", type=int, default=1, help="frames in flight in the end-to-end run at N=1")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -344,39 +345,68 @@ def main():
                 (hbm_peak * world)}
 
     # ---------------- end to end through the public API: pinned host scene in, results out
+    # Every frame uploads the scene from pinned host memory and reads the hologram
+    # and intensities back.  At N = 1 the frames rotate over `inflight` contexts on
+    # their own streams, so one frame's upload, another's compute and a third's
+    # download overlap on the two copy engines; at N > 1 each rank runs its shard
+    # frame by frame.
     e2e = None
     if rank == 0 or world > 1:
         arrays = [np.ascontiguousarray(a, dtype=np.float64) for a in
                   (scene.positions, scene.rotations, scene.log_scales, scene.amplitudes, scene.opacity_logits,
                    scene.phases, scene.plane_logits)]
         pinned = [torch.from_numpy(a).pin_memory() for a in arrays]
+        ptrs = [p.data_ptr() for p in pinned]
         h2d = sum(a.nbytes for a in arrays)
-        holo_h = torch.empty(Cn * P * 2, dtype=torch.float32).pin_memory()
-        int_h = torch.empty((pe - pb) * Cn * P, dtype=torch.float32).pin_memory()
-        d2h = int_h.numel() * 4 + (holo_h.numel() * 4 if rank == 0 else 0)
-        n_e2e = min(args.steps, 20)
+        n_e2e = max(20, min(args.steps, 60))
+        nctx = max(1, args.e2e_inflight) if world == 1 else 1
+        ectxs = [Context(local, use_torch_stream=False) for _ in range(nctx)] if world == 1 else [ctx]
+        bufs = []
+        for cx_ in ectxs:
+            holo_h = torch.empty(Cn * P * 2, dtype=torch.float32).pin_memory() if rank == 0 else None
+            int_h = torch.empty((pe - pb) * Cn * P, dtype=torch.float32).pin_memory()
+            bufs.append((holo_h, int_h))
+        d2h = bufs[0][1].numel() * 4 + (bufs[0][0].numel() * 4 if rank == 0 else 0)
 
-        def e2e_step():
-            ctx.upload_scene_pointers(c.n, Lp, [p.data_ptr() for p in pinned], device=False)
-            frame()
-            if rank == 0:
-                ctx.download_into(L.BUF_HOLOGRAM, holo_h.data_ptr(), holo_h.numel() * 4)
-            ctx.download_into(L.BUF_INTENSITY, int_h.data_ptr(), int_h.numel() * 4)
+        def e2e_step(i):
+            cx_ = ectxs[i % len(ectxs)]
+            holo_h, int_h = bufs[i % len(ectxs)]
+            cx_.upload_scene_pointers(c.n, Lp, ptrs, device=False)
+            if world == 1:
+                cx_.render(cam, wave, None, None, outputs=outs)
+            else:
+                frame()
+            if holo_h is not None:
+                cx_.download_into(L.BUF_HOLOGRAM, holo_h.data_ptr(), holo_h.numel() * 4, wait=False)
+            cx_.download_into(L.BUF_INTENSITY, int_h.data_ptr(), int_h.numel() * 4, wait=False)
 
-        for _ in range(2):
-            e2e_step()
+        for i in range(len(ectxs)):  # synchronous first frames size the buffers, then asynchronous
+            e2e_step(i)
+            ectxs[i].synchronize()
+            ectxs[i].set_async(True)
+        for i in range(len(ectxs)):
+            e2e_step(i)
+        for cx_ in ectxs:
+            cx_.synchronize()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        for _ in range(n_e2e):
-            e2e_step()
+        for i in range(n_e2e):
+            e2e_step(i)
+        for cx_ in ectxs:
+            cx_.synchronize()
         torch.cuda.synchronize()
         el = torch.tensor([time.perf_counter() - t0], device=f"cuda:{local}")
+        for cx_ in ectxs:
+            cx_.frame_status()
         if world > 1:
             dist.all_reduce(el, op=dist.ReduceOp.MAX)
         e2e = {"value": n_e2e / float(el.item()), "unit": "frames/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "steps": n_e2e}
+               "d2h_bytes_per_step": d2h, "steps": n_e2e, "frames_in_flight": len(ectxs)}
+        if world == 1:
+            for cx_ in ectxs:
+                cx_.close()
 
     # ---------------- CPU baseline (rank 0, N = 1 only)
     cpu = None

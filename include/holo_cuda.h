@@ -158,6 +158,9 @@ int holo_ctx_set_stream(holo_ctx* ctx, void* stream);
 /* Back to the context's own non-blocking stream. */
 int holo_ctx_use_own_stream(holo_ctx* ctx);
 void* holo_ctx_get_stream(holo_ctx* ctx);
+/* The context's copy streams (0: host uploads, 1: asynchronous downloads), for
+ * callers that order their own work after them. */
+void* holo_ctx_get_copy_stream(holo_ctx* ctx, int which);
 int holo_ctx_synchronize(holo_ctx* ctx);
 /* Optional per-stage CUDA-event timing (ms), accumulated over renders until reset.
  * Stage ids: 0 preprocess, 1 binning, 2 composite, 3 row FFT, 4 column forward,
@@ -214,6 +217,9 @@ int holo_render_end(holo_ctx* ctx, const holo_wave* wave, const holo_prop_option
 int holo_frame_buffer(holo_ctx* ctx, int buffer, void** dev_ptr, size_t* bytes);
 /* Synchronous device-to-host copy of one output buffer (bytes must match). */
 int holo_frame_download(holo_ctx* ctx, int buffer, void* host, size_t bytes);
+/* The same copy enqueued on the context stream (pinned host memory overlaps it
+ * with other streams' work); complete after holo_ctx_synchronize. */
+int holo_frame_download_async(holo_ctx* ctx, int buffer, void* host, size_t bytes);
 
 /* ---- operators on device fields (propagation.hpp:27-40, fft.hpp:11-12, field.hpp:45) ---- */
 /* fft2 / ifft2 (fft.cpp:33-44): in place, batch fields of h x w; inverse carries 1/(w h). */

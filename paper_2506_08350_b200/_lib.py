@@ -102,6 +102,7 @@ def lib() -> C.CDLL:
         "holo_ctx_set_stream": (i, [vp, vp]),
         "holo_ctx_use_own_stream": (i, [vp]),
         "holo_ctx_get_stream": (vp, [vp]),
+        "holo_ctx_get_copy_stream": (vp, [vp, i]),
         "holo_ctx_synchronize": (i, [vp]),
         "holo_ctx_enable_timing": (i, [vp, i]),
         "holo_ctx_stage_times": (i, [vp, P(d), P(i), i]),
@@ -118,6 +119,7 @@ def lib() -> C.CDLL:
         "holo_render_end": (i, [vp, P(Wave), P(PropOptions), i, i, vp, u]),
         "holo_frame_buffer": (i, [vp, i, P(vp), P(sz)]),
         "holo_frame_download": (i, [vp, i, vp, sz]),
+        "holo_frame_download_async": (i, [vp, i, vp, sz]),
         "holo_fft2": (i, [vp, vp, i, i, i, i, i]),
         "holo_transfer_function": (i, [vp, P(Wave), d, P(PropOptions), vp, i]),
         "holo_propagate": (i, [vp, vp, vp, i, i, i, P(Wave), d, P(PropOptions), i]),

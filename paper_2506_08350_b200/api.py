@@ -135,6 +135,10 @@ class Context:
     def stream(self) -> int:
         return int(self.lib.holo_ctx_get_stream(self.h) or 0)
 
+    def copy_stream(self, which: int) -> int:
+        """Copy stream handle: 0 = host uploads, 1 = asynchronous downloads."""
+        return int(self.lib.holo_ctx_get_copy_stream(self.h, int(which)) or 0)
+
     def synchronize(self) -> None:
         L.check(self.lib.holo_ctx_synchronize(self.h))
 
@@ -226,8 +230,11 @@ class Context:
         L.check(self.lib.holo_frame_download(self.h, int(which), out.ctypes.data, out.nbytes))
         return out
 
-    def download_into(self, which: int, host_ptr: int, nbytes: int) -> None:
-        L.check(self.lib.holo_frame_download(self.h, int(which), C.c_void_p(host_ptr), int(nbytes)))
+    def download_into(self, which: int, host_ptr: int, nbytes: int, wait: bool = True) -> None:
+        """Copy an output buffer to host memory; wait=False only enqueues it on the
+        context stream (pinned memory; complete after synchronize())."""
+        fn = self.lib.holo_frame_download if wait else self.lib.holo_frame_download_async
+        L.check(fn(self.h, int(which), C.c_void_p(host_ptr), int(nbytes)))
 
     def tensor(self, which: int, dtype: str, shape):
         """Zero-copy torch view of an output buffer (valid until the next render)."""

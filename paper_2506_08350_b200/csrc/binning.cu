@@ -284,4 +284,20 @@ void entry_depths(holo_ctx* ctx, const int* egidx, const double* zc, double* ede
     HC_LAUNCHED(ctx);
 }
 
+namespace {
+// status words -> pinned host memory, stored by the SMs: no copy-engine transfer,
+// which would queue behind the large downloads of earlier frames
+__global__ void k_publish_status(const unsigned* __restrict__ misc, const unsigned* __restrict__ total,
+                                 volatile unsigned* host) {
+    const int t = threadIdx.x;
+    if (t < 3) host[t] = misc[t];
+    if (t == 4) host[4] = *total;
+}
+}  // namespace
+
+void publish_status(holo_ctx* ctx, const unsigned* misc, const unsigned* total, unsigned* host_pinned) {
+    k_publish_status<<<1, 32, 0, ctx->stream>>>(misc, total, host_pinned);
+    HC_LAUNCHED(ctx);
+}
+
 }  // namespace holo_cuda

@@ -91,6 +91,7 @@ void* holo_ctx::buffer(const std::string& name, size_t bytes) {
             HC_CUDA(cudaFree(b.p));
             b.p = nullptr;
             b.bytes = 0;
+            small_cache.clear();  // a freed address may come back for another buffer
         }
         const size_t want = bytes + bytes / 8;  // headroom for frame-to-frame growth
         HC_CUDA(cudaMalloc(&b.p, want));
@@ -162,8 +163,15 @@ cudaEvent_t take_event(holo_ctx* ctx) {
     return e;
 }
 
-// async upload of a small host table via a pinned ring slot (no stream stall)
+// async upload of a small host table via a pinned ring slot (no stream stall).
+// A table identical to the last one uploaded to the same buffer is not sent again:
+// frame after frame the render stream then issues no host-to-device copy, which
+// would otherwise queue on the copy engine behind the next frame's scene upload.
 void upload_small(holo_ctx* ctx, void* dev, const void* host, size_t bytes) {
+    auto hit = ctx->small_cache.find(dev);
+    if (hit != ctx->small_cache.end() && hit->second.size() == bytes && std::memcmp(hit->second.data(), host, bytes) == 0)
+        return;
+    ctx->small_cache[dev].assign(static_cast<const unsigned char*>(host), static_cast<const unsigned char*>(host) + bytes);
     if (bytes > holo_ctx::kRingSlotBytes) {
         HC_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
         HC_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -241,6 +249,22 @@ void consume_status(holo_ctx* ctx, bool wait_all) {
     }
 }
 
+// Outputs written only by the last pass of a frame: a render waits for their
+// in-flight asynchronous downloads just before that pass; any other downloaded
+// buffer makes it wait before its first kernel.
+constexpr unsigned kLateBufs = (1u << HOLO_BUF_HOLOGRAM) | (1u << HOLO_BUF_REPLAYED) | (1u << HOLO_BUF_INTENSITY);
+
+void wait_downloads(holo_ctx* ctx, int set, unsigned mask) {
+    for (int k = 0; k < 2; ++k) {
+        if ((set >= 0 && k != set) || !(ctx->out_pending[k] & mask)) continue;
+        HC_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_out_done[k], 0));
+        ctx->out_pending[k] = 0;
+    }
+}
+
+// device buffer name of a final output in set k
+std::string out_name(const char* base, int k) { return k ? std::string(base) + ".1" : std::string(base); }
+
 void fill_info(const holo_ctx* ctx, holo_frame_info* info) {
     *info = holo_frame_info{};
     info->num_entries = ctx->f_E;
@@ -316,9 +340,15 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     HC_CUDA(cudaMemsetAsync(misc, 0, sizeof(unsigned) * 4, ctx->stream));
     HC_CUDA(cudaMemsetAsync(bcount, 0, sizeof(unsigned) * (B + 1), ctx->stream));
 
+    const int sk = ctx->scene_cur;  // the scene set this frame reads (only preprocess reads it)
+    if (ctx->scene_wait[sk]) {
+        HC_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_scene_ready[sk], 0));
+        ctx->scene_wait[sk] = false;
+    }
     ctx->stage_begin();
     preprocess(ctx, cc, st, near_clip, L, g.tiles_x, g.tiles_y, pre);
     ctx->stage_end(0);
+    HC_CUDA(cudaEventRecord(ctx->ev_scene_free[sk], ctx->stream));
 
     ctx->stage_begin();
     bucket_count(ctx, pre, N, L, pb, pe, g.tiles_x, g.num_tiles, st.soft_assignment, bcount);
@@ -329,8 +359,7 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     if (!ctx->async) {
         // synchronous frame: one host round trip for the entry count and the
         // validation flags, so errors surface from this call like the reference's
-        HC_CUDA(cudaMemcpyAsync(hp, misc, sizeof(unsigned) * 3, cudaMemcpyDeviceToHost, ctx->stream));
-        HC_CUDA(cudaMemcpyAsync(hp + 4, bstart + B, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+        publish_status(ctx, misc, bstart + B, hp);
         HC_CUDA(cudaStreamSynchronize(ctx->stream));
         if (hp[0] & kFlagDegenerateQuat) config_error("degenerate quaternion in scene");  // scene.cpp:27
         if (hp[0] & kFlagNegativeAmp) config_error("amplitudes must be non-negative");    // scene.cpp:30
@@ -390,7 +419,7 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     ctx->f_cap = capacity;
     if (!ctx->async) {
         // flags / counters after the whole raster (overflow cannot happen here)
-        HC_CUDA(cudaMemcpyAsync(hp, misc, sizeof(unsigned) * 3, cudaMemcpyDeviceToHost, ctx->stream));
+        publish_status(ctx, misc, bstart + B, hp);
         HC_CUDA(cudaStreamSynchronize(ctx->stream));
         ctx->f_E = hp[4];
         ctx->f_num_valid = hp[1];
@@ -403,8 +432,7 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     const int slot = ctx->status_next;
     ctx->status_next = (slot + 1) % holo_ctx::kStatusSlots;
     hp = ctx->host_status + slot * holo_ctx::kStatusWords;
-    HC_CUDA(cudaMemcpyAsync(hp, misc, sizeof(unsigned) * 3, cudaMemcpyDeviceToHost, ctx->stream));
-    HC_CUDA(cudaMemcpyAsync(hp + 4, bstart + B, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+    publish_status(ctx, misc, bstart + B, hp);
     HC_CUDA(cudaEventRecord(ctx->status_events[slot], ctx->stream));
     ctx->status_order[ctx->status_pending_n++] = slot;
     if (info) *info = holo_frame_info{};  // known after holo_ctx_frame_status
@@ -548,6 +576,14 @@ int holo_ctx_create(int device, holo_ctx** out) {
                                sizeof(unsigned) * (holo_ctx::kStatusSlots + 1) * holo_ctx::kStatusWords));
         std::memset(ctx->host_status, 0, sizeof(unsigned) * (holo_ctx::kStatusSlots + 1) * holo_ctx::kStatusWords);
         for (auto& e : ctx->status_events) HC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        HC_CUDA(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking));
+        HC_CUDA(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
+        for (int k = 0; k < 2; ++k) {
+            HC_CUDA(cudaEventCreateWithFlags(&ctx->ev_scene_ready[k], cudaEventDisableTiming));
+            HC_CUDA(cudaEventCreateWithFlags(&ctx->ev_scene_free[k], cudaEventDisableTiming));
+        }
+        HC_CUDA(cudaEventCreateWithFlags(&ctx->ev_out_src, cudaEventDisableTiming));
+        for (auto& e : ctx->ev_out_done) HC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         *out = ctx;
     });
 }
@@ -557,12 +593,21 @@ int holo_ctx_destroy(holo_ctx* ctx) {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
+        cudaStreamSynchronize(ctx->copy_in);
+        cudaStreamSynchronize(ctx->copy_out);
         for (auto& kv : ctx->scratch) cudaFree(kv.second.p);
         for (auto& kv : ctx->twiddles) cudaFree(kv.second);
         for (auto& kv : ctx->freqs) cudaFree(kv.second);
-        for (double* p : {ctx->d_positions, ctx->d_rotations, ctx->d_log_scales, ctx->d_amplitudes, ctx->d_opacity,
-                          ctx->d_phases, ctx->d_plane_logits})
-            cudaFree(p);
+        for (auto& set : ctx->scene_sets)
+            for (double* p : set.a) cudaFree(p);
+        for (int k = 0; k < 2; ++k) {
+            cudaEventDestroy(ctx->ev_scene_ready[k]);
+            cudaEventDestroy(ctx->ev_scene_free[k]);
+        }
+        cudaEventDestroy(ctx->ev_out_src);
+        for (auto e : ctx->ev_out_done) cudaEventDestroy(e);
+        cudaStreamDestroy(ctx->copy_in);
+        cudaStreamDestroy(ctx->copy_out);
         if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
         if (ctx->host_status) cudaFreeHost(ctx->host_status);
         for (auto e : ctx->status_events)
@@ -599,10 +644,18 @@ int holo_ctx_use_own_stream(holo_ctx* ctx) {
 
 void* holo_ctx_get_stream(holo_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 
+void* holo_ctx_get_copy_stream(holo_ctx* ctx, int which) {
+    if (!ctx) return nullptr;
+    return static_cast<void*>(which == 0 ? ctx->copy_in : ctx->copy_out);
+}
+
 int holo_ctx_synchronize(holo_ctx* ctx) {
     return guarded([&] {
         require(ctx != nullptr, HOLO_ERR_USAGE, "null context");
         HC_CUDA(cudaStreamSynchronize(ctx->stream));
+        HC_CUDA(cudaStreamSynchronize(ctx->copy_in));
+        HC_CUDA(cudaStreamSynchronize(ctx->copy_out));
+        ctx->out_pending[0] = ctx->out_pending[1] = 0;
         consume_status(ctx, true);
     });
 }
@@ -678,26 +731,45 @@ static int scene_upload(holo_ctx* ctx, const holo_scene_arrays* s, cudaMemcpyKin
                         s->plane_logits,
                     HOLO_ERR_CONFIG, "scene arrays have inconsistent sizes");
         HC_CUDA(cudaSetDevice(ctx->device));
-        struct A {
-            double** dst;
-            const double* src;
-            size_t count;
-        } arrays[] = {{&ctx->d_positions, s->positions, 3 * n},       {&ctx->d_rotations, s->rotations, 4 * n},
-                      {&ctx->d_log_scales, s->log_scales, 3 * n},     {&ctx->d_amplitudes, s->amplitudes, 3 * n},
-                      {&ctx->d_opacity, s->opacity_logits, n},        {&ctx->d_phases, s->phases, 3 * n},
-                      {&ctx->d_plane_logits, s->plane_logits, n * static_cast<size_t>(s->num_planes)}};
-        const bool grow = n > ctx->n || static_cast<size_t>(s->num_planes) * n >
-                                            static_cast<size_t>(ctx->scene_planes) * ctx->n;
+        const double* src[7] = {s->positions, s->rotations, s->log_scales, s->amplitudes,
+                                s->opacity_logits, s->phases, s->plane_logits};
+        const size_t count[7] = {3 * n, 4 * n, 3 * n, 3 * n, n, 3 * n, n * static_cast<size_t>(s->num_planes)};
+        // fill the set the last render is not reading
+        const int k = ctx->scene_cur ^ 1;
+        holo_ctx::SceneSet& set = ctx->scene_sets[k];
+        bool grow = false;
+        for (int a = 0; a < 7; ++a) grow = grow || count[a] > set.cap[a] || !set.a[a];
         if (grow) {
             HC_CUDA(cudaStreamSynchronize(ctx->stream));
-            for (auto& a : arrays) {
-                cudaFree(*a.dst);
-                *a.dst = nullptr;
-                HC_CUDA(cudaMalloc(a.dst, sizeof(double) * (a.count ? a.count : 1)));
+            HC_CUDA(cudaStreamSynchronize(ctx->copy_in));
+            for (int a = 0; a < 7; ++a) {
+                cudaFree(set.a[a]);
+                set.a[a] = nullptr;
+                HC_CUDA(cudaMalloc(&set.a[a], sizeof(double) * (count[a] ? count[a] : 1)));
+                set.cap[a] = count[a];
             }
         }
-        for (auto& a : arrays)
-            if (a.count) HC_CUDA(cudaMemcpyAsync(*a.dst, a.src, sizeof(double) * a.count, kind, ctx->stream));
+        if (kind == cudaMemcpyHostToDevice) {
+            // copy-in stream: after the last preprocess that read this set
+            HC_CUDA(cudaStreamWaitEvent(ctx->copy_in, ctx->ev_scene_free[k], 0));
+            for (int a = 0; a < 7; ++a)
+                if (count[a])
+                    HC_CUDA(cudaMemcpyAsync(set.a[a], src[a], sizeof(double) * count[a], kind, ctx->copy_in));
+            HC_CUDA(cudaEventRecord(ctx->ev_scene_ready[k], ctx->copy_in));
+            ctx->scene_wait[k] = true;
+        } else {
+            // device arrays are ordered on the context stream; an earlier host upload
+            // into this set may still be in flight
+            if (ctx->scene_wait[k]) HC_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_scene_ready[k], 0));
+            ctx->scene_wait[k] = false;
+            for (int a = 0; a < 7; ++a)
+                if (count[a])
+                    HC_CUDA(cudaMemcpyAsync(set.a[a], src[a], sizeof(double) * count[a], kind, ctx->stream));
+        }
+        ctx->scene_cur = k;
+        double** cur[7] = {&ctx->d_positions, &ctx->d_rotations, &ctx->d_log_scales, &ctx->d_amplitudes,
+                           &ctx->d_opacity, &ctx->d_phases, &ctx->d_plane_logits};
+        for (int a = 0; a < 7; ++a) *cur[a] = set.a[a];
         ctx->n = n;
         ctx->scene_planes = s->num_planes;
     });
@@ -731,9 +803,13 @@ struct OutBufs {
 
 OutBufs output_buffers(holo_ctx* ctx, unsigned outputs, int np, int C, size_t P) {
     OutBufs o;
-    if (outputs & HOLO_OUT_HOLOGRAM) o.holo = buf<cx<float>>(ctx, "hologram", static_cast<size_t>(C) * P);
-    if (outputs & HOLO_OUT_REPLAYED) o.rep = buf<cx<float>>(ctx, "replayed", static_cast<size_t>(np) * C * P);
-    if (outputs & HOLO_OUT_INTENSITY) o.ints = buf<float>(ctx, "intensity", static_cast<size_t>(np) * C * P);
+    const int k = ctx->out_sel;
+    if (outputs & HOLO_OUT_HOLOGRAM)
+        o.holo = buf<cx<float>>(ctx, out_name("hologram", k).c_str(), static_cast<size_t>(C) * P);
+    if (outputs & HOLO_OUT_REPLAYED)
+        o.rep = buf<cx<float>>(ctx, out_name("replayed", k).c_str(), static_cast<size_t>(np) * C * P);
+    if (outputs & HOLO_OUT_INTENSITY)
+        o.ints = buf<float>(ctx, out_name("intensity", k).c_str(), static_cast<size_t>(np) * C * P);
     return o;
 }
 
@@ -763,6 +839,7 @@ void render_back(holo_ctx* ctx, const holo_wave& wave, const holo_prop_options& 
         static_row(ctx, kModeReplay, nullptr, const_cast<cx<float>*>(spec), stage, W, H, C, np, has_holo,
                    O - has_holo, tfc, wave.pitch, po.local_band_limit != 0);
         ctx->stage_end(5);
+        wait_downloads(ctx, ctx->out_sel, ~0u);
         ctx->stage_begin();
         static_col_inv(ctx, stage, W, H, C, O, has_holo, ob.holo, ob.rep, ob.ints);
         ctx->stage_end(6);
@@ -771,6 +848,7 @@ void render_back(holo_ctx* ctx, const holo_wave& wave, const holo_prop_options& 
     ctx->stage_begin();
     col_replay<float>(ctx, spec, stage, W, H, C, O, d_plane_of, tfc, wave.pitch);
     ctx->stage_end(5);
+    wait_downloads(ctx, ctx->out_sel, ~0u);
     ctx->stage_begin();
     rows_epilogue(ctx, stage, W, H, C, O, has_holo, ob.holo, ob.rep, ob.ints);
     ctx->stage_end(6);
@@ -785,6 +863,9 @@ void render_front(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, 
     const FrameGeom g = check_render(ctx, cam, wave, st);
     require(pb >= 0 && pe <= g.L && pb <= pe, HOLO_ERR_USAGE, "plane range outside [0, num_planes]");
     require(!po.pad2x || full, HOLO_ERR_CONFIG, "plane-sharded rendering does not support pad2x");
+    ctx->out_sel ^= 1;  // this frame's final outputs go to the other set
+    wait_downloads(ctx, -1, ~kLateBufs);
+    if (po.pad2x) wait_downloads(ctx, ctx->out_sel, ~0u);
     ctx->f_L = g.L;
     ctx->f_C = g.C;
     ctx->f_W = g.W;
@@ -834,6 +915,7 @@ void render_front(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, 
         static_row(ctx, kModeFull, work, nullptr, stage, g.W, g.H, g.C, np, has_holo, O - has_holo, tfc, wave.pitch,
                    po.local_band_limit != 0);
         ctx->stage_end(4);
+        wait_downloads(ctx, ctx->out_sel, ~0u);
         ctx->stage_begin();
         static_col_inv(ctx, stage, g.W, g.H, g.C, O, (outputs & HOLO_OUT_HOLOGRAM) ? 1 : 0, ob.holo, ob.rep,
                        ob.ints);
@@ -896,13 +978,14 @@ int holo_render(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave, co
         const size_t P = static_cast<size_t>(W) * H;
         if (!(outputs & (HOLO_OUT_HOLOGRAM | HOLO_OUT_REPLAYED | HOLO_OUT_INTENSITY))) return;
         const cx<float>* layers = static_cast<const cx<float>*>(ctx->buffer("layers", 1));
-        cx<float>* d_holo = buf<cx<float>>(ctx, "hologram", static_cast<size_t>(C) * P);
+        const int k = ctx->out_sel;
+        cx<float>* d_holo = buf<cx<float>>(ctx, out_name("hologram", k).c_str(), static_cast<size_t>(C) * P);
         op_forward_record<float>(ctx, layers, L, d_holo, *wave, po);
         if (outputs & (HOLO_OUT_REPLAYED | HOLO_OUT_INTENSITY)) {
-            cx<float>* d_rep = buf<cx<float>>(ctx, "replayed", static_cast<size_t>(L) * C * P);
+            cx<float>* d_rep = buf<cx<float>>(ctx, out_name("replayed", k).c_str(), static_cast<size_t>(L) * C * P);
             op_inverse_propagate<float>(ctx, d_holo, d_rep, *wave, po);
             if (outputs & HOLO_OUT_INTENSITY)
-                intensity<float>(ctx, d_rep, buf<float>(ctx, "intensity", static_cast<size_t>(L) * C * P),
+                intensity<float>(ctx, d_rep, buf<float>(ctx, out_name("intensity", k).c_str(), static_cast<size_t>(L) * C * P),
                                  static_cast<size_t>(L) * C * P);
         }
     });
@@ -915,16 +998,16 @@ int holo_frame_buffer(holo_ctx* ctx, int which, void** dev_ptr, size_t* bytes) {
         const size_t np = static_cast<size_t>(ctx->f_plane_end - ctx->f_plane_begin);
         const size_t C = static_cast<size_t>(ctx->f_C);
         const size_t B = np * ctx->f_tiles;
-        const char* name = nullptr;
+        std::string name;
         size_t sz = 0;
         if (which == HOLO_BUF_ENTRY_GIDX || which == HOLO_BUF_ENTRY_DEPTH)
             consume_status(ctx, true);  // E of an asynchronous frame
         const size_t E = std::min<uint64_t>(ctx->f_E, ctx->f_cap);
         switch (which) {
             case HOLO_BUF_LAYERS: name = "layers"; sz = np * C * P * 8; break;
-            case HOLO_BUF_HOLOGRAM: name = "hologram"; sz = C * P * 8; break;
-            case HOLO_BUF_REPLAYED: name = "replayed"; sz = np * C * P * 8; break;
-            case HOLO_BUF_INTENSITY: name = "intensity"; sz = np * C * P * 4; break;
+            case HOLO_BUF_HOLOGRAM: name = out_name("hologram", ctx->out_sel); sz = C * P * 8; break;
+            case HOLO_BUF_REPLAYED: name = out_name("replayed", ctx->out_sel); sz = np * C * P * 8; break;
+            case HOLO_BUF_INTENSITY: name = out_name("intensity", ctx->out_sel); sz = np * C * P * 4; break;
             case HOLO_BUF_T_FINAL: name = "t_final"; sz = np * P * 4; break;
             case HOLO_BUF_N_CONTRIB: name = "n_contrib"; sz = np * P * 4; break;
             case HOLO_BUF_ENTRY_GIDX: name = "egidx"; sz = E * 4; break;
@@ -953,6 +1036,24 @@ int holo_frame_download(holo_ctx* ctx, int which, void* host, size_t bytes) {
         require(bytes == sz, HOLO_ERR_USAGE, "holo_frame_download: size mismatch");
         HC_CUDA(cudaMemcpyAsync(host, d, sz, cudaMemcpyDeviceToHost, ctx->stream));
         HC_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int holo_frame_download_async(holo_ctx* ctx, int which, void* host, size_t bytes) {
+    void* d = nullptr;
+    size_t sz = 0;
+    int rc = holo_frame_buffer(ctx, which, &d, &sz);
+    if (rc) return rc;
+    return guarded([&] {
+        require(bytes == sz, HOLO_ERR_USAGE, "holo_frame_download_async: size mismatch");
+        // copy-out stream, after the frame work enqueued so far; the next render
+        // waits for it before overwriting the buffer (wait_downloads)
+        HC_CUDA(cudaEventRecord(ctx->ev_out_src, ctx->stream));
+        HC_CUDA(cudaStreamWaitEvent(ctx->copy_out, ctx->ev_out_src, 0));
+        HC_CUDA(cudaMemcpyAsync(host, d, sz, cudaMemcpyDeviceToHost, ctx->copy_out));
+        const int k = ((1u << which) & kLateBufs) ? ctx->out_sel : 0;  // single-buffered ids count in set 0
+        HC_CUDA(cudaEventRecord(ctx->ev_out_done[k], ctx->copy_out));
+        ctx->out_pending[k] |= 1u << which;
     });
 }
 

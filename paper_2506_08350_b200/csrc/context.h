@@ -54,7 +54,9 @@ struct holo_ctx {
     void* host_pinned = nullptr;
     size_t host_pinned_bytes = 0;
 
-    // resident scene (device, f64 SoA)
+    // resident scene (device, f64 SoA), double-buffered: a host upload fills the set
+    // the previous frame is not reading, on the copy-in stream, while that frame
+    // renders; d_* point at the set the next render reads
     size_t n = 0;
     int scene_planes = 0;
     double* d_positions = nullptr;
@@ -64,6 +66,23 @@ struct holo_ctx {
     double* d_opacity = nullptr;
     double* d_phases = nullptr;
     double* d_plane_logits = nullptr;
+    struct SceneSet {
+        double* a[7] = {};  // positions, rotations, log_scales, amplitudes, opacity, phases, plane_logits
+        size_t cap[7] = {};
+    };
+    SceneSet scene_sets[2];
+    int scene_cur = 0;
+    cudaStream_t copy_in = nullptr, copy_out = nullptr;  // non-blocking copy streams
+    cudaEvent_t ev_scene_ready[2] = {};  // upload into set k complete (copy_in)
+    cudaEvent_t ev_scene_free[2] = {};   // last reader of set k (preprocess) done (stream)
+    bool scene_wait[2] = {};             // the next render must wait for ev_scene_ready[k]
+    // the final outputs (hologram, replayed, intensity) alternate between two buffer
+    // sets frame by frame, so a frame's last pass need not wait for the download of
+    // the previous frame's outputs
+    int out_sel = 0;                        // set written by the last render
+    cudaEvent_t ev_out_src = nullptr;       // frame work enqueued before an async download
+    cudaEvent_t ev_out_done[2] = {};        // async downloads from set k complete (copy_out)
+    unsigned out_pending[2] = {};           // buffer ids (bit per HOLO_BUF_*) with downloads in flight, per set
 
     // last frame
     int f_L = 0, f_C = 0, f_W = 0, f_H = 0, f_tiles = 0;
@@ -98,6 +117,7 @@ struct holo_ctx {
     // pinned ring for small asynchronous table uploads
     static constexpr int kRingSlots = 64;
     static constexpr size_t kRingSlotBytes = 64 * 1024;
+    std::map<const void*, std::vector<unsigned char>> small_cache;  // last table uploaded per device buffer
     unsigned char* ring = nullptr;
     cudaEvent_t ring_ev[kRingSlots] = {};
     bool ring_used[kRingSlots] = {};

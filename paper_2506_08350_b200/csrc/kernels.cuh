@@ -123,6 +123,8 @@ void sort_large_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsi
                         unsigned long long* ekey, int* egidx, unsigned* d_nlist);
 void entry_depths(holo_ctx* ctx, const int* egidx, const double* zc, double* edepth, const unsigned* d_E,
                   unsigned capacity);
+// host[0..2] = misc[0..2] (flags, num_valid, max bucket), host[4] = *total (E); host is pinned
+void publish_status(holo_ctx* ctx, const unsigned* misc, const unsigned* total, unsigned* host_pinned);
 
 // ---- render_static.cu (compile-time FFT plans for the common grid sizes)
 enum { kModeFull = 0, kModeSpec = 1, kModeReplay = 2 };

@@ -283,6 +283,42 @@ def test_async_capacity_and_validation_reported_by_frame_status():
     ctx.close()
 
 
+def test_async_upload_render_download_pipeline():
+    # scene uploads on the copy-in stream into the set the running frame does not
+    # read, downloads on the copy-out stream: several frames enqueued back to back
+    # must each see their own scene and land in their own host buffers
+    import torch
+
+    cfg = WaveConfig(nx=256, ny=192, wavelengths=RGB, num_planes=4)
+    scenes = [synthetic_scene(15000, cfg, 50 + i) for i in range(4)]
+    cam = wide_camera(cfg)
+    ctx = api.Context(0, use_torch_stream=False)
+    want = []
+    for s in scenes:
+        ctx.upload_scene(s)
+        ctx.render(cam, cfg)
+        want.append(_frame(ctx, 3, 192, 256, 4))
+    ctx.set_async(True)
+    pins = []
+    for s in scenes:
+        arrs = [torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).pin_memory() for a in
+                (s.positions, s.rotations, s.log_scales, s.amplitudes, s.opacity_logits, s.phases, s.plane_logits)]
+        pins.append(arrs)
+    outs = [(torch.empty((3, 192, 256), dtype=torch.complex64).pin_memory(),
+             torch.empty((4, 3, 192, 256), dtype=torch.float32).pin_memory()) for _ in scenes]
+    for rep in range(2):
+        for s, arrs, (hh, ih) in zip(scenes, pins, outs):
+            ctx.upload_scene_pointers(s.size(), 4, [a.data_ptr() for a in arrs], device=False)
+            ctx.render(cam, cfg)
+            ctx.download_into(L.BUF_HOLOGRAM, hh.data_ptr(), hh.numel() * 8, wait=False)
+            ctx.download_into(L.BUF_INTENSITY, ih.data_ptr(), ih.numel() * 4, wait=False)
+        ctx.synchronize()
+        ctx.frame_status()
+        for w, (hh, ih) in zip(want, outs):
+            assert np.array_equal(hh.numpy(), w[0]) and np.array_equal(ih.numpy(), w[1])
+    ctx.close()
+
+
 def test_two_async_contexts_overlap_and_agree():
     import torch
 
