@@ -148,15 +148,42 @@ __global__ void __launch_bounds__(256) k_bucket_emit(PreOut pre, size_t N, int L
     if (i >= N) return;
     const unsigned long long key = static_cast<unsigned long long>(__double_as_longlong(pre.zc[i]));
     bool over = false;
-    for_each_bucket(pre, i, L, pb, pe, tiles_x, num_tiles, soft, [&](int b) {
-        const unsigned e = bstart[b] + atomicAdd(cursor + b, 1u);
-        if (e >= capacity) {  // asynchronous frames: entries beyond the reserved capacity are dropped
+    // entries beyond the reserved capacity (asynchronous frames) are dropped and flagged
+    auto put = [&](int b, unsigned slot) {
+        const unsigned e = bstart[b] + slot;
+        if (e >= capacity) {
             over = true;
             return;
         }
         ekey[e] = key;
         egidx[e] = static_cast<int>(i);
-    });
+    };
+    if (!soft) {
+        // hard assignment: the rect's tiles 4 at a time, so the slot atomics of a
+        // group are in flight together instead of one round trip per entry
+        if (pre.count[i] == 0) return;
+        const int l = pre.plane[i];
+        if (l < pb || l >= pe) return;
+        const int4 r = pre.rect[i];
+        const int w = r.y - r.x, n = w * (r.w - r.z);
+        const int b0 = (l - pb) * num_tiles + r.z * tiles_x + r.x;
+        for (int k = 0; k < n; k += 4) {
+            int b[4];
+            unsigned s[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int idx = k + u;
+                b[u] = b0 + (idx / w) * tiles_x + idx % w;
+                if (idx < n) s[u] = atomicAdd(cursor + b[u], 1u);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (k + u < n) put(b[u], s[u]);
+        }
+    } else {
+        for_each_bucket(pre, i, L, pb, pe, tiles_x, num_tiles, soft,
+                        [&](int b) { put(b, atomicAdd(cursor + b, 1u)); });
+    }
     if (over) atomicOr(flags, kFlagOverflow);
 }
 

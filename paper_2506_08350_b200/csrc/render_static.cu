@@ -225,17 +225,25 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
                 }
             }
     }
-    // H_{Z_l} at owned sample (q, r): the plane-independent part G and the plane's
-    // (phase0, 2 pi z); local band limits (rare) take the full f64 path
+    // H_{Z_l} at owned sample (q, r) inside the propagating band: the
+    // plane-independent part G and the plane's (phase0, 2 pi z); local band limits
+    // (rare) take the full f64 path.  The band mask (H = 0 outside, for every plane)
+    // is applied once to S instead of per plane: S = sum_l H_l X_l vanishes there,
+    // and so does every S . conj(H_l).
     auto tf = [&](int l, int q, int r, int b, int i) -> cx<float> {
         if constexpr (LOCAL) {
             const TfChan p = tfc[l * C + c];
             if (p.local) return tf_value<float>(p, fx[i], fy[(row0 + b) - c * H]);
         }
-        const float g = G[q][r];
-        if (g < 0.0f) return czf();
         const float2 t = s_tf[l];
-        return phasor_reduced(t.x - t.y * g);
+        return phasor_reduced(t.x - t.y * G[q][r]);
+    };
+    auto band_mask = [&]() {
+#pragma unroll
+        for (int q = 0; q < LS::kBPT; ++q)
+#pragma unroll
+            for (int r = 0; r < LS::kR; ++r)
+                if (G[q][r] < 0.0f) S[q][r] = czf();
     };
 
     if constexpr (MODE != kModeReplay) {
@@ -249,6 +257,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
             auto store = [&](int q, int r, int b, int i, cx<float> v) { S[q][r] = S[q][r] + v * tf(l, q, r, b, i); };
             fft_static<float, -1, B, P>(sm, tw, load, store);
         }
+        band_mask();
     }
     if constexpr (MODE == kModeSpec) {
         cx<float>* dst = spec + static_cast<size_t>(row0) * W;
@@ -270,6 +279,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
                 int b, i;
                 if (owner(q, r, b, i)) S[q][r] = srcs[static_cast<size_t>(b) * W + i];
             }
+        band_mask();
     }
     // outputs: [hologram] then planes 0..nrep-1 (output_planes in capi.cu)
     if (has_holo) {

@@ -109,6 +109,15 @@ def test_posed_camera_and_reference_helpers(gpu_ctx, oracle):
     check_pipeline(gpu_ctx, oracle, overlapping_scene(40, cfg, 24), front_camera(cfg), cfg)
 
 
+@pytest.mark.parametrize("local", [False, True])
+def test_evanescent_band_pipeline(gpu_ctx, oracle, local):
+    # pitch 0.3 um: the grid's corner frequencies exceed 1/lambda, so H = 0 there
+    # (propagation.cpp:41-44); with local band limits on, the per-plane limits too
+    cfg = WaveConfig(nx=64, ny=48, pitch=0.3e-6, wavelengths=RGB, num_planes=3)
+    check_pipeline(gpu_ctx, oracle, synthetic_scene(500, cfg, 26), wide_camera(cfg), cfg,
+                   prop=PropagationOptions(local_band_limit=local))
+
+
 def test_pad2x_pipeline(gpu_ctx, oracle):
     cfg = WaveConfig(nx=48, ny=32, wavelengths=RGB, num_planes=2)
     check_pipeline(gpu_ctx, oracle, synthetic_scene(200, cfg, 25), wide_camera(cfg), cfg,
