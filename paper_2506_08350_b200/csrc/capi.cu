@@ -332,12 +332,13 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     pre.rho = (st.soft_assignment || want_proj) ? buf<double>(ctx, "rho", N * L) : nullptr;
     pre.touched = buf<unsigned char>(ctx, "touched", N);
     pre.projected = want_proj ? buf<holo_projected>(ctx, "projected", N) : nullptr;
-    unsigned* misc = buf<unsigned>(ctx, "misc", 4);  // flags, num_valid, max bucket
+    // flags, num_valid, max bucket, large-bucket count
+    unsigned* misc = buf<unsigned>(ctx, "misc", 8);
     pre.flags = misc;
     pre.num_valid = misc + 1;
     unsigned* bcount = buf<unsigned>(ctx, "bcount", B + 1);
     unsigned* bstart = buf<unsigned>(ctx, "bstart", B + 1);
-    HC_CUDA(cudaMemsetAsync(misc, 0, sizeof(unsigned) * 4, ctx->stream));
+    HC_CUDA(cudaMemsetAsync(misc, 0, sizeof(unsigned) * 8, ctx->stream));
     HC_CUDA(cudaMemsetAsync(bcount, 0, sizeof(unsigned) * (B + 1), ctx->stream));
 
     const int sk = ctx->scene_cur;  // the scene set this frame reads (only preprocess reads it)

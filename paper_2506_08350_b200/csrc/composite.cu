@@ -136,25 +136,26 @@ __device__ unsigned long long g_counts[4];
 __device__ __forceinline__ float eval_alpha(const Staged* e, float fx, float fy, float clamp, float4& B) {
     const float4 A = e->a;
     B = e->b;
-    const float dx = fx - A.x, dy = fy - A.y;
+    const cx<float> d = mk(fx, fy) - mk(A.x, A.y);  // one FADD2
+    const float dx = d.x, dy = d.y;
     const float t = fmaf(A.w, dy, A.z * dx);
     const float u = fmaf(dx, t, B.y);
     const float q = fmaf(B.x * dy, dy, u);
     return fminf(ex2_approx(q), clamp);
 }
 
+// acc_c += w * (amp_c cos phi_c, amp_c sin phi_c): one FFMA2 per channel
+__device__ __forceinline__ cx<float> axpy(float w, float re, float im, cx<float> acc) {
+    return f32x2::unpack(f32x2::fma(f32x2::pack(w, w), f32x2::pack(re, im), f32x2::pack(acc.x, acc.y)));
+}
+
 template <int C>
-__device__ __forceinline__ void blend(const Staged* e, const float4& B, float w, float (&acc)[2 * C]) {
-    acc[0] = fmaf(w, B.z, acc[0]);
-    acc[1] = fmaf(w, B.w, acc[1]);
+__device__ __forceinline__ void blend(const Staged* e, const float4& B, float w, cx<float> (&acc)[C]) {
+    acc[0] = axpy(w, B.z, B.w, acc[0]);
     if constexpr (C > 1) {
         const float4 Cc = e->c;
-        acc[2 % (2 * C)] = fmaf(w, Cc.x, acc[2 % (2 * C)]);
-        acc[3 % (2 * C)] = fmaf(w, Cc.y, acc[3 % (2 * C)]);
-        if constexpr (C > 2) {
-            acc[4 % (2 * C)] = fmaf(w, Cc.z, acc[4 % (2 * C)]);
-            acc[5 % (2 * C)] = fmaf(w, Cc.w, acc[5 % (2 * C)]);
-        }
+        acc[1 % C] = axpy(w, Cc.x, Cc.y, acc[1 % C]);
+        if constexpr (C > 2) acc[2 % C] = axpy(w, Cc.z, Cc.w, acc[2 % C]);
     }
 }
 
@@ -200,9 +201,9 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
 
     float T = 1.0f;
     int contrib = 0;
-    float acc[2 * C];
+    cx<float> acc[C];
 #pragma unroll
-    for (int c = 0; c < 2 * C; ++c) acc[c] = 0.0f;
+    for (int c = 0; c < C; ++c) acc[c] = mk(0.0f, 0.0f);
     // the reference checks T < term_eps before every entry; T never increases, so
     // "stopped" is exactly !(T >= eps) (outside pixels are parked as stopped)
     bool done = !inside || !(1.0f >= eps);
@@ -350,7 +351,7 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
         const size_t pix = static_cast<size_t>(py) * a.W + px;
 #pragma unroll
         for (int c = 0; c < C; ++c)
-            a.layers[(static_cast<size_t>(lplane) * C + c) * P + pix] = mk(acc[2 * c], acc[2 * c + 1]);
+            a.layers[(static_cast<size_t>(lplane) * C + c) * P + pix] = acc[c];
         if (a.t_final) a.t_final[static_cast<size_t>(lplane) * P + pix] = T;
         if (a.n_contrib) a.n_contrib[static_cast<size_t>(lplane) * P + pix] = contrib;
     }

@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
             mbar_wait(&s_bar[l & 1], (l >> 1) & 1);
             const cx<float>* src = pre + (l & 1) * NBR * SM::kRowPad;
             auto load = [&](int, int, int b, int i) -> cx<float> { return src[b * SM::kRowPad + i]; };
-            auto store = [&](int q, int r, int b, int i, cx<float> v) { S[q][r] = S[q][r] + v * tf(l, q, r, b, i); };
+            auto store = [&](int q, int r, int b, int i, cx<float> v) { S[q][r] = cfma(v, tf(l, q, r, b, i), S[q][r]); };
             fft_static<float, -1, B, P>(sm, tw, load, store);
         }
         band_mask();
