@@ -83,8 +83,9 @@ struct Stage {
         Dft<R, DIR, T>::run(v);
     }
 
-    template <class Load, class Store>
-    static __device__ __forceinline__ void run(cx<T>* sm, const cx<T>* __restrict__ tw, Load& load, Store& store) {
+    template <class Load, class Store, class Hook>
+    static __device__ __forceinline__ void run(cx<T>* sm, const cx<T>* __restrict__ tw, Load& load, Store& store,
+                                               Hook& hook) {
         if constexpr (FIRST || LAST) {
             // Streaming stage: it either only writes sm (first) or only reads it
             // (last), so butterflies go one by one with R live values each.
@@ -118,6 +119,7 @@ struct Stage {
             // first: writes visible to the next stage; last: every sm read done
             // before the caller (or its next transform) writes sm again
             if constexpr (!(FIRST && LAST)) __syncthreads();
+            if constexpr (FIRST) hook();  // every load of the first stage has completed
             return;
         }
         // Middle stage, in place: hold all of this thread's butterflies, barrier, write.
@@ -153,27 +155,34 @@ struct Stages;
 
 template <class T, int DIR, class B, int NS, bool FIRST, int R>
 struct Stages<T, DIR, B, NS, FIRST, Radices<R>> {
-    template <class Load, class Store>
-    static __device__ __forceinline__ void run(cx<T>* sm, const cx<T>* tw, Load& load, Store& store) {
-        Stage<T, DIR, B, R, NS, FIRST, true>::run(sm, tw, load, store);
+    template <class Load, class Store, class Hook>
+    static __device__ __forceinline__ void run(cx<T>* sm, const cx<T>* tw, Load& load, Store& store, Hook& hook) {
+        Stage<T, DIR, B, R, NS, FIRST, true>::run(sm, tw, load, store, hook);
     }
 };
 
 template <class T, int DIR, class B, int NS, bool FIRST, int R, int R2, int... Rs>
 struct Stages<T, DIR, B, NS, FIRST, Radices<R, R2, Rs...>> {
-    template <class Load, class Store>
-    static __device__ __forceinline__ void run(cx<T>* sm, const cx<T>* tw, Load& load, Store& store) {
-        Stage<T, DIR, B, R, NS, FIRST, false>::run(sm, tw, load, store);
-        Stages<T, DIR, B, NS * R, false, Radices<R2, Rs...>>::run(sm, tw, load, store);
+    template <class Load, class Store, class Hook>
+    static __device__ __forceinline__ void run(cx<T>* sm, const cx<T>* tw, Load& load, Store& store, Hook& hook) {
+        Stage<T, DIR, B, R, NS, FIRST, false>::run(sm, tw, load, store, hook);
+        Stages<T, DIR, B, NS * R, false, Radices<R2, Rs...>>::run(sm, tw, load, store, hook);
     }
 };
 
 // Transform a batch: load(q, r, b, i) feeds stage 0, store(q, r, b, i, v) takes the result.
 // The caller must separate two consecutive calls that share sm by a barrier only if
 // it touches sm itself in between (the last stage ends its sm reads with a barrier).
+// hook() runs once every thread has finished the first stage's loads (after its
+// barrier; plans of two or more stages), e.g. to refill the load source.
+template <class T, int DIR, class B, class P, class Load, class Store, class Hook>
+__device__ __forceinline__ void fft_static(cx<T>* sm, const cx<T>* __restrict__ tw, Load load, Store store,
+                                           Hook hook) {
+    Stages<T, DIR, B, 1, true, P>::run(sm, tw, load, store, hook);
+}
 template <class T, int DIR, class B, class P, class Load, class Store>
 __device__ __forceinline__ void fft_static(cx<T>* sm, const cx<T>* __restrict__ tw, Load load, Store store) {
-    Stages<T, DIR, B, 1, true, P>::run(sm, tw, load, store);
+    fft_static<T, DIR, B, P>(sm, tw, load, store, [] {});
 }
 
 // Asynchronous 16-byte global -> shared copies (LDGSTS), grouped by commit.
