@@ -63,7 +63,13 @@ __device__ __forceinline__ double sigmoid_ref(double x) {
     return e / (1.0 + e);
 }
 
-__global__ void __launch_bounds__(256) k_preprocess(PreArgs a, PreOut o) {
+// PROJ: also fill the full f64 detail::Projected record (HOLO_OUT_PROJECTED); the
+// render path compiles it out, which keeps the kernel at 64 registers.
+#ifndef HOLO_PRE_MINB
+#define HOLO_PRE_MINB 4
+#endif
+template <bool PROJ>
+__global__ void __launch_bounds__(256, PROJ ? 1 : HOLO_PRE_MINB) k_preprocess(PreArgs a, PreOut o) {
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     if (i >= a.n) return;
     const int L = a.L;
@@ -257,7 +263,7 @@ __global__ void __launch_bounds__(256) k_preprocess(PreArgs a, PreOut o) {
     o.count[i] = count;
     o.zc[i] = p.zc;
     if (o.touched) o.touched[i] = count > 0 ? 1 : 0;
-    if (o.projected) o.projected[i] = p;
+    if constexpr (PROJ) o.projected[i] = p;
 }
 
 }  // namespace
@@ -287,7 +293,10 @@ void preprocess(holo_ctx* ctx, const CameraConsts& cc, const holo_raster_setting
     a.tiles_x = tiles_x;
     a.tiles_y = tiles_y;
     const unsigned grid = static_cast<unsigned>((ctx->n + 255) / 256);
-    k_preprocess<<<grid, 256, 0, ctx->stream>>>(a, out);
+    if (out.projected)
+        k_preprocess<true><<<grid, 256, 0, ctx->stream>>>(a, out);
+    else
+        k_preprocess<false><<<grid, 256, 0, ctx->stream>>>(a, out);
     HC_LAUNCHED(ctx);
 }
 

@@ -31,7 +31,17 @@ template <> struct PlanOf<256> { using type = Radices<16, 16>; };
 template <> struct PlanOf<512> { using type = Radices<8, 8, 8>; };
 template <> struct PlanOf<1024> { using type = Radices<16, 16, 4>; };
 template <> struct PlanOf<1080> { using type = Radices<8, 9, 15>; };
+// HOLO_ROW1920 selects the 1920-point plan and row-pass shape (tuning).  Measured
+// row pass at C3: 1 = [16,8,15], 2 rows x 256 threads, 2 CTAs/SM: 0.451 ms;
+// 2 = [16,15,8] 1 row, 3 CTAs: 0.554; 3 = 2 rows x 512: 0.566; 4 = 4 CTAs: 0.626.
+#ifndef HOLO_ROW1920
+#define HOLO_ROW1920 1
+#endif
+#if HOLO_ROW1920 == 1
 template <> struct PlanOf<1920> { using type = Radices<16, 8, 15>; };
+#else
+template <> struct PlanOf<1920> { using type = Radices<16, 15, 8>; };
+#endif
 template <> struct PlanOf<2048> { using type = Radices<16, 16, 8>; };
 template <> struct PlanOf<2160> { using type = Radices<16, 9, 15>; };
 template <> struct PlanOf<3840> { using type = Radices<16, 16, 15>; };
@@ -54,7 +64,18 @@ struct RowCfgT {
     using B = Batch<W, NBR, NT>;
 };
 template <int W>
-using RowCfg = RowCfgT<W, (W <= 512 ? 4 : (W <= 2048 ? 2 : 1)), (W >= 1024 ? 256 : 128), 2>;
+struct RowCfgSel {
+    using type = RowCfgT<W, (W <= 512 ? 4 : (W <= 2048 ? 2 : 1)), (W >= 1024 ? 256 : 128), 2>;
+};
+#if HOLO_ROW1920 == 2
+template <> struct RowCfgSel<1920> { using type = RowCfgT<1920, 1, 256, 3>; };
+#elif HOLO_ROW1920 == 3
+template <> struct RowCfgSel<1920> { using type = RowCfgT<1920, 2, 512, 1>; };
+#elif HOLO_ROW1920 == 4
+template <> struct RowCfgSel<1920> { using type = RowCfgT<1920, 1, 256, 4>; };
+#endif
+template <int W>
+using RowCfg = typename RowCfgSel<W>::type;
 
 // Shape variants for tuning at the C3 sizes (HOLO_COL_VARIANT / HOLO_ROW_VARIANT).
 int env_variant(const char* name) {
