@@ -154,14 +154,20 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
-// Row-pass shared memory: FFT work area, two prefetch buffers of NBR rows (each
-// row padded by 8 complex = 16 banks, FULL / SPEC), per-plane TF constants.
+// Row-pass shared memory: FFT work area; the prefetch buffer for the next plane's
+// NBR rows (each row padded by 8 complex = 16 banks; FULL / SPEC); the twiddle
+// table; the plane-independent TF factor G of every owned spectral sample
+// ([slot][thread], conflict-free); per-plane TF constants.
 template <class Cfg, int MODE>
 struct RowSmem {
+    using LS = LastStage<typename Cfg::B, typename PlanOf<Cfg::W>::type>;
     static constexpr int kRowPad = Cfg::W + 8;
     static constexpr size_t kWork = sizeof(cx<float>) * Cfg::B::kSmemElems;
-    static constexpr size_t kPre = MODE == kModeReplay ? 0 : sizeof(cx<float>) * 2 * Cfg::NBR * kRowPad;
-    static size_t bytes(int Lloc) { return kWork + kPre + sizeof(float2) * (Lloc > 0 ? Lloc : 1); }
+    static constexpr size_t kPre = MODE == kModeReplay ? 0 : sizeof(cx<float>) * Cfg::NBR * kRowPad;
+    static constexpr size_t kTw = sizeof(cx<float>) * Cfg::W;
+    static constexpr size_t kG = sizeof(float) * LS::kBPT * LS::kR * Cfg::NT;
+    static constexpr size_t kTf = kWork + kPre + kTw + kG;  // offset of the per-plane constants
+    static size_t bytes(int Lloc) { return kTf + sizeof(float2) * (Lloc > 0 ? Lloc : 1); }
 };
 
 template <class Cfg, int MODE, bool LOCAL>
@@ -181,30 +187,32 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<float>* sm = reinterpret_cast<cx<float>*>(smem_raw);
     cx<float>* pre = reinterpret_cast<cx<float>*>(smem_raw + SM::kWork);
-    float2* s_tf = reinterpret_cast<float2*>(smem_raw + SM::kWork + SM::kPre);  // (phase0, 2 pi z) per plane
-    __shared__ unsigned long long s_bar[2];
+    cx<float>* s_tw = reinterpret_cast<cx<float>*>(smem_raw + SM::kWork + SM::kPre);
+    float* s_G = reinterpret_cast<float*>(smem_raw + SM::kWork + SM::kPre + SM::kTw);
+    float2* s_tf = reinterpret_cast<float2*>(smem_raw + SM::kTf);  // (phase0, 2 pi z) per plane
+    __shared__ unsigned long long s_bar;
 
     const int row0 = blockIdx.x * NBR;  // row = c * H + y; a CTA never spans two channels
     const int c = row0 / H;
     const size_t plane_stride = static_cast<size_t>(C) * H * W;
     const int nplanes = MODE == kModeReplay ? nrep : Lloc;
     for (int l = threadIdx.x; l < nplanes; l += Cfg::NT) s_tf[l] = make_float2(tfc[l * C + c].phase0, tfc[l * C + c].two_pi_z_f);
+    for (int k = threadIdx.x; k < W; k += Cfg::NT) s_tw[k] = tw[k];
 
-    // prefetch of plane l's NBR rows into buffer l & 1 (one thread issues)
+    // prefetch of plane l's NBR rows (one thread issues; the buffer is free once
+    // every thread has finished the previous plane's first FFT stage)
     auto issue = [&](int l) {
-        const int bsel = l & 1;
         const cx<float>* src = layers + l * plane_stride + static_cast<size_t>(row0) * W;
         fence_proxy_async_smem();  // the buffer's previous generic reads precede the async writes
-        mbar_expect_tx(&s_bar[bsel], NBR * W * static_cast<unsigned>(sizeof(cx<float>)));
+        mbar_expect_tx(&s_bar, NBR * W * static_cast<unsigned>(sizeof(cx<float>)));
 #pragma unroll
         for (int b = 0; b < NBR; ++b)
-            bulk_g2s(pre + (bsel * NBR + b) * SM::kRowPad, src + static_cast<size_t>(b) * W,
-                     W * static_cast<unsigned>(sizeof(cx<float>)), &s_bar[bsel]);
+            bulk_g2s(pre + b * SM::kRowPad, src + static_cast<size_t>(b) * W,
+                     W * static_cast<unsigned>(sizeof(cx<float>)), &s_bar);
     };
     if constexpr (MODE != kModeReplay) {
         if (threadIdx.x == 0) {
-            mbar_init(&s_bar[0], 1);
-            mbar_init(&s_bar[1], 1);
+            mbar_init(&s_bar, 1);
             mbar_init_fence();
         }
         __syncthreads();
@@ -226,8 +234,9 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
     // Plane-independent part of the transfer-function phase for each owned spectral
     // sample: g = f^2 / (1/l + sqrt(1/l^2 - f^2)), or -1 outside the propagating
     // band (band test in f64, reference order).  Per plane the phase is then
-    // phase0 - 2 pi z g (see tf_value<float>).
-    float G[LS::kBPT][LS::kR];
+    // phase0 - 2 pi z g (see tf_value<float>).  Kept in shared memory, one slot
+    // per (q, r) and thread (registers go to the FFT).
+    auto G = [&](int q, int r) -> float& { return s_G[(q * LS::kR + r) * Cfg::NT + threadIdx.x]; };
     {
         const TfChan p0 = tfc[c];  // 1/l^2, 1/l depend on the channel only
 #pragma unroll
@@ -235,15 +244,16 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
 #pragma unroll
             for (int r = 0; r < LS::kR; ++r) {
                 S[q][r] = czf();
-                G[q][r] = -1.0f;
+                float g = -1.0f;
                 int b, i;
                 if (owner(q, r, b, i)) {
                     const double fxv = fx[i], fyv = fy[(row0 + b) - c * H];
                     const double fx2 = __dmul_rn(fxv, fxv), fy2 = __dmul_rn(fyv, fyv);
                     const double arg = __dsub_rn(__dsub_rn(p0.inv_l2, fx2), fy2);
                     if (!(arg < 0.0))
-                        G[q][r] = static_cast<float>(__dadd_rn(fx2, fy2)) / (p0.inv_l + sqrtf(static_cast<float>(arg)));
+                        g = static_cast<float>(__dadd_rn(fx2, fy2)) / (p0.inv_l + sqrtf(static_cast<float>(arg)));
                 }
+                G(q, r) = g;
             }
     }
     // H_{Z_l} at owned sample (q, r) inside the propagating band: the
@@ -257,26 +267,26 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
             if (p.local) return tf_value<float>(p, fx[i], fy[(row0 + b) - c * H]);
         }
         const float2 t = s_tf[l];
-        return phasor_reduced(t.x - t.y * G[q][r]);
+        return phasor_reduced(t.x - t.y * G(q, r));
     };
     auto band_mask = [&]() {
 #pragma unroll
         for (int q = 0; q < LS::kBPT; ++q)
 #pragma unroll
             for (int r = 0; r < LS::kR; ++r)
-                if (G[q][r] < 0.0f) S[q][r] = czf();
+                if (G(q, r) < 0.0f) S[q][r] = czf();
     };
 
     if constexpr (MODE != kModeReplay) {
         for (int l = 0; l < Lloc; ++l) {
-            // buffer (l + 1) & 1 was last read by plane l - 1's first stage, which
-            // ended with a barrier
-            if (threadIdx.x == 0 && l + 1 < Lloc) issue(l + 1);
-            mbar_wait(&s_bar[l & 1], (l >> 1) & 1);
-            const cx<float>* src = pre + (l & 1) * NBR * SM::kRowPad;
-            auto load = [&](int, int, int b, int i) -> cx<float> { return src[b * SM::kRowPad + i]; };
+            mbar_wait(&s_bar, l & 1);
+            auto load = [&](int, int, int b, int i) -> cx<float> { return pre[b * SM::kRowPad + i]; };
             auto store = [&](int q, int r, int b, int i, cx<float> v) { S[q][r] = cfma(v, tf(l, q, r, b, i), S[q][r]); };
-            fft_static<float, -1, B, P>(sm, tw, load, store);
+            // once the first stage has read the buffer, start loading the next plane
+            auto hook = [&] {
+                if (threadIdx.x == 0 && l + 1 < Lloc) issue(l + 1);
+            };
+            fft_static<float, -1, B, P>(sm, s_tw, load, store, hook);
         }
         band_mask();
     }
@@ -307,13 +317,13 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
         cx<float>* dst = out + static_cast<size_t>(row0) * W;
         auto load = [&](int q, int r, int, int) -> cx<float> { return S[q][r]; };
         auto store = [&](int, int, int b, int i, cx<float> v) { dst[static_cast<size_t>(b) * W + i] = v; };
-        fft_static<float, +1, B, Pinv>(sm, tw, load, store);
+        fft_static<float, +1, B, Pinv>(sm, s_tw, load, store);
     }
     for (int l = 0; l < nrep; ++l) {
         cx<float>* dst = out + (static_cast<size_t>(l + has_holo) * C * H + row0) * W;
         auto load = [&](int q, int r, int b, int i) -> cx<float> { return S[q][r] * conj(tf(l, q, r, b, i)); };
         auto store = [&](int, int, int b, int i, cx<float> v) { dst[static_cast<size_t>(b) * W + i] = v; };
-        fft_static<float, +1, B, Pinv>(sm, tw, load, store);
+        fft_static<float, +1, B, Pinv>(sm, s_tw, load, store);
     }
 }
 
