@@ -47,12 +47,29 @@ template <> struct PlanOf<2160> { using type = Radices<16, 9, 15>; };
 template <> struct PlanOf<3840> { using type = Radices<16, 16, 15>; };
 
 // column passes: strips of NB columns, NT threads, MINB CTAs per SM (register cap)
+// The twiddle table is copied to shared memory behind the FFT work area
+// (HOLO_COL_SMEM_TW=0 reads it from global memory instead).
+#ifndef HOLO_COL_SMEM_TW
+#define HOLO_COL_SMEM_TW 1
+#endif
 template <int H_, int NB_, int NT_, int MINB_>
 struct ColCfgT {
     static constexpr int H = H_, NB = NB_, NT = NT_, kMinBlocks = MINB_;
     using B = Batch<H, NB, NT>;
-    static constexpr size_t kSmem = sizeof(cx<float>) * B::kSmemElems;
+    static constexpr size_t kSmem = sizeof(cx<float>) * (B::kSmemElems + (HOLO_COL_SMEM_TW ? H : 0));
 };
+
+// twiddles for a column pass: staged into shared memory before the first stage
+// (whose closing barrier publishes them; stage 1 uses none)
+template <class Cfg>
+__device__ __forceinline__ const cx<float>* col_twiddles(cx<float>* sm, const cx<float>* __restrict__ tw) {
+    if constexpr (HOLO_COL_SMEM_TW) {
+        cx<float>* s_tw = sm + Cfg::B::kSmemElems;
+        for (int k = threadIdx.x; k < Cfg::H; k += Cfg::NT) s_tw[k] = tw[k];
+        return s_tw;
+    }
+    return tw;
+}
 // default: 8-column strips (64-byte row segments); 2 CTAs per SM while 64 registers suffice
 template <int H>
 using ColCfg = ColCfgT<H, 8, (H >= 1024 ? 512 : 256), (H <= 1280 ? 2 : 1)>;
@@ -114,7 +131,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_col_fwd(cx<float>*
         const int x = x0 + b;
         if (x < W) base[static_cast<size_t>(i) * W + x] = v;
     };
-    fft_static<float, -1, typename Cfg::B, typename PlanOf<H>::type>(sm, tw, load, store);
+    fft_static<float, -1, typename Cfg::B, typename PlanOf<H>::type>(sm, col_twiddles<Cfg>(sm, tw), load, store);
 }
 
 // ---------------------------------------------------------------- 2. row pass with the spectrum in registers
@@ -362,7 +379,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_col_inv_epi(const 
         }
     };
     using Pinv = typename RevPlan<typename PlanOf<H>::type>::type;
-    fft_static<float, +1, typename Cfg::B, Pinv>(sm, tw, load, store);
+    fft_static<float, +1, typename Cfg::B, Pinv>(sm, col_twiddles<Cfg>(sm, tw), load, store);
 }
 
 template <class K>
