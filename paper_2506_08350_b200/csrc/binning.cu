@@ -47,7 +47,9 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* total)
     return warp_prefix + inc - v;
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_partials(const unsigned* __restrict__ in, long long n,
+// the scanned sequence is in[i] + in2[i] (in2 may be null)
+__global__ void __launch_bounds__(kScanThreads) k_scan_partials(const unsigned* __restrict__ in,
+                                                                const unsigned* __restrict__ in2, long long n,
                                                                 unsigned* __restrict__ partials,
                                                                 unsigned* __restrict__ dmax) {
     const long long base = static_cast<long long>(blockIdx.x) * kScanTile;
@@ -55,7 +57,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_partials(const unsigned* 
     for (int k = 0; k < kScanItems; ++k) {
         const long long i = base + static_cast<long long>(k) * kScanThreads + threadIdx.x;
         if (i < n) {
-            const unsigned v = in[i];
+            const unsigned v = in[i] + (in2 ? in2[i] : 0u);
             s += v;
             m = v > m ? v : m;
         }
@@ -84,7 +86,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_top(unsigned* __restrict_
     if (threadIdx.x == 0) partials[nblocks] = carry;
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_final(const unsigned* __restrict__ in, long long n,
+__global__ void __launch_bounds__(kScanThreads) k_scan_final(const unsigned* __restrict__ in,
+                                                             const unsigned* __restrict__ in2, long long n,
                                                              const unsigned* __restrict__ partials,
                                                              unsigned* __restrict__ out, int nblocks) {
     // each thread owns kScanItems consecutive elements
@@ -93,7 +96,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_final(const unsigned* __r
     unsigned s = 0;
     for (int k = 0; k < kScanItems; ++k) {
         const long long i = base + k;
-        v[k] = i < n ? in[i] : 0u;
+        v[k] = i < n ? in[i] + (in2 ? in2[i] : 0u) : 0u;
         s += v[k];
     }
     unsigned total;
@@ -159,14 +162,23 @@ __global__ void __launch_bounds__(256) k_bucket_emit(PreOut pre, size_t N, int L
         egidx[e] = static_cast<int>(i);
     };
     if (!soft) {
-        // hard assignment: the rect's tiles 4 at a time, so the slot atomics of a
-        // group are in flight together instead of one round trip per entry
         if (pre.count[i] == 0) return;
         const int l = pre.plane[i];
         if (l < pb || l >= pe) return;
         const int4 r = pre.rect[i];
         const int w = r.y - r.x, n = w * (r.w - r.z);
         const int b0 = (l - pb) * num_tiles + r.z * tiles_x + r.x;
+        if (pre.slots && n <= kSlots) {
+            // slots taken in preprocess: no atomics
+#pragma unroll
+            for (int k = 0; k < kSlots; ++k)
+                if (k < n) put(b0 + (k / w) * tiles_x + k % w, pre.slots[static_cast<size_t>(k) * N + i]);
+            if (over) atomicOr(flags, kFlagOverflow);
+            return;
+        }
+        // the rect's tiles 4 at a time, so the slot atomics of a group are in flight
+        // together instead of one round trip per entry; with preprocess slots, the
+        // large Gaussians' slots follow the small ones' (bcount) in each bucket
         for (int k = 0; k < n; k += 4) {
             int b[4];
             unsigned s[4];
@@ -174,7 +186,7 @@ __global__ void __launch_bounds__(256) k_bucket_emit(PreOut pre, size_t N, int L
             for (int u = 0; u < 4; ++u) {
                 const int idx = k + u;
                 b[u] = b0 + (idx / w) * tiles_x + idx % w;
-                if (idx < n) s[u] = atomicAdd(cursor + b[u], 1u);
+                if (idx < n) s[u] = atomicAdd(cursor + b[u], 1u) + (pre.slots ? pre.bcount[b[u]] : 0u);
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u)
@@ -258,15 +270,16 @@ __global__ void k_entry_depths(const int* __restrict__ egidx, const double* __re
 
 }  // namespace
 
-void exclusive_scan_u32(holo_ctx* ctx, const unsigned* in, unsigned* out, long long n, unsigned* d_max) {
+void exclusive_scan_u32(holo_ctx* ctx, const unsigned* in, unsigned* out, long long n, unsigned* d_max,
+                        const unsigned* in2) {
     const int nblocks = static_cast<int>((n + kScanTile - 1) / kScanTile);
     const int nb = nblocks > 0 ? nblocks : 1;
     unsigned* partials = static_cast<unsigned*>(ctx->buffer("scan_partials", sizeof(unsigned) * (nb + 1)));
-    k_scan_partials<<<nb, kScanThreads, 0, ctx->stream>>>(in, n, partials, d_max);
+    k_scan_partials<<<nb, kScanThreads, 0, ctx->stream>>>(in, in2, n, partials, d_max);
     HC_LAUNCHED(ctx);
     k_scan_top<<<1, kScanThreads, 0, ctx->stream>>>(partials, nb);
     HC_LAUNCHED(ctx);
-    k_scan_final<<<nb, kScanThreads, 0, ctx->stream>>>(in, n, partials, out, nb);
+    k_scan_final<<<nb, kScanThreads, 0, ctx->stream>>>(in, in2, n, partials, out, nb);
     HC_LAUNCHED(ctx);
 }
 

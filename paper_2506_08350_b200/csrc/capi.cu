@@ -340,6 +340,16 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     unsigned* bstart = buf<unsigned>(ctx, "bstart", B + 1);
     HC_CUDA(cudaMemsetAsync(misc, 0, sizeof(unsigned) * 8, ctx->stream));
     HC_CUDA(cudaMemsetAsync(bcount, 0, sizeof(unsigned) * (B + 1), ctx->stream));
+    // hard assignment: preprocess counts the buckets and hands out entry slots
+    const bool hard = !st.soft_assignment;
+    unsigned* bbig = hard ? buf<unsigned>(ctx, "bbig", B + 1) : nullptr;
+    if (hard) HC_CUDA(cudaMemsetAsync(bbig, 0, sizeof(unsigned) * (B + 1), ctx->stream));
+    pre.slots = hard ? buf<unsigned>(ctx, "slots", static_cast<size_t>(kSlots) * N) : nullptr;
+    pre.bcount = bcount;
+    pre.bbig = bbig;
+    pre.pb = pb;
+    pre.pe = pe;
+    pre.num_tiles = g.num_tiles;
 
     const int sk = ctx->scene_cur;  // the scene set this frame reads (only preprocess reads it)
     if (ctx->scene_wait[sk]) {
@@ -352,8 +362,8 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     HC_CUDA(cudaEventRecord(ctx->ev_scene_free[sk], ctx->stream));
 
     ctx->stage_begin();
-    bucket_count(ctx, pre, N, L, pb, pe, g.tiles_x, g.num_tiles, st.soft_assignment, bcount);
-    exclusive_scan_u32(ctx, bcount, bstart, B, misc + 2);
+    if (!hard) bucket_count(ctx, pre, N, L, pb, pe, g.tiles_x, g.num_tiles, st.soft_assignment, bcount);
+    exclusive_scan_u32(ctx, bcount, bstart, B, misc + 2, bbig);
     // pinned status words: flags, num_valid, max bucket, -, E
     unsigned* hp = ctx->host_status + holo_ctx::kStatusSlots * holo_ctx::kStatusWords;
     unsigned capacity;
@@ -374,7 +384,9 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     }
     auto* ekey = buf<unsigned long long>(ctx, "ekey", capacity);
     int* egidx = buf<int>(ctx, "egidx", capacity);
-    unsigned* cursor = bcount;  // reuse: zero it and count again during emission
+    // emission cursors: soft mode counts again from zero in bcount; hard mode keeps
+    // bcount (the small Gaussians' slot counts) and counts the large ones in bbig
+    unsigned* cursor = hard ? bbig : bcount;
     HC_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned) * (B + 1), ctx->stream));
     bucket_emit(ctx, pre, N, L, pb, pe, g.tiles_x, g.num_tiles, st.soft_assignment, bstart, cursor, ekey, egidx,
                 capacity, misc);

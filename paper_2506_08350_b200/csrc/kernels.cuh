@@ -100,7 +100,16 @@ struct PreOut {
     holo_projected* projected;  // optional full f64 record
     unsigned* flags;         // bit0 degenerate quaternion, bit1 negative amplitude
     unsigned* num_valid;
+    // Hard assignment: preprocess also counts the entries per bucket of planes
+    // [pb, pe).  A Gaussian with at most kSlots entries takes its in-bucket slots
+    // there (atomic with return on bcount, stored in slots[k][N]); larger ones only
+    // count into bbig and take slots bcount[b] + (0..bbig[b]) at emission.
+    unsigned* slots;         // null: counting left to k_bucket_count (soft mode)
+    unsigned* bcount;
+    unsigned* bbig;
+    int pb, pe, num_tiles;
 };
+constexpr int kSlots = 8;
 
 void host_world_to_cam(const holo_camera& cam, double wc[9]);
 void preprocess(holo_ctx* ctx, const CameraConsts& cc, const holo_raster_settings& st, double near_clip, int L,
@@ -110,7 +119,9 @@ constexpr int kSortCap = 1024;     // largest bucket the compositing CTA sorts i
 constexpr int kWarpSortCap = 128;  // buckets up to this size are sorted one warp each (k_sort_small)
 
 // ---- binning.cu
-void exclusive_scan_u32(holo_ctx* ctx, const unsigned* in, unsigned* out, long long n, unsigned* d_max);
+// out = exclusive scan of in (+ in2 when given), out[n] = total; *d_max = max element
+void exclusive_scan_u32(holo_ctx* ctx, const unsigned* in, unsigned* out, long long n, unsigned* d_max,
+                        const unsigned* in2 = nullptr);
 void bucket_count(holo_ctx* ctx, const PreOut& pre, size_t N, int L, int plane_begin, int plane_end, int tiles_x,
                   int num_tiles, int soft, unsigned* bcount);
 // validation / status flags written by the frame's kernels (misc[0])

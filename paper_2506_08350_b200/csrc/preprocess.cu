@@ -257,6 +257,23 @@ __global__ void __launch_bounds__(256, PROJ ? 1 : HOLO_PRE_MINB) k_preprocess(Pr
             count = static_cast<unsigned>(nplanes) * static_cast<unsigned>((x1 - x0) * (y1 - y0));
         }
         atomicAdd(o.num_valid, 1u);
+        // bucket counting for hard assignment (see PreOut): the slot atomics are
+        // issued together and their latency hides behind the other warps' math
+        if (o.slots && count > 0 && best >= o.pb && best < o.pe) {
+            const int w = x1 - x0, n = static_cast<int>(count);
+            const int b0 = (best - o.pb) * o.num_tiles + y0 * a.tiles_x + x0;
+            if (n <= kSlots) {
+                unsigned s[kSlots];
+#pragma unroll
+                for (int k = 0; k < kSlots; ++k)
+                    if (k < n) s[k] = atomicAdd(o.bcount + b0 + (k / w) * a.tiles_x + k % w, 1u);
+#pragma unroll
+                for (int k = 0; k < kSlots; ++k)
+                    if (k < n) o.slots[static_cast<size_t>(k) * a.n + i] = s[k];
+            } else {
+                for (int k = 0; k < n; ++k) atomicAdd(o.bbig + b0 + (k / w) * a.tiles_x + k % w, 1u);
+            }
+        }
     }
     o.rec[i] = r;
     o.rect[i] = rect;
