@@ -213,6 +213,42 @@ int holo_render_begin(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wa
 int holo_render_end(holo_ctx* ctx, const holo_wave* wave, const holo_prop_options* prop, int plane_begin,
                     int plane_end, const void* spectrum, unsigned outputs);
 
+/* ---- gradients (rasterizer.hpp:79-81 raster_backward; pipeline.cpp:63-91) ----
+ * Scene-shaped gradient arrays, device f64 (SceneGradients, scene.hpp:40-46;
+ * mu_screen is N x 2).  NULL members are not written; the others are overwritten. */
+typedef struct {
+    double* positions;      /* n*3 */
+    double* rotations;      /* n*4 */
+    double* log_scales;     /* n*3 */
+    double* amplitudes;     /* n*3 */
+    double* opacity_logits; /* n */
+    double* phases;         /* n*3 */
+    double* plane_logits;   /* n*num_planes */
+    double* mu_screen;      /* n*2 */
+} holo_scene_grads;
+
+/* raster_backward (rasterizer.cpp:332-528) of the context's last holo_render,
+ * which must have requested HOLO_OUT_AUX, on the same camera / wave / settings,
+ * with the scene not re-uploaded since.  grad_layers = dL/d(layers): device
+ * float2 [L][C][H][W].  Per-entry gradients are fp32 (reduced in a fixed
+ * per-warp order, across a tile's warps by shared-memory float atomics); the
+ * per-Gaussian merge (entry order, as the reference) and the chain to the
+ * parameters are f64. */
+int holo_raster_backward(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave,
+                         const holo_raster_settings* settings, const void* grad_layers, holo_scene_grads* grads);
+
+/* The gradient branch of total_loss (pipeline.cpp:63-80) for a given
+ * dL/d(intensities) (device float [L][C][H][W]): gv_l = 2 replayed_l dL/dI_l, the
+ * adjoint of the replay and of the recording (grad_hologram = sum_l propagate(gv_l,
+ * +Z_l), grad_layers_l = propagate(grad_hologram, -Z_l): the forward propagation
+ * applied to gv), then raster_backward.  Needs the last holo_render with
+ * HOLO_OUT_REPLAYED | HOLO_OUT_AUX.  grad_layers_out (float2 [L][C][H][W]) and
+ * grad_hologram_out (float2 [C][H][W]) are optional device outputs. */
+int holo_pipeline_backward(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave,
+                           const holo_raster_settings* settings, const holo_prop_options* prop,
+                           const void* grad_intensities, holo_scene_grads* grads, void* grad_layers_out,
+                           void* grad_hologram_out);
+
 /* Device pointer and size of one output buffer of the last render. */
 int holo_frame_buffer(holo_ctx* ctx, int buffer, void** dev_ptr, size_t* bytes);
 /* Synchronous device-to-host copy of one output buffer (bytes must match). */

@@ -78,6 +78,11 @@ class _Raster(C.Structure):
                 ("bucket_start", C.POINTER(C.c_uint32))]
 
 
+class _Grads(C.Structure):
+    _fields_ = [(k, _dp) for k in ("positions", "rotations", "log_scales", "amplitudes", "opacity_logits", "phases",
+                                   "plane_logits", "mu_screen")]
+
+
 class OracleError(RuntimeError):
     """Mirror of holo::HoloError (common.hpp:76-79): ``kind`` in config/io/usage/numeric."""
 
@@ -339,6 +344,49 @@ class Oracle:
         self._check(rc)
         ras = self._unpack_raster(r, sa.s.n) if raster else None
         return SimpleNamespace(hologram=holo, replayed=rep, intensities=ints, raster=ras, stage_seconds=secs)
+
+    # -------------------------------------------------------------- gradients (reference build only)
+    _GRAD_FIELDS = ("positions", "rotations", "log_scales", "amplitudes", "opacity_logits", "phases",
+                    "plane_logits", "mu_screen")
+
+    def _grads(self, n, L):
+        shapes = {"positions": (n, 3), "rotations": (n, 4), "log_scales": (n, 3), "amplitudes": (n, 3),
+                  "opacity_logits": (n,), "phases": (n, 3), "plane_logits": (n, L), "mu_screen": (n, 2)}
+        arrays = {k: np.zeros(shapes[k]) for k in self._GRAD_FIELDS}
+        g = _Grads()
+        for k in self._GRAD_FIELDS:
+            setattr(g, k, arrays[k].ctypes.data_as(_dp))
+        return g, arrays
+
+    def raster_backward(self, scene, cam, wave, settings, grad_layers):
+        """holo::raster_backward (rasterizer.cpp:332-528) of raster_forward's
+        output for dL/d(layers) [L,3,H,W]; returns a dict of scene gradients."""
+        if self.kind != "ref":
+            raise OracleError(3, "raster_backward needs the reference build")
+        sa = _SceneArgs(scene)
+        g, arrays = self._grads(sa.s.n, sa.s.num_planes)
+        gl = _c128(grad_layers)
+        self._check(self.lib.ref_raster_backward(C.byref(sa.s), C.byref(_camera(cam)), C.byref(_wave(wave)),
+                                                 C.byref(_settings(settings)), _ptr(gl), C.byref(g)))
+        return arrays
+
+    def pipeline_backward(self, scene, cam, wave, settings, prop, grad_intensities):
+        """The gradient branch of holo::total_loss (pipeline.cpp:63-80) for
+        dL/d(intensities) [L,C,H,W]: returns (scene gradients, grad_hologram,
+        grad_layers)."""
+        if self.kind != "ref":
+            raise OracleError(3, "pipeline_backward needs the reference build")
+        sa = _SceneArgs(scene)
+        wv = _wave(wave)
+        L, Cn, h, w = wv.num_planes, wv.channels, wv.ny, wv.nx
+        g, arrays = self._grads(sa.s.n, L)
+        gi = np.ascontiguousarray(grad_intensities, dtype=np.float64)
+        gh = np.zeros((Cn, h, w), dtype=np.complex128)
+        gl = np.zeros((L, Cn, h, w), dtype=np.complex128)
+        self._check(self.lib.ref_pipeline_backward(C.byref(sa.s), C.byref(_camera(cam)), C.byref(wv),
+                                                   C.byref(_settings(settings)), C.byref(_prop(prop)), _ptr(gi),
+                                                   _ptr(gh), _ptr(gl), C.byref(g)))
+        return arrays, gh, gl
 
 
 def psnr(a, b) -> float:

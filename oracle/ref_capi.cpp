@@ -297,4 +297,72 @@ int ref_pipeline_forward(const ho_scene* s, const ho_camera* cam, const ho_wave*
     });
 }
 
+// Gradient outputs (caller-allocated, scene-shaped; mu_screen is N x 2).
+struct ref_grads {
+    double *positions, *rotations, *log_scales, *amplitudes, *opacity_logits, *phases, *plane_logits, *mu_screen;
+};
+
+static void copy_grads(const holo::SceneGradients& g, ref_grads* o) {
+    auto put = [](const std::vector<double>& v, double* d) {
+        if (d && !v.empty()) std::memcpy(d, v.data(), sizeof(double) * v.size());
+    };
+    put(g.positions, o->positions);
+    put(g.rotations, o->rotations);
+    put(g.log_scales, o->log_scales);
+    put(g.amplitudes, o->amplitudes);
+    put(g.opacity_logits, o->opacity_logits);
+    put(g.phases, o->phases);
+    put(g.plane_logits, o->plane_logits);
+    put(g.mu_screen, o->mu_screen);
+}
+
+// holo::raster_backward (rasterizer.cpp:332-528) after holo::raster_forward;
+// grad_layers: [L][3][H][W] complex128.
+int ref_raster_backward(const ho_scene* s, const ho_camera* cam, const ho_wave* cfg, const ho_settings* st,
+                        const double* grad_layers, ref_grads* out) {
+    return guarded([&] {
+        const holo::GaussianScene scene = to_scene(s);
+        const holo::WaveConfig wc = to_wave(cfg);
+        const holo::RenderSettings rs = to_settings(st);
+        const holo::RasterForward r = holo::raster_forward(scene, to_camera(cam), wc, rs);
+        std::vector<holo::ComplexField> gl;
+        const size_t n = static_cast<size_t>(cfg->nx) * cfg->ny * 3;
+        for (int l = 0; l < cfg->num_planes; ++l) gl.push_back(to_field(grad_layers + 2 * n * l, cfg->nx, cfg->ny, 3, cfg->pitch));
+        copy_grads(holo::raster_backward(scene, to_camera(cam), wc, rs, r, gl), out);
+    });
+}
+
+// The gradient branch of holo::total_loss (pipeline.cpp:63-80) for a given
+// dL/d(intensities) [L][C][H][W] (f64), C = 3: pipeline_forward, the adjoint of
+// the replay and of the recording, then raster_backward.  grad_hologram [C][H][W]
+// and grad_layers [L][C][H][W] (complex128) are optional outputs.  The loss terms
+// themselves (losses.cpp) are not on this path.
+int ref_pipeline_backward(const ho_scene* s, const ho_camera* cam, const ho_wave* cfg, const ho_settings* st,
+                          const ho_prop* opt, const double* grad_intensities, double* grad_hologram,
+                          double* grad_layers, ref_grads* out) {
+    return guarded([&] {
+        const holo::GaussianScene scene = to_scene(s);
+        const holo::WaveConfig wc = to_wave(cfg);
+        holo::PipelineOptions po;
+        po.raster = to_settings(st);
+        po.prop = to_prop(opt);
+        const holo::PipelineForward f = holo::pipeline_forward(scene, to_camera(cam), wc, po);
+        const size_t P = static_cast<size_t>(wc.nx) * wc.ny * wc.channels();
+        const auto z = holo::plane_positions(wc);
+        holo::ComplexField gh(wc.nx, wc.ny, wc.channels(), wc.pitch);
+        for (size_t l = 0; l < f.replayed.size(); ++l) {  // pipeline.cpp:66-73
+            holo::ComplexField gv = f.replayed[l];
+            for (size_t i = 0; i < gv.data.size(); ++i) gv.data[i] = 2.0 * gv.data[i] * grad_intensities[l * P + i];
+            const holo::ComplexField gp = holo::propagate(gv, wc, z[l], po.prop);
+            for (size_t i = 0; i < gp.data.size(); ++i) gh.data[i] += gp.data[i];
+        }
+        std::vector<holo::ComplexField> gl;  // pipeline.cpp:75-78
+        for (size_t l = 0; l < z.size(); ++l) gl.push_back(holo::propagate(gh, wc, -z[l], po.prop));
+        if (grad_hologram) std::memcpy(grad_hologram, gh.data.data(), sizeof(double) * 2 * P);
+        for (size_t l = 0; l < gl.size(); ++l)
+            if (grad_layers) std::memcpy(grad_layers + 2 * P * l, gl[l].data.data(), sizeof(double) * 2 * P);
+        copy_grads(holo::raster_backward(scene, to_camera(cam), wc, po.raster, f.raster, gl), out);
+    });
+}
+
 }  // extern "C"

@@ -74,6 +74,14 @@ class Projected(C.Structure):
                 ("amp", C.c_double * 3), ("phase", C.c_double * 3), ("plane", C.c_int32), ("pad_", C.c_int32)]
 
 
+GRAD_FIELDS = ("positions", "rotations", "log_scales", "amplitudes", "opacity_logits", "phases", "plane_logits",
+               "mu_screen")
+
+
+class SceneGrads(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in GRAD_FIELDS]
+
+
 class FrameInfo(C.Structure):
     _fields_ = [("num_entries", C.c_uint64), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32),
                 ("num_buckets", C.c_int32), ("max_bucket", C.c_int32), ("num_valid", C.c_int32),
@@ -120,6 +128,9 @@ def lib() -> C.CDLL:
         "holo_frame_buffer": (i, [vp, i, P(vp), P(sz)]),
         "holo_frame_download": (i, [vp, i, vp, sz]),
         "holo_frame_download_async": (i, [vp, i, vp, sz]),
+        "holo_raster_backward": (i, [vp, P(Camera), P(Wave), P(RasterSettings), vp, P(SceneGrads)]),
+        "holo_pipeline_backward": (i, [vp, P(Camera), P(Wave), P(RasterSettings), P(PropOptions), vp,
+                                       P(SceneGrads), vp, vp]),
         "holo_fft2": (i, [vp, vp, i, i, i, i, i]),
         "holo_transfer_function": (i, [vp, P(Wave), d, P(PropOptions), vp, i]),
         "holo_propagate": (i, [vp, vp, vp, i, i, i, P(Wave), d, P(PropOptions), i]),

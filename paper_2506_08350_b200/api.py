@@ -219,6 +219,44 @@ class Context:
         L.check(self.lib.holo_render_end(self.h, C.byref(_wave(cfg)), C.byref(_prop(prop)), int(plane_begin),
                                          int(plane_end), C.c_void_p(spectrum_ptr or None), int(outputs)))
 
+    # ------------------------------------------------------------- gradients
+    def _grad_tensors(self, n: int, num_planes: int):
+        torch = _torch()
+        shapes = {"positions": (n, 3), "rotations": (n, 4), "log_scales": (n, 3), "amplitudes": (n, 3),
+                  "opacity_logits": (n,), "phases": (n, 3), "plane_logits": (n, num_planes), "mu_screen": (n, 2)}
+        out = {k: torch.empty(shapes[k], dtype=torch.float64, device=f"cuda:{self.device}") for k in L.GRAD_FIELDS}
+        g = L.SceneGrads()
+        for k in L.GRAD_FIELDS:
+            setattr(g, k, out[k].data_ptr())
+        return g, out
+
+    def raster_backward(self, cam: CameraView, cfg: WaveConfig, settings: Optional[RenderSettings],
+                        grad_layers, n: int):
+        """raster_backward (rasterizer.cpp:332-528) of this context's last render
+        (outputs must include OUT_AUX).  grad_layers: device complex64 tensor
+        [L, C, H, W].  Returns a dict of f64 device tensors (SceneGradients)."""
+        g, out = self._grad_tensors(n, cfg.num_planes)
+        L.check(self.lib.holo_raster_backward(self.h, C.byref(_camera(cam)), C.byref(_wave(cfg)),
+                                              C.byref(_settings(settings)), C.c_void_p(grad_layers.data_ptr()),
+                                              C.byref(g)))
+        return out
+
+    def pipeline_backward(self, cam: CameraView, cfg: WaveConfig, settings: Optional[RenderSettings],
+                          prop: Optional[PropagationOptions], grad_intensities, n: int):
+        """The gradient branch of total_loss (pipeline.cpp:63-80) for dL/dI (device
+        float32 tensor [L, C, H, W]) of the last render (outputs must include
+        OUT_REPLAYED | OUT_AUX).  Returns (grads, grad_layers, grad_hologram)."""
+        torch = _torch()
+        Cn, H, W = cfg.channels(), cfg.ny, cfg.nx
+        gl = torch.empty((cfg.num_planes, Cn, H, W), dtype=torch.complex64, device=f"cuda:{self.device}")
+        gh = torch.empty((Cn, H, W), dtype=torch.complex64, device=f"cuda:{self.device}")
+        g, out = self._grad_tensors(n, cfg.num_planes)
+        L.check(self.lib.holo_pipeline_backward(self.h, C.byref(_camera(cam)), C.byref(_wave(cfg)),
+                                                C.byref(_settings(settings)), C.byref(_prop(prop)),
+                                                C.c_void_p(grad_intensities.data_ptr()), C.byref(g),
+                                                C.c_void_p(gl.data_ptr()), C.c_void_p(gh.data_ptr())))
+        return out, gl, gh
+
     def buffer(self, which: int):
         p = C.c_void_p()
         n = C.c_size_t()
@@ -393,6 +431,36 @@ def pipeline_forward(scene: GaussianScene, cam: CameraView, cfg: WaveConfig,
         rep = [r[l] for l in range(Ln)]
     ras = _collect_raster(ctx, scene, cfg, Cn, info) if raster else None
     return PipelineForward(raster=ras, hologram=holo, replayed=rep, intensities=[ints[l] for l in range(Ln)])
+
+
+def raster_backward(scene: GaussianScene, cam: CameraView, cfg: WaveConfig, settings: Optional[RenderSettings],
+                    grad_layers, ctx: Optional[Context] = None) -> dict:
+    """rasterizer.hpp:79-81: scene gradients for dL/d(layers) [L, C, H, W] (numpy);
+    renders the raster forward first, as the reference's caller does."""
+    torch = _torch()
+    _check_shapes(scene, cam, cfg)
+    ctx = ctx or default_context()
+    ctx.upload_scene(scene)
+    ctx.render(cam, cfg, settings, None, outputs=L.OUT_LAYERS | L.OUT_AUX)
+    gl = torch.from_numpy(np.ascontiguousarray(grad_layers, dtype=np.complex64)).to(f"cuda:{ctx.device}")
+    out = ctx.raster_backward(cam, cfg, settings, gl, scene.size())
+    return {k: v.cpu().numpy() for k, v in out.items()}
+
+
+def pipeline_backward(scene: GaussianScene, cam: CameraView, cfg: WaveConfig, opt: Optional[PipelineOptions],
+                      grad_intensities, ctx: Optional[Context] = None):
+    """The gradient branch of total_loss (pipeline.cpp:63-80) for dL/dI [L, C, H, W]
+    (numpy): returns (scene gradients, grad_layers, grad_hologram) as numpy."""
+    torch = _torch()
+    _check_shapes(scene, cam, cfg)
+    opt = opt or PipelineOptions()
+    ctx = ctx or default_context()
+    ctx.upload_scene(scene)
+    ctx.render(cam, cfg, opt.raster, opt.prop, outputs=L.OUT_HOLOGRAM | L.OUT_REPLAYED | L.OUT_AUX)
+    gi = torch.from_numpy(np.ascontiguousarray(grad_intensities, dtype=np.float32)).to(f"cuda:{ctx.device}")
+    out, gl, gh = ctx.pipeline_backward(cam, cfg, opt.raster, opt.prop, gi, scene.size())
+    return ({k: v.cpu().numpy() for k, v in out.items()}, gl.cpu().numpy().astype(np.complex128),
+            gh.cpu().numpy().astype(np.complex128))
 
 
 def propagate(u, cfg: WaveConfig, z: float, opt: Optional[PropagationOptions] = None, precision: str = "f64"):

@@ -352,6 +352,7 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     pre.num_tiles = g.num_tiles;
 
     const int sk = ctx->scene_cur;  // the scene set this frame reads (only preprocess reads it)
+    ctx->f_scene_set = sk;
     if (ctx->scene_wait[sk]) {
         HC_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_scene_ready[sk], 0));
         ctx->scene_wait[sk] = false;
@@ -887,6 +888,8 @@ void render_front(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, 
     ctx->f_outputs = outputs;
     ctx->f_plane_begin = pb;
     ctx->f_plane_end = pe;
+    ctx->f_cam = cam;
+    ctx->f_st = st;
     raster_planes(ctx, cam, wave, st, g, pb, pe, outputs, info);
     if (po.pad2x) return;  // holo_render runs the padded operators on the spatial layers
     const int np = pe - pb;
@@ -946,9 +949,171 @@ void render_front(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, 
     if (full) render_back(ctx, wave, po, pb, pe, spec, outputs);
 }
 
+// ---------------------------------------------------------------- backward
+
+// the backward runs on the context's last frame: check that it is the one meant
+void check_backward_frame(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
+                          const holo_raster_settings& st) {
+    validate_wave(wave);
+    require((ctx->f_outputs & HOLO_OUT_AUX) != 0, HOLO_ERR_USAGE,
+            "backward needs the last render with HOLO_OUT_AUX (t_final, n_contrib)");
+    require(ctx->f_W == wave.nx && ctx->f_H == wave.ny && ctx->f_C == wave.channels && ctx->f_L == wave.num_planes,
+            HOLO_ERR_USAGE, "backward: wave config differs from the last render's");
+    require(std::memcmp(&ctx->f_cam, &cam, sizeof cam) == 0 && std::memcmp(&ctx->f_st, &st, sizeof st) == 0,
+            HOLO_ERR_USAGE, "backward: camera or render settings differ from the last render's");
+    require(ctx->f_plane_begin == 0 && ctx->f_plane_end == wave.num_planes, HOLO_ERR_USAGE,
+            "backward needs a full (unsharded) render");
+}
+
+// raster_backward (rasterizer.cpp:332-528) on the last frame's lists and records
+void raster_backward(holo_ctx* ctx, const holo_wave& wave, const holo_raster_settings& st,
+                     const cx<float>* grad_layers, const holo_scene_grads& grads) {
+    consume_status(ctx, true);  // E of an asynchronous frame
+    const size_t N = ctx->n;
+    const int L = wave.num_planes, C = wave.channels;
+    const unsigned capacity = ctx->f_cap;
+    const size_t E = std::min<uint64_t>(ctx->f_E, capacity);
+    const holo_ctx::SceneSet& set = ctx->scene_sets[ctx->f_scene_set];
+    const GRec* rec = static_cast<const GRec*>(ctx->buffer("rec", 1));
+    BwdRec* brec = buf<BwdRec>(ctx, "bwd_rec", N);
+    float* egrad = buf<float>(ctx, "bwd_egrad", E * 13);
+    bwd_prep(ctx, N, set.a[3], set.a[5], rec, brec);  // amplitudes, phases of the rendered scene set
+
+    RasterBwdArgs ra{};
+    ra.bstart = static_cast<const unsigned*>(ctx->buffer("bstart", 1));
+    ra.egidx = static_cast<const int*>(ctx->buffer("egidx", 1));
+    ra.rec = rec;
+    ra.brec = brec;
+    ra.rho = st.soft_assignment ? static_cast<const double*>(ctx->buffer("rho", 1)) : nullptr;
+    ra.L = L;
+    ra.C = C;
+    ra.W = wave.nx;
+    ra.H = wave.ny;
+    ra.tiles_x = ctx->f_tiles_x;
+    ra.num_tiles = ctx->f_tiles;
+    ra.plane_begin = 0;
+    ra.num_buckets = static_cast<int>(ctx->f_buckets);
+    ra.soft = st.soft_assignment;
+    ra.capacity = capacity;
+    ra.alpha_floor = static_cast<float>(st.alpha_floor);
+    ra.alpha_clamp = static_cast<float>(st.alpha_clamp);
+    ra.floor_positive = st.alpha_floor > 0.0 ? 1 : 0;
+    ra.grad_layers = grad_layers;
+    ra.t_final = static_cast<const float*>(ctx->buffer("t_final", 1));
+    ra.n_contrib = static_cast<const int*>(ctx->buffer("n_contrib", 1));
+    ra.egrad = egrad;
+    raster_backward_entries(ctx, ra, st.tile);
+
+    double* outs[8] = {grads.positions, grads.rotations, grads.log_scales, grads.amplitudes,
+                       grads.opacity_logits, grads.phases, grads.plane_logits, grads.mu_screen};
+    const size_t per[8] = {3, 4, 3, 3, 1, 3, static_cast<size_t>(L), 2};
+    for (int k = 0; k < 8; ++k)
+        if (outs[k]) HC_CUDA(cudaMemsetAsync(outs[k], 0, sizeof(double) * per[k] * N, ctx->stream));
+
+    GaussBwdArgs ga{};
+    ga.n = N;
+    ga.L = L;
+    ga.pb = 0;
+    ga.pe = L;
+    ga.num_tiles = ctx->f_tiles;
+    ga.tiles_x = ctx->f_tiles_x;
+    ga.soft = st.soft_assignment;
+    ga.capacity = capacity;
+    ga.bstart = ra.bstart;
+    ga.egidx = ra.egidx;
+    ga.egrad = egrad;
+    ga.rect = static_cast<const int4*>(ctx->buffer("rect", 1));
+    ga.count = static_cast<const unsigned*>(ctx->buffer("count", 1));
+    ga.plane = static_cast<const int*>(ctx->buffer("plane", 1));
+    ga.pmask = st.soft_assignment ? static_cast<const unsigned long long*>(ctx->buffer("pmask", 1)) : nullptr;
+    ga.positions = set.a[0];
+    ga.rotations = set.a[1];
+    ga.log_scales = set.a[2];
+    ga.opacity_logits = set.a[4];
+    ga.plane_logits = set.a[6];
+    host_world_to_cam(ctx->f_cam, ga.cam.wc);
+    for (int i = 0; i < 3; ++i) ga.cam.pos[i] = ctx->f_cam.pose[i];
+    ga.cam.focal = ctx->f_cam.focal_px;
+    ga.cam.ppx = ctx->f_cam.cx >= 0.0 ? ctx->f_cam.cx : ctx->f_cam.width / 2.0;
+    ga.cam.ppy = ctx->f_cam.cy >= 0.0 ? ctx->f_cam.cy : ctx->f_cam.height / 2.0;
+    ga.near_clip = st.near_clip > 0.0 ? st.near_clip : 0.2 * wave.distance;  // rasterizer.hpp:25-27
+    ga.dilation = st.dilation;
+    ga.alpha_floor = st.alpha_floor;
+    ga.soft_tau = st.soft_tau;
+    ga.ste_tau = st.ste_tau;
+    ga.g = grads;
+    gauss_backward(ctx, ga);
+}
+
+// The adjoint of pipeline_forward's propagation (pipeline.cpp:63-80): the
+// recording + replay of the forward, applied to gv = 2 replayed dL/dI.
+void adjoint_propagation(holo_ctx* ctx, const holo_wave& wave, const holo_prop_options& po, cx<float>* gv,
+                         cx<float>* gholo, cx<float>* glayers) {
+    const int W = wave.nx, H = wave.ny, C = wave.channels, L = wave.num_planes;
+    const size_t P = static_cast<size_t>(W) * H;
+    if (po.pad2x) {  // literal operators, as holo_render does
+        op_forward_record<float>(ctx, gv, L, gholo, wave, po);
+        op_inverse_propagate<float>(ctx, gholo, glayers, wave, po);
+        return;
+    }
+    const std::vector<double> z = plane_positions(wave);
+    const TfChan* tfc = upload_tf(ctx, "tf_bwd", wave, z, W, H, po.local_band_limit);
+    const int O = L + 1;  // the hologram, then every plane
+    cx<float>* stage = buf<cx<float>>(ctx, "bwd_stage", static_cast<size_t>(O) * C * P);
+    if (static_render_supported(W, H)) {
+        static_col_fwd(ctx, gv, W, H, L * C);
+        static_row(ctx, kModeFull, gv, nullptr, stage, W, H, C, L, 1, L, tfc, wave.pitch, po.local_band_limit != 0);
+        static_col_inv(ctx, stage, W, H, C, O, 1, gholo, glayers, nullptr);
+        return;
+    }
+    cx<float>* spec = buf<cx<float>>(ctx, "bwd_spectrum", static_cast<size_t>(C) * P);
+    rows_fft<float>(ctx, gv, gv, W, static_cast<long long>(L) * C * H, -1, 1.0f);
+    col_spectrum<float>(ctx, gv, spec, W, H, C, L, tfc, wave.pitch);
+    std::vector<int> plane_of(1, -1);
+    for (int l = 0; l < L; ++l) plane_of.push_back(l);
+    int* d_plane_of = buf<int>(ctx, "plane_of_bwd", O);
+    upload_small(ctx, d_plane_of, plane_of.data(), sizeof(int) * O);
+    col_replay<float>(ctx, spec, stage, W, H, C, O, d_plane_of, tfc, wave.pitch);
+    rows_epilogue(ctx, stage, W, H, C, O, 1, gholo, glayers, nullptr);
+}
+
 }  // namespace
 
 extern "C" {
+
+int holo_raster_backward(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave,
+                         const holo_raster_settings* settings, const void* grad_layers, holo_scene_grads* grads) {
+    return guarded([&] {
+        require(ctx && cam && wave && settings && grad_layers && grads, HOLO_ERR_USAGE, "null argument");
+        HC_CUDA(cudaSetDevice(ctx->device));
+        check_backward_frame(ctx, *cam, *wave, *settings);
+        raster_backward(ctx, *wave, *settings, static_cast<const cx<float>*>(grad_layers), *grads);
+    });
+}
+
+int holo_pipeline_backward(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave,
+                           const holo_raster_settings* settings, const holo_prop_options* prop,
+                           const void* grad_intensities, holo_scene_grads* grads, void* grad_layers_out,
+                           void* grad_hologram_out) {
+    return guarded([&] {
+        require(ctx && cam && wave && settings && grad_intensities && grads, HOLO_ERR_USAGE, "null argument");
+        HC_CUDA(cudaSetDevice(ctx->device));
+        check_backward_frame(ctx, *cam, *wave, *settings);
+        require((ctx->f_outputs & HOLO_OUT_REPLAYED) != 0, HOLO_ERR_USAGE,
+                "pipeline backward needs the last render with HOLO_OUT_REPLAYED");
+        const holo_prop_options po = prop ? *prop : holo_prop_options{0, 0};
+        const int W = wave->nx, H = wave->ny, C = wave->channels, L = wave->num_planes;
+        const size_t P = static_cast<size_t>(W) * H, n = static_cast<size_t>(L) * C * P;
+        const cx<float>* rep = static_cast<const cx<float>*>(ctx->buffer(out_name("replayed", ctx->out_sel), 1));
+        cx<float>* gv = buf<cx<float>>(ctx, "bwd_gv", n);
+        bwd_seed(ctx, rep, static_cast<const float*>(grad_intensities), gv, n);
+        cx<float>* gl = grad_layers_out ? static_cast<cx<float>*>(grad_layers_out) : buf<cx<float>>(ctx, "bwd_glayers", n);
+        cx<float>* gh = grad_hologram_out ? static_cast<cx<float>*>(grad_hologram_out)
+                                          : buf<cx<float>>(ctx, "bwd_gholo", static_cast<size_t>(C) * P);
+        adjoint_propagation(ctx, *wave, po, gv, gh, gl);
+        raster_backward(ctx, *wave, *settings, gl, *grads);
+    });
+}
 
 int holo_render_begin(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave,
                       const holo_raster_settings* settings, const holo_prop_options* prop, int plane_begin,

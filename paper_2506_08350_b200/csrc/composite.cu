@@ -16,18 +16,11 @@
 // evaluations are independent; only the blend is serial).  Evaluation is fp32
 // with the centre offset formed in f64 per entry, so dx, dy keep full fp32
 // precision, and alpha folded into the exponent: a = 2^(q + log2 alpha).
-#include "kernels.cuh"
+#include "raster_eval.cuh"
 
 namespace holo_cuda {
 
 namespace {
-
-// 2^x on the MUFU pipe (max rel. error 2^-22.5); x <= 0 here, results below 2^-126 flush to 0.
-__device__ __forceinline__ float ex2_approx(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
 
 template <int TILE>
 struct TileGeom {
@@ -121,28 +114,9 @@ __global__ void __launch_bounds__(256) k_sort_small(const unsigned* __restrict__
         warp_sort_bucket<4>(ekey, egidx, e0, n, lane);
 }
 
-// One staged entry: 48 bytes, read with three 16-byte shared loads from one base;
-// its accept box lives in a separate array read only by the ballot test.
-struct alignas(16) Staged {
-    float4 a;  // mx, my, ca, cb   (centre relative to the tile origin; conic, log2-scaled)
-    float4 b;  // cc, log2(alpha), col0 re, col0 im
-    float4 c;  // col1 re, col1 im, col2 re, col2 im
-};
-
 #ifdef HOLO_COUNT
 __device__ unsigned long long g_counts[4];
 #endif
-
-__device__ __forceinline__ float eval_alpha(const Staged* e, float fx, float fy, float clamp, float4& B) {
-    const float4 A = e->a;
-    B = e->b;
-    const cx<float> d = mk(fx, fy) - mk(A.x, A.y);  // one FADD2
-    const float dx = d.x, dy = d.y;
-    const float t = fmaf(A.w, dy, A.z * dx);
-    const float u = fmaf(dx, t, B.y);
-    const float q = fmaf(B.x * dy, dy, u);
-    return fminf(ex2_approx(q), clamp);
-}
 
 // acc_c += w * (amp_c cos phi_c, amp_c sin phi_c): one FFMA2 per channel
 __device__ __forceinline__ cx<float> axpy(float w, float re, float im, cx<float> acc) {
@@ -259,8 +233,9 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
                 for (int t = tid; t < n; t += G::kThreads) s_ord[t] = sm.sort.gid[t];
             }
             __syncthreads();
-            if (a.write_lists)
-                for (int t = tid; t < n; t += G::kThreads) a.egidx[e0 + t] = s_ord[t];
+            // the lists stay in reference order for the frame's other consumers
+            // (HOLO_BUF_ENTRY_*, the backward pass)
+            for (int t = tid; t < n; t += G::kThreads) a.egidx[e0 + t] = s_ord[t];
         }
 
         const float fx = static_cast<float>(lx) + 0.5f, fy = static_cast<float>(ly) + 0.5f;
@@ -277,17 +252,10 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
             for (int t = tid; t < cnt; t += G::kThreads) {
                 const int g = presorted ? a.egidx[e0 + base + t] : s_ord[base + t];
                 const GRec r = a.rec[g];
-                const float mx = static_cast<float>(r.mu_x - static_cast<double>(px0));
-                const float my = static_cast<float>(r.mu_y - static_cast<double>(py0));
                 float alpha = r.alpha;
                 if (a.soft)
                     alpha = static_cast<float>(static_cast<double>(r.alpha) * a.rho[static_cast<size_t>(g) * a.L + plane]);
-                Staged st;
-                st.a = make_float4(mx, my, r.ca, r.cb);
-                st.b = make_float4(r.cc, log2f(alpha), r.col[0], r.col[1]);
-                st.c = make_float4(r.col[2], r.col[3], r.col[4], r.col[5]);
-                sm.st.rec[t] = st;
-                sm.st.box[t] = make_float4(mx - r.hx, mx + r.hx, my - r.hy, my + r.hy);
+                stage_entry(r, px0, py0, alpha, sm.st.rec[t], sm.st.box[t]);
             }
             __syncthreads();
             if (!__all_sync(0xffffffffu, done)) {
@@ -298,7 +266,7 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
                     bool hit = false;
                     if (c0 + lane < cnt) {
                         const float4 bb = sm.st.box[c0 + lane];
-                        hit = !(bb.y < bxlo || bb.x > bxhi || bb.w < bylo || bb.z > byhi);
+                        hit = box_hits(bb, bxlo, bxhi, bylo, byhi);
                     }
                     unsigned mask = __ballot_sync(0xffffffffu, hit);
 #ifdef HOLO_COUNT

@@ -92,6 +92,9 @@ struct holo_ctx {
     unsigned f_num_valid = 0, f_max_bucket = 0;
     unsigned f_outputs = 0;
     int f_plane_begin = 0, f_plane_end = 0;
+    holo_camera f_cam{};            // camera and settings of the last render (the backward
+    holo_raster_settings f_st{};    // must be called with the same ones)
+    int f_scene_set = 0;            // scene set the last render read
 
     // asynchronous frames (holo_ctx_set_async): no host round trip inside a frame;
     // the entry buffers hold e_cap entries and each frame's status words

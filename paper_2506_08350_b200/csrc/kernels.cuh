@@ -164,6 +164,51 @@ struct CompositeArgs {
     int* n_contrib;           // optional
 };
 void composite(holo_ctx* ctx, const CompositeArgs& a, int tile);
+
+// ---- backward.cu
+struct alignas(16) BwdRec {  // per Gaussian: cos / sin of the phases, amplitudes, sigmoid(opacity)
+    float cs[6];
+    float amp[3];
+    float alpha;
+    float pad[2];
+};
+struct RasterBwdArgs {
+    const unsigned* bstart;
+    const int* egidx;          // bucket-major, depth-sorted (the forward's lists)
+    const GRec* rec;
+    const BwdRec* brec;
+    const double* rho;         // soft mode
+    int L, C, W, H, tiles_x, num_tiles, plane_begin, num_buckets;
+    int soft;
+    unsigned capacity;
+    float alpha_floor, alpha_clamp;
+    int floor_positive;
+    const cx<float>* grad_layers;  // [planes][C][H][W]
+    const float* t_final;          // the forward's aux outputs
+    const int* n_contrib;
+    float* egrad;                  // [E][13]
+};
+struct GaussBwdArgs {
+    size_t n;
+    int L, pb, pe, num_tiles, tiles_x, soft;
+    unsigned capacity;
+    const unsigned* bstart;
+    const int* egidx;
+    const float* egrad;
+    const int4* rect;
+    const unsigned* count;
+    const int* plane;
+    const unsigned long long* pmask;
+    const double *positions, *rotations, *log_scales, *opacity_logits, *plane_logits;
+    CameraConsts cam;
+    double near_clip, dilation, alpha_floor, soft_tau, ste_tau;
+    holo_scene_grads g;
+};
+void bwd_seed(holo_ctx* ctx, const cx<float>* rep, const float* gi, cx<float>* gv, size_t n);
+void bwd_prep(holo_ctx* ctx, size_t N, const double* amplitudes, const double* phases, const GRec* rec,
+              BwdRec* out);
+void raster_backward_entries(holo_ctx* ctx, const RasterBwdArgs& a, int tile);
+void gauss_backward(holo_ctx* ctx, const GaussBwdArgs& a);
 // (zc, gidx) order for buckets of 2..kWarpSortCap entries, written back to egidx
 void sort_small_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsigned capacity,
                         const unsigned long long* ekey, int* egidx);
