@@ -53,11 +53,17 @@ __global__ void k_bwd_prep(const double* __restrict__ amplitudes, const double* 
     out[i] = r;
 }
 
-// warp sum of v over all lanes (every lane gets the total)
-__device__ __forceinline__ float warp_sum(float v) {
+// One step of a warp reduce-scatter over 2H values: lanes with bit D set keep
+// (and receive the partner's copy of) the upper half, the others the lower half.
+template <int D, int H>
+__device__ __forceinline__ void reduce_scatter_step(float (&w)[16], int lane) {
+    const bool up = (lane & D) != 0;
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-    return v;
+    for (int i = 0; i < H; ++i) {
+        const float send = up ? w[i] : w[i + H];
+        const float keep = up ? w[i + H] : w[i];
+        w[i] = keep + __shfl_xor_sync(0xffffffffu, send, D);
+    }
 }
 
 template <int TILE, int C>
@@ -213,17 +219,34 @@ __global__ void __launch_bounds__(TILE * TILE) k_raster_bwd(RasterBwdArgs a) {
                         v[kGI11] = gg * (-0.5f * dy * dy);
                     }
                 }
+                // reduce-scatter over the warp: afterwards lanes 2q, 2q+1 hold the
+                // warp's sum of value q (16 shuffles instead of 13 x 5)
+                float w[16];
 #pragma unroll
-                for (int q = 0; q < kGradVals; ++q) v[q] = warp_sum(v[q]);
-                if (lane == 0)
-#pragma unroll
-                    for (int q = 0; q < kGradVals; ++q)
-                        if (v[q] != 0.0f) atomicAdd(&s_acc[(c0 + j) * kGradVals + q], v[q]);
+                for (int q = 0; q < 16; ++q) w[q] = q < kGradVals ? v[q] : 0.0f;
+                reduce_scatter_step<16, 8>(w, lane);
+                reduce_scatter_step<8, 4>(w, lane);
+                reduce_scatter_step<4, 2>(w, lane);
+                reduce_scatter_step<2, 1>(w, lane);
+                w[0] += __shfl_xor_sync(0xffffffffu, w[0], 1);
+                const int q = (lane >> 1) & 15;
+                if ((lane & 1) == 0 && q < kGradVals && w[0] != 0.0f) atomicAdd(&s_acc[(c0 + j) * kGradVals + q], w[0]);
             }
         }
         __syncthreads();
-        float* dst = a.egrad + static_cast<size_t>(e0 + base) * kGradVals;
-        for (int t = tid; t < cnt * kGradVals; t += NT) dst[t] = s_acc[t];
+        // egrad is ordered per Gaussian: its k-th entry (bucket order: plane, then
+        // tile row, then tile column) at goff[g] + k, so the merge reads it in the
+        // reference's order without searching the buckets
+        for (int t = tid; t < cnt; t += NT) {
+            const int gi = s_g[t];
+            const int4 r = a.rect[gi];
+            const int area = (r.y - r.x) * (r.w - r.z);
+            int k = (ty - r.z) * (r.y - r.x) + (tx - r.x);
+            if (a.soft) k += __popcll(a.pmask[gi] & ((1ull << plane) - 1ull)) * area;
+            float* dst = a.egrad + (static_cast<size_t>(a.goff[gi]) + k) * kGradVals;
+#pragma unroll
+            for (int q = 0; q < kGradVals; ++q) dst[q] = s_acc[t * kGradVals + q];
+        }
         __syncthreads();
     }
 }
@@ -246,23 +269,20 @@ __global__ void __launch_bounds__(256) k_bwd_gauss(GaussBwdArgs a) {
     double rho_grad[64];
     const int Lg = L < 64 ? L : 64;
     for (int l = 0; l < Lg; ++l) rho_grad[l] = 0.0;
-    if (a.count[i] > 0) {
+    const unsigned cnt = a.count[i];
+    if (cnt > 0) {
         const int4 r = a.rect[i];
-        for (int l = a.pb; l < a.pe && l < 64; ++l) {
-            const bool in_plane = a.soft ? ((a.pmask[i] >> l) & 1ull) != 0 : a.plane[i] == l;
-            if (!in_plane) continue;
-            for (int ty = r.z; ty < r.w; ++ty)
-                for (int tx = r.x; tx < r.y; ++tx) {
-                    const int b = (l - a.pb) * a.num_tiles + ty * a.tiles_x + tx;
-                    const unsigned s0 = min(a.bstart[b], a.capacity), s1 = min(a.bstart[b + 1], a.capacity);
-                    for (unsigned e = s0; e < s1; ++e) {
-                        if (a.egidx[e] != static_cast<int>(i)) continue;
-                        const float* eg = a.egrad + static_cast<size_t>(e) * kGradVals;
-                        for (int q = 0; q < kGradVals; ++q) acc[q] += static_cast<double>(eg[q]);
-                        rho_grad[l] += static_cast<double>(eg[kGRho]);
-                        break;
-                    }
-                }
+        const unsigned area = static_cast<unsigned>((r.y - r.x) * (r.w - r.z));
+        unsigned long long planes = a.soft ? a.pmask[i] : 0ull;
+        int l = a.soft ? -1 : a.plane[i];
+        const float* eg = a.egrad + static_cast<size_t>(a.goff[i]) * kGradVals;
+        for (unsigned k = 0; k < cnt; ++k, eg += kGradVals) {
+            if (a.soft && k % area == 0) {  // next assigned plane
+                l = __ffsll(static_cast<long long>(planes)) - 1;
+                planes &= planes - 1;
+            }
+            for (int q = 0; q < kGradVals; ++q) acc[q] += static_cast<double>(eg[q]);
+            if (l >= 0 && l < 64) rho_grad[l] += static_cast<double>(eg[kGRho]);
         }
     }
 

@@ -977,6 +977,10 @@ void raster_backward(holo_ctx* ctx, const holo_wave& wave, const holo_raster_set
     const GRec* rec = static_cast<const GRec*>(ctx->buffer("rec", 1));
     BwdRec* brec = buf<BwdRec>(ctx, "bwd_rec", N);
     float* egrad = buf<float>(ctx, "bwd_egrad", E * 13);
+    // per-Gaussian offsets into the Gaussian-major entry gradients
+    const unsigned* count = static_cast<const unsigned*>(ctx->buffer("count", 1));
+    unsigned* goff = buf<unsigned>(ctx, "bwd_goff", N + 1);
+    if (N > 0) exclusive_scan_u32(ctx, count, goff, static_cast<long long>(N), nullptr);
     bwd_prep(ctx, N, set.a[3], set.a[5], rec, brec);  // amplitudes, phases of the rendered scene set
 
     RasterBwdArgs ra{};
@@ -1001,6 +1005,9 @@ void raster_backward(holo_ctx* ctx, const holo_wave& wave, const holo_raster_set
     ra.grad_layers = grad_layers;
     ra.t_final = static_cast<const float*>(ctx->buffer("t_final", 1));
     ra.n_contrib = static_cast<const int*>(ctx->buffer("n_contrib", 1));
+    ra.goff = goff;
+    ra.rect = static_cast<const int4*>(ctx->buffer("rect", 1));
+    ra.pmask = st.soft_assignment ? static_cast<const unsigned long long*>(ctx->buffer("pmask", 1)) : nullptr;
     ra.egrad = egrad;
     raster_backward_entries(ctx, ra, st.tile);
 
@@ -1022,6 +1029,7 @@ void raster_backward(holo_ctx* ctx, const holo_wave& wave, const holo_raster_set
     ga.bstart = ra.bstart;
     ga.egidx = ra.egidx;
     ga.egrad = egrad;
+    ga.goff = goff;
     ga.rect = static_cast<const int4*>(ctx->buffer("rect", 1));
     ga.count = static_cast<const unsigned*>(ctx->buffer("count", 1));
     ga.plane = static_cast<const int*>(ctx->buffer("plane", 1));

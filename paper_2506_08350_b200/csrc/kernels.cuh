@@ -186,7 +186,10 @@ struct RasterBwdArgs {
     const cx<float>* grad_layers;  // [planes][C][H][W]
     const float* t_final;          // the forward's aux outputs
     const int* n_contrib;
-    float* egrad;                  // [E][13]
+    const unsigned* goff;          // exclusive scan of the per-Gaussian entry counts
+    const int4* rect;
+    const unsigned long long* pmask;  // soft mode
+    float* egrad;                  // [E][13], Gaussian-major (goff[g] + k-th entry of g)
 };
 struct GaussBwdArgs {
     size_t n;
@@ -195,6 +198,7 @@ struct GaussBwdArgs {
     const unsigned* bstart;
     const int* egidx;
     const float* egrad;
+    const unsigned* goff;
     const int4* rect;
     const unsigned* count;
     const int* plane;
