@@ -25,7 +25,7 @@ namespace {
 // per-entry gradient slots (EntryGrad, rasterizer.cpp:321-328)
 enum { kGMuX = 0, kGMuY, kGI00, kGI01, kGI11, kGAlpha, kGRho, kGAmp, kGPh = kGAmp + 3, kGradVals = kGPh + 3 };
 
-constexpr float kLog2Scale = -0.72134752044448170368f;  // GRec conic scale: -log2(e) / 2
+constexpr float kInvScale = -1.38629436111989061883f;  // 1 / (GRec conic scale -log2(e) / 2) = -2 ln 2
 
 __global__ void k_bwd_seed(const cx<float>* __restrict__ rep, const float* __restrict__ gi, cx<float>* __restrict__ gv,
                            size_t n) {
@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(TILE * TILE) k_raster_bwd(RasterBwdArgs a) {
     __shared__ Staged s_rec[kStage];
     __shared__ float4 s_box[kStage];
     __shared__ int s_g[kStage];
+    __shared__ BwdRec s_brec[kStage];  // pad[0] carries rho
     __shared__ float s_acc[kStage * kGradVals];
 
     const int tx = blockIdx.x, ty = blockIdx.y, lplane = blockIdx.z;
@@ -118,9 +119,15 @@ __global__ void __launch_bounds__(TILE * TILE) k_raster_bwd(RasterBwdArgs a) {
         for (int t = tid; t < cnt; t += NT) {
             const int gi = a.egidx[e0 + base + t];
             const GRec r = a.rec[gi];
-            float alpha = r.alpha;
-            if (a.soft) alpha = static_cast<float>(static_cast<double>(r.alpha) * a.rho[static_cast<size_t>(gi) * a.L + plane]);
+            float alpha = r.alpha, rho = 1.0f;
+            if (a.soft) {
+                rho = static_cast<float>(a.rho[static_cast<size_t>(gi) * a.L + plane]);
+                alpha = static_cast<float>(static_cast<double>(r.alpha) * a.rho[static_cast<size_t>(gi) * a.L + plane]);
+            }
             stage_entry(r, px0, py0, alpha, s_rec[t], s_box[t]);
+            BwdRec br = a.brec[gi];
+            br.pad[0] = rho;
+            s_brec[t] = br;
             s_g[t] = gi;
         }
     };
@@ -160,7 +167,7 @@ __global__ void __launch_bounds__(TILE * TILE) k_raster_bwd(RasterBwdArgs a) {
     for (int bi = nb - 1; bi >= 0; --bi) {
         const int base = bi * kStage;
         const int cnt = min(n - base, kStage);
-        stage(base, cnt);
+        if (nb > 1) stage(base, cnt);  // one batch: still staged from pass 1
         for (int t = tid; t < cnt * kGradVals; t += NT) s_acc[t] = 0.0f;
         __syncthreads();
         for (int c0 = ((cnt - 1) / 32) * 32; c0 >= 0; c0 -= 32) {
@@ -181,8 +188,8 @@ __global__ void __launch_bounds__(TILE * TILE) k_raster_bwd(RasterBwdArgs a) {
 #pragma unroll
                 for (int q = 0; q < kGradVals; ++q) v[q] = 0.0f;
                 if (acc) {
-                    const BwdRec br = a.brec[s_g[c0 + j]];
-                    T = T / (1.0f - al);
+                    const BwdRec& br = s_brec[c0 + j];
+                    T = __fdividef(T, 1.0f - al);
                     const float aw = al * T;
                     float d_alpha = 0.0f;
                     const float4 Cc = e->c;
@@ -206,12 +213,11 @@ __global__ void __launch_bounds__(TILE * TILE) k_raster_bwd(RasterBwdArgs a) {
                         const float t = fmaf(A.w, dy, A.z * dx);
                         const float gauss = ex2_approx(fmaf(B.x * dy, dy, dx * t));
                         const float alpha_sig = br.alpha;
-                        const float rho =
-                            a.soft ? static_cast<float>(a.rho[static_cast<size_t>(s_g[c0 + j]) * a.L + plane]) : 1.0f;
+                        const float rho = br.pad[0];
                         v[kGAlpha] = d_alpha * gauss * rho;
                         v[kGRho] = d_alpha * alpha_sig * gauss;
                         const float gg = d_alpha * alpha_sig * rho * gauss;
-                        const float i00 = A.z / kLog2Scale, i01 = A.w / (2.0f * kLog2Scale), i11 = B.x / kLog2Scale;
+                        const float i00 = A.z * kInvScale, i01 = A.w * (0.5f * kInvScale), i11 = B.x * kInvScale;
                         v[kGMuX] = gg * (i00 * dx + i01 * dy);
                         v[kGMuY] = gg * (i01 * dx + i11 * dy);
                         v[kGI00] = gg * (-0.5f * dx * dx);
