@@ -29,6 +29,14 @@ struct GaussianScene {
     void renormalize();
 };
 
+// d(loss)/d(scene parameters), scene.hpp:40-46 of the reference
+struct SceneGradients {
+    std::vector<double> positions, rotations, log_scales, amplitudes, opacity_logits, phases, plane_logits;
+    std::vector<double> mu_screen;  // N * 2, screen-space mean gradient (pixels)
+    void resize_like(const GaussianScene& s);
+    void clear();
+};
+
 // Sigma = R diag(e^s)^2 R^T for the normalised quaternion
 Mat3 covariance_3d(const double* quat, const double* log_scales);
 

@@ -576,6 +576,70 @@ RasterForward raster_forward(const GaussianScene& scene, const CameraView& cam, 
     return collect_raster(scene, cfg, GaussianScene::kChannels, info);
 }
 
+void SceneGradients::resize_like(const GaussianScene& s) {
+    const size_t n = s.size();
+    positions.assign(3 * n, 0.0);
+    rotations.assign(4 * n, 0.0);
+    log_scales.assign(3 * n, 0.0);
+    amplitudes.assign(3 * n, 0.0);
+    opacity_logits.assign(n, 0.0);
+    phases.assign(3 * n, 0.0);
+    plane_logits.assign(n * static_cast<size_t>(s.num_planes), 0.0);
+    mu_screen.assign(2 * n, 0.0);
+}
+
+void SceneGradients::clear() {
+    for (auto* v : {&positions, &rotations, &log_scales, &amplitudes, &opacity_logits, &phases, &plane_logits,
+                    &mu_screen})
+        std::fill(v->begin(), v->end(), 0.0);
+}
+
+// rasterizer.cpp:332-528 on the device
+SceneGradients raster_backward(const GaussianScene& scene, const CameraView& cam, const WaveConfig& cfg,
+                               const RenderSettings& settings, const RasterForward& fwd,
+                               const std::vector<ComplexField>& grad_layers) {
+    const int L = cfg.num_planes;
+    if (grad_layers.size() != static_cast<size_t>(L))
+        throw HoloError("config", "raster_backward: upstream gradient count mismatch");  // rasterizer.cpp:342-343
+    check_raster_inputs(scene, cam, cfg);
+    if (fwd.projected.size() != scene.size()) throw HoloError("usage", "raster_backward: forward is for another scene");
+    // the device keeps its own forward state: render the same frame there
+    const holo_scene_arrays sa = scene_arrays(scene);
+    check(holo_scene_upload(ctx(), &sa));
+    holo_wave w = to_c(cfg);
+    w.channels = GaussianScene::kChannels;
+    for (int c = cfg.channels(); c < w.channels; ++c) w.wavelengths[c] = cfg.wavelengths.back();
+    const holo_camera c = to_c(cam);
+    const holo_raster_settings st = to_c(settings);
+    const holo_prop_options po{0, 0};
+    holo_frame_info info{};
+    check(holo_render(ctx(), &c, &w, &st, &po, HOLO_OUT_LAYERS | HOLO_OUT_AUX, &info));
+    const size_t P = static_cast<size_t>(cfg.nx) * cfg.ny, per = 3 * P;
+    std::vector<std::complex<float>> g(static_cast<size_t>(L) * per);
+    for (int l = 0; l < L; ++l) {
+        if (grad_layers[l].c != 3 || grad_layers[l].w != cfg.nx || grad_layers[l].h != cfg.ny)
+            throw HoloError("config", "raster_backward: upstream gradient shape mismatch");
+        for (size_t i = 0; i < per; ++i)
+            g[l * per + i] = std::complex<float>(static_cast<float>(grad_layers[l].data[i].real()),
+                                                 static_cast<float>(grad_layers[l].data[i].imag()));
+    }
+    DevMem dg(sizeof(std::complex<float>) * g.size());
+    h2d(dg.p, g.data(), sizeof(std::complex<float>) * g.size());
+    SceneGradients out;
+    out.resize_like(scene);
+    std::vector<std::vector<double>*> vs = {&out.positions, &out.rotations, &out.log_scales, &out.amplitudes,
+                                            &out.opacity_logits, &out.phases, &out.plane_logits, &out.mu_screen};
+    std::vector<std::unique_ptr<DevMem>> dm;
+    for (auto* v : vs) dm.push_back(std::make_unique<DevMem>(sizeof(double) * v->size()));
+    holo_scene_grads hg{};
+    double** slots[8] = {&hg.positions, &hg.rotations, &hg.log_scales, &hg.amplitudes,
+                         &hg.opacity_logits, &hg.phases, &hg.plane_logits, &hg.mu_screen};
+    for (int k = 0; k < 8; ++k) *slots[k] = static_cast<double*>(dm[k]->p);
+    check(holo_raster_backward(ctx(), &c, &w, &st, dg.p, &hg));
+    for (int k = 0; k < 8; ++k) d2h(vs[k]->data(), dm[k]->p, sizeof(double) * vs[k]->size());
+    return out;
+}
+
 // pipeline.cpp:20-29
 PipelineForward pipeline_forward(const GaussianScene& scene, const CameraView& cam, const WaveConfig& cfg,
                                  const PipelineOptions& opt) {

@@ -69,6 +69,33 @@ TEST_CASE("blending recurrence matches the hand-computed cases") {
     CHECK(r.entries[0].gidx == 0);  // equal depth: index order
 }
 
+TEST_CASE("raster_backward: amplitude and phase gradients of a linear loss") {
+    // L = Re sum_p <g, layer_p>: with g = 1 on channel 0, dL/d amp_0 = sum_p Re layer_p
+    // (amp = 1, phase 0); with g = i, dL/d phase_0 is the same sum
+    const WaveConfig cfg = desk(32, 1);
+    const CameraView cam = front(cfg);
+    GaussianScene s = centred(1, cam);
+    s.opacity_logits = {logit(0.8)};
+    const RasterForward r = raster_forward(s, cam, cfg, RenderSettings{});
+    double sum_re = 0.0;
+    for (int y = 0; y < 32; ++y)
+        for (int x = 0; x < 32; ++x) sum_re += r.layers[0].at(0, y, x).real();
+    std::vector<ComplexField> g(1, ComplexField(32, 32, 3, cfg.pitch));
+    for (int y = 0; y < 32; ++y)
+        for (int x = 0; x < 32; ++x) g[0].at(0, y, x) = c64(1.0, 0.0);
+    SceneGradients gr = raster_backward(s, cam, cfg, RenderSettings{}, r, g);
+    CHECK(gr.positions.size() == 3);
+    CHECK(gr.plane_logits.size() == 1);
+    CHECK(gr.amplitudes[0] == doctest::Approx(sum_re).epsilon(1e-5));
+    CHECK(gr.amplitudes[1] == 0.0);
+    for (int y = 0; y < 32; ++y)
+        for (int x = 0; x < 32; ++x) g[0].at(0, y, x) = c64(0.0, 1.0);
+    gr = raster_backward(s, cam, cfg, RenderSettings{}, r, g);
+    CHECK(gr.phases[0] == doctest::Approx(sum_re).epsilon(1e-5));
+    std::vector<ComplexField> wrong;
+    CHECK_THROWS_AS(raster_backward(s, cam, cfg, RenderSettings{}, r, wrong), HoloError);
+}
+
 TEST_CASE("projection lands where the pinhole model says, f64 exact") {
     const WaveConfig cfg = desk(32, 1);
     const CameraView cam = front(cfg);
