@@ -62,6 +62,12 @@ def main():
             entry_bucket=r.raster.entry_bucket, bucket_start=r.raster.bucket_start,
             mu_x=r.raster.projected["mu_x"], mu_y=r.raster.projected["mu_y"], zc=r.raster.projected["zc"],
         )
+        if cfg.channels() == 3:
+            # the gradient branch of total_loss (pipeline.cpp:63-80) for a seeded dL/dI
+            gi = np.random.default_rng(100 + len(name)).standard_normal(r.intensities.shape)
+            grads, gh, gl = ref.pipeline_backward(scene, cam, cfg, st, prop, gi)
+            out.update(bwd_gi=gi, bwd_gholo=gh, bwd_glayers=gl, **{f"bwd_{k}": v for k, v in grads.items()})
+        # (deterministic: re-running reproduces the committed files bit for bit)
         path = os.path.join(HERE, f"{name}.npz")
         np.savez_compressed(path, **out)
         print(name, os.path.getsize(path), "bytes, E =", len(r.raster.entry_gidx))

@@ -71,3 +71,30 @@ def test_gpu_matches_golden(gpu_ctx, name):
     assert np.array_equal(out.raster.bucket_start, g["bucket_start"])
     assert np.array_equal(out.raster.projected["mu_x"], g["mu_x"])
     assert np.array_equal(out.raster.projected["zc"], g["zc"])
+
+
+BWD_CASES = [n for n in CASES if "bwd_gi" in np.load(os.path.join(HERE, "golden", n + ".npz")).files]
+
+
+def test_backward_golden_cases_present():
+    assert len(BWD_CASES) >= 4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", BWD_CASES)
+def test_gpu_backward_matches_golden(gpu_ctx, name):
+    # the reference's gradient branch of total_loss (pipeline.cpp:63-80) stored by
+    # make_golden.py: gradients within rel-L2 1e-3, adjoint fields within 1e-4
+    from paper_2506_08350_b200 import api
+
+    g, scene, cam, cfg, st, prop = load(name)
+    grads, gl, gh = api.pipeline_backward(scene, cam, cfg, PipelineOptions(raster=st, prop=prop), g["bwd_gi"],
+                                          ctx=gpu_ctx)
+    assert rel_l2(gh, g["bwd_gholo"]) <= 1e-4
+    assert rel_l2(gl, g["bwd_glayers"]) <= 1e-4
+    for k, v in grads.items():
+        ref = g[f"bwd_{k}"]
+        if np.abs(ref).max() == 0.0:
+            assert np.abs(v).max() <= 1e-12, k
+        else:
+            assert rel_l2(v, ref) <= 1e-3, (k, rel_l2(v, ref))
