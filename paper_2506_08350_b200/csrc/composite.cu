@@ -139,7 +139,8 @@ __device__ __forceinline__ void blend(const Staged* e, const float4& B, float w,
 #define HOLO_COMP_MINB 6
 #endif
 
-template <int TILE, int C>
+// AUX: count contributions for n_contrib (HOLO_OUT_AUX); compiled out otherwise
+template <int TILE, int C, bool AUX>
 __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) k_composite(CompositeArgs a) {
     using G = TileGeom<TILE>;
     constexpr int kStage = 256;  // records staged per batch
@@ -285,12 +286,12 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
                         const float w0 = acc0 ? al0 * T : 0.0f;
                         blend<C>(e0p, B0, w0, acc);
                         T -= w0;  // T (1 - a)
-                        contrib += acc0 ? 1 : 0;
+                        if constexpr (AUX) contrib += acc0 ? 1 : 0;
                         const bool acc1 = two && (al1 > thr) && (T >= eps);
                         const float w1 = acc1 ? al1 * T : 0.0f;
                         blend<C>(e1p, B1, w1, acc);
                         T -= w1;
-                        contrib += acc1 ? 1 : 0;
+                        if constexpr (AUX) contrib += acc1 ? 1 : 0;
 #ifdef HOLO_COUNT
                         n_eval += two ? 2 : 1;
                         n_any += (__ballot_sync(0xffffffffu, acc0) ? 1 : 0) + (__ballot_sync(0xffffffffu, acc1) ? 1 : 0);
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
         for (int c = 0; c < C; ++c)
             a.layers[(static_cast<size_t>(lplane) * C + c) * P + pix] = acc[c];
         if (a.t_final) a.t_final[static_cast<size_t>(lplane) * P + pix] = T;
-        if (a.n_contrib) a.n_contrib[static_cast<size_t>(lplane) * P + pix] = contrib;
+        if constexpr (AUX) a.n_contrib[static_cast<size_t>(lplane) * P + pix] = contrib;
     }
 }
 
@@ -339,9 +340,13 @@ void launch_tile(holo_ctx* ctx, const CompositeArgs& a) {
     const int tiles_y = a.num_tiles / a.tiles_x;
     const dim3 grid(a.tiles_x, tiles_y, a.num_buckets / a.num_tiles);
     switch (a.C) {
-        case 1: k_composite<TILE, 1><<<grid, TILE * TILE, 0, ctx->stream>>>(a); break;
-        case 2: k_composite<TILE, 2><<<grid, TILE * TILE, 0, ctx->stream>>>(a); break;
-        case 3: k_composite<TILE, 3><<<grid, TILE * TILE, 0, ctx->stream>>>(a); break;
+#define HC_COMP(CC)                                                                   \
+    (a.n_contrib ? k_composite<TILE, CC, true><<<grid, TILE * TILE, 0, ctx->stream>>>(a) \
+                 : k_composite<TILE, CC, false><<<grid, TILE * TILE, 0, ctx->stream>>>(a))
+        case 1: HC_COMP(1); break;
+        case 2: HC_COMP(2); break;
+        case 3: HC_COMP(3); break;
+#undef HC_COMP
         default: throw Error(HOLO_ERR_CONFIG, "render supports 1 to 3 wavelength channels");
     }
     HC_LAUNCHED(ctx);
