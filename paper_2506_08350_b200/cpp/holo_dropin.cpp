@@ -24,6 +24,7 @@
 #include "holo/propagation.hpp"
 #include "holo/rasterizer.hpp"
 #include "holo/scene.hpp"
+#include "holo/scene_io.hpp"
 #include "holo/wave_config.hpp"
 #include "holo_cuda.h"
 
@@ -718,6 +719,74 @@ ComplexField read_field(const std::string& path, double pitch) {
     ComplexField f(static_cast<int>(dims[0]), static_cast<int>(dims[1]), static_cast<int>(dims[2]), pitch);
     if (std::fread(f.data.data(), sizeof(c64), n, fp.get()) != n) throw HoloError("io", "truncated payload: " + path);
     return f;
+}
+
+// ------------------------------------------------------------------ HOLOSCENE1 I/O (scene_io.cpp:29-95)
+
+namespace {
+constexpr char kSceneMagic[10] = {'H', 'O', 'L', 'O', 'S', 'C', 'E', 'N', 'E', '1'};
+
+// the integer value of "key" in a flat JSON object (the header's N and L)
+bool json_uint(const std::string& js, const char* key, unsigned long long* out) {
+    const std::string k = std::string("\"") + key + "\"";
+    size_t p = js.find(k);
+    if (p == std::string::npos) return false;
+    p = js.find(':', p + k.size());
+    if (p == std::string::npos) return false;
+    ++p;
+    while (p < js.size() && (js[p] == ' ' || js[p] == '\t' || js[p] == '\n' || js[p] == '\r')) ++p;
+    if (p >= js.size() || js[p] < '0' || js[p] > '9') return false;
+    unsigned long long v = 0;
+    while (p < js.size() && js[p] >= '0' && js[p] <= '9') v = v * 10 + static_cast<unsigned>(js[p++] - '0');
+    *out = v;
+    return true;
+}
+}  // namespace
+
+void write_scene(const std::string& path, const GaussianScene& s) {
+    s.validate();
+    // the header as nlohmann::json::dump() writes it (keys sorted)
+    const std::string hs =
+        "{\"L\":" + std::to_string(s.num_planes) + ",\"N\":" + std::to_string(s.size()) +
+        ",\"units\":{\"amplitudes\":\"linear\",\"opacities\":\"logit\",\"phases\":\"rad\",\"plane_logits\":\"logit\","
+        "\"positions\":\"m\",\"rotations\":\"unit_quaternion_wxyz\",\"scales\":\"log_m\"}}";
+    File fp(std::fopen(path.c_str(), "wb"));
+    if (!fp) throw HoloError("io", "cannot open for writing: " + path);
+    const std::uint32_t hlen = static_cast<std::uint32_t>(hs.size());
+    bool ok = std::fwrite(kSceneMagic, 1, 10, fp.get()) == 10 && std::fwrite(&hlen, 4, 1, fp.get()) == 1 &&
+              std::fwrite(hs.data(), 1, hs.size(), fp.get()) == hs.size();
+    for (const auto* v : {&s.positions, &s.rotations, &s.log_scales, &s.amplitudes, &s.opacity_logits, &s.phases,
+                          &s.plane_logits})
+        ok = ok && std::fwrite(v->data(), sizeof(double), v->size(), fp.get()) == v->size();
+    if (!ok || std::fflush(fp.get()) != 0) throw HoloError("io", "short write: " + path);
+}
+
+GaussianScene read_scene(const std::string& path) {
+    File fp(std::fopen(path.c_str(), "rb"));
+    if (!fp) throw HoloError("io", "cannot open: " + path);
+    char magic[10];
+    if (std::fread(magic, 1, 10, fp.get()) != 10) throw HoloError("io", "truncated header: " + path);
+    if (std::memcmp(magic, kSceneMagic, 10) != 0) throw HoloError("io", "bad magic, not a HOLOSCENE1 file: " + path);
+    std::uint32_t hlen = 0;
+    if (std::fread(&hlen, 4, 1, fp.get()) != 1) throw HoloError("io", "truncated header: " + path);
+    if (hlen == 0 || hlen > (1u << 20)) throw HoloError("io", "implausible header length in " + path);
+    std::string hs(hlen, '\0');
+    if (std::fread(hs.data(), 1, hlen, fp.get()) != hlen) throw HoloError("io", "truncated header: " + path);
+    unsigned long long n = 0, L = 0;
+    if (!json_uint(hs, "N", &n) || !json_uint(hs, "L", &L)) throw HoloError("io", "scene header missing N or L: " + path);
+    if (L < 1 || n > (1ull << 26)) throw HoloError("io", "implausible scene dimensions in " + path);
+    GaussianScene s;
+    s.num_planes = static_cast<int>(L);
+    const size_t counts[7] = {n * 3, n * 4, n * 3, n * 3, n, n * 3, n * L};
+    std::vector<double>* arrays[7] = {&s.positions, &s.rotations, &s.log_scales, &s.amplitudes,
+                                      &s.opacity_logits, &s.phases, &s.plane_logits};
+    for (int k = 0; k < 7; ++k) {
+        arrays[k]->resize(counts[k]);
+        if (std::fread(arrays[k]->data(), sizeof(double), counts[k], fp.get()) != counts[k])
+            throw HoloError("io", "truncated payload: " + path);
+    }
+    s.validate();
+    return s;
 }
 
 }  // namespace holo
