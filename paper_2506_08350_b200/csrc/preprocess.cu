@@ -111,6 +111,16 @@ __global__ void __launch_bounds__(256, PROJ ? 1 : HOLO_PRE_MINB) k_preprocess(Pr
         mask = (best < 64) ? (1ull << best) : 0ull;
     }
     if (o.pmask) o.pmask[i] = mask;
+    if constexpr (!PROJ) {
+        // plane-sharded frame (hard assignment): a Gaussian of another rank's
+        // planes emits no entry here, so its projection is skipped
+        if (o.slots && (best < o.pb || best >= o.pe)) {
+            o.count[i] = 0;
+            o.rect[i] = make_int4(0, 0, 0, 0);
+            if (o.touched) o.touched[i] = 0;
+            return;
+        }
+    }
 
     // ---- projection (rasterizer.cpp:10-70)
     holo_projected p;
