@@ -249,6 +249,62 @@ int holo_pipeline_backward(holo_ctx* ctx, const holo_camera* cam, const holo_wav
                            const void* grad_intensities, holo_scene_grads* grads, void* grad_layers_out,
                            void* grad_hologram_out);
 
+/* ---- training step: losses (losses.hpp, ssim.hpp), total_loss (pipeline.cpp:30-95),
+ * optimizer_step (optimizer.hpp) ---- */
+/* PipelineOptions' loss weights (pipeline.hpp:26-28): defaults 0.005, 1e-4, 0. */
+typedef struct {
+    double lambda_ssim;
+    double lambda_opacity;
+    int use_plain_mse;
+} holo_loss_options;
+
+/* LossBreakdown (pipeline.hpp:44-48); the per-plane PSNR goes to a separate array. */
+typedef struct {
+    double total, recon, ssim, opacity, psnr_mean;
+} holo_loss_breakdown;
+
+/* loss_recon (or loss_mse) + loss_ssim + psnr (losses.cpp) over device f64 focal
+ * stacks: intensities / targets [L][C][H][W], masks [L][H][W] (unused by plain MSE).
+ * out->opacity = 0; psnr (host, [L]) optional; grad (device f64 [L][C][H][W],
+ * optional) receives dL/dI.  f64 throughout; the row sums are folded in the
+ * reference's order.  Needs H, W >= 11 (ssim.cpp:71-72) unless lambda_ssim = 0, which
+ * leaves the SSIM term out (the loss_mse / loss_recon / psnr of losses.hpp alone). */
+int holo_losses(holo_ctx* ctx, const double* intensities, const double* targets, const double* masks, int L, int C,
+                int H, int W, const holo_loss_options* opt, holo_loss_breakdown* out, double* psnr, double* grad);
+
+/* total_loss (pipeline.cpp:30-95) on the context's resident scene: render
+ * (pipeline_forward), losses against targets / masks (device f64 as above), and
+ * with grads != NULL the full gradient (holo_pipeline_backward + the opacity decay
+ * term, pipeline.cpp:82-88).  The frame's outputs stay readable as after holo_render
+ * with HOLO_OUT_INTENSITY | HOLO_OUT_REPLAYED | HOLO_OUT_AUX. */
+int holo_total_loss(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave, const holo_raster_settings* settings,
+                    const holo_prop_options* prop, const holo_loss_options* opt, const double* targets,
+                    const double* masks, holo_loss_breakdown* out, double* psnr, holo_scene_grads* grads);
+
+/* OptimizerConfig (optimizer.hpp:17-31). */
+typedef struct {
+    double lr_positions, lr_rotations, lr_log_scales, lr_amplitudes, lr_phases, lr_opacities, lr_plane_logits;
+    double beta1, beta2, beta3, eps;
+    int use_adam;
+    long long schedule_total;
+    double lr_floor;
+} holo_optimizer_config;
+
+/* OptimState (optimizer.hpp:37-52): device moments, sized at the first step. */
+typedef struct holo_optim holo_optim;
+int holo_optim_create(holo_ctx* ctx, holo_optim** out);
+int holo_optim_destroy(holo_optim* st);
+/* optimizer_step (optimizer.cpp:102-133) on the context's resident scene, in place
+ * (the arrays the next render reads): *applied = 0 and the skip counted when any
+ * gradient entry is non-finite.  grads as from holo_total_loss (all seven groups). */
+int holo_optim_step(holo_ctx* ctx, holo_optim* st, const holo_scene_grads* grads, const holo_optimizer_config* cfg,
+                    int* applied);
+int holo_optim_counts(const holo_optim* st, long long* step, long long* skipped);
+
+/* Copies the resident scene to host arrays (the members are written despite the
+ * const qualifiers of holo_scene_arrays; n and num_planes must match). */
+int holo_scene_download(holo_ctx* ctx, const holo_scene_arrays* host);
+
 /* Device pointer and size of one output buffer of the last render. */
 int holo_frame_buffer(holo_ctx* ctx, int buffer, void** dev_ptr, size_t* bytes);
 /* Synchronous device-to-host copy of one output buffer (bytes must match). */

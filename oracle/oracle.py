@@ -156,13 +156,15 @@ def _f64(a, n=None):
 class _SceneArgs:
     """Keeps the contiguous f64 arrays alive for the duration of a call."""
 
-    def __init__(self, sc):
+    def __init__(self, sc, copy=False):
         n = len(np.asarray(_get(sc, "opacity_logits")).ravel())
         L = int(_get(sc, "num_planes"))
         self.arrays = [_f64(_get(sc, "positions"), 3 * n), _f64(_get(sc, "rotations"), 4 * n),
                        _f64(_get(sc, "log_scales"), 3 * n), _f64(_get(sc, "amplitudes"), 3 * n),
                        _f64(_get(sc, "opacity_logits"), n), _f64(_get(sc, "phases"), 3 * n),
                        _f64(_get(sc, "plane_logits"), n * L)]
+        if copy:  # callee writes the arrays: never alias the caller's scene
+            self.arrays = [a.copy() for a in self.arrays]
         self.s = _Scene()
         self.s.n, self.s.num_planes = n, L
         for name, arr in zip(["positions", "rotations", "log_scales", "amplitudes", "opacity_logits", "phases",
@@ -369,6 +371,52 @@ class Oracle:
         self._check(self.lib.ref_raster_backward(C.byref(sa.s), C.byref(_camera(cam)), C.byref(_wave(wave)),
                                                  C.byref(_settings(settings)), _ptr(gl), C.byref(g)))
         return arrays
+
+    def losses(self, I, I_gt, masks, lambda_ssim=0.005, plain=False):
+        """The loss terms of total_loss (losses.cpp) on given stacks [L,C,H,W]:
+        returns (recon, ssim, psnr [L], dL/dI [L,C,H,W])."""
+        a = np.ascontiguousarray(I, dtype=np.float64)
+        b = np.ascontiguousarray(I_gt, dtype=np.float64)
+        L, Cn, H, W = a.shape
+        m = np.ascontiguousarray(masks if masks is not None else np.zeros((L, H, W)), dtype=np.float64)
+        out = np.zeros(2)
+        ps = np.zeros(L)
+        g = np.zeros_like(a)
+        self._check(self.lib.ref_losses(_ptr(a), _ptr(b), _ptr(m), L, Cn, H, W, C.c_double(lambda_ssim), int(plain),
+                                        _ptr(out), _ptr(ps), _ptr(g)))
+        return out[0], out[1], ps, g
+
+    def total_loss(self, scene, cam, wave, settings, prop, targets, masks, lambda_ssim=0.005, lambda_opacity=1e-4,
+                   plain=False, grads=True):
+        """holo::total_loss (pipeline.cpp:30-95): returns (breakdown dict, psnr [L], scene gradients or None)."""
+        sa = _SceneArgs(scene)
+        wv = _wave(wave)
+        t = np.ascontiguousarray(targets, dtype=np.float64)
+        m = np.ascontiguousarray(masks, dtype=np.float64)
+        bd = np.zeros(5)
+        ps = np.zeros(wv.num_planes)
+        g, arrays = self._grads(sa.s.n, wv.num_planes)
+        self._check(self.lib.ref_total_loss(C.byref(sa.s), C.byref(_camera(cam)), C.byref(wv),
+                                            C.byref(_settings(settings)), C.byref(_prop(prop)),
+                                            C.c_double(lambda_ssim), C.c_double(lambda_opacity), int(plain), _ptr(t),
+                                            _ptr(m), _ptr(bd), _ptr(ps), C.byref(g) if grads else None))
+        keys = ("recon", "ssim", "opacity", "total", "psnr_mean")
+        return dict(zip(keys, bd.tolist())), ps, (arrays if grads else None)
+
+    def optimizer_run(self, scene, grads_list, cfg, use_adam=False, schedule_total=20000):
+        """holo::optimizer_step (optimizer.cpp:102-133) for each gradient dict of
+        grads_list from fresh moments; returns (updated scene arrays, applied flags).
+        cfg: [lr_pos, lr_rot, lr_logs, lr_amp, lr_phase, lr_opac, lr_plane, b1, b2, b3, eps, lr_floor]."""
+        sa = _SceneArgs(scene, copy=True)
+        order = ("positions", "rotations", "log_scales", "amplitudes", "opacity_logits", "phases", "plane_logits")
+        packed = np.concatenate([np.concatenate([np.ravel(g[k]) for k in order]) for g in grads_list])
+        applied = np.zeros(len(grads_list), dtype=np.int32)
+        cv = np.ascontiguousarray(cfg, dtype=np.float64)
+        self._check(self.lib.ref_optimizer_run(C.byref(sa.s), _ptr(packed), len(grads_list), _ptr(cv), int(use_adam),
+                                               C.c_longlong(schedule_total),
+                                               applied.ctypes.data_as(C.POINTER(C.c_int32))))
+        names = order
+        return {k: a.copy() for k, a in zip(names, sa.arrays)}, applied
 
     def pipeline_backward(self, scene, cam, wave, settings, prop, grad_intensities):
         """The gradient branch of holo::total_loss (pipeline.cpp:63-80) for

@@ -15,6 +15,8 @@
 #include "holo/pipeline.hpp"
 #include "holo/propagation.hpp"
 #include "holo/rasterizer.hpp"
+#include "holo/losses.hpp"
+#include "holo/optimizer.hpp"
 
 namespace {
 
@@ -362,6 +364,117 @@ int ref_pipeline_backward(const ho_scene* s, const ho_camera* cam, const ho_wave
         for (size_t l = 0; l < gl.size(); ++l)
             if (grad_layers) std::memcpy(grad_layers + 2 * P * l, gl[l].data.data(), sizeof(double) * 2 * P);
         copy_grads(holo::raster_backward(scene, to_camera(cam), wc, po.raster, f.raster, gl), out);
+    });
+}
+
+// The loss terms of total_loss (pipeline.cpp:43-45, losses.cpp) on given focal
+// stacks I, I_gt ([L][C][H][W] f64) and masks ([L][H][W] f64, ignored when plain):
+// out = {recon, ssim}; psnr [L]; grad [L][C][H][W] (dL/dI, written).
+int ref_losses(const double* I, const double* I_gt, const double* masks, int L, int C, int H, int W,
+               double lambda_ssim, int plain, double* out, double* psnr_out, double* grad) {
+    return guarded([&] {
+        const size_t n = static_cast<size_t>(C) * H * W, P = static_cast<size_t>(H) * W;
+        std::vector<holo::IntensityImage> a, b, m, g;
+        for (int l = 0; l < L; ++l) {
+            a.emplace_back(W, H, C);
+            b.emplace_back(W, H, C);
+            m.emplace_back(W, H, 1);
+            g.emplace_back(W, H, C);
+            std::memcpy(a.back().data.data(), I + l * n, sizeof(double) * n);
+            std::memcpy(b.back().data.data(), I_gt + l * n, sizeof(double) * n);
+            if (masks) std::memcpy(m.back().data.data(), masks + l * P, sizeof(double) * P);
+        }
+        out[0] = plain ? holo::loss_mse(a, b, &g) : holo::loss_recon(a, b, m, &g);
+        out[1] = holo::loss_ssim(a, b, lambda_ssim, &g);
+        for (int l = 0; l < L; ++l) {
+            if (psnr_out) psnr_out[l] = holo::psnr(a[l], b[l]);
+            if (grad) std::memcpy(grad + l * n, g[l].data.data(), sizeof(double) * n);
+        }
+    });
+}
+
+// holo::total_loss (pipeline.cpp:30-95) with grads: breakdown = {recon, ssim,
+// opacity, total, psnr_mean}; psnr [L]; targets [L][C][H][W], masks [L][H][W].
+int ref_total_loss(const ho_scene* s, const ho_camera* cam, const ho_wave* cfg, const ho_settings* st,
+                   const ho_prop* opt, double lambda_ssim, double lambda_opacity, int plain, const double* targets,
+                   const double* masks, double* breakdown, double* psnr_out, ref_grads* grads) {
+    return guarded([&] {
+        const holo::GaussianScene scene = to_scene(s);
+        const holo::WaveConfig wc = to_wave(cfg);
+        holo::PipelineOptions po;
+        po.raster = to_settings(st);
+        po.prop = to_prop(opt);
+        po.lambda_ssim = lambda_ssim;
+        po.lambda_opacity = lambda_opacity;
+        po.use_plain_mse = plain != 0;
+        holo::FocalStackTarget t;
+        t.camera = to_camera(cam);
+        const size_t n = static_cast<size_t>(wc.nx) * wc.ny * wc.channels(), P = static_cast<size_t>(wc.nx) * wc.ny;
+        for (int l = 0; l < wc.num_planes; ++l) {
+            t.images.emplace_back(wc.nx, wc.ny, wc.channels());
+            t.masks.emplace_back(wc.nx, wc.ny, 1);
+            std::memcpy(t.images.back().data.data(), targets + l * n, sizeof(double) * n);
+            std::memcpy(t.masks.back().data.data(), masks + l * P, sizeof(double) * P);
+        }
+        holo::SceneGradients g;
+        const holo::LossBreakdown lb = holo::total_loss(scene, t.camera, wc, t, po, grads ? &g : nullptr);
+        breakdown[0] = lb.recon;
+        breakdown[1] = lb.ssim;
+        breakdown[2] = lb.opacity;
+        breakdown[3] = lb.total;
+        breakdown[4] = lb.psnr_mean;
+        for (size_t l = 0; l < lb.psnr.size(); ++l)
+            if (psnr_out) psnr_out[l] = lb.psnr[l];
+        if (grads) copy_grads(g, grads);
+    });
+}
+
+// holo::optimizer_step (optimizer.cpp:102-133) applied `steps` times from fresh
+// moments, step k using grads + k * grad_stride (each a scene-shaped ref_grads
+// layout packed as positions | rotations | log_scales | amplitudes | opacity |
+// phases | plane_logits).  The scene arrays are updated in place; applied[k]
+// records whether step k was taken.
+int ref_optimizer_run(ho_scene* s, const double* grads, int steps, const double* cfgv, int use_adam,
+                      long long schedule_total, int* applied) {
+    return guarded([&] {
+        holo::GaussianScene scene = to_scene(s);
+        holo::OptimizerConfig oc;
+        oc.lr_positions = cfgv[0];
+        oc.lr_rotations = cfgv[1];
+        oc.lr_log_scales = cfgv[2];
+        oc.lr_amplitudes = cfgv[3];
+        oc.lr_phases = cfgv[4];
+        oc.lr_opacities = cfgv[5];
+        oc.lr_plane_logits = cfgv[6];
+        oc.beta1 = cfgv[7];
+        oc.beta2 = cfgv[8];
+        oc.beta3 = cfgv[9];
+        oc.eps = cfgv[10];
+        oc.lr_floor = cfgv[11];
+        oc.use_adam = use_adam != 0;
+        oc.schedule_total = schedule_total;
+        holo::OptimState st;
+        st.resize_like(scene);
+        const size_t n = scene.size(), L = static_cast<size_t>(scene.num_planes);
+        const size_t stride = n * (3 + 4 + 3 + 3 + 1 + 3 + L);
+        for (int k = 0; k < steps; ++k) {
+            const double* p = grads + k * stride;
+            holo::SceneGradients g;
+            g.resize_like(scene);
+            for (auto* v : {&g.positions, &g.rotations, &g.log_scales, &g.amplitudes, &g.opacity_logits, &g.phases,
+                            &g.plane_logits}) {
+                std::memcpy(v->data(), p, sizeof(double) * v->size());
+                p += v->size();
+            }
+            applied[k] = holo::optimizer_step(st, scene, g, oc) ? 1 : 0;
+        }
+        std::memcpy(const_cast<double*>(s->positions), scene.positions.data(), sizeof(double) * 3 * n);
+        std::memcpy(const_cast<double*>(s->rotations), scene.rotations.data(), sizeof(double) * 4 * n);
+        std::memcpy(const_cast<double*>(s->log_scales), scene.log_scales.data(), sizeof(double) * 3 * n);
+        std::memcpy(const_cast<double*>(s->amplitudes), scene.amplitudes.data(), sizeof(double) * 3 * n);
+        std::memcpy(const_cast<double*>(s->opacity_logits), scene.opacity_logits.data(), sizeof(double) * n);
+        std::memcpy(const_cast<double*>(s->phases), scene.phases.data(), sizeof(double) * 3 * n);
+        std::memcpy(const_cast<double*>(s->plane_logits), scene.plane_logits.data(), sizeof(double) * n * L);
     });
 }
 

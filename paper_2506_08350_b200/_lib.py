@@ -82,6 +82,24 @@ class SceneGrads(C.Structure):
     _fields_ = [(k, C.c_void_p) for k in GRAD_FIELDS]
 
 
+class LossOptions(C.Structure):
+    _fields_ = [("lambda_ssim", C.c_double), ("lambda_opacity", C.c_double), ("use_plain_mse", C.c_int)]
+
+
+class LossBreakdown(C.Structure):
+    _fields_ = [("total", C.c_double), ("recon", C.c_double), ("ssim", C.c_double), ("opacity", C.c_double),
+                ("psnr_mean", C.c_double)]
+
+
+OPTIM_FIELDS = ("lr_positions", "lr_rotations", "lr_log_scales", "lr_amplitudes", "lr_phases", "lr_opacities",
+                "lr_plane_logits", "beta1", "beta2", "beta3", "eps")
+
+
+class OptimizerConfig(C.Structure):
+    _fields_ = [(k, C.c_double) for k in OPTIM_FIELDS] + [("use_adam", C.c_int), ("schedule_total", C.c_longlong),
+                                                          ("lr_floor", C.c_double)]
+
+
 class FrameInfo(C.Structure):
     _fields_ = [("num_entries", C.c_uint64), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32),
                 ("num_buckets", C.c_int32), ("max_bucket", C.c_int32), ("num_valid", C.c_int32),
@@ -131,6 +149,14 @@ def lib() -> C.CDLL:
         "holo_raster_backward": (i, [vp, P(Camera), P(Wave), P(RasterSettings), vp, P(SceneGrads)]),
         "holo_pipeline_backward": (i, [vp, P(Camera), P(Wave), P(RasterSettings), P(PropOptions), vp,
                                        P(SceneGrads), vp, vp]),
+        "holo_losses": (i, [vp, vp, vp, vp, i, i, i, i, P(LossOptions), P(LossBreakdown), P(d), vp]),
+        "holo_total_loss": (i, [vp, P(Camera), P(Wave), P(RasterSettings), P(PropOptions), P(LossOptions), vp, vp,
+                                P(LossBreakdown), P(d), P(SceneGrads)]),
+        "holo_optim_create": (i, [vp, P(vp)]),
+        "holo_optim_destroy": (i, [vp]),
+        "holo_optim_step": (i, [vp, vp, P(SceneGrads), P(OptimizerConfig), P(i)]),
+        "holo_optim_counts": (i, [vp, P(C.c_longlong), P(C.c_longlong)]),
+        "holo_scene_download": (i, [vp, P(SceneArrays)]),
         "holo_fft2": (i, [vp, vp, i, i, i, i, i]),
         "holo_transfer_function": (i, [vp, P(Wave), d, P(PropOptions), vp, i]),
         "holo_propagate": (i, [vp, vp, vp, i, i, i, P(Wave), d, P(PropOptions), i]),

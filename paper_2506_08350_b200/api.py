@@ -10,6 +10,10 @@ Function names, arguments and errors follow proj/include/holo/*.hpp:
 * transfer_function(cfg, z, opt)                 propagation.hpp:27
 * fft2 / ifft2                                   fft.hpp:11-12
 * intensity(u)                                   field.hpp:45
+* raster_backward / pipeline_backward            rasterizer.hpp:79-81, pipeline.cpp:63-91
+* losses(I, I_gt, masks, opt)                    losses.hpp (loss_recon / loss_mse, loss_ssim, psnr)
+* total_loss(scene, cam, cfg, target, opt)       pipeline.hpp:54-56
+* Optimizer(ctx).step(grads, cfg)                optimizer.hpp:55-58 (optimizer_step)
 
 Host data is numpy (complex128 fields [C, H, W], like the reference's f64
 ComplexField); every call runs on the GPU through the C-ABI.  The render path
@@ -29,8 +33,8 @@ import numpy as np
 
 from . import _lib as L
 from ._lib import HoloError
-from .holotypes import (CameraView, GaussianScene, PipelineForward, PipelineOptions, PropagationOptions,
-                        RasterForward, RenderSettings, WaveConfig, plane_positions)
+from .holotypes import (CameraView, GaussianScene, LossBreakdown, OptimizerConfig, PipelineForward, PipelineOptions,
+                        PropagationOptions, RasterForward, RenderSettings, WaveConfig, plane_positions)
 
 _NP = {"f32": (L.F32, np.complex64, np.float32), "f64": (L.F64, np.complex128, np.float64)}
 
@@ -70,6 +74,30 @@ def _settings(st: Optional[RenderSettings]) -> L.RasterSettings:
     s.soft_assignment = int(bool(st.soft_assignment))
     s.tile = int(st.tile)
     return s
+
+
+def _loss_opts(opt: Optional[PipelineOptions]) -> L.LossOptions:
+    opt = opt or PipelineOptions()
+    o = L.LossOptions()
+    o.lambda_ssim = float(opt.lambda_ssim)
+    o.lambda_opacity = float(opt.lambda_opacity)
+    o.use_plain_mse = int(bool(opt.use_plain_mse))
+    return o
+
+
+def _optim_cfg(cfg: Optional[OptimizerConfig]) -> L.OptimizerConfig:
+    cfg = cfg or OptimizerConfig()
+    c = L.OptimizerConfig()
+    for k in L.OPTIM_FIELDS + ("lr_floor",):
+        setattr(c, k, float(getattr(cfg, k)))
+    c.use_adam = int(bool(cfg.use_adam))
+    c.schedule_total = int(cfg.schedule_total)
+    return c
+
+
+def _breakdown(b: L.LossBreakdown, psnr) -> LossBreakdown:
+    return LossBreakdown(total=b.total, recon=b.recon, ssim=b.ssim, opacity=b.opacity, psnr_mean=b.psnr_mean,
+                         psnr=[float(x) for x in psnr])
 
 
 def _prop(opt: Optional[PropagationOptions]) -> L.PropOptions:
@@ -257,6 +285,51 @@ class Context:
                                                 C.c_void_p(gl.data_ptr()), C.c_void_p(gh.data_ptr())))
         return out, gl, gh
 
+    # ---------------------------------------------------------- training step
+    def losses(self, intensities, targets, masks, opt: Optional[PipelineOptions] = None, grad: bool = True):
+        """loss_recon (or loss_mse) + loss_ssim + psnr (losses.cpp) over device f64
+        tensors [L, C, H, W] (masks [L, H, W]).  Returns (LossBreakdown, dL/dI or None)."""
+        torch = _torch()
+        Ln, Cn, H, W = (int(x) for x in intensities.shape)
+        b = L.LossBreakdown()
+        psnr = (C.c_double * Ln)()
+        g = torch.empty_like(intensities) if grad else None
+        L.check(self.lib.holo_losses(self.h, C.c_void_p(intensities.data_ptr()), C.c_void_p(targets.data_ptr()),
+                                     C.c_void_p(masks.data_ptr() if masks is not None else None), Ln, Cn, H, W,
+                                     C.byref(_loss_opts(opt)), C.byref(b), psnr,
+                                     C.c_void_p(g.data_ptr() if g is not None else None)))
+        return _breakdown(b, psnr), g
+
+    def total_loss(self, cam: CameraView, cfg: WaveConfig, targets, masks, opt: Optional[PipelineOptions] = None,
+                   n: Optional[int] = None):
+        """total_loss (pipeline.cpp:30-95) on the resident scene; targets / masks are
+        device f64 tensors [L, C, H, W] / [L, H, W].  With n (the scene size) the
+        gradients are computed and returned as a dict of f64 device tensors."""
+        opt = opt or PipelineOptions()
+        b = L.LossBreakdown()
+        psnr = (C.c_double * cfg.num_planes)()
+        g = out = None
+        if n is not None:
+            g, out = self._grad_tensors(n, cfg.num_planes)
+        L.check(self.lib.holo_total_loss(self.h, C.byref(_camera(cam)), C.byref(_wave(cfg)),
+                                         C.byref(_settings(opt.raster)), C.byref(_prop(opt.prop)),
+                                         C.byref(_loss_opts(opt)), C.c_void_p(targets.data_ptr()),
+                                         C.c_void_p(masks.data_ptr() if masks is not None else None), C.byref(b),
+                                         psnr, C.byref(g) if g is not None else None))
+        return _breakdown(b, psnr), out
+
+    def download_scene(self, n: int, num_planes: int) -> GaussianScene:
+        """The resident scene back on the host (checkpointing after optimizer steps)."""
+        arrs = {"positions": np.empty((n, 3)), "rotations": np.empty((n, 4)), "log_scales": np.empty((n, 3)),
+                "amplitudes": np.empty((n, 3)), "opacity_logits": np.empty((n,)), "phases": np.empty((n, 3)),
+                "plane_logits": np.empty((n, num_planes))}
+        s = L.SceneArrays()
+        s.n, s.num_planes = int(n), int(num_planes)
+        for k, a in arrs.items():
+            setattr(s, k, a.ctypes.data)
+        L.check(self.lib.holo_scene_download(self.h, C.byref(s)))
+        return GaussianScene(num_planes=int(num_planes), **arrs)
+
     def buffer(self, which: int):
         p = C.c_void_p()
         n = C.c_size_t()
@@ -336,6 +409,45 @@ class Context:
         out = torch.empty(d.shape, dtype=torch.float32 if precision == "f32" else torch.float64, device=d.device)
         L.check(self.lib.holo_intensity(self.h, d.data_ptr(), out.data_ptr(), d.numel(), _NP[precision][0]))
         return out.cpu().numpy()
+
+
+class Optimizer:
+    """OptimState + optimizer_step (optimizer.hpp:37-58) on a context's resident
+    scene: device moments, updates in place in HBM."""
+
+    def __init__(self, ctx: "Context"):
+        self.ctx = ctx
+        h = C.c_void_p()
+        L.check(ctx.lib.holo_optim_create(ctx.h, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            L.check(self.ctx.lib.holo_optim_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self, grads: dict, cfg: Optional[OptimizerConfig] = None) -> bool:
+        """One update from device f64 gradient tensors (as total_loss returns);
+        False (and a counted skip) when a gradient is non-finite."""
+        g = L.SceneGrads()
+        for k in L.GRAD_FIELDS:
+            if k != "mu_screen":
+                setattr(g, k, grads[k].data_ptr())
+        applied = C.c_int(0)
+        L.check(self.ctx.lib.holo_optim_step(self.ctx.h, self.h, C.byref(g), C.byref(_optim_cfg(cfg)),
+                                             C.byref(applied)))
+        return bool(applied.value)
+
+    def counts(self):
+        s, k = C.c_longlong(), C.c_longlong()
+        L.check(self.ctx.lib.holo_optim_counts(self.h, C.byref(s), C.byref(k)))
+        return int(s.value), int(k.value)
 
 
 _DEFAULT: dict = {}
@@ -461,6 +573,32 @@ def pipeline_backward(scene: GaussianScene, cam: CameraView, cfg: WaveConfig, op
     out, gl, gh = ctx.pipeline_backward(cam, cfg, opt.raster, opt.prop, gi, scene.size())
     return ({k: v.cpu().numpy() for k, v in out.items()}, gl.cpu().numpy().astype(np.complex128),
             gh.cpu().numpy().astype(np.complex128))
+
+
+def losses(I, I_gt, masks, opt: Optional[PipelineOptions] = None, ctx: Optional[Context] = None):
+    """losses.hpp on numpy stacks [L, C, H, W] (masks [L, H, W] or None for plain
+    MSE): returns (LossBreakdown, dL/dI as numpy)."""
+    torch = _torch()
+    ctx = ctx or default_context()
+    dev = f"cuda:{ctx.device}"
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)  # noqa: E731
+    b, g = ctx.losses(t(I), t(I_gt), t(masks) if masks is not None else None, opt)
+    return b, g.cpu().numpy()
+
+
+def total_loss(scene: GaussianScene, cam: CameraView, cfg: WaveConfig, images, masks,
+               opt: Optional[PipelineOptions] = None, want_grads: bool = True, ctx: Optional[Context] = None):
+    """pipeline.hpp:54-56 (FocalStackTarget given as images [L, C, H, W] and masks
+    [L, H, W]): returns (LossBreakdown, gradients as numpy or None)."""
+    torch = _torch()
+    _check_shapes(scene, cam, cfg)
+    ctx = ctx or default_context()
+    ctx.upload_scene(scene)
+    dev = f"cuda:{ctx.device}"
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)  # noqa: E731
+    b, out = ctx.total_loss(cam, cfg, t(images), t(masks) if masks is not None else None, opt,
+                            scene.size() if want_grads else None)
+    return b, ({k: v.cpu().numpy() for k, v in out.items()} if out is not None else None)
 
 
 def propagate(u, cfg: WaveConfig, z: float, opt: Optional[PropagationOptions] = None, precision: str = "f64"):

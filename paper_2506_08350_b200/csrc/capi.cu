@@ -1085,6 +1085,48 @@ void adjoint_propagation(holo_ctx* ctx, const holo_wave& wave, const holo_prop_o
     rows_epilogue(ctx, stage, W, H, C, O, 1, gholo, glayers, nullptr);
 }
 
+// holo_render's body (pipeline_forward, pipeline.cpp:20-29)
+void render_full(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, const holo_raster_settings& st,
+                 const holo_prop_options& po, unsigned outputs, holo_frame_info* info) {
+    render_front(ctx, cam, wave, st, po, 0, wave.num_planes, nullptr, outputs, info, true);
+    if (!po.pad2x) return;
+    // pad2x: the spectrum shortcut does not hold (the crop after each propagate,
+    // propagation.cpp:100), so run forward_record / inverse_propagate literally.
+    const int W = wave.nx, H = wave.ny, C = wave.channels, L = wave.num_planes;
+    const size_t P = static_cast<size_t>(W) * H;
+    if (!(outputs & (HOLO_OUT_HOLOGRAM | HOLO_OUT_REPLAYED | HOLO_OUT_INTENSITY))) return;
+    const cx<float>* layers = static_cast<const cx<float>*>(ctx->buffer("layers", 1));
+    const int k = ctx->out_sel;
+    cx<float>* d_holo = buf<cx<float>>(ctx, out_name("hologram", k).c_str(), static_cast<size_t>(C) * P);
+    op_forward_record<float>(ctx, layers, L, d_holo, wave, po);
+    if (outputs & (HOLO_OUT_REPLAYED | HOLO_OUT_INTENSITY)) {
+        cx<float>* d_rep = buf<cx<float>>(ctx, out_name("replayed", k).c_str(), static_cast<size_t>(L) * C * P);
+        op_inverse_propagate<float>(ctx, d_holo, d_rep, wave, po);
+        if (outputs & HOLO_OUT_INTENSITY)
+            intensity<float>(ctx, d_rep, buf<float>(ctx, out_name("intensity", k).c_str(), static_cast<size_t>(L) * C * P),
+                             static_cast<size_t>(L) * C * P);
+    }
+}
+
+// holo_pipeline_backward's body (pipeline.cpp:63-91 without the opacity term)
+void pipeline_backward(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, const holo_raster_settings& st,
+                       const holo_prop_options& po, const float* grad_intensities, const holo_scene_grads& grads,
+                       void* grad_layers_out, void* grad_hologram_out) {
+    check_backward_frame(ctx, cam, wave, st);
+    require((ctx->f_outputs & HOLO_OUT_REPLAYED) != 0, HOLO_ERR_USAGE,
+            "pipeline backward needs the last render with HOLO_OUT_REPLAYED");
+    const int W = wave.nx, H = wave.ny, C = wave.channels, L = wave.num_planes;
+    const size_t P = static_cast<size_t>(W) * H, n = static_cast<size_t>(L) * C * P;
+    const cx<float>* rep = static_cast<const cx<float>*>(ctx->buffer(out_name("replayed", ctx->out_sel), 1));
+    cx<float>* gv = buf<cx<float>>(ctx, "bwd_gv", n);
+    bwd_seed(ctx, rep, grad_intensities, gv, n);
+    cx<float>* gl = grad_layers_out ? static_cast<cx<float>*>(grad_layers_out) : buf<cx<float>>(ctx, "bwd_glayers", n);
+    cx<float>* gh = grad_hologram_out ? static_cast<cx<float>*>(grad_hologram_out)
+                                      : buf<cx<float>>(ctx, "bwd_gholo", static_cast<size_t>(C) * P);
+    adjoint_propagation(ctx, wave, po, gv, gh, gl);
+    raster_backward(ctx, wave, st, gl, grads);
+}
+
 }  // namespace
 
 extern "C" {
@@ -1106,20 +1148,9 @@ int holo_pipeline_backward(holo_ctx* ctx, const holo_camera* cam, const holo_wav
     return guarded([&] {
         require(ctx && cam && wave && settings && grad_intensities && grads, HOLO_ERR_USAGE, "null argument");
         HC_CUDA(cudaSetDevice(ctx->device));
-        check_backward_frame(ctx, *cam, *wave, *settings);
-        require((ctx->f_outputs & HOLO_OUT_REPLAYED) != 0, HOLO_ERR_USAGE,
-                "pipeline backward needs the last render with HOLO_OUT_REPLAYED");
         const holo_prop_options po = prop ? *prop : holo_prop_options{0, 0};
-        const int W = wave->nx, H = wave->ny, C = wave->channels, L = wave->num_planes;
-        const size_t P = static_cast<size_t>(W) * H, n = static_cast<size_t>(L) * C * P;
-        const cx<float>* rep = static_cast<const cx<float>*>(ctx->buffer(out_name("replayed", ctx->out_sel), 1));
-        cx<float>* gv = buf<cx<float>>(ctx, "bwd_gv", n);
-        bwd_seed(ctx, rep, static_cast<const float*>(grad_intensities), gv, n);
-        cx<float>* gl = grad_layers_out ? static_cast<cx<float>*>(grad_layers_out) : buf<cx<float>>(ctx, "bwd_glayers", n);
-        cx<float>* gh = grad_hologram_out ? static_cast<cx<float>*>(grad_hologram_out)
-                                          : buf<cx<float>>(ctx, "bwd_gholo", static_cast<size_t>(C) * P);
-        adjoint_propagation(ctx, *wave, po, gv, gh, gl);
-        raster_backward(ctx, *wave, *settings, gl, *grads);
+        pipeline_backward(ctx, *cam, *wave, *settings, po, static_cast<const float*>(grad_intensities), *grads,
+                          grad_layers_out, grad_hologram_out);
     });
 }
 
@@ -1156,24 +1187,7 @@ int holo_render(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave, co
         require(ctx && cam && wave && settings, HOLO_ERR_USAGE, "null argument");
         HC_CUDA(cudaSetDevice(ctx->device));
         const holo_prop_options po = prop ? *prop : holo_prop_options{0, 0};
-        render_front(ctx, *cam, *wave, *settings, po, 0, wave->num_planes, nullptr, outputs, info, true);
-        if (!po.pad2x) return;
-        // pad2x: the spectrum shortcut does not hold (the crop after each propagate,
-        // propagation.cpp:100), so run forward_record / inverse_propagate literally.
-        const int W = wave->nx, H = wave->ny, C = wave->channels, L = wave->num_planes;
-        const size_t P = static_cast<size_t>(W) * H;
-        if (!(outputs & (HOLO_OUT_HOLOGRAM | HOLO_OUT_REPLAYED | HOLO_OUT_INTENSITY))) return;
-        const cx<float>* layers = static_cast<const cx<float>*>(ctx->buffer("layers", 1));
-        const int k = ctx->out_sel;
-        cx<float>* d_holo = buf<cx<float>>(ctx, out_name("hologram", k).c_str(), static_cast<size_t>(C) * P);
-        op_forward_record<float>(ctx, layers, L, d_holo, *wave, po);
-        if (outputs & (HOLO_OUT_REPLAYED | HOLO_OUT_INTENSITY)) {
-            cx<float>* d_rep = buf<cx<float>>(ctx, out_name("replayed", k).c_str(), static_cast<size_t>(L) * C * P);
-            op_inverse_propagate<float>(ctx, d_holo, d_rep, *wave, po);
-            if (outputs & HOLO_OUT_INTENSITY)
-                intensity<float>(ctx, d_rep, buf<float>(ctx, out_name("intensity", k).c_str(), static_cast<size_t>(L) * C * P),
-                                 static_cast<size_t>(L) * C * P);
-        }
+        render_full(ctx, *cam, *wave, *settings, po, outputs, info);
     });
 }
 
@@ -1328,6 +1342,208 @@ int holo_intensity(holo_ctx* ctx, const void* field, void* out, size_t samples, 
             intensity<float>(ctx, static_cast<const cx<float>*>(field), static_cast<float*>(out), samples);
         else
             intensity<double>(ctx, static_cast<const cx<double>*>(field), static_cast<double*>(out), samples);
+    });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- training step
+
+struct holo_optim {
+    int device = 0;
+    size_t n = 0;
+    int planes = 0;
+    bool sized = false;
+    double* mom[7][4] = {};  // per group: m, v, n, prev_grad (OptimState::Moments)
+    long long step = 0, skipped = 0;
+};
+
+namespace {
+
+holo_loss_options loss_defaults(const holo_loss_options* o) {
+    return o ? *o : holo_loss_options{0.005, 1e-4, 0};  // pipeline.hpp:26-28
+}
+
+// the loss terms of total_loss (pipeline.cpp:43-62) on device f64 stacks
+void loss_terms(holo_ctx* ctx, const double* I, const double* G, const double* masks, int L, int C, int H, int W,
+                const holo_loss_options& lo, bool with_ssim, double* grad, holo_loss_breakdown* out,
+                double* psnr) {
+    const size_t n = static_cast<size_t>(L) * C * H * W;
+    if (grad) HC_CUDA(cudaMemsetAsync(grad, 0, sizeof(double) * n, ctx->stream));
+    double* d_out = buf<double>(ctx, "loss_out", 1 + 2 * static_cast<size_t>(L));
+    losses_gpu(ctx, I, G, masks, L, C, H, W, lo.use_plain_mse != 0, with_ssim, lo.lambda_ssim, grad, d_out);
+    std::vector<double> h(1 + 2 * static_cast<size_t>(L));
+    HC_CUDA(cudaMemcpyAsync(h.data(), d_out, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    HC_CUDA(cudaStreamSynchronize(ctx->stream));
+    out->recon = h[0];
+    const double scale = lo.lambda_ssim / static_cast<double>(L);  // losses.cpp:98-104
+    double ss = 0.0;
+    for (int l = 0; l < L; ++l) ss += scale * (1.0 - h[1 + l]);
+    out->ssim = ss;
+    double acc = 0.0;
+    for (int l = 0; l < L; ++l) {
+        const double mse = h[1 + L + l];  // losses.cpp:129-131
+        const double p = mse <= 0.0 ? 99.0 : std::min(99.0, 10.0 * std::log10(1.0 / mse));
+        if (psnr) psnr[l] = p;
+        acc += p;
+    }
+    out->psnr_mean = acc / static_cast<double>(L);
+    out->opacity = 0.0;
+    out->total = out->recon + out->ssim;
+}
+
+double cosine_lr(double base, double floor, long long t, long long total) {  // optimizer.cpp:7-11
+    if (total <= 0 || t >= total) return floor;
+    const double phase = 3.14159265358979323846 * static_cast<double>(t) / static_cast<double>(total);
+    return floor + 0.5 * (base - floor) * (1.0 + std::cos(phase));
+}
+
+// the scene arrays the next render reads, ordered after any upload into them
+holo_ctx::SceneSet& resident_scene(holo_ctx* ctx) {
+    const int k = ctx->scene_cur;
+    if (ctx->scene_wait[k]) {
+        HC_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_scene_ready[k], 0));
+        ctx->scene_wait[k] = false;
+    }
+    return ctx->scene_sets[k];
+}
+
+}  // namespace
+
+extern "C" {
+
+int holo_losses(holo_ctx* ctx, const double* intensities, const double* targets, const double* masks, int L, int C,
+                int H, int W, const holo_loss_options* opt, holo_loss_breakdown* out, double* psnr, double* grad) {
+    return guarded([&] {
+        require(ctx && intensities && targets && out, HOLO_ERR_USAGE, "null argument");
+        require(L >= 1 && C >= 1 && H >= 1 && W >= 1, HOLO_ERR_CONFIG, "focal stack shape must be positive");
+        const holo_loss_options lo = loss_defaults(opt);
+        require(lo.use_plain_mse || masks, HOLO_ERR_USAGE, "masks are required unless use_plain_mse");
+        HC_CUDA(cudaSetDevice(ctx->device));
+        loss_terms(ctx, intensities, targets, masks, L, C, H, W, lo, lo.lambda_ssim != 0.0, grad, out, psnr);
+    });
+}
+
+int holo_total_loss(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave, const holo_raster_settings* settings,
+                    const holo_prop_options* prop, const holo_loss_options* opt, const double* targets,
+                    const double* masks, holo_loss_breakdown* out, double* psnr, holo_scene_grads* grads) {
+    return guarded([&] {
+        require(ctx && cam && wave && settings && targets && out, HOLO_ERR_USAGE, "null argument");
+        const holo_loss_options lo = loss_defaults(opt);
+        require(lo.use_plain_mse || masks, HOLO_ERR_USAGE, "masks are required unless use_plain_mse");
+        HC_CUDA(cudaSetDevice(ctx->device));
+        validate_wave(*wave);
+        const holo_prop_options po = prop ? *prop : holo_prop_options{0, 0};
+        const int W = wave->nx, H = wave->ny, C = wave->channels, L = wave->num_planes;
+        const size_t n = static_cast<size_t>(L) * C * H * W;
+        render_full(ctx, *cam, *wave, *settings, po, HOLO_OUT_INTENSITY | HOLO_OUT_REPLAYED | HOLO_OUT_AUX, nullptr);
+        const float* i32 = static_cast<const float*>(ctx->buffer(out_name("intensity", ctx->out_sel), 1));
+        double* i64 = buf<double>(ctx, "loss_I", n);
+        f32_to_f64(ctx, i32, i64, n);
+        double* gi = grads ? buf<double>(ctx, "loss_gI", n) : nullptr;
+        loss_terms(ctx, i64, targets, masks, L, C, H, W, lo, true, gi, out, psnr);
+        if (grads) {
+            float* gi32 = buf<float>(ctx, "loss_gI32", n);
+            f64_to_f32(ctx, gi, gi32, n);
+            pipeline_backward(ctx, *cam, *wave, *settings, po, gi32, *grads, nullptr, nullptr);
+        }
+        // opacity decay (pipeline.cpp:47-52, 82-88) on the rendered scene
+        const double* opac = ctx->scene_sets[ctx->f_scene_set].a[4];
+        out->opacity = opacity_term(ctx, opac, ctx->n, lo.lambda_opacity, grads ? grads->opacity_logits : nullptr);
+        out->total = out->recon + out->ssim + out->opacity;
+    });
+}
+
+int holo_optim_create(holo_ctx* ctx, holo_optim** out) {
+    return guarded([&] {
+        require(ctx && out, HOLO_ERR_USAGE, "null argument");
+        *out = new holo_optim();
+        (*out)->device = ctx->device;
+    });
+}
+
+int holo_optim_destroy(holo_optim* st) {
+    if (!st) return HOLO_OK;
+    cudaSetDevice(st->device);
+    for (auto& g : st->mom)
+        for (double* p : g) cudaFree(p);
+    delete st;
+    return HOLO_OK;
+}
+
+int holo_optim_counts(const holo_optim* st, long long* step, long long* skipped) {
+    return guarded([&] {
+        require(st, HOLO_ERR_USAGE, "null argument");
+        if (step) *step = st->step;
+        if (skipped) *skipped = st->skipped;
+    });
+}
+
+int holo_optim_step(holo_ctx* ctx, holo_optim* st, const holo_scene_grads* grads, const holo_optimizer_config* cfg,
+                    int* applied) {
+    return guarded([&] {
+        require(ctx && st && grads && cfg, HOLO_ERR_USAGE, "null argument");
+        require(st->device == ctx->device, HOLO_ERR_USAGE, "optimizer state belongs to another device");
+        HC_CUDA(cudaSetDevice(ctx->device));
+        if (applied) *applied = 0;
+        const size_t N = ctx->n;
+        const int L = ctx->scene_planes;
+        const size_t count[7] = {3 * N, 4 * N, 3 * N, 3 * N, N, 3 * N, N * static_cast<size_t>(L)};
+        const double* g[7] = {grads->positions, grads->rotations, grads->log_scales, grads->amplitudes,
+                              grads->opacity_logits, grads->phases, grads->plane_logits};
+        for (int k = 0; k < 7; ++k)
+            require(g[k] || count[k] == 0, HOLO_ERR_USAGE, "optimizer: every gradient group is required");
+        if (!st->sized) {  // OptimState::resize_like (optimizer.cpp:41-49)
+            for (int k = 0; k < 7; ++k)
+                for (int j = 0; j < 4; ++j) {
+                    HC_CUDA(cudaMalloc(&st->mom[k][j], sizeof(double) * (count[k] ? count[k] : 1)));
+                    HC_CUDA(cudaMemsetAsync(st->mom[k][j], 0, sizeof(double) * (count[k] ? count[k] : 1), ctx->stream));
+                }
+            st->n = N;
+            st->planes = L;
+            st->sized = true;
+        }
+        require(st->n == N && st->planes == L, HOLO_ERR_CONFIG, "optimizer: moment buffers do not match the scene");
+        holo_ctx::SceneSet& set = resident_scene(ctx);
+        if (!grads_finite(ctx, g, count, 7)) {  // optimizer.cpp:110-115
+            ++st->skipped;
+            return;
+        }
+        const long long t = st->step;  // 0-based schedule position
+        ++st->step;
+        const double lr[7] = {cosine_lr(cfg->lr_positions, cfg->lr_floor, t, cfg->schedule_total),
+                              cfg->lr_rotations,
+                              cfg->lr_log_scales,
+                              cfg->lr_amplitudes,
+                              cfg->lr_opacities,
+                              cfg->lr_phases,
+                              cosine_lr(cfg->lr_plane_logits, cfg->lr_floor, t, cfg->schedule_total)};
+        for (int k = 0; k < 7; ++k)
+            adaptive_update(ctx, set.a[k], g[k], st->mom[k][0], st->mom[k][1], st->mom[k][2], st->mom[k][3], count[k],
+                            lr[k], st->step, cfg->beta1, cfg->beta2, cfg->beta3, cfg->eps, cfg->use_adam != 0);
+        renormalize_scene(ctx, set.a[1], set.a[3], N);  // scene.cpp:34-47
+        if (applied) *applied = 1;
+    });
+}
+
+int holo_scene_download(holo_ctx* ctx, const holo_scene_arrays* host) {
+    return guarded([&] {
+        require(ctx && host, HOLO_ERR_USAGE, "null argument");
+        require(host->n == ctx->n && host->num_planes == ctx->scene_planes, HOLO_ERR_USAGE,
+                "scene download: n / num_planes differ from the resident scene");
+        HC_CUDA(cudaSetDevice(ctx->device));
+        const size_t N = ctx->n;
+        const size_t count[7] = {3 * N, 4 * N, 3 * N, 3 * N, N, 3 * N, N * static_cast<size_t>(ctx->scene_planes)};
+        const double* dst[7] = {host->positions, host->rotations, host->log_scales, host->amplitudes,
+                                host->opacity_logits, host->phases, host->plane_logits};
+        holo_ctx::SceneSet& set = resident_scene(ctx);
+        for (int k = 0; k < 7; ++k)
+            if (count[k]) {
+                require(dst[k] != nullptr, HOLO_ERR_USAGE, "scene download: null array");
+                HC_CUDA(cudaMemcpyAsync(const_cast<double*>(dst[k]), set.a[k], sizeof(double) * count[k],
+                                        cudaMemcpyDeviceToHost, ctx->stream));
+            }
+        HC_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }
 

@@ -217,4 +217,15 @@ void gauss_backward(holo_ctx* ctx, const GaussBwdArgs& a);
 void sort_small_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsigned capacity,
                         const unsigned long long* ekey, int* egidx);
 
+// ---- training step (training.cu): losses, opacity decay, optimizer
+void losses_gpu(holo_ctx* ctx, const double* I, const double* G, const double* masks, int L, int C, int H, int W,
+                bool plain, bool with_ssim, double lambda_ssim, double* grad, double* d_out);
+double opacity_term(holo_ctx* ctx, const double* logits, size_t n, double lambda, double* gopac);
+void f32_to_f64(holo_ctx* ctx, const float* in, double* out, size_t n);
+void f64_to_f32(holo_ctx* ctx, const double* in, float* out, size_t n);
+bool grads_finite(holo_ctx* ctx, const double* const* g, const size_t* n, int groups);
+void adaptive_update(holo_ctx* ctx, double* p, const double* g, double* m, double* v, double* nn, double* prev,
+                     size_t n, double lr, long long step, double b1, double b2, double b3, double eps, bool adam);
+void renormalize_scene(holo_ctx* ctx, double* rot, double* amp, size_t n);
+
 }  // namespace holo_cuda

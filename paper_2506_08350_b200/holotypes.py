@@ -180,8 +180,42 @@ class PropagationOptions:
 
 @dataclass
 class PipelineOptions:
+    """pipeline.hpp:23-29."""
     raster: RenderSettings = field(default_factory=RenderSettings)
     prop: PropagationOptions = field(default_factory=PropagationOptions)
+    lambda_ssim: float = 0.005
+    lambda_opacity: float = 1e-4
+    use_plain_mse: bool = False
+
+
+@dataclass
+class LossBreakdown:
+    """pipeline.hpp:44-48."""
+    total: float = 0.0
+    recon: float = 0.0
+    ssim: float = 0.0
+    opacity: float = 0.0
+    psnr_mean: float = 0.0
+    psnr: List[float] = field(default_factory=list)
+
+
+@dataclass
+class OptimizerConfig:
+    """optimizer.hpp:17-31 (Adan; use_adam selects the two-moment fallback)."""
+    lr_positions: float = 0.01
+    lr_rotations: float = 0.001
+    lr_log_scales: float = 0.005
+    lr_amplitudes: float = 0.0025
+    lr_phases: float = 0.0025
+    lr_opacities: float = 0.025
+    lr_plane_logits: float = 0.01
+    beta1: float = 0.9
+    beta2: float = 0.99
+    beta3: float = 0.99
+    eps: float = 1e-8
+    use_adam: bool = False
+    schedule_total: int = 20000
+    lr_floor: float = 1e-5
 
 
 @dataclass
