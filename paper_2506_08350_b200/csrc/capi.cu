@@ -1368,8 +1368,6 @@ holo_loss_options loss_defaults(const holo_loss_options* o) {
 void loss_terms(holo_ctx* ctx, const double* I, const double* G, const double* masks, int L, int C, int H, int W,
                 const holo_loss_options& lo, bool with_ssim, double* grad, holo_loss_breakdown* out,
                 double* psnr) {
-    const size_t n = static_cast<size_t>(L) * C * H * W;
-    if (grad) HC_CUDA(cudaMemsetAsync(grad, 0, sizeof(double) * n, ctx->stream));
     double* d_out = buf<double>(ctx, "loss_out", 1 + 2 * static_cast<size_t>(L));
     losses_gpu(ctx, I, G, masks, L, C, H, W, lo.use_plain_mse != 0, with_ssim, lo.lambda_ssim, grad, d_out);
     std::vector<double> h(1 + 2 * static_cast<size_t>(L));

@@ -2,14 +2,15 @@
 // (proj/src/losses.cpp, ssim.cpp) with their gradient dL/dI, the opacity decay
 // term (pipeline.cpp:47-52, 82-88) and the Adan / Adam update (optimizer.cpp).
 //
-// Precision and order: f64 throughout, like the reference.  Sums that the
-// reference folds row by row (fold_partials, common.hpp:70-74) are formed the
-// same way -- one thread per row summing along x, then one thread folding the
-// rows in order -- so on identical inputs the loss values match the reference
-// build to the last bit or two; the SSIM blurs are the reference's separable
-// 11-tap correlations with zero extension (ssim.cpp:29-62).  The opacity mean is
-// a fixed-shape tree reduction (deterministic, not the reference's sequential
-// order).  The loss kernels are HBM-bound elementwise / stencil passes.
+// Precision and order: f64 throughout, like the reference, compiled without FMA
+// contraction.  Sums that the reference folds row by row (fold_partials,
+// common.hpp:70-74) are formed the same way -- each row summed along x in order
+// (coalesced loads, transposed through shared memory), the rows then
+// folded in order -- and the SSIM blurs are the reference's separable 11-tap
+// correlations with zero extension (ssim.cpp:29-62) fused per 2-D tile, so on
+// identical inputs the loss values and dL/dI equal the reference build's.  The
+// opacity mean is a fixed-shape tree reduction (deterministic, not the
+// reference's sequential order).
 #include <cmath>
 #include <vector>
 
@@ -25,144 +26,283 @@ constexpr double kC1 = 0.01 * 0.01, kC2 = 0.03 * 0.03;
 
 __constant__ double c_win[kWin];
 
-// ---- pointwise loss rows: (I - I_gt)^2 weighted by 1 + m^2 + b^2 (recon) or 1 (mse)
+// ---- row sums in the reference's order, coalesced
+// One warp owns 32 rows.  Per 32-column chunk every lane loads its column of the
+// 32 x 32 block (32 independent coalesced loads per array in flight), forms the
+// per-element terms (and the elementwise gradient) there, and the block is
+// transposed through shared memory so that lane r adds row r's 32 terms in x
+// order -- the sequential fold of losses.cpp / ssim.cpp, so the row sums are the
+// reference's bit for bit.
+constexpr int kRowWarps = 2;
+
+// loss_recon / loss_mse and the psnr rows (losses.cpp:28-132) over rows r of
+// [L][C][H] (length W); grad = the pointwise term's gradient
 template <bool PLAIN>
-__global__ void k_loss_rows(const double* __restrict__ I, const double* __restrict__ G,
-                            const double* __restrict__ masks, int C, int H, int W, int L, double gscale,
-                            double* __restrict__ rows, double* __restrict__ grad) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;  // row over L * C * H
-    if (r >= L * C * H) return;
-    const int l = r / (C * H);
-    const int y = r % H;
-    const size_t off = static_cast<size_t>(r) * W;
-    const double* a = I + off;
-    const double* b = G + off;
-    const double* m = PLAIN ? nullptr : masks + (static_cast<size_t>(l) * H + y) * W;
-    double* g = grad ? grad + off : nullptr;
-    double acc = 0.0;
-    for (int x = 0; x < W; ++x) {
-        const double e = a[x] - b[x];
-        const double weight = PLAIN ? 1.0 : 1.0 + m[x] * m[x] + b[x] * b[x];
-        acc += weight * e * e;
-        if (g) g[x] += gscale * weight * e;
+__global__ void __launch_bounds__(32 * kRowWarps) k_loss_row_sums(const double* __restrict__ I,
+                                                                 const double* __restrict__ G,
+                                                                 const double* __restrict__ masks, int C, int H,
+                                                                 int W, long long nrows, double gscale,
+                                                                 double* __restrict__ grad,
+                                                                 double* __restrict__ rec_rows,
+                                                                 double* __restrict__ mse_rows) {
+    __shared__ double tile[kRowWarps][PLAIN ? 1 : 2][32][33];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long r0 = (static_cast<long long>(blockIdx.x) * kRowWarps + warp) * 32;
+    if (r0 >= nrows) return;
+    const int nr = static_cast<int>(min(32LL, nrows - r0));
+    // per-row offsets, computed once by lane j for row r0 + j and broadcast
+    const long long myrow = r0 + min(lane, nr - 1);
+    const long long moff_l = PLAIN ? 0 : (myrow / (static_cast<long long>(C) * H) * H + myrow % H) * W;
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int c0 = 0; c0 < W; c0 += 32) {
+        const int nc = min(32, W - c0);
+        // every lane loads (the tail lanes repeat the last column) so that the row
+        // offsets can be broadcast with full-warp shuffles
+        const bool live = lane < nc;
+        const int x = c0 + (live ? lane : nc - 1);
+        double a[32], b[32], m[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            if (j < nr) {
+                const size_t i = static_cast<size_t>(r0 + j) * W + x;
+                a[j] = I[i];
+                b[j] = G[i];
+                if (!PLAIN) m[j] = masks[__shfl_sync(0xffffffffu, moff_l, j) + x];
+            }
+        }
+        if (live) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                if (j < nr) {
+                    const size_t i = static_cast<size_t>(r0 + j) * W + x;
+                    const double e = a[j] - b[j];
+                    if (PLAIN) {
+                        tile[warp][0][j][lane] = e * e;
+                        if (grad) grad[i] = gscale * e;
+                    } else {
+                        const double weight = 1.0 + m[j] * m[j] + b[j] * b[j];
+                        tile[warp][0][j][lane] = weight * e * e;
+                        tile[warp][PLAIN ? 0 : 1][j][lane] = e * e;
+                        if (grad) grad[i] = gscale * weight * e;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane < nr) {
+            for (int k = 0; k < nc; ++k) {
+                acc0 += tile[warp][0][lane][k];
+                if (!PLAIN) acc1 += tile[warp][PLAIN ? 0 : 1][lane][k];
+            }
+        }
+        __syncwarp();
     }
-    rows[r] = acc;
+    if (lane < nr) {
+        rec_rows[r0 + lane] = acc0;
+        mse_rows[r0 + lane] = PLAIN ? acc0 : acc1;
+    }
 }
 
-// sum of n values in order (fold_partials), one thread: out = mul * sum / div
-__global__ void k_fold(const double* __restrict__ v, int n, double mul, double div, double* out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// SSIM map row sums over the valid window centres (ssim.cpp:100-121): rows r of
+// [L][C][vrows], columns [5, W - 5)
+__global__ void __launch_bounds__(32 * kRowWarps) k_ssim_row_sums(const double* __restrict__ smap, int W, int H,
+                                                                 int vrows, long long nrows,
+                                                                 double* __restrict__ out) {
+    __shared__ double tile[kRowWarps][32][33];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long r0 = (static_cast<long long>(blockIdx.x) * kRowWarps + warp) * 32;
+    if (r0 >= nrows) return;
+    const int nr = static_cast<int>(min(32LL, nrows - r0));
+    const long long myrow = r0 + min(lane, nr - 1);
+    const long long off_l = myrow / vrows * static_cast<long long>(W) * H + (myrow % vrows + 5) * W + 5;
+    const int ncols = W - 10;
     double acc = 0.0;
-    for (int i = 0; i < n; ++i) acc += v[i];
-    *out = mul * acc / div;
+    for (int c0 = 0; c0 < ncols; c0 += 32) {
+        const int nc = min(32, ncols - c0);
+        const int x = c0 + min(lane, nc - 1);  // all lanes load: full-warp shuffles
+        double v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < nr) v[j] = smap[__shfl_sync(0xffffffffu, off_l, j) + x];
+        if (lane < nc) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (j < nr) tile[warp][j][lane] = v[j];
+        }
+        __syncwarp();
+        if (lane < nr)
+            for (int k = 0; k < nc; ++k) acc += tile[warp][lane][k];
+        __syncwarp();
+    }
+    if (lane < nr) out[r0 + lane] = acc;
+}
+
+// out[t] = mul * (sum of v[t * len .. t * len + len) in order) / div, one warp per
+// segment: coalesced 32-value chunks, lane 0 adds them in order via shuffles
+__global__ void k_fold_seg(const double* __restrict__ v, int nseg, int len, double mul, double div,
+                           double* __restrict__ out) {
+    const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (t >= nseg) return;
+    const double* p = v + static_cast<size_t>(t) * len;
+    double acc = 0.0;
+    for (int c0 = 0; c0 < len; c0 += 32) {
+        const int nc = min(32, len - c0);
+        const double x = lane < nc ? p[c0 + lane] : 0.0;
+        for (int k = 0; k < nc; ++k) {
+            const double y = __shfl_sync(0xffffffffu, x, k);
+            acc += y;
+        }
+    }
+    if (lane == 0) out[t] = mul * acc / div;
 }
 
 __global__ void k_fill(double* p, int n, double v) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = v;
 }
 
-// ---- SSIM (ssim.cpp:64-147), one (plane, channel) image pair at a time
-// horizontal 11-tap correlations of x, y, x^2, y^2, x y (zero extension)
-__global__ void k_blur_h5(const double* __restrict__ x, const double* __restrict__ y, int W, int H,
-                          double* __restrict__ out /* 5 planes */) {
-    const size_t P = static_cast<size_t>(W) * H;
-    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-    if (i >= P) return;
-    const int px = static_cast<int>(i % W);
-    const size_t row = i - px;
-    const int k0 = max(0, kHalf - px), k1 = min(kWin, W + kHalf - px);
-    double s[5] = {0, 0, 0, 0, 0};
-    for (int k = k0; k < k1; ++k) {
-        const double w = c_win[k];
-        const double xv = x[row + px + k - kHalf], yv = y[row + px + k - kHalf];
-        s[0] += w * xv;
-        s[1] += w * yv;
-        s[2] += w * (xv * xv);
-        s[3] += w * (yv * yv);
-        s[4] += w * (xv * yv);
+// ---- SSIM (ssim.cpp:64-147), fused per 2-D tile
+// Forward: the tile's I and I_gt with a 5-pixel halo (zeros outside the image:
+// the zero extension of corr_h / corr_v adds exact zeros) go to shared memory;
+// the horizontal 11-tap pass forms mx, my, qx, qy, qxy for the tile's rows plus
+// the halo rows, the vertical pass finishes them per pixel, and the SSIM value and
+// the three gradient maps (zero outside the valid window centres) are written.
+// Backward: the same two passes over the gradient maps, then
+// grad -= scale (inv_n (t1 + 2 x t2 + y t3)).  Each tap sum runs k = 0..10 in
+// order with separate multiply and add, as the reference's loops.
+constexpr int kTW = 32, kTH = 32, kHW = kTW + 2 * kHalf, kHH = kTH + 2 * kHalf;
+constexpr size_t kSsimFwdSmem = sizeof(double) * (2 * kHH * kHW + 5 * kHH * kTW);
+constexpr size_t kSsimBwdSmem = sizeof(double) * (3 * kHH * kHW + 3 * kHH * kTW);
+
+template <int Q>
+__device__ __forceinline__ void load_halo(const double* const* src, size_t base, int W, int H, int x0, int y0,
+                                          double* dst) {
+    for (int i = threadIdx.x; i < kHH * kHW; i += blockDim.x) {
+        const int r = i / kHW, c = i % kHW;
+        const int gy = y0 - kHalf + r, gx = x0 - kHalf + c;
+        const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+        const size_t gi = base + static_cast<size_t>(gy) * W + gx;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) dst[q * kHH * kHW + i] = in ? src[q][gi] : 0.0;
     }
-    for (int q = 0; q < 5; ++q) out[q * P + i] = s[q];
 }
 
-// horizontal correlation of `n` planes
-__global__ void k_blur_h(const double* __restrict__ in, int W, int H, int n, double* __restrict__ out) {
+template <bool GRAD>
+__global__ void __launch_bounds__(256) k_ssim_fwd(const double* __restrict__ X, const double* __restrict__ Y, int W,
+                                                  int H, double* __restrict__ smap, double* __restrict__ gmaps,
+                                                  size_t gstride) {
+    extern __shared__ double sm[];
+    double* sxy = sm;                 // [2][kHH][kHW]
+    double* hb = sm + 2 * kHH * kHW;  // [5][kHH][kTW]
     const size_t P = static_cast<size_t>(W) * H;
-    const size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-    if (t >= P * n) return;
-    const size_t i = t % P, base = t - i;
-    const int px = static_cast<int>(i % W);
-    const size_t row = base + i - px;
-    const int k0 = max(0, kHalf - px), k1 = min(kWin, W + kHalf - px);
-    double acc = 0.0;
-    for (int k = k0; k < k1; ++k) acc += c_win[k] * in[row + px + k - kHalf];
-    out[t] = acc;
-}
-
-// vertical correlation of `n` planes
-__global__ void k_blur_v(const double* __restrict__ in, int W, int H, int n, double* __restrict__ out) {
-    const size_t P = static_cast<size_t>(W) * H;
-    const size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-    if (t >= P * n) return;
-    const size_t i = t % P, base = t - i;
-    const int py = static_cast<int>(i / W), px = static_cast<int>(i % W);
-    const int k0 = max(0, kHalf - py), k1 = min(kWin, H + kHalf - py);
-    double acc = 0.0;
-    for (int k = k0; k < k1; ++k) acc += c_win[k] * in[base + static_cast<size_t>(py + k - kHalf) * W + px];
-    out[t] = acc;
-}
-
-// SSIM map over the interior window centres; gradient maps (zero outside)
-__global__ void k_ssim_map(const double* __restrict__ mom /* mx my qx qy qxy */, int W, int H, int want_grad,
-                           double* __restrict__ smap, double* __restrict__ gmaps /* gmu gqx gqxy */) {
-    const size_t P = static_cast<size_t>(W) * H;
-    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-    if (i >= P) return;
-    const int py = static_cast<int>(i / W), px = static_cast<int>(i % W);
-    const bool valid = px >= kHalf && px < W - kHalf && py >= kHalf && py < H - kHalf;
-    double s = 0.0, gmu = 0.0, gqx = 0.0, gqxy = 0.0;
-    if (valid) {
-        const double ux = mom[i], uy = mom[P + i];
-        const double vxv = mom[2 * P + i] - ux * ux;
-        const double vyv = mom[3 * P + i] - uy * uy;
-        const double vxy = mom[4 * P + i] - ux * uy;
-        const double a1 = 2.0 * ux * uy + kC1;
-        const double a2 = 2.0 * vxy + kC2;
-        const double b1 = ux * ux + uy * uy + kC1;
-        const double b2 = vxv + vyv + kC2;
-        const double d = b1 * b2;
-        s = (a1 * a2) / d;
-        if (want_grad) {
-            gmu = (2.0 * uy * (a2 - a1) - s * 2.0 * ux * (b2 - b1)) / d;
-            gqx = -s / b2;
-            gqxy = 2.0 * a1 / d;
+    const size_t base = blockIdx.z * P;
+    const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH;
+    const double* src[2] = {X, Y};
+    load_halo<2>(src, base, W, H, x0, y0, sxy);
+    __syncthreads();
+    for (int i = threadIdx.x; i < kHH * kTW; i += blockDim.x) {
+        const int r = i / kTW, c = i % kTW;
+        const double* xr = sxy + r * kHW + c;
+        const double* yr = xr + kHH * kHW;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
+#pragma unroll
+        for (int k = 0; k < kWin; ++k) {
+            const double w = c_win[k], xv = xr[k], yv = yr[k];
+            s0 += w * xv;
+            s1 += w * yv;
+            s2 += w * (xv * xv);
+            s3 += w * (yv * yv);
+            s4 += w * (xv * yv);
+        }
+        hb[0 * kHH * kTW + i] = s0;
+        hb[1 * kHH * kTW + i] = s1;
+        hb[2 * kHH * kTW + i] = s2;
+        hb[3 * kHH * kTW + i] = s3;
+        hb[4 * kHH * kTW + i] = s4;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kTH * kTW; i += blockDim.x) {
+        const int r = i / kTW, c = i % kTW;
+        const int py = y0 + r, px = x0 + c;
+        if (py >= H || px >= W) continue;
+        double m[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const double* col = hb + q * kHH * kTW + r * kTW + c;
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < kWin; ++k) acc += c_win[k] * col[k * kTW];
+            m[q] = acc;
+        }
+        const bool valid = px >= kHalf && px < W - kHalf && py >= kHalf && py < H - kHalf;
+        double s = 0.0, gmu = 0.0, gqx = 0.0, gqxy = 0.0;
+        if (valid) {
+            const double ux = m[0], uy = m[1];
+            const double vxv = m[2] - ux * ux;
+            const double vyv = m[3] - uy * uy;
+            const double vxy = m[4] - ux * uy;
+            const double a1 = 2.0 * ux * uy + kC1;
+            const double a2 = 2.0 * vxy + kC2;
+            const double b1 = ux * ux + uy * uy + kC1;
+            const double b2 = vxv + vyv + kC2;
+            const double d = b1 * b2;
+            s = (a1 * a2) / d;
+            if (GRAD) {
+                gmu = (2.0 * uy * (a2 - a1) - s * 2.0 * ux * (b2 - b1)) / d;
+                gqx = -s / b2;
+                gqxy = 2.0 * a1 / d;
+            }
+        }
+        const size_t gi = base + static_cast<size_t>(py) * W + px;
+        smap[gi] = s;
+        if (GRAD) {
+            const size_t li = blockIdx.z * P + static_cast<size_t>(py) * W + px;
+            gmaps[li] = gmu;
+            gmaps[gstride + li] = gqx;
+            gmaps[2 * gstride + li] = gqxy;
         }
     }
-    smap[i] = s;
-    if (want_grad) {
-        gmaps[i] = gmu;
-        gmaps[P + i] = gqx;
-        gmaps[2 * P + i] = gqxy;
+}
+
+__global__ void __launch_bounds__(256) k_ssim_bwd(const double* __restrict__ gmaps, size_t gstride,
+                                                  const double* __restrict__ X, const double* __restrict__ Y, int W,
+                                                  int H, double inv_n, double scale, double* __restrict__ grad) {
+    extern __shared__ double sm[];
+    double* sg = sm;                  // [3][kHH][kHW]
+    double* hb = sm + 3 * kHH * kHW;  // [3][kHH][kTW]
+    const size_t P = static_cast<size_t>(W) * H;
+    const size_t lbase = blockIdx.z * P;
+    const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH;
+    const double* src[3] = {gmaps, gmaps + gstride, gmaps + 2 * gstride};
+    load_halo<3>(src, lbase, W, H, x0, y0, sg);
+    __syncthreads();
+    for (int i = threadIdx.x; i < kHH * kTW; i += blockDim.x) {
+        const int r = i / kTW, c = i % kTW;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const double* row = sg + q * kHH * kHW + r * kHW + c;
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < kWin; ++k) acc += c_win[k] * row[k];
+            hb[q * kHH * kTW + i] = acc;
+        }
     }
-}
-
-// row sums of the SSIM map over the valid columns, one thread per valid row
-__global__ void k_ssim_rows(const double* __restrict__ smap, int W, int H, double* __restrict__ rows) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    const int nrows = H - 2 * kHalf;
-    if (r >= nrows) return;
-    const double* s = smap + static_cast<size_t>(r + kHalf) * W;
-    double acc = 0.0;
-    for (int x = kHalf; x < W - kHalf; ++x) acc += s[x];
-    rows[r] = acc;
-}
-
-// grad -= scale * (inv_n (t1 + 2 x t2 + y t3))
-__global__ void k_ssim_grad(const double* __restrict__ t /* t1 t2 t3 */, const double* __restrict__ x,
-                            const double* __restrict__ y, size_t P, double inv_n, double scale,
-                            double* __restrict__ grad) {
-    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-    if (i >= P) return;
-    grad[i] -= scale * (inv_n * (t[i] + 2.0 * x[i] * t[P + i] + y[i] * t[2 * P + i]));
+    __syncthreads();
+    for (int i = threadIdx.x; i < kTH * kTW; i += blockDim.x) {
+        const int r = i / kTW, c = i % kTW;
+        const int py = y0 + r, px = x0 + c;
+        if (py >= H || px >= W) continue;
+        double t[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const double* col = hb + q * kHH * kTW + r * kTW + c;
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < kWin; ++k) acc += c_win[k] * col[k * kTW];
+            t[q] = acc;
+        }
+        const size_t gi = lbase + static_cast<size_t>(py) * W + px;
+        grad[gi] -= scale * (inv_n * (t[0] + 2.0 * X[gi] * t[1] + Y[gi] * t[2]));
+    }
 }
 
 __global__ void k_f32_to_f64(const float* __restrict__ in, double* __restrict__ out, size_t n) {
@@ -259,12 +399,12 @@ unsigned blocks_for(size_t n, unsigned cap = 8192) {
 }  // namespace
 
 // loss_recon / loss_mse + loss_ssim + psnr over device f64 stacks [L][C][H][W]
-// (masks [L][H][W]); grad (optional, zeroed by the caller) accumulates dL/dI.
+// (masks [L][H][W]); grad (optional) is overwritten with dL/dI.
 // d_out[0] = recon, d_out[1 + l] = mean SSIM of plane l, d_out[1 + L + l] =
 // the mse of plane l; the host finishes the scalar algebra.
 void losses_gpu(holo_ctx* ctx, const double* I, const double* G, const double* masks, int L, int C, int H, int W,
                 bool plain, bool with_ssim, double lambda_ssim, double* grad, double* d_out) {
-    const size_t n = static_cast<size_t>(C) * H * W, P = static_cast<size_t>(H) * W;
+    const size_t n = static_cast<size_t>(C) * H * W;
     if (with_ssim && (W < kWin || H < kWin))
         throw Error(HOLO_ERR_CONFIG, "ssim needs images at least 11 pixels in each dimension");
     static bool win_set = false;
@@ -277,31 +417,36 @@ void losses_gpu(holo_ctx* ctx, const double* I, const double* G, const double* m
         }
         for (double& v : w) v /= sum;
         HC_CUDA(cudaMemcpyToSymbol(c_win, w, sizeof w));
+        HC_CUDA(cudaFuncSetAttribute(k_ssim_fwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kSsimFwdSmem)));
+        HC_CUDA(cudaFuncSetAttribute(k_ssim_fwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kSsimFwdSmem)));
+        HC_CUDA(cudaFuncSetAttribute(k_ssim_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kSsimBwdSmem)));
         win_set = true;
     }
-    const int rows_n = L * C * H;
-    double* rows = static_cast<double*>(ctx->buffer("loss_rows", sizeof(double) * rows_n));
-    double* prow = static_cast<double*>(ctx->buffer("psnr_rows", sizeof(double) * rows_n));
+    const long long rows_n = static_cast<long long>(L) * C * H;
+    double* rows = static_cast<double*>(ctx->buffer("loss_rows", sizeof(double) * 2 * rows_n));
+    double* prow = rows + rows_n;
     double* lsum = static_cast<double*>(ctx->buffer("loss_plane", sizeof(double) * L));
     const double inv_l = 1.0 / static_cast<double>(L), inv_n = 1.0 / static_cast<double>(n);
-    const unsigned rb = (rows_n + 127) / 128;
-    // recon / mse (losses.cpp:28-94): every plane has the same n, so one pass
+    // recon / mse and the psnr rows in one pass (losses.cpp:28-132); grad = the
+    // pointwise term's gradient (the reference adds it to a zeroed stack)
+    const unsigned rb = static_cast<unsigned>((rows_n + 32 * kRowWarps - 1) / (32 * kRowWarps));
+    const double gscale = 2.0 * inv_l * inv_n;
     if (plain)
-        k_loss_rows<true><<<rb, 128, 0, ctx->stream>>>(I, G, masks, C, H, W, L, 2.0 * inv_l * inv_n, rows, grad);
+        k_loss_row_sums<true><<<rb, 32 * kRowWarps, 0, ctx->stream>>>(I, G, masks, C, H, W, rows_n, gscale, grad,
+                                                                      rows, prow);
     else
-        k_loss_rows<false><<<rb, 128, 0, ctx->stream>>>(I, G, masks, C, H, W, L, 2.0 * inv_l * inv_n, rows, grad);
+        k_loss_row_sums<false><<<rb, 32 * kRowWarps, 0, ctx->stream>>>(I, G, masks, C, H, W, rows_n, gscale, grad,
+                                                                       rows, prow);
     HC_LAUNCHED(ctx);
-    // psnr (losses.cpp:113-132): plain squared-error rows
-    k_loss_rows<true><<<rb, 128, 0, ctx->stream>>>(I, G, nullptr, C, H, W, L, 0.0, prow, nullptr);
+    const unsigned lb = (L + 3) / 4;  // 4 warps (segments) per block
+    k_fold_seg<<<lb, 128, 0, ctx->stream>>>(rows, L, C * H, inv_l * inv_n, 1.0, lsum);
     HC_LAUNCHED(ctx);
-    for (int l = 0; l < L; ++l) {
-        const size_t ro = static_cast<size_t>(l) * C * H;
-        k_fold<<<1, 32, 0, ctx->stream>>>(rows + ro, C * H, inv_l * inv_n, 1.0, lsum + l);
-        HC_LAUNCHED(ctx);
-        k_fold<<<1, 32, 0, ctx->stream>>>(prow + ro, C * H, 1.0, static_cast<double>(n), d_out + 1 + L + l);
-        HC_LAUNCHED(ctx);
-    }
-    k_fold<<<1, 32, 0, ctx->stream>>>(lsum, L, 1.0, 1.0, d_out);
+    k_fold_seg<<<lb, 128, 0, ctx->stream>>>(prow, L, C * H, 1.0, static_cast<double>(n), d_out + 1 + L);
+    HC_LAUNCHED(ctx);
+    k_fold_seg<<<1, 32, 0, ctx->stream>>>(lsum, 1, L, 1.0, 1.0, d_out);
     HC_LAUNCHED(ctx);
 
     if (!with_ssim) {  // the SSIM term left out: mean SSIM 1 contributes 0
@@ -312,41 +457,34 @@ void losses_gpu(holo_ctx* ctx, const double* I, const double* G, const double* m
     // ssim (losses.cpp:96-111, ssim.cpp:64-147): lambda / L (1 - mean SSIM) per plane
     const int vrows = H - 2 * kHalf;
     const size_t n_valid = static_cast<size_t>(W - 2 * kHalf) * vrows * C;
-    const double inv_valid = 1.0 / static_cast<double>(n_valid);
-    double* mom = static_cast<double*>(ctx->buffer("ssim_mom", sizeof(double) * 5 * P));
-    double* scratch = static_cast<double*>(ctx->buffer("ssim_scratch", sizeof(double) * 5 * P));
-    double* smap = static_cast<double*>(ctx->buffer("ssim_map", sizeof(double) * P));
-    double* gmaps = grad ? static_cast<double*>(ctx->buffer("ssim_gmaps", sizeof(double) * 3 * P)) : nullptr;
-    double* srows = static_cast<double*>(ctx->buffer("ssim_rows", sizeof(double) * vrows));
-    double* ssum = static_cast<double*>(ctx->buffer("ssim_sum", sizeof(double) * C));
-    const unsigned pb = blocks_for(P, 1u << 30);
+    double* smap = static_cast<double*>(ctx->buffer("ssim_map", sizeof(double) * L * n));
+    double* gmaps = grad ? static_cast<double*>(ctx->buffer("ssim_gmaps", sizeof(double) * 3 * n)) : nullptr;
+    const dim3 tg((W + kTW - 1) / kTW, (H + kTH - 1) / kTH, C);
     for (int l = 0; l < L; ++l) {
-        for (int c = 0; c < C; ++c) {
-            const size_t off = (static_cast<size_t>(l) * C + c) * P;
-            k_blur_h5<<<pb, 256, 0, ctx->stream>>>(I + off, G + off, W, H, scratch);
+        const size_t off = static_cast<size_t>(l) * n;
+        if (grad) {
+            k_ssim_fwd<true><<<tg, 256, kSsimFwdSmem, ctx->stream>>>(I + off, G + off, W, H, smap + off, gmaps, n);
             HC_LAUNCHED(ctx);
-            k_blur_v<<<blocks_for(5 * P, 1u << 30), 256, 0, ctx->stream>>>(scratch, W, H, 5, mom);
+            k_ssim_bwd<<<tg, 256, kSsimBwdSmem, ctx->stream>>>(gmaps, n, I + off, G + off, W, H,
+                                                              1.0 / static_cast<double>(n_valid),
+                                                              lambda_ssim / static_cast<double>(L), grad + off);
             HC_LAUNCHED(ctx);
-            k_ssim_map<<<pb, 256, 0, ctx->stream>>>(mom, W, H, grad != nullptr, smap, gmaps);
+        } else {
+            k_ssim_fwd<false><<<tg, 256, kSsimFwdSmem, ctx->stream>>>(I + off, G + off, W, H, smap + off, nullptr, 0);
             HC_LAUNCHED(ctx);
-            k_ssim_rows<<<(vrows + 127) / 128, 128, 0, ctx->stream>>>(smap, W, H, srows);
-            HC_LAUNCHED(ctx);
-            k_fold<<<1, 32, 0, ctx->stream>>>(srows, vrows, 1.0, 1.0, ssum + c);
-            HC_LAUNCHED(ctx);
-            if (grad) {
-                k_blur_h<<<blocks_for(3 * P, 1u << 30), 256, 0, ctx->stream>>>(gmaps, W, H, 3, scratch);
-                HC_LAUNCHED(ctx);
-                k_blur_v<<<blocks_for(3 * P, 1u << 30), 256, 0, ctx->stream>>>(scratch, W, H, 3, mom);
-                HC_LAUNCHED(ctx);
-                k_ssim_grad<<<pb, 256, 0, ctx->stream>>>(mom, I + off, G + off, P, inv_valid,
-                                                         lambda_ssim / static_cast<double>(L), grad + off);
-                HC_LAUNCHED(ctx);
-            }
         }
-        // channels folded in order, / n_valid (ssim.cpp:123, 146)
-        k_fold<<<1, 32, 0, ctx->stream>>>(ssum, C, 1.0, static_cast<double>(n_valid), d_out + 1 + l);
-        HC_LAUNCHED(ctx);
     }
+    const long long srows_n = static_cast<long long>(L) * C * vrows;
+    double* srows = static_cast<double*>(ctx->buffer("ssim_rows", sizeof(double) * srows_n));
+    double* ssum = static_cast<double*>(ctx->buffer("ssim_sum", sizeof(double) * L * C));
+    k_ssim_row_sums<<<static_cast<unsigned>((srows_n + 32 * kRowWarps - 1) / (32 * kRowWarps)), 32 * kRowWarps, 0,
+                      ctx->stream>>>(smap, W, H, vrows, srows_n, srows);
+    HC_LAUNCHED(ctx);
+    // per (plane, channel) the rows in order; per plane the channels in order, / n_valid
+    k_fold_seg<<<(L * C + 3) / 4, 128, 0, ctx->stream>>>(srows, L * C, vrows, 1.0, 1.0, ssum);
+    HC_LAUNCHED(ctx);
+    k_fold_seg<<<lb, 128, 0, ctx->stream>>>(ssum, L, C, 1.0, static_cast<double>(n_valid), d_out + 1);
+    HC_LAUNCHED(ctx);
 }
 
 double opacity_term(holo_ctx* ctx, const double* logits, size_t n, double lambda, double* gopac) {
