@@ -25,6 +25,37 @@ from paper_2506_08350_b200.holotypes import CameraView, PropagationOptions, Rend
 from paper_2506_08350_b200.scenes import front_camera, synthetic_scene  # noqa: E402
 
 RGB = (639e-9, 532e-9, 473e-9)
+TL_KEYS = ("recon", "ssim", "opacity", "total", "psnr_mean")
+OPT_CFG = (0.01, 0.001, 0.005, 0.0025, 0.0025, 0.025, 0.01, 0.9, 0.99, 0.99, 1e-8, 1e-5)
+GROUPS = ("positions", "rotations", "log_scales", "amplitudes", "opacity_logits", "phases", "plane_logits")
+
+
+def training_golden(ref):
+    """losses.cpp on seeded stacks and optimizer_step runs (Adan and Adam, a
+    non-finite step skipped) from fresh moments -> training.npz."""
+    rng = np.random.default_rng(300)
+    I = rng.random((2, 3, 20, 24))
+    G = np.clip(I + 0.2 * rng.standard_normal(I.shape), 0.0, 1.0)
+    M = (rng.random((2, 20, 24)) > 0.5).astype(np.float64)
+    out = dict(ls_I=I, ls_G=G, ls_M=M)
+    for plain in (0, 1):
+        r, s, ps, g = ref.losses(I, G, M, lambda_ssim=0.2, plain=bool(plain))
+        out.update({f"ls{plain}_recon": r, f"ls{plain}_ssim": s, f"ls{plain}_psnr": ps, f"ls{plain}_grad": g})
+    cfg = WaveConfig(nx=48, ny=48, wavelengths=RGB, num_planes=3)
+    scene = synthetic_scene(50, cfg, 16)
+    steps = []
+    for k in range(5):
+        gr = np.random.default_rng(400 + k)
+        steps.append({n: gr.standard_normal(np.shape(getattr(scene, n))) for n in GROUPS})
+    steps[2]["phases"][3, 1] = np.inf
+    out.update(op_num_planes=scene.num_planes, **{f"op_scene_{n}": getattr(scene, n) for n in GROUPS},
+               **{f"op_g{k}_{n}": steps[k][n] for k in range(5) for n in GROUPS}, op_cfg=np.array(OPT_CFG))
+    for adam in (0, 1):
+        want, applied = ref.optimizer_run(scene, steps, OPT_CFG, use_adam=bool(adam), schedule_total=3)
+        out.update({f"op{adam}_applied": applied, **{f"op{adam}_{n}": want[n] for n in GROUPS}})
+    path = os.path.join(HERE, "training.npz")
+    np.savez_compressed(path, **out)
+    print("training", os.path.getsize(path), "bytes")
 
 
 def cases():
@@ -67,10 +98,18 @@ def main():
             gi = np.random.default_rng(100 + len(name)).standard_normal(r.intensities.shape)
             grads, gh, gl = ref.pipeline_backward(scene, cam, cfg, st, prop, gi)
             out.update(bwd_gi=gi, bwd_gholo=gh, bwd_glayers=gl, **{f"bwd_{k}": v for k, v in grads.items()})
+            # total_loss (pipeline.cpp:30-95) against a seeded focal-stack target
+            rng = np.random.default_rng(200 + len(name))
+            tgt = 0.5 * rng.random(r.intensities.shape)
+            msk = (rng.random((cfg.num_planes, cfg.ny, cfg.nx)) > 0.6).astype(np.float64)
+            bd, ps, tg = ref.total_loss(scene, cam, cfg, st, prop, tgt, msk, lambda_ssim=0.05, lambda_opacity=1e-2)
+            out.update(tl_targets=tgt, tl_masks=msk, tl_breakdown=np.array([bd[k] for k in TL_KEYS]), tl_psnr=ps,
+                       **{f"tl_{k}": v for k, v in tg.items()})
         # (deterministic: re-running reproduces the committed files bit for bit)
         path = os.path.join(HERE, f"{name}.npz")
         np.savez_compressed(path, **out)
         print(name, os.path.getsize(path), "bytes, E =", len(r.raster.entry_gidx))
+    training_golden(ref)
 
 
 if __name__ == "__main__":
