@@ -305,6 +305,29 @@ int holo_optim_counts(const holo_optim* st, long long* step, long long* skipped)
  * const qualifiers of holo_scene_arrays; n and num_planes must match). */
 int holo_scene_download(holo_ctx* ctx, const holo_scene_arrays* host);
 
+/* ---- phase-only conversion (phase_only.hpp) ----
+ * PhaseOnlyOptions (phase_only.hpp:22-32): defaults lambda_ssim 1.0, prop.pad2x 1,
+ * use_adam 0.  Fields are device complex128 [C][H][W] (H = wave->ny, W = wave->nx,
+ * C = wave->channels), phases device f64 [C][H][W]. */
+typedef struct {
+    double lambda_ssim;
+    holo_prop_options prop;
+    int use_adam;
+} holo_phase_options;
+
+/* phase_only_loss (phase_only.cpp:104-111): *loss (host) and, when grad != NULL,
+ * d loss / d theta (device). */
+int holo_phase_only_loss(holo_ctx* ctx, const void* P, const double* theta, const holo_wave* wave,
+                         const holo_phase_options* opt, double* loss, double* grad);
+/* convert_phase_only (phase_only.cpp:113-160): adaptive-moment descent on theta
+ * with the reference's backtracking; phase_out (device) receives the best iterate,
+ * trace (host, iters + 1) the loss at initialisation and after every iteration.
+ * theta0 (device, optional) is the starting phase; NULL starts from arg(P)
+ * computed on the device (the reference's std::arg may differ in the last bit --
+ * callers holding P on the host pass their own arg for bit-equal extraction). */
+int holo_convert_phase_only(holo_ctx* ctx, const void* P, const holo_wave* wave, int iters, double lr,
+                            const holo_phase_options* opt, const double* theta0, double* phase_out, double* trace);
+
 /* Device pointer and size of one output buffer of the last render. */
 int holo_frame_buffer(holo_ctx* ctx, int buffer, void** dev_ptr, size_t* bytes);
 /* Synchronous device-to-host copy of one output buffer (bytes must match). */

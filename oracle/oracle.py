@@ -418,6 +418,30 @@ class Oracle:
         names = order
         return {k: a.copy() for k, a in zip(names, sa.arrays)}, applied
 
+    def phase_only_loss(self, P, theta, wave, lambda_ssim=1.0, prop=None, use_adam=False, grad=True):
+        """holo::phase_only_loss (phase_only.cpp:104-111): (loss, d loss / d theta or None).
+        prop defaults to PhaseOnlyOptions' pad2x = true."""
+        a = _c128(P)
+        th = np.ascontiguousarray(theta, dtype=np.float64)
+        pr = _prop(prop) if prop is not None else _prop({"pad2x": True})
+        loss = C.c_double()
+        g = np.zeros(a.shape) if grad else None
+        self._check(self.lib.ref_phase_only_loss(_ptr(a), _ptr(th), C.byref(_wave(wave)), C.c_double(lambda_ssim),
+                                                 C.byref(pr), int(use_adam), C.byref(loss),
+                                                 _ptr(g) if grad else None))
+        return loss.value, g
+
+    def convert_phase_only(self, P, wave, iters=1000, lr=0.02, lambda_ssim=1.0, prop=None, use_adam=False):
+        """holo::convert_phase_only (phase_only.cpp:113-160): (best phase [C,H,W], trace)."""
+        a = _c128(P)
+        pr = _prop(prop) if prop is not None else _prop({"pad2x": True})
+        out = np.zeros(a.shape)
+        trace = np.zeros(iters + 1)
+        self._check(self.lib.ref_convert_phase_only(_ptr(a), C.byref(_wave(wave)), int(iters), C.c_double(lr),
+                                                    C.c_double(lambda_ssim), C.byref(pr), int(use_adam), _ptr(out),
+                                                    _ptr(trace)))
+        return out, trace
+
     def pipeline_backward(self, scene, cam, wave, settings, prop, grad_intensities):
         """The gradient branch of holo::total_loss (pipeline.cpp:63-80) for
         dL/d(intensities) [L,C,H,W]: returns (scene gradients, grad_hologram,

@@ -17,6 +17,7 @@
 #include "holo/rasterizer.hpp"
 #include "holo/losses.hpp"
 #include "holo/optimizer.hpp"
+#include "holo/phase_only.hpp"
 
 namespace {
 
@@ -475,6 +476,41 @@ int ref_optimizer_run(ho_scene* s, const double* grads, int steps, const double*
         std::memcpy(const_cast<double*>(s->opacity_logits), scene.opacity_logits.data(), sizeof(double) * n);
         std::memcpy(const_cast<double*>(s->phases), scene.phases.data(), sizeof(double) * 3 * n);
         std::memcpy(const_cast<double*>(s->plane_logits), scene.plane_logits.data(), sizeof(double) * n * L);
+    });
+}
+
+}  // extern "C"
+
+// ---- phase-only conversion (phase_only.cpp) on interleaved complex128 [C][H][W]
+extern "C" {
+
+int ref_phase_only_loss(const double* P, const double* theta, const ho_wave* cfg, double lambda_ssim,
+                        const ho_prop* prop, int use_adam, double* loss, double* grad) {
+    return guarded([&] {
+        const holo::WaveConfig wc = to_wave(cfg);
+        const holo::ComplexField f = to_field(P, wc.nx, wc.ny, wc.channels(), wc.pitch);
+        holo::PhaseOnlyOptions opt;
+        opt.lambda_ssim = lambda_ssim;
+        opt.prop = to_prop(prop);
+        opt.use_adam = use_adam != 0;
+        std::vector<double> th(theta, theta + f.data.size()), g;
+        *loss = holo::phase_only_loss(f, th, wc, opt, grad ? &g : nullptr);
+        if (grad) std::memcpy(grad, g.data(), sizeof(double) * g.size());
+    });
+}
+
+int ref_convert_phase_only(const double* P, const ho_wave* cfg, int iters, double lr, double lambda_ssim,
+                           const ho_prop* prop, int use_adam, double* phase_out, double* trace) {
+    return guarded([&] {
+        const holo::WaveConfig wc = to_wave(cfg);
+        const holo::ComplexField f = to_field(P, wc.nx, wc.ny, wc.channels(), wc.pitch);
+        holo::PhaseOnlyOptions opt;
+        opt.lambda_ssim = lambda_ssim;
+        opt.prop = to_prop(prop);
+        opt.use_adam = use_adam != 0;
+        const holo::PhaseOnlyResult r = holo::convert_phase_only(f, wc, iters, lr, opt);
+        std::memcpy(phase_out, r.hologram.phase.data(), sizeof(double) * r.hologram.phase.size());
+        std::memcpy(trace, r.trace.data(), sizeof(double) * r.trace.size());
     });
 }
 

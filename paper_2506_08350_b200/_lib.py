@@ -100,6 +100,10 @@ class OptimizerConfig(C.Structure):
                                                           ("lr_floor", C.c_double)]
 
 
+class PhaseOptions(C.Structure):
+    _fields_ = [("lambda_ssim", C.c_double), ("prop", PropOptions), ("use_adam", C.c_int)]
+
+
 class FrameInfo(C.Structure):
     _fields_ = [("num_entries", C.c_uint64), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32),
                 ("num_buckets", C.c_int32), ("max_bucket", C.c_int32), ("num_valid", C.c_int32),
@@ -157,6 +161,8 @@ def lib() -> C.CDLL:
         "holo_optim_step": (i, [vp, vp, P(SceneGrads), P(OptimizerConfig), P(i)]),
         "holo_optim_counts": (i, [vp, P(C.c_longlong), P(C.c_longlong)]),
         "holo_scene_download": (i, [vp, P(SceneArrays)]),
+        "holo_phase_only_loss": (i, [vp, vp, vp, P(Wave), P(PhaseOptions), P(d), vp]),
+        "holo_convert_phase_only": (i, [vp, vp, P(Wave), i, d, P(PhaseOptions), vp, vp, P(d)]),
         "holo_fft2": (i, [vp, vp, i, i, i, i, i]),
         "holo_transfer_function": (i, [vp, P(Wave), d, P(PropOptions), vp, i]),
         "holo_propagate": (i, [vp, vp, vp, i, i, i, P(Wave), d, P(PropOptions), i]),

@@ -14,6 +14,8 @@ Function names, arguments and errors follow proj/include/holo/*.hpp:
 * losses(I, I_gt, masks, opt)                    losses.hpp (loss_recon / loss_mse, loss_ssim, psnr)
 * total_loss(scene, cam, cfg, target, opt)       pipeline.hpp:54-56
 * Optimizer(ctx).step(grads, cfg)                optimizer.hpp:55-58 (optimizer_step)
+* phase_only_loss / convert_phase_only /
+  phase_gradient_oracle                          phase_only.hpp:39-62
 
 Host data is numpy (complex128 fields [C, H, W], like the reference's f64
 ComplexField); every call runs on the GPU through the C-ABI.  The render path
@@ -33,8 +35,9 @@ import numpy as np
 
 from . import _lib as L
 from ._lib import HoloError
-from .holotypes import (CameraView, GaussianScene, LossBreakdown, OptimizerConfig, PipelineForward, PipelineOptions,
-                        PropagationOptions, RasterForward, RenderSettings, WaveConfig, plane_positions)
+from .holotypes import (CameraView, GaussianScene, LossBreakdown, OptimizerConfig, PhaseOnlyHologram, PhaseOnlyOptions,
+                        PhaseOnlyResult, PipelineForward, PipelineOptions, PropagationOptions, RasterForward,
+                        RenderSettings, WaveConfig, plane_positions)
 
 _NP = {"f32": (L.F32, np.complex64, np.float32), "f64": (L.F64, np.complex128, np.float64)}
 
@@ -98,6 +101,15 @@ def _optim_cfg(cfg: Optional[OptimizerConfig]) -> L.OptimizerConfig:
 def _breakdown(b: L.LossBreakdown, psnr) -> LossBreakdown:
     return LossBreakdown(total=b.total, recon=b.recon, ssim=b.ssim, opacity=b.opacity, psnr_mean=b.psnr_mean,
                          psnr=[float(x) for x in psnr])
+
+
+def _phase_opts(opt: Optional[PhaseOnlyOptions]) -> L.PhaseOptions:
+    opt = opt or PhaseOnlyOptions()
+    o = L.PhaseOptions()
+    o.lambda_ssim = float(opt.lambda_ssim)
+    o.prop = _prop(opt.prop)
+    o.use_adam = int(bool(opt.use_adam))
+    return o
 
 
 def _prop(opt: Optional[PropagationOptions]) -> L.PropOptions:
@@ -317,6 +329,28 @@ class Context:
                                          C.c_void_p(masks.data_ptr() if masks is not None else None), C.byref(b),
                                          psnr, C.byref(g) if g is not None else None))
         return _breakdown(b, psnr), out
+
+    # ------------------------------------------------------- phase-only conversion
+    def phase_only_loss(self, P, theta, cfg: WaveConfig, opt: Optional[PhaseOnlyOptions] = None, grad=None) -> float:
+        """phase_only_loss on device tensors: P complex128 [C, H, W], theta f64 [C, H, W];
+        grad (f64 tensor, optional) receives d loss / d theta."""
+        loss = C.c_double()
+        L.check(self.lib.holo_phase_only_loss(self.h, C.c_void_p(P.data_ptr()), C.c_void_p(theta.data_ptr()),
+                                              C.byref(_wave(cfg)), C.byref(_phase_opts(opt)), C.byref(loss),
+                                              C.c_void_p(grad.data_ptr() if grad is not None else None)))
+        return loss.value
+
+    def convert_phase_only(self, P, cfg: WaveConfig, iters: int = 1000, lr: float = 0.02,
+                           opt: Optional[PhaseOnlyOptions] = None, theta0=None):
+        """convert_phase_only on a device complex128 tensor: (best phase tensor, trace)."""
+        torch = _torch()
+        out = torch.empty(P.shape, dtype=torch.float64, device=P.device)
+        trace = (C.c_double * (max(int(iters), 0) + 1))()
+        L.check(self.lib.holo_convert_phase_only(self.h, C.c_void_p(P.data_ptr()), C.byref(_wave(cfg)), int(iters),
+                                                 float(lr), C.byref(_phase_opts(opt)),
+                                                 C.c_void_p(theta0.data_ptr() if theta0 is not None else None),
+                                                 C.c_void_p(out.data_ptr()), trace))
+        return out, list(trace)
 
     def download_scene(self, n: int, num_planes: int) -> GaussianScene:
         """The resident scene back on the host (checkpointing after optimizer steps)."""
@@ -599,6 +633,73 @@ def total_loss(scene: GaussianScene, cam: CameraView, cfg: WaveConfig, images, m
     b, out = ctx.total_loss(cam, cfg, t(images), t(masks) if masks is not None else None, opt,
                             scene.size() if want_grads else None)
     return b, ({k: v.cpu().numpy() for k, v in out.items()} if out is not None else None)
+
+
+def _phase_inputs(P, cfg: WaveConfig, ctx: "Context"):
+    torch = _torch()
+    P = np.ascontiguousarray(P, dtype=np.complex128)
+    if P.ndim != 3 or P.shape != (cfg.channels(), cfg.ny, cfg.nx):
+        raise HoloError("config", "hologram shape does not match the wave config")  # phase_only.cpp:24-25
+    return P, torch.from_numpy(P).to(f"cuda:{ctx.device}")
+
+
+def phase_only_loss(P, theta, cfg: WaveConfig, opt: Optional[PhaseOnlyOptions] = None, want_grad: bool = False,
+                    ctx: Optional[Context] = None):
+    """phase_only.hpp:39-40 on numpy arrays ([C, H, W]): the loss, and with
+    want_grad also d loss / d theta."""
+    torch = _torch()
+    ctx = ctx or default_context()
+    P, dP = _phase_inputs(P, cfg, ctx)
+    theta = np.ascontiguousarray(theta, dtype=np.float64)
+    if theta.size != P.size:
+        raise HoloError("config", "phase vector does not match the hologram shape")
+    dt = torch.from_numpy(theta.reshape(P.shape)).to(dP.device)
+    g = torch.empty_like(dt) if want_grad else None
+    loss = ctx.phase_only_loss(dP, dt, cfg, opt, g)
+    return (loss, g.cpu().numpy()) if want_grad else loss
+
+
+def convert_phase_only(P, cfg: WaveConfig, iters: int = 1000, lr: float = 0.02,
+                       opt: Optional[PhaseOnlyOptions] = None, ctx: Optional[Context] = None) -> PhaseOnlyResult:
+    """phase_only.hpp:49-50.  The starting phase arg(P) is taken on the host (the
+    reference's std::arg, bit for bit); the iterations run on the GPU."""
+    torch = _torch()
+    ctx = ctx or default_context()
+    P, dP = _phase_inputs(P, cfg, ctx)
+    theta0 = torch.from_numpy(np.ascontiguousarray(np.angle(P))).to(dP.device)
+    out, trace = ctx.convert_phase_only(dP, cfg, iters, lr, opt, theta0)
+    return PhaseOnlyResult(hologram=PhaseOnlyHologram(phase=out.cpu().numpy()), trace=trace)
+
+
+def phase_gradient_oracle(P, theta, cfg: WaveConfig, indices: Optional[Sequence[int]] = None, fd_step: float = 1e-5,
+                          opt: Optional[PhaseOnlyOptions] = None, ctx: Optional[Context] = None) -> np.ndarray:
+    """phase_only.hpp:56-62: central differences of the matching loss at the sampled
+    entries (all when indices is empty), each loss evaluated on the GPU."""
+    torch = _torch()
+    if cfg.num_planes < 1:
+        raise HoloError("config", "oracle needs at least one depth plane")
+    if cfg.nx > 64 or cfg.ny > 64:
+        raise HoloError("config", "oracle is limited to grids up to 64x64")
+    ctx = ctx or default_context()
+    P, dP = _phase_inputs(P, cfg, ctx)
+    theta = np.ascontiguousarray(theta, dtype=np.float64).ravel()
+    if theta.size != P.size:
+        raise HoloError("config", "phase vector does not match the hologram shape")
+    if not fd_step > 0.0:
+        raise HoloError("config", "difference step must be positive")
+    idx = list(range(theta.size)) if not indices else [int(i) for i in indices]
+    g = np.zeros(theta.size)
+    probe = theta.copy()
+    for i in idx:
+        if i < 0 or i >= theta.size:
+            raise HoloError("config", "sampled phase index out of range")
+        vals = []
+        for v in (theta[i] + fd_step, theta[i] - fd_step):
+            probe[i] = v
+            vals.append(ctx.phase_only_loss(dP, torch.from_numpy(probe.reshape(P.shape)).to(dP.device), cfg, opt))
+        probe[i] = theta[i]
+        g[i] = (vals[0] - vals[1]) / (2.0 * fd_step)
+    return g
 
 
 def propagate(u, cfg: WaveConfig, z: float, opt: Optional[PropagationOptions] = None, precision: str = "f64"):

@@ -1546,3 +1546,153 @@ int holo_scene_download(holo_ctx* ctx, const holo_scene_arrays* host) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- phase-only conversion
+
+namespace {
+
+// phase_only.cpp:22-101 on device f64 fields.  The reference stack is replayed
+// once (MatchTargets); each evaluation replays e^{j theta} to every plane from one
+// spectrum, and the gradient pulls all planes back through one summed spectrum
+// (the sum of the per-plane propagate(+z) calls, by linearity, crop included).
+struct PhaseProblem {
+    holo_wave wave{};
+    holo_prop_options po{};
+    int w = 0, h = 0, C = 0, L = 0, pw = 0, ph = 0;
+    bool pad = false;
+    size_t n = 0, gn = 0;
+    std::vector<double> z;
+    cx<double>* tf = nullptr;  // target fields [L][C][h][w]
+    double* timg = nullptr;    // target intensities
+};
+
+PhaseProblem phase_problem(holo_ctx* ctx, const cx<double>* P, const holo_wave& wave, const holo_prop_options& po) {
+    validate_wave(wave);  // cfg.validate (phase_only.cpp:23)
+    PhaseProblem p;
+    p.wave = wave;
+    p.po = po;
+    p.w = wave.nx;
+    p.h = wave.ny;
+    p.C = wave.channels;
+    p.L = wave.num_planes;
+    p.pad = po.pad2x != 0;
+    p.pw = p.pad ? 2 * p.w : p.w;
+    p.ph = p.pad ? 2 * p.h : p.h;
+    p.n = static_cast<size_t>(p.C) * p.w * p.h;
+    p.gn = static_cast<size_t>(p.C) * p.pw * p.ph;
+    p.z = plane_positions(wave);
+    if (p.w < 11 || p.h < 11) config_error("ssim needs images at least 11 pixels in each dimension");
+    if (!all_finite_c128(ctx, P, p.n)) throw Error(HOLO_ERR_NUMERIC, "hologram contains non-finite samples");
+    p.tf = buf<cx<double>>(ctx, "po_tf", p.n * p.L);
+    p.timg = buf<double>(ctx, "po_timg", p.n * p.L);
+    op_inverse_propagate<double>(ctx, P, p.tf, wave, po);  // replay_targets (phase_only.cpp:31-38)
+    intensity<double>(ctx, p.tf, p.timg, p.n * p.L);
+    return p;
+}
+
+// eval_loss (phase_only.cpp:48-101); grad (device, optional) = d loss / d theta
+double phase_eval(holo_ctx* ctx, const PhaseProblem& p, const double* theta, double lambda_ssim, double* grad) {
+    const int w = p.w, h = p.h, C = p.C, L = p.L;
+    cx<double>* cand = buf<cx<double>>(ctx, "po_cand", p.gn);
+    cx<double>* rep = buf<cx<double>>(ctx, "po_rep", p.gn * L);
+    double* img = buf<double>(ctx, "po_img", p.n * L);
+    double* sums = buf<double>(ctx, "po_sums", 2 * static_cast<size_t>(L));
+    phase_field(ctx, theta, cand, w, h, C, p.pad);
+    op_fft2<double>(ctx, cand, p.pw, p.ph, C, false);
+    std::vector<int> plane_of(L);
+    for (int l = 0; l < L; ++l) plane_of[l] = l;
+    replay_from_spectrum<double>(ctx, cand, rep, p.pw, p.ph, C, p.wave, p.z, plane_of, p.po.local_band_limit);
+    phase_match(ctx, rep, p.tf, w, h, C, L, p.pad, img, sums);
+    double* gi = nullptr;
+    if (grad) {
+        gi = buf<double>(ctx, "po_gi", p.n * L);
+        HC_CUDA(cudaMemsetAsync(gi, 0, sizeof(double) * p.n * L, ctx->stream));
+    }
+    if (lambda_ssim != 0.0) ssim_gpu(ctx, img, p.timg, L, C, h, w, lambda_ssim / L, gi, sums + L);
+    std::vector<double> hs(2 * static_cast<size_t>(L), 1.0);
+    HC_CUDA(cudaMemcpyAsync(hs.data(), sums, sizeof(double) * (lambda_ssim != 0.0 ? 2 * L : L),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    const double inv_lm = 1.0 / (static_cast<double>(L) * static_cast<double>(p.n));
+    if (grad) {
+        phase_seed(ctx, rep, p.tf, gi, w, h, C, L, p.pad, inv_lm);
+        spectrum_of_layers<double>(ctx, rep, rep, cand, p.pw, p.ph, C, p.wave, p.z, p.po.local_band_limit);
+        cx<double>* acc = buf<cx<double>>(ctx, "po_acc", p.gn);
+        replay_from_spectrum<double>(ctx, cand, acc, p.pw, p.ph, C, p.wave, p.z, std::vector<int>{-1},
+                                     p.po.local_band_limit);
+        phase_grad(ctx, acc, theta, grad, w, h, C, p.pad);
+    }
+    HC_CUDA(cudaStreamSynchronize(ctx->stream));
+    double field_term = 0.0, ssim_term = 0.0;
+    for (int l = 0; l < L; ++l) field_term += hs[l] * inv_lm;
+    const double scale = lambda_ssim / static_cast<double>(L);  // losses.cpp:98-104
+    for (int l = 0; l < L; ++l) ssim_term += scale * (1.0 - hs[L + l]);
+    return field_term + ssim_term;
+}
+
+}  // namespace
+
+extern "C" {
+
+int holo_phase_only_loss(holo_ctx* ctx, const void* P, const double* theta, const holo_wave* wave,
+                         const holo_phase_options* opt, double* loss, double* grad) {
+    return guarded([&] {
+        require(ctx && P && theta && wave && opt && loss, HOLO_ERR_USAGE, "null argument");
+        HC_CUDA(cudaSetDevice(ctx->device));
+        const PhaseProblem p = phase_problem(ctx, static_cast<const cx<double>*>(P), *wave, opt->prop);
+        *loss = phase_eval(ctx, p, theta, opt->lambda_ssim, grad);
+    });
+}
+
+int holo_convert_phase_only(holo_ctx* ctx, const void* P, const holo_wave* wave, int iters, double lr,
+                            const holo_phase_options* opt, const double* theta0, double* phase_out, double* trace) {
+    return guarded([&] {
+        require(ctx && P && wave && opt && phase_out && trace, HOLO_ERR_USAGE, "null argument");
+        HC_CUDA(cudaSetDevice(ctx->device));
+        const cx<double>* Pd = static_cast<const cx<double>*>(P);
+        validate_wave(*wave);
+        if (iters < 0) config_error("iteration count must be non-negative");  // phase_only.cpp:116-117
+        if (!(lr > 0.0)) config_error("step size must be positive");
+        const PhaseProblem p = phase_problem(ctx, Pd, *wave, opt->prop);
+        const size_t N = p.n;
+        double* theta = buf<double>(ctx, "po_theta", N);
+        if (theta0)
+            HC_CUDA(cudaMemcpyAsync(theta, theta0, sizeof(double) * N, cudaMemcpyDeviceToDevice, ctx->stream));
+        else
+            phase_arg(ctx, Pd, theta, N);  // theta = arg(P) (phase_only.cpp:124-126)
+        double* g = buf<double>(ctx, "po_g", N);
+        double loss = phase_eval(ctx, p, theta, opt->lambda_ssim, iters > 0 ? g : nullptr);
+        trace[0] = loss;
+        if (iters == 0) {
+            HC_CUDA(cudaMemcpyAsync(phase_out, theta, sizeof(double) * N, cudaMemcpyDeviceToDevice, ctx->stream));
+            HC_CUDA(cudaStreamSynchronize(ctx->stream));
+            return;
+        }
+        // OptimizerConfig defaults with use_adam from the options (phase_only.cpp:138-141)
+        const double b1 = 0.9, b2 = 0.99, b3 = 0.99, eps = 1e-8;
+        double* mom = buf<double>(ctx, "po_mom", 4 * N);
+        HC_CUDA(cudaMemsetAsync(mom, 0, sizeof(double) * 4 * N, ctx->stream));
+        double* best = buf<double>(ctx, "po_best", N);
+        HC_CUDA(cudaMemcpyAsync(best, theta, sizeof(double) * N, cudaMemcpyDeviceToDevice, ctx->stream));
+        double best_loss = loss, prev = loss, step_lr = lr;
+        for (int it = 1; it <= iters; ++it) {
+            adaptive_update(ctx, theta, g, mom, mom + N, mom + 2 * N, mom + 3 * N, N, step_lr, it, b1, b2, b3, eps,
+                            opt->use_adam != 0);
+            loss = phase_eval(ctx, p, theta, opt->lambda_ssim, g);
+            trace[it] = loss;
+            if (loss < best_loss) {
+                best_loss = loss;
+                HC_CUDA(cudaMemcpyAsync(best, theta, sizeof(double) * N, cudaMemcpyDeviceToDevice, ctx->stream));
+            }
+            if (loss > prev) {  // backtrack: halve the step, restart from the best iterate
+                step_lr *= 0.5;
+                HC_CUDA(cudaMemcpyAsync(theta, best, sizeof(double) * N, cudaMemcpyDeviceToDevice, ctx->stream));
+                loss = phase_eval(ctx, p, theta, opt->lambda_ssim, g);
+            }
+            prev = loss;
+        }
+        HC_CUDA(cudaMemcpyAsync(phase_out, best, sizeof(double) * N, cudaMemcpyDeviceToDevice, ctx->stream));
+        HC_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+}  // extern "C"

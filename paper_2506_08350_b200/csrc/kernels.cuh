@@ -220,7 +220,25 @@ void sort_small_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsi
 // ---- training step (training.cu): losses, opacity decay, optimizer
 void losses_gpu(holo_ctx* ctx, const double* I, const double* G, const double* masks, int L, int C, int H, int W,
                 bool plain, bool with_ssim, double lambda_ssim, double* grad, double* d_out);
+void ssim_gpu(holo_ctx* ctx, const double* I, const double* G, int L, int C, int H, int W, double gscale,
+              double* grad, double* d_mean);
 double opacity_term(holo_ctx* ctx, const double* logits, size_t n, double lambda, double* gopac);
+
+// ---- phase-only conversion (phase_only.cu), f64 fields; "padded" = the 2w x 2h
+// grid of pad2x with the w x h field centred (propagation.cpp:64-82)
+// e^{j theta} [C][h][w] into the (padded) grid, zeros around it
+void phase_field(holo_ctx* ctx, const double* theta, cx<double>* out, int w, int h, int C, bool pad);
+// per plane: sum |rep - tf|^2 over the crop (deterministic), images = |rep|^2 [L][C][h][w]
+void phase_match(holo_ctx* ctx, const cx<double>* rep, const cx<double>* tf, int w, int h, int C, int L, bool pad,
+                 double* images, double* plane_sums);
+// in place over rep: gv = 2 inv_lm (rep - tf) + 2 rep gi on the crop, 0 around it
+void phase_seed(holo_ctx* ctx, cx<double>* rep, const cx<double>* tf, const double* gi, int w, int h, int C, int L,
+                bool pad, double inv_lm);
+// grad = Im(acc conj(e^{j theta})) over the crop of acc
+void phase_grad(holo_ctx* ctx, const cx<double>* acc, const double* theta, double* grad, int w, int h, int C,
+                bool pad);
+void phase_arg(holo_ctx* ctx, const cx<double>* P, double* theta, size_t n);
+bool all_finite_c128(holo_ctx* ctx, const cx<double>* P, size_t n);
 void f32_to_f64(holo_ctx* ctx, const float* in, double* out, size_t n);
 void f64_to_f32(holo_ctx* ctx, const double* in, float* out, size_t n);
 bool grads_finite(holo_ctx* ctx, const double* const* g, const size_t* n, int groups);

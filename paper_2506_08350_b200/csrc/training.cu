@@ -402,11 +402,7 @@ unsigned blocks_for(size_t n, unsigned cap = 8192) {
 // (masks [L][H][W]); grad (optional) is overwritten with dL/dI.
 // d_out[0] = recon, d_out[1 + l] = mean SSIM of plane l, d_out[1 + L + l] =
 // the mse of plane l; the host finishes the scalar algebra.
-void losses_gpu(holo_ctx* ctx, const double* I, const double* G, const double* masks, int L, int C, int H, int W,
-                bool plain, bool with_ssim, double lambda_ssim, double* grad, double* d_out) {
-    const size_t n = static_cast<size_t>(C) * H * W;
-    if (with_ssim && (W < kWin || H < kWin))
-        throw Error(HOLO_ERR_CONFIG, "ssim needs images at least 11 pixels in each dimension");
+void ssim_setup() {
     static bool win_set = false;
     if (!win_set) {  // ssim.cpp:16-26
         double w[kWin], sum = 0.0;
@@ -425,6 +421,14 @@ void losses_gpu(holo_ctx* ctx, const double* I, const double* G, const double* m
                                      static_cast<int>(kSsimBwdSmem)));
         win_set = true;
     }
+}
+
+void losses_gpu(holo_ctx* ctx, const double* I, const double* G, const double* masks, int L, int C, int H, int W,
+                bool plain, bool with_ssim, double lambda_ssim, double* grad, double* d_out) {
+    const size_t n = static_cast<size_t>(C) * H * W;
+    if (with_ssim && (W < kWin || H < kWin))
+        throw Error(HOLO_ERR_CONFIG, "ssim needs images at least 11 pixels in each dimension");
+    ssim_setup();
     const long long rows_n = static_cast<long long>(L) * C * H;
     double* rows = static_cast<double*>(ctx->buffer("loss_rows", sizeof(double) * 2 * rows_n));
     double* prow = rows + rows_n;
@@ -454,7 +458,17 @@ void losses_gpu(holo_ctx* ctx, const double* I, const double* G, const double* m
         HC_LAUNCHED(ctx);
         return;
     }
-    // ssim (losses.cpp:96-111, ssim.cpp:64-147): lambda / L (1 - mean SSIM) per plane
+    ssim_gpu(ctx, I, G, L, C, H, W, lambda_ssim / static_cast<double>(L), grad, d_out + 1);
+}
+
+// mean SSIM per plane (ssim_mean, ssim.cpp:64-147) of stacks [L][C][H][W] into
+// d_mean[L]; with grad, grad -= gscale * d(mean SSIM_l)/dI_l (loss_ssim's
+// accumulation, losses.cpp:104-108)
+void ssim_gpu(holo_ctx* ctx, const double* I, const double* G, int L, int C, int H, int W, double gscale,
+              double* grad, double* d_mean) {
+    if (W < kWin || H < kWin) throw Error(HOLO_ERR_CONFIG, "ssim needs images at least 11 pixels in each dimension");
+    ssim_setup();
+    const size_t n = static_cast<size_t>(C) * H * W;
     const int vrows = H - 2 * kHalf;
     const size_t n_valid = static_cast<size_t>(W - 2 * kHalf) * vrows * C;
     double* smap = static_cast<double*>(ctx->buffer("ssim_map", sizeof(double) * L * n));
@@ -467,7 +481,7 @@ void losses_gpu(holo_ctx* ctx, const double* I, const double* G, const double* m
             HC_LAUNCHED(ctx);
             k_ssim_bwd<<<tg, 256, kSsimBwdSmem, ctx->stream>>>(gmaps, n, I + off, G + off, W, H,
                                                               1.0 / static_cast<double>(n_valid),
-                                                              lambda_ssim / static_cast<double>(L), grad + off);
+                                                              gscale, grad + off);
             HC_LAUNCHED(ctx);
         } else {
             k_ssim_fwd<false><<<tg, 256, kSsimFwdSmem, ctx->stream>>>(I + off, G + off, W, H, smap + off, nullptr, 0);
@@ -483,7 +497,7 @@ void losses_gpu(holo_ctx* ctx, const double* I, const double* G, const double* m
     // per (plane, channel) the rows in order; per plane the channels in order, / n_valid
     k_fold_seg<<<(L * C + 3) / 4, 128, 0, ctx->stream>>>(srows, L * C, vrows, 1.0, 1.0, ssum);
     HC_LAUNCHED(ctx);
-    k_fold_seg<<<lb, 128, 0, ctx->stream>>>(ssum, L, C, 1.0, static_cast<double>(n_valid), d_out + 1);
+    k_fold_seg<<<(L + 3) / 4, 128, 0, ctx->stream>>>(ssum, L, C, 1.0, static_cast<double>(n_valid), d_mean);
     HC_LAUNCHED(ctx);
 }
 

@@ -218,6 +218,33 @@ class OptimizerConfig:
     lr_floor: float = 1e-5
 
 
+def _pad_default():
+    return PropagationOptions(pad2x=True)
+
+
+@dataclass
+class PhaseOnlyOptions:
+    """phase_only.hpp:22-32 (conversion propagates padded by default)."""
+    lambda_ssim: float = 1.0
+    prop: PropagationOptions = field(default_factory=_pad_default)
+    use_adam: bool = False
+
+
+@dataclass
+class PhaseOnlyHologram:
+    """phase_only.hpp:13-19: unit-amplitude hologram e^{j phase}, phase [C, H, W]."""
+    phase: np.ndarray
+
+    def field(self, pitch: float = 3.74e-6) -> np.ndarray:
+        return np.exp(1j * self.phase) if self.phase.size else self.phase.astype(np.complex128)
+
+
+@dataclass
+class PhaseOnlyResult:
+    hologram: PhaseOnlyHologram
+    trace: List[float]
+
+
 @dataclass
 class RasterForward:
     layers: List[np.ndarray]          # L x [C, H, W] complex
