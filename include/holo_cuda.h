@@ -281,6 +281,12 @@ int holo_total_loss(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave
                     const holo_prop_options* prop, const holo_loss_options* opt, const double* targets,
                     const double* masks, holo_loss_breakdown* out, double* psnr, holo_scene_grads* grads);
 
+/* ssim_mean (ssim.cpp:64-147) of every plane of device f64 stacks [L][C][H][W]:
+ * mean_ssim (host, [L]); grad (device, optional) = d(mean SSIM_l)/dx_l, overwritten.
+ * Bit-equal to the reference's ssim_mean on the same inputs. */
+int holo_ssim(holo_ctx* ctx, const double* x, const double* y, int L, int C, int H, int W, double* mean_ssim,
+              double* grad);
+
 /* OptimizerConfig (optimizer.hpp:17-31). */
 typedef struct {
     double lr_positions, lr_rotations, lr_log_scales, lr_amplitudes, lr_phases, lr_opacities, lr_plane_logits;
@@ -300,6 +306,12 @@ int holo_optim_destroy(holo_optim* st);
 int holo_optim_step(holo_ctx* ctx, holo_optim* st, const holo_scene_grads* grads, const holo_optimizer_config* cfg,
                     int* applied);
 int holo_optim_counts(const holo_optim* st, long long* step, long long* skipped);
+/* adaptive_moment_update (optimizer.cpp:70-100) on one flat group of device f64
+ * arrays (params, grads, moments m / v / n / prev_grad); step counts from 1.
+ * optimizer_step = this per group + the cosine schedule + renormalize. */
+int holo_adaptive_update(holo_ctx* ctx, double* params, const double* grads, double* m, double* v, double* n,
+                         double* prev_grad, size_t count, double lr, long long step,
+                         const holo_optimizer_config* cfg);
 
 /* Copies the resident scene to host arrays (the members are written despite the
  * const qualifiers of holo_scene_arrays; n and num_planes must match). */

@@ -20,11 +20,15 @@
 #include "holo/fft.hpp"
 #include "holo/field.hpp"
 #include "holo/field_io.hpp"
+#include "holo/losses.hpp"
+#include "holo/optimizer.hpp"
+#include "holo/phase_only.hpp"
 #include "holo/pipeline.hpp"
 #include "holo/propagation.hpp"
 #include "holo/rasterizer.hpp"
 #include "holo/scene.hpp"
 #include "holo/scene_io.hpp"
+#include "holo/ssim.hpp"
 #include "holo/wave_config.hpp"
 #include "holo_cuda.h"
 
@@ -787,6 +791,438 @@ GaussianScene read_scene(const std::string& path) {
     }
     s.validate();
     return s;
+}
+
+// ------------------------------------------------------------------ losses (losses.cpp, ssim.cpp)
+
+namespace {
+
+void check_stack(const std::vector<IntensityImage>& I, const std::vector<IntensityImage>& I_gt) {  // losses.cpp:11-17
+    if (I.size() != I_gt.size() || I.empty()) throw HoloError("config", "focal stacks have different plane counts");
+    for (size_t l = 0; l < I.size(); ++l)
+        if (I[l].w != I_gt[l].w || I[l].h != I_gt[l].h || I[l].c != I_gt[l].c)
+            throw HoloError("config", "focal stack image shapes differ");
+    // one batched device call: the planes of a stack share one shape (they always
+    // do in the reference's pipeline; mixed shapes are rejected here)
+    for (size_t l = 1; l < I.size(); ++l)
+        if (I[l].w != I[0].w || I[l].h != I[0].h || I[l].c != I[0].c)
+            throw HoloError("config", "focal stack planes must share one image shape");
+}
+
+void check_grad(const std::vector<IntensityImage>& I, std::vector<IntensityImage>* grad) {
+    if (!grad) return;
+    if (grad->size() != I.size()) throw HoloError("config", "loss gradient stack has the wrong plane count");
+    for (size_t l = 0; l < I.size(); ++l)
+        if ((*grad)[l].data.size() != I[l].data.size()) throw HoloError("config", "loss gradient image shapes differ");
+}
+
+// a stack of equal-shape images as one device f64 array [L][C][H][W]
+std::unique_ptr<DevMem> upload_stack(const std::vector<IntensityImage>& v) {
+    size_t n = 0;
+    for (const IntensityImage& im : v) n += im.data.size();
+    auto d = std::make_unique<DevMem>(sizeof(double) * n);
+    size_t off = 0;
+    for (const IntensityImage& im : v) {
+        h2d(static_cast<double*>(d->p) + off, im.data.data(), sizeof(double) * im.data.size());
+        off += im.data.size();
+    }
+    return d;
+}
+
+void accumulate(std::vector<IntensityImage>* grad, const std::vector<double>& g, double sign = 1.0) {
+    size_t off = 0;
+    for (IntensityImage& im : *grad) {
+        for (size_t i = 0; i < im.data.size(); ++i) im.data[i] += sign * g[off + i];
+        off += im.data.size();
+    }
+}
+
+// the pointwise terms through holo_losses (SSIM left out): value, psnr per plane
+double pointwise_loss(const std::vector<IntensityImage>& I, const std::vector<IntensityImage>& I_gt,
+                      const std::vector<IntensityImage>* masks, std::vector<IntensityImage>* grad,
+                      std::vector<double>* psnr_out) {
+    const int L = static_cast<int>(I.size()), C = I[0].c, H = I[0].h, W = I[0].w;
+    const auto dI = upload_stack(I), dG = upload_stack(I_gt);
+    std::unique_ptr<DevMem> dM;
+    if (masks) dM = upload_stack(*masks);
+    const size_t n = static_cast<size_t>(L) * C * H * W;
+    std::unique_ptr<DevMem> dg;
+    if (grad) dg = std::make_unique<DevMem>(sizeof(double) * n);
+    const holo_loss_options lo{0.0, 0.0, masks ? 0 : 1};
+    holo_loss_breakdown b{};
+    std::vector<double> ps(L);
+    check(holo_losses(ctx(), static_cast<const double*>(dI->p), static_cast<const double*>(dG->p),
+                      dM ? static_cast<const double*>(dM->p) : nullptr, L, C, H, W, &lo, &b, ps.data(),
+                      dg ? static_cast<double*>(dg->p) : nullptr));
+    if (grad) {
+        std::vector<double> g(n);
+        d2h(g.data(), dg->p, sizeof(double) * n);
+        accumulate(grad, g);
+    }
+    if (psnr_out) *psnr_out = ps;
+    return b.recon;
+}
+
+// mean SSIM per plane of equal-shape stacks, and d(mean SSIM_l)/dx_l when asked
+std::vector<double> ssim_planes(const std::vector<IntensityImage>& x, const std::vector<IntensityImage>& y,
+                                std::vector<double>* grad) {
+    const int L = static_cast<int>(x.size()), C = x[0].c, H = x[0].h, W = x[0].w;
+    const auto dx = upload_stack(x), dy = upload_stack(y);
+    const size_t n = static_cast<size_t>(L) * C * H * W;
+    std::unique_ptr<DevMem> dg;
+    if (grad) dg = std::make_unique<DevMem>(sizeof(double) * n);
+    std::vector<double> s(L);
+    check(holo_ssim(ctx(), static_cast<const double*>(dx->p), static_cast<const double*>(dy->p), L, C, H, W, s.data(),
+                    dg ? static_cast<double*>(dg->p) : nullptr));
+    if (grad) {
+        grad->resize(n);
+        d2h(grad->data(), dg->p, sizeof(double) * n);
+    }
+    return s;
+}
+
+}  // namespace
+
+double loss_mse(const std::vector<IntensityImage>& I, const std::vector<IntensityImage>& I_gt,
+                std::vector<IntensityImage>* grad) {
+    check_stack(I, I_gt);
+    check_grad(I, grad);
+    return pointwise_loss(I, I_gt, nullptr, grad, nullptr);
+}
+
+double loss_recon(const std::vector<IntensityImage>& I, const std::vector<IntensityImage>& I_gt,
+                  const std::vector<IntensityImage>& masks, std::vector<IntensityImage>* grad) {
+    check_stack(I, I_gt);
+    check_grad(I, grad);
+    if (masks.size() != I.size()) throw HoloError("config", "mask stack has the wrong plane count");
+    for (size_t l = 0; l < I.size(); ++l)
+        if (masks[l].w != I[l].w || masks[l].h != I[l].h || masks[l].c != 1)
+            throw HoloError("config", "masks must be single-channel and match the image size");
+    return pointwise_loss(I, I_gt, &masks, grad, nullptr);
+}
+
+double loss_ssim(const std::vector<IntensityImage>& I, const std::vector<IntensityImage>& I_gt, double lambda,
+                 std::vector<IntensityImage>* grad) {
+    check_stack(I, I_gt);
+    check_grad(I, grad);
+    std::vector<double> gs;
+    const std::vector<double> s = ssim_planes(I, I_gt, grad ? &gs : nullptr);
+    const double scale = lambda / static_cast<double>(I.size());  // losses.cpp:98-110
+    double total = 0.0;
+    for (size_t l = 0; l < I.size(); ++l) total += scale * (1.0 - s[l]);
+    if (grad) {
+        size_t off = 0;
+        for (IntensityImage& im : *grad) {
+            for (size_t i = 0; i < im.data.size(); ++i) im.data[i] -= scale * gs[off + i];
+            off += im.data.size();
+        }
+    }
+    return total;
+}
+
+double psnr(const IntensityImage& I, const IntensityImage& I_gt) {
+    if (I.w != I_gt.w || I.h != I_gt.h || I.c != I_gt.c) throw HoloError("config", "psnr: image shapes differ");
+    std::vector<double> ps;
+    pointwise_loss({I}, {I_gt}, nullptr, nullptr, &ps);
+    return ps[0];
+}
+
+double ssim_mean(const IntensityImage& x, const IntensityImage& y, IntensityImage* grad_x) {
+    if (x.w != y.w || x.h != y.h || x.c != y.c) throw HoloError("config", "ssim: image shapes differ");
+    if (x.w < 11 || x.h < 11) throw HoloError("config", "ssim needs images at least 11 pixels in each dimension");
+    std::vector<double> g;
+    const std::vector<double> s = ssim_planes({x}, {y}, grad_x ? &g : nullptr);
+    if (grad_x) {
+        *grad_x = IntensityImage(x.w, x.h, x.c);
+        grad_x->data = std::move(g);
+    }
+    return s[0];
+}
+
+// ------------------------------------------------------------------ total_loss, targets (pipeline.cpp:9-127)
+
+void FocalStackTarget::validate(const WaveConfig& cfg) const {
+    if (images.size() != static_cast<size_t>(cfg.num_planes) || masks.size() != images.size())
+        throw HoloError("config", "target plane count does not match the wave config");
+    for (size_t l = 0; l < images.size(); ++l) {
+        if (images[l].w != cfg.nx || images[l].h != cfg.ny || images[l].c != cfg.channels())
+            throw HoloError("config", "target image shape does not match the grid");
+        if (masks[l].w != cfg.nx || masks[l].h != cfg.ny || masks[l].c != 1)
+            throw HoloError("config", "target masks must be single-channel at grid size");
+    }
+}
+
+LossBreakdown total_loss(const GaussianScene& scene, const CameraView& cam, const WaveConfig& cfg,
+                         const FocalStackTarget& target, const PipelineOptions& opt, SceneGradients* grads,
+                         PipelineForward* fwd_out) {
+    target.validate(cfg);
+    check_raster_inputs(scene, cam, cfg);
+    if (cfg.channels() != GaussianScene::kChannels)
+        throw HoloError("config", "propagate: field does not match the configured grid");
+    const holo_scene_arrays sa = scene_arrays(scene);
+    check(holo_scene_upload(ctx(), &sa));
+    const auto dT = upload_stack(target.images), dM = upload_stack(target.masks);
+    const holo_wave w = to_c(cfg);
+    const holo_camera c = to_c(cam);
+    const holo_raster_settings st = to_c(opt.raster);
+    const holo_prop_options po = to_c(opt.prop);
+    const holo_loss_options lo{opt.lambda_ssim, opt.lambda_opacity, opt.use_plain_mse ? 1 : 0};
+    LossBreakdown out;
+    out.psnr.assign(cfg.num_planes, 0.0);
+    holo_loss_breakdown b{};
+    std::vector<std::unique_ptr<DevMem>> dm;
+    holo_scene_grads hg{};
+    std::vector<std::vector<double>*> vs;
+    if (grads) {
+        grads->resize_like(scene);
+        vs = {&grads->positions, &grads->rotations, &grads->log_scales, &grads->amplitudes,
+              &grads->opacity_logits, &grads->phases, &grads->plane_logits, &grads->mu_screen};
+        double** slots[8] = {&hg.positions, &hg.rotations, &hg.log_scales, &hg.amplitudes,
+                             &hg.opacity_logits, &hg.phases, &hg.plane_logits, &hg.mu_screen};
+        for (int k = 0; k < 8; ++k) {
+            dm.push_back(std::make_unique<DevMem>(sizeof(double) * vs[k]->size()));
+            *slots[k] = static_cast<double*>(dm[k]->p);
+        }
+    }
+    check(holo_total_loss(ctx(), &c, &w, &st, &po, &lo, static_cast<const double*>(dT->p),
+                          static_cast<const double*>(dM->p), &b, out.psnr.data(), grads ? &hg : nullptr));
+    out.total = b.total;
+    out.recon = b.recon;
+    out.ssim = b.ssim;
+    out.opacity = b.opacity;
+    out.psnr_mean = b.psnr_mean;
+    for (size_t k = 0; k < vs.size(); ++k) d2h(vs[k]->data(), dm[k]->p, sizeof(double) * vs[k]->size());
+    if (fwd_out) *fwd_out = pipeline_forward(scene, cam, cfg, opt);
+    return out;
+}
+
+FocalStackTarget make_target_from_scene(const GaussianScene& oracle, const CameraView& cam, const WaveConfig& cfg,
+                                        const PipelineOptions& opt) {
+    PipelineForward f = pipeline_forward(oracle, cam, cfg, opt);
+    FocalStackTarget t;
+    t.camera = cam;
+    t.images = std::move(f.intensities);
+    const int L = cfg.num_planes;
+    t.masks.assign(L, IntensityImage(cfg.nx, cfg.ny, 1));
+    // the plane whose rasterised amplitude dominates (pipeline.cpp:106-124)
+    for (int y = 0; y < cfg.ny; ++y)
+        for (int x = 0; x < cfg.nx; ++x) {
+            int best = -1;
+            double best_amp = 0.0;
+            for (int l = 0; l < L; ++l) {
+                double amp = 0.0;
+                for (int ch = 0; ch < f.raster.layers[l].c; ++ch) amp += std::abs(f.raster.layers[l].at(ch, y, x));
+                if (amp > best_amp) {
+                    best_amp = amp;
+                    best = l;
+                }
+            }
+            if (best >= 0) t.masks[best].at(0, y, x) = 1.0;
+        }
+    return t;
+}
+
+// ------------------------------------------------------------------ optimizer (optimizer.cpp)
+
+double cosine_lr(double base, double floor, long long t, long long total) {
+    if (total <= 0 || t >= total) return floor;
+    const double phase = kPi * static_cast<double>(t) / static_cast<double>(total);
+    return floor + 0.5 * (base - floor) * (1.0 + std::cos(phase));
+}
+
+void OptimState::Moments::resize(size_t count) {
+    m.assign(count, 0.0);
+    v.assign(count, 0.0);
+    n.assign(count, 0.0);
+    prev_grad.assign(count, 0.0);
+}
+
+void OptimState::Moments::remap_rows(const std::vector<int>& src_index, size_t stride) {
+    std::vector<double>* arrs[4] = {&m, &v, &n, &prev_grad};
+    for (std::vector<double>* a : arrs) {
+        std::vector<double> out(src_index.size() * stride, 0.0);
+        for (size_t j = 0; j < src_index.size(); ++j) {
+            const int src = src_index[j];
+            if (src < 0) continue;
+            std::copy_n(a->begin() + static_cast<std::ptrdiff_t>(src * stride), stride,
+                        out.begin() + static_cast<std::ptrdiff_t>(j * stride));
+        }
+        a->swap(out);
+    }
+}
+
+void OptimState::resize_like(const GaussianScene& s) {
+    positions.resize(s.positions.size());
+    rotations.resize(s.rotations.size());
+    log_scales.resize(s.log_scales.size());
+    amplitudes.resize(s.amplitudes.size());
+    opacities.resize(s.opacity_logits.size());
+    phases.resize(s.phases.size());
+    plane_logits.resize(s.plane_logits.size());
+}
+
+void OptimState::remap(const std::vector<int>& src_index, const GaussianScene& new_scene) {
+    positions.remap_rows(src_index, 3);
+    rotations.remap_rows(src_index, 4);
+    log_scales.remap_rows(src_index, 3);
+    amplitudes.remap_rows(src_index, 3);
+    opacities.remap_rows(src_index, 1);
+    phases.remap_rows(src_index, 3);
+    plane_logits.remap_rows(src_index, static_cast<size_t>(new_scene.num_planes));
+}
+
+void adaptive_moment_update(std::vector<double>& params, const std::vector<double>& grads, OptimState::Moments& mom,
+                            double lr, long long step, const OptimizerConfig& cfg) {
+    const size_t n = params.size();
+    if (grads.size() != n || mom.m.size() != n || mom.v.size() != n || mom.n.size() != n || mom.prev_grad.size() != n)
+        throw HoloError("config", "optimizer: gradient or moment sizes do not match the parameters");
+    if (n == 0) return;
+    // six f64 arrays through one device call (holo_adaptive_update)
+    DevMem d(sizeof(double) * 6 * n);
+    double* p = static_cast<double*>(d.p);
+    const std::vector<double>* src[6] = {&params, &grads, &mom.m, &mom.v, &mom.n, &mom.prev_grad};
+    for (int k = 0; k < 6; ++k) h2d(p + k * n, src[k]->data(), sizeof(double) * n);
+    const holo_optimizer_config c{cfg.lr_positions, cfg.lr_rotations, cfg.lr_log_scales, cfg.lr_amplitudes,
+                                  cfg.lr_phases,    cfg.lr_opacities, cfg.lr_plane_logits, cfg.beta1,
+                                  cfg.beta2,        cfg.beta3,        cfg.eps,             cfg.use_adam ? 1 : 0,
+                                  cfg.schedule_total, cfg.lr_floor};
+    check(holo_adaptive_update(ctx(), p, p + n, p + 2 * n, p + 3 * n, p + 4 * n, p + 5 * n, n, lr, step, &c));
+    std::vector<double>* dst[6] = {&params, nullptr, &mom.m, &mom.v, &mom.n, &mom.prev_grad};
+    for (int k = 0; k < 6; ++k)
+        if (dst[k]) d2h(dst[k]->data(), p + k * n, sizeof(double) * n);
+}
+
+bool optimizer_step(OptimState& st, GaussianScene& scene, const SceneGradients& grads, const OptimizerConfig& cfg) {
+    if (grads.positions.size() != scene.positions.size() || grads.plane_logits.size() != scene.plane_logits.size())
+        throw HoloError("config", "optimizer: gradient shapes do not match the scene");
+    if (st.positions.m.size() != scene.positions.size())
+        throw HoloError("config", "optimizer: moment buffers do not match the scene");
+    for (const std::vector<double>* g : {&grads.positions, &grads.rotations, &grads.log_scales, &grads.amplitudes,
+                                         &grads.opacity_logits, &grads.phases, &grads.plane_logits})
+        for (double x : *g)
+            if (!std::isfinite(x)) {
+                ++st.skipped;
+                return false;
+            }
+    const long long t = st.step;
+    ++st.step;
+    const double lr_pos = cosine_lr(cfg.lr_positions, cfg.lr_floor, t, cfg.schedule_total);
+    const double lr_rho = cosine_lr(cfg.lr_plane_logits, cfg.lr_floor, t, cfg.schedule_total);
+    adaptive_moment_update(scene.positions, grads.positions, st.positions, lr_pos, st.step, cfg);
+    adaptive_moment_update(scene.rotations, grads.rotations, st.rotations, cfg.lr_rotations, st.step, cfg);
+    adaptive_moment_update(scene.log_scales, grads.log_scales, st.log_scales, cfg.lr_log_scales, st.step, cfg);
+    adaptive_moment_update(scene.amplitudes, grads.amplitudes, st.amplitudes, cfg.lr_amplitudes, st.step, cfg);
+    adaptive_moment_update(scene.opacity_logits, grads.opacity_logits, st.opacities, cfg.lr_opacities, st.step, cfg);
+    adaptive_moment_update(scene.phases, grads.phases, st.phases, cfg.lr_phases, st.step, cfg);
+    adaptive_moment_update(scene.plane_logits, grads.plane_logits, st.plane_logits, lr_rho, st.step, cfg);
+    scene.renormalize();
+    return true;
+}
+
+// ------------------------------------------------------------------ phase-only conversion (phase_only.cpp)
+
+ComplexField PhaseOnlyHologram::field(double pitch) const {
+    ComplexField f(w, h, c, pitch);
+    for (size_t i = 0; i < phase.size(); ++i) f.data[i] = std::polar(1.0, phase[i]);
+    return f;
+}
+
+namespace {
+
+void check_phase_input(const ComplexField& P, const WaveConfig& cfg) {  // phase_only.cpp:22-29
+    cfg.validate();
+    if (P.w != cfg.nx || P.h != cfg.ny || P.c != cfg.channels())
+        throw HoloError("config", "hologram shape does not match the wave config");
+    for (const c64& v : P.data)
+        if (!std::isfinite(v.real()) || !std::isfinite(v.imag()))
+            throw HoloError("numeric", "hologram contains non-finite samples");
+}
+
+holo_phase_options to_c(const PhaseOnlyOptions& o) { return {o.lambda_ssim, to_c(o.prop), o.use_adam ? 1 : 0}; }
+
+std::unique_ptr<DevMem> upload_c128(const ComplexField& P) {
+    auto d = std::make_unique<DevMem>(sizeof(c64) * P.data.size());
+    h2d(d->p, P.data.data(), sizeof(c64) * P.data.size());
+    return d;
+}
+
+double phase_loss_dev(const DevMem& dP, const std::vector<double>& theta, const WaveConfig& cfg,
+                      const PhaseOnlyOptions& opt, std::vector<double>* grad) {
+    DevMem dt(sizeof(double) * theta.size());
+    h2d(dt.p, theta.data(), sizeof(double) * theta.size());
+    std::unique_ptr<DevMem> dg;
+    if (grad) dg = std::make_unique<DevMem>(sizeof(double) * theta.size());
+    const holo_wave w = to_c(cfg);
+    const holo_phase_options po = to_c(opt);
+    double loss = 0.0;
+    check(holo_phase_only_loss(ctx(), dP.p, static_cast<const double*>(dt.p), &w, &po, &loss,
+                               dg ? static_cast<double*>(dg->p) : nullptr));
+    if (grad) {
+        grad->resize(theta.size());
+        d2h(grad->data(), dg->p, sizeof(double) * theta.size());
+    }
+    return loss;
+}
+
+}  // namespace
+
+double phase_only_loss(const ComplexField& P, const std::vector<double>& theta, const WaveConfig& cfg,
+                       const PhaseOnlyOptions& opt, std::vector<double>* grad) {
+    check_phase_input(P, cfg);
+    if (theta.size() != P.data.size()) throw HoloError("config", "phase vector does not match the hologram shape");
+    const auto dP = upload_c128(P);
+    return phase_loss_dev(*dP, theta, cfg, opt, grad);
+}
+
+PhaseOnlyResult convert_phase_only(const ComplexField& P, const WaveConfig& cfg, int iters, double lr,
+                                   const PhaseOnlyOptions& opt) {
+    check_phase_input(P, cfg);
+    if (iters < 0) throw HoloError("config", "iteration count must be non-negative");
+    if (lr <= 0.0) throw HoloError("config", "step size must be positive");
+    PhaseOnlyResult out;
+    out.hologram.w = P.w;
+    out.hologram.h = P.h;
+    out.hologram.c = P.c;
+    std::vector<double> theta(P.data.size());
+    for (size_t i = 0; i < theta.size(); ++i) theta[i] = std::arg(P.data[i]);  // the reference's extraction
+    const auto dP = upload_c128(P);
+    DevMem dt(sizeof(double) * theta.size()), dphase(sizeof(double) * theta.size());
+    h2d(dt.p, theta.data(), sizeof(double) * theta.size());
+    const holo_wave w = to_c(cfg);
+    const holo_phase_options po = to_c(opt);
+    out.trace.assign(static_cast<size_t>(iters) + 1, 0.0);
+    check(holo_convert_phase_only(ctx(), dP->p, &w, iters, lr, &po, static_cast<const double*>(dt.p),
+                                  static_cast<double*>(dphase.p), out.trace.data()));
+    out.hologram.phase.resize(theta.size());
+    d2h(out.hologram.phase.data(), dphase.p, sizeof(double) * theta.size());
+    return out;
+}
+
+std::vector<double> phase_gradient_oracle(const ComplexField& P, const std::vector<double>& theta,
+                                          const WaveConfig& cfg, const std::vector<size_t>& indices, double fd_step,
+                                          const PhaseOnlyOptions& opt) {
+    if (cfg.num_planes < 1) throw HoloError("config", "oracle needs at least one depth plane");
+    if (cfg.nx > 64 || cfg.ny > 64) throw HoloError("config", "oracle is limited to grids up to 64x64");
+    check_phase_input(P, cfg);
+    if (theta.size() != P.data.size()) throw HoloError("config", "phase vector does not match the hologram shape");
+    if (fd_step <= 0.0) throw HoloError("config", "difference step must be positive");
+    std::vector<size_t> idx = indices;
+    if (idx.empty()) {
+        idx.resize(theta.size());
+        for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
+    }
+    const auto dP = upload_c128(P);
+    std::vector<double> g(theta.size(), 0.0), probe = theta;
+    for (size_t i : idx) {
+        if (i >= theta.size()) throw HoloError("config", "sampled phase index out of range");
+        probe[i] = theta[i] + fd_step;
+        const double up = phase_loss_dev(*dP, probe, cfg, opt, nullptr);
+        probe[i] = theta[i] - fd_step;
+        const double dn = phase_loss_dev(*dP, probe, cfg, opt, nullptr);
+        probe[i] = theta[i];
+        g[i] = (up - dn) / (2.0 * fd_step);
+    }
+    return g;
 }
 
 }  // namespace holo

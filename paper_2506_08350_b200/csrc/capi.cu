@@ -1452,6 +1452,34 @@ int holo_total_loss(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave
     });
 }
 
+int holo_ssim(holo_ctx* ctx, const double* x, const double* y, int L, int C, int H, int W, double* mean_ssim,
+              double* grad) {
+    return guarded([&] {
+        require(ctx && x && y && mean_ssim, HOLO_ERR_USAGE, "null argument");
+        require(L >= 1 && C >= 1 && H >= 1 && W >= 1, HOLO_ERR_CONFIG, "image shape must be positive");
+        HC_CUDA(cudaSetDevice(ctx->device));
+        const size_t n = static_cast<size_t>(L) * C * H * W;
+        if (grad) HC_CUDA(cudaMemsetAsync(grad, 0, sizeof(double) * n, ctx->stream));
+        double* d_mean = buf<double>(ctx, "ssim_mean_out", static_cast<size_t>(L));
+        ssim_gpu(ctx, x, y, L, C, H, W, -1.0, grad, d_mean);  // grad = 0 - (-1) g = g exactly
+        HC_CUDA(cudaMemcpyAsync(mean_ssim, d_mean, sizeof(double) * L, cudaMemcpyDeviceToHost, ctx->stream));
+        HC_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int holo_adaptive_update(holo_ctx* ctx, double* params, const double* grads, double* m, double* v, double* n,
+                         double* prev_grad, size_t count, double lr, long long step,
+                         const holo_optimizer_config* cfg) {
+    return guarded([&] {
+        require(ctx && cfg, HOLO_ERR_USAGE, "null argument");
+        require(count == 0 || (params && grads && m && v && n && prev_grad), HOLO_ERR_USAGE, "null array");
+        require(step >= 1, HOLO_ERR_USAGE, "step counts from 1");
+        HC_CUDA(cudaSetDevice(ctx->device));
+        adaptive_update(ctx, params, grads, m, v, n, prev_grad, count, lr, step, cfg->beta1, cfg->beta2, cfg->beta3,
+                        cfg->eps, cfg->use_adam != 0);
+    });
+}
+
 int holo_optim_create(holo_ctx* ctx, holo_optim** out) {
     return guarded([&] {
         require(ctx && out, HOLO_ERR_USAGE, "null argument");

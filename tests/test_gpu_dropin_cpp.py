@@ -2,8 +2,10 @@
 
 GPU: runs tests/cpp/test_dropin.cpp and -- compiled against the drop-in headers
 by paper_2506_08350_b200/cpp/Makefile where /root/reference exists -- the
-reference's OWN unit tests test_field.cpp and test_propagation.cpp, unmodified,
-at the reference's tolerances (f64 operators on the GPU).
+reference's OWN unit tests test_field.cpp, test_propagation.cpp,
+test_losses.cpp, test_optimizer.cpp and test_phase_only.cpp, unmodified, at the
+reference's tolerances (f64 operators, losses, optimizer and phase-only
+conversion on the GPU).
 CPU: libholo.so exports the reference API symbols."""
 import os
 import subprocess
@@ -21,12 +23,16 @@ def test_libholo_exports_reference_api():
     syms = subprocess.run(["nm", "-DC", "--defined-only", so], capture_output=True, text=True).stdout
     for name in ("holo::pipeline_forward(", "holo::raster_forward(", "holo::propagate(", "holo::forward_record(",
                  "holo::inverse_propagate(", "holo::transfer_function(", "holo::fft2(", "holo::ifft2(",
-                 "holo::intensity(", "holo::plane_positions(", "holo::read_field(", "holo::write_field("):
+                 "holo::intensity(", "holo::plane_positions(", "holo::read_field(", "holo::write_field(",
+                 "holo::total_loss(", "holo::loss_recon(", "holo::loss_ssim(", "holo::ssim_mean(", "holo::psnr(",
+                 "holo::optimizer_step(", "holo::convert_phase_only(", "holo::phase_only_loss(",
+                 "holo::make_target_from_scene("):
         assert name in syms, name
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("binary", ["test_dropin", "ref_test_field", "ref_test_propagation"])
+@pytest.mark.parametrize("binary", ["test_dropin", "ref_test_field", "ref_test_propagation", "ref_test_losses",
+                                    "ref_test_optimizer", "ref_test_phase_only"])
 def test_cpp_suite(binary, tmp_path):
     path = os.path.join(LIB, binary)
     if not os.path.exists(path):
