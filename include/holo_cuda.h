@@ -275,8 +275,10 @@ int holo_losses(holo_ctx* ctx, const double* intensities, const double* targets,
 /* total_loss (pipeline.cpp:30-95) on the context's resident scene: render
  * (pipeline_forward), losses against targets / masks (device f64 as above), and
  * with grads != NULL the full gradient (holo_pipeline_backward + the opacity decay
- * term, pipeline.cpp:82-88).  The frame's outputs stay readable as after holo_render
- * with HOLO_OUT_INTENSITY | HOLO_OUT_REPLAYED | HOLO_OUT_AUX. */
+ * term, pipeline.cpp:82-88).  The intensities entering the losses are |replayed|^2
+ * in f64 of the fp32 replay (what holo_intensity(HOLO_F64) gives for the widened
+ * field).  The frame's outputs stay readable as after holo_render with
+ * HOLO_OUT_REPLAYED | HOLO_OUT_AUX. */
 int holo_total_loss(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave, const holo_raster_settings* settings,
                     const holo_prop_options* prop, const holo_loss_options* opt, const double* targets,
                     const double* masks, holo_loss_breakdown* out, double* psnr, holo_scene_grads* grads);

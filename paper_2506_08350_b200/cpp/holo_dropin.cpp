@@ -666,20 +666,19 @@ PipelineForward pipeline_forward(const GaussianScene& scene, const CameraView& c
     f.raster = collect_raster(scene, cfg, C, info);
     const std::vector<std::complex<float>> holo = download_buf<std::complex<float>>(HOLO_BUF_HOLOGRAM);
     const std::vector<std::complex<float>> rep = download_buf<std::complex<float>>(HOLO_BUF_REPLAYED);
-    const std::vector<float> ints = download_buf<float>(HOLO_BUF_INTENSITY);
     f.hologram = ComplexField(cfg.nx, cfg.ny, C, cfg.pitch);
     for (size_t i = 0; i < n; ++i) f.hologram.data[i] = c64(holo[i].real(), holo[i].imag());
     for (int l = 0; l < L; ++l) {
         ComplexField r(cfg.nx, cfg.ny, C, cfg.pitch);
-        IntensityImage im(cfg.nx, cfg.ny, C);
         for (size_t i = 0; i < n; ++i) {
             const std::complex<float> v = rep[static_cast<size_t>(l) * n + i];
             r.data[i] = c64(v.real(), v.imag());
-            im.data[i] = ints[static_cast<size_t>(l) * n + i];
         }
         f.replayed.push_back(std::move(r));
-        f.intensities.push_back(std::move(im));
     }
+    // intensities = intensity(replayed) of the returned fields, literally as
+    // pipeline.cpp:26-27 (f64 squares of the widened fp32 replay)
+    for (int l = 0; l < L; ++l) f.intensities.push_back(intensity(f.replayed[l]));
     return f;
 }
 

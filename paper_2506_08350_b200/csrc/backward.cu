@@ -69,13 +69,17 @@ __device__ __forceinline__ void reduce_scatter_step(float (&w)[16], int lane) {
 template <int TILE, int C>
 __global__ void __launch_bounds__(TILE * TILE) k_raster_bwd(RasterBwdArgs a) {
     constexpr int NT = TILE * TILE;
-    constexpr int kStage = 256;
+    constexpr int kStage = 128;  // with the per-warp partials: 4 CTAs of 256 threads per SM
     constexpr int kBlocksX = TILE / 8;
     __shared__ Staged s_rec[kStage];
     __shared__ float4 s_box[kStage];
     __shared__ int s_g[kStage];
     __shared__ BwdRec s_brec[kStage];  // pad[0] carries rho
     __shared__ float s_acc[kStage * kGradVals];
+    // per-warp partials of the current 32-entry chunk, summed over the warps in a
+    // fixed order (deterministic: no float atomics)
+    extern __shared__ float s_part[];  // [NT / 32][32][kGradVals]
+    constexpr int NW = NT / 32;
 
     const int tx = blockIdx.x, ty = blockIdx.y, lplane = blockIdx.z;
     const int lb = (lplane * gridDim.y + ty) * gridDim.x + tx;
@@ -168,78 +172,90 @@ __global__ void __launch_bounds__(TILE * TILE) k_raster_bwd(RasterBwdArgs a) {
         const int base = bi * kStage;
         const int cnt = min(n - base, kStage);
         if (nb > 1) stage(base, cnt);  // one batch: still staged from pass 1
-        for (int t = tid; t < cnt * kGradVals; t += NT) s_acc[t] = 0.0f;
         __syncthreads();
+        float* my_part = s_part + warp * 32 * kGradVals;
         for (int c0 = ((cnt - 1) / 32) * 32; c0 >= 0; c0 -= 32) {
+            for (int i = lane; i < 32 * kGradVals; i += 32) my_part[i] = 0.0f;
+            __syncwarp();
             const bool live = active && e_last >= base + c0;
-            if (!__any_sync(0xffffffffu, live)) continue;
-            const bool hit = c0 + lane < cnt && box_hits(s_box[c0 + lane], bxlo, bxhi, bylo, byhi);
-            unsigned mask = __ballot_sync(0xffffffffu, hit);
-            while (mask) {
-                const int j = 31 - __clz(mask);  // highest first
-                mask &= ~(1u << j);
-                const int er = base + c0 + j;
-                const Staged* e = &s_rec[c0 + j];
-                float4 B;
-                const float al = eval_alpha(e, fx, fy, clamp, B);
-                const bool acc = active && er <= e_last && al > thr;
-                if (!__any_sync(0xffffffffu, acc)) continue;
-                float v[kGradVals];
+            if (__any_sync(0xffffffffu, live)) {
+                const bool hit = c0 + lane < cnt && box_hits(s_box[c0 + lane], bxlo, bxhi, bylo, byhi);
+                unsigned mask = __ballot_sync(0xffffffffu, hit);
+                while (mask) {
+                    const int j = 31 - __clz(mask);  // highest first
+                    mask &= ~(1u << j);
+                    const int er = base + c0 + j;
+                    const Staged* e = &s_rec[c0 + j];
+                    float4 B;
+                    const float al = eval_alpha(e, fx, fy, clamp, B);
+                    const bool acc = active && er <= e_last && al > thr;
+                    if (!__any_sync(0xffffffffu, acc)) continue;
+                    float v[kGradVals];
 #pragma unroll
-                for (int q = 0; q < kGradVals; ++q) v[q] = 0.0f;
-                if (acc) {
-                    const BwdRec& br = s_brec[c0 + j];
-                    T = __fdividef(T, 1.0f - al);
-                    const float aw = al * T;
-                    float d_alpha = 0.0f;
-                    const float4 Cc = e->c;
+                    for (int q = 0; q < kGradVals; ++q) v[q] = 0.0f;
+                    if (acc) {
+                        const BwdRec& br = s_brec[c0 + j];
+                        T = __fdividef(T, 1.0f - al);
+                        const float aw = al * T;
+                        float d_alpha = 0.0f;
+                        const float4 Cc = e->c;
 #pragma unroll
-                    for (int c = 0; c < C; ++c) {
-                        const cx<float> vc = c == 0 ? mk(B.z, B.w) : (c == 1 ? mk(Cc.x, Cc.y) : mk(Cc.z, Cc.w));
-                        accum[c] = mk(last_alpha * last[c].x + (1.0f - last_alpha) * accum[c].x,
-                                      last_alpha * last[c].y + (1.0f - last_alpha) * accum[c].y);
-                        last[c] = vc;
-                        d_alpha += (vc.x - accum[c].x) * g[c].x + (vc.y - accum[c].y) * g[c].y;
-                        const float co = br.cs[2 * c], si = br.cs[2 * c + 1];
-                        v[kGAmp + c] = aw * (co * g[c].x + si * g[c].y);
-                        v[kGPh + c] = aw * br.amp[c] * (-si * g[c].x + co * g[c].y);
+                        for (int c = 0; c < C; ++c) {
+                            const cx<float> vc = c == 0 ? mk(B.z, B.w) : (c == 1 ? mk(Cc.x, Cc.y) : mk(Cc.z, Cc.w));
+                            accum[c] = mk(last_alpha * last[c].x + (1.0f - last_alpha) * accum[c].x,
+                                          last_alpha * last[c].y + (1.0f - last_alpha) * accum[c].y);
+                            last[c] = vc;
+                            d_alpha += (vc.x - accum[c].x) * g[c].x + (vc.y - accum[c].y) * g[c].y;
+                            const float co = br.cs[2 * c], si = br.cs[2 * c + 1];
+                            v[kGAmp + c] = aw * (co * g[c].x + si * g[c].y);
+                            v[kGPh + c] = aw * br.amp[c] * (-si * g[c].x + co * g[c].y);
+                        }
+                        last_alpha = al;
+                        d_alpha *= T;
+                        if (al < clamp) {
+                            // alpha_eff = alpha_sig * gauss * rho below the clamp
+                            const float4 A = e->a;
+                            const float dx = fx - A.x, dy = fy - A.y;
+                            const float t = fmaf(A.w, dy, A.z * dx);
+                            const float gauss = ex2_approx(fmaf(B.x * dy, dy, dx * t));
+                            const float alpha_sig = br.alpha;
+                            const float rho = br.pad[0];
+                            v[kGAlpha] = d_alpha * gauss * rho;
+                            v[kGRho] = d_alpha * alpha_sig * gauss;
+                            const float gg = d_alpha * alpha_sig * rho * gauss;
+                            const float i00 = A.z * kInvScale, i01 = A.w * (0.5f * kInvScale), i11 = B.x * kInvScale;
+                            v[kGMuX] = gg * (i00 * dx + i01 * dy);
+                            v[kGMuY] = gg * (i01 * dx + i11 * dy);
+                            v[kGI00] = gg * (-0.5f * dx * dx);
+                            v[kGI01] = gg * (-dx * dy);
+                            v[kGI11] = gg * (-0.5f * dy * dy);
+                        }
                     }
-                    last_alpha = al;
-                    d_alpha *= T;
-                    if (al < clamp) {
-                        // alpha_eff = alpha_sig * gauss * rho below the clamp
-                        const float4 A = e->a;
-                        const float dx = fx - A.x, dy = fy - A.y;
-                        const float t = fmaf(A.w, dy, A.z * dx);
-                        const float gauss = ex2_approx(fmaf(B.x * dy, dy, dx * t));
-                        const float alpha_sig = br.alpha;
-                        const float rho = br.pad[0];
-                        v[kGAlpha] = d_alpha * gauss * rho;
-                        v[kGRho] = d_alpha * alpha_sig * gauss;
-                        const float gg = d_alpha * alpha_sig * rho * gauss;
-                        const float i00 = A.z * kInvScale, i01 = A.w * (0.5f * kInvScale), i11 = B.x * kInvScale;
-                        v[kGMuX] = gg * (i00 * dx + i01 * dy);
-                        v[kGMuY] = gg * (i01 * dx + i11 * dy);
-                        v[kGI00] = gg * (-0.5f * dx * dx);
-                        v[kGI01] = gg * (-dx * dy);
-                        v[kGI11] = gg * (-0.5f * dy * dy);
-                    }
+                    // reduce-scatter over the warp: afterwards lanes 2q, 2q+1 hold the
+                    // warp's sum of value q (16 shuffles instead of 13 x 5)
+                    float w[16];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) w[q] = q < kGradVals ? v[q] : 0.0f;
+                    reduce_scatter_step<16, 8>(w, lane);
+                    reduce_scatter_step<8, 4>(w, lane);
+                    reduce_scatter_step<4, 2>(w, lane);
+                    reduce_scatter_step<2, 1>(w, lane);
+                    w[0] += __shfl_xor_sync(0xffffffffu, w[0], 1);
+                    const int q = (lane >> 1) & 15;
+                    if ((lane & 1) == 0 && q < kGradVals) my_part[j * kGradVals + q] = w[0];
                 }
-                // reduce-scatter over the warp: afterwards lanes 2q, 2q+1 hold the
-                // warp's sum of value q (16 shuffles instead of 13 x 5)
-                float w[16];
-#pragma unroll
-                for (int q = 0; q < 16; ++q) w[q] = q < kGradVals ? v[q] : 0.0f;
-                reduce_scatter_step<16, 8>(w, lane);
-                reduce_scatter_step<8, 4>(w, lane);
-                reduce_scatter_step<4, 2>(w, lane);
-                reduce_scatter_step<2, 1>(w, lane);
-                w[0] += __shfl_xor_sync(0xffffffffu, w[0], 1);
-                const int q = (lane >> 1) & 15;
-                if ((lane & 1) == 0 && q < kGradVals && w[0] != 0.0f) atomicAdd(&s_acc[(c0 + j) * kGradVals + q], w[0]);
             }
+            __syncthreads();
+            // the chunk's entries: warp partials summed in warp order
+            const int nc = min(32, cnt - c0);
+            for (int i = tid; i < nc * kGradVals; i += NT) {
+                float sum = 0.0f;
+#pragma unroll
+                for (int wi = 0; wi < NW; ++wi) sum += s_part[wi * 32 * kGradVals + i];
+                s_acc[c0 * kGradVals + i] = sum;
+            }
+            __syncthreads();
         }
-        __syncthreads();
         // egrad is ordered per Gaussian: its k-th entry (bucket order: plane, then
         // tile row, then tile column) at goff[g] + k, so the merge reads it in the
         // reference's order without searching the buckets
@@ -441,14 +457,26 @@ __global__ void __launch_bounds__(256) k_bwd_gauss(GaussBwdArgs a) {
     }
 }
 
+template <int TILE, int C>
+void launch_bwd_c(holo_ctx* ctx, const RasterBwdArgs& a, dim3 grid) {
+    constexpr size_t kPart = sizeof(float) * (TILE * TILE / 32) * 32 * kGradVals;
+    static bool attr = false;
+    if (!attr) {
+        HC_CUDA(cudaFuncSetAttribute(k_raster_bwd<TILE, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kPart)));
+        attr = true;
+    }
+    k_raster_bwd<TILE, C><<<grid, TILE * TILE, kPart, ctx->stream>>>(a);
+}
+
 template <int TILE>
 void launch_raster_bwd_tile(holo_ctx* ctx, const RasterBwdArgs& a) {
     const int tiles_y = a.num_tiles / a.tiles_x;
     const dim3 grid(a.tiles_x, tiles_y, a.num_buckets / a.num_tiles);
     switch (a.C) {
-        case 1: k_raster_bwd<TILE, 1><<<grid, TILE * TILE, 0, ctx->stream>>>(a); break;
-        case 2: k_raster_bwd<TILE, 2><<<grid, TILE * TILE, 0, ctx->stream>>>(a); break;
-        case 3: k_raster_bwd<TILE, 3><<<grid, TILE * TILE, 0, ctx->stream>>>(a); break;
+        case 1: launch_bwd_c<TILE, 1>(ctx, a, grid); break;
+        case 2: launch_bwd_c<TILE, 2>(ctx, a, grid); break;
+        case 3: launch_bwd_c<TILE, 3>(ctx, a, grid); break;
         default: throw Error(HOLO_ERR_CONFIG, "render supports 1 to 3 wavelength channels");
     }
     HC_LAUNCHED(ctx);

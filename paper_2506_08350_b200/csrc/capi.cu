@@ -1434,10 +1434,12 @@ int holo_total_loss(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave
         const holo_prop_options po = prop ? *prop : holo_prop_options{0, 0};
         const int W = wave->nx, H = wave->ny, C = wave->channels, L = wave->num_planes;
         const size_t n = static_cast<size_t>(L) * C * H * W;
-        render_full(ctx, *cam, *wave, *settings, po, HOLO_OUT_INTENSITY | HOLO_OUT_REPLAYED | HOLO_OUT_AUX, nullptr);
-        const float* i32 = static_cast<const float*>(ctx->buffer(out_name("intensity", ctx->out_sel), 1));
+        render_full(ctx, *cam, *wave, *settings, po, HOLO_OUT_REPLAYED | HOLO_OUT_AUX, nullptr);
+        // the intensities in f64 of the replayed fields (as intensity() of the
+        // widened replay, so equal to what pipeline_forward's caller sees)
+        const cx<float>* rep = static_cast<const cx<float>*>(ctx->buffer(out_name("replayed", ctx->out_sel), 1));
         double* i64 = buf<double>(ctx, "loss_I", n);
-        f32_to_f64(ctx, i32, i64, n);
+        replay_intensity_f64(ctx, rep, i64, n);
         double* gi = grads ? buf<double>(ctx, "loss_gI", n) : nullptr;
         loss_terms(ctx, i64, targets, masks, L, C, H, W, lo, true, gi, out, psnr);
         if (grads) {

@@ -241,6 +241,7 @@ void phase_arg(holo_ctx* ctx, const cx<double>* P, double* theta, size_t n);
 bool all_finite_c128(holo_ctx* ctx, const cx<double>* P, size_t n);
 void f32_to_f64(holo_ctx* ctx, const float* in, double* out, size_t n);
 void f64_to_f32(holo_ctx* ctx, const double* in, float* out, size_t n);
+void replay_intensity_f64(holo_ctx* ctx, const cx<float>* rep, double* out, size_t n);
 bool grads_finite(holo_ctx* ctx, const double* const* g, const size_t* n, int groups);
 void adaptive_update(holo_ctx* ctx, double* p, const double* g, double* m, double* v, double* nn, double* prev,
                      size_t n, double lr, long long step, double b1, double b2, double b3, double eps, bool adam);

@@ -228,7 +228,10 @@ __global__ void k_intensity(const cx<T>* __restrict__ f, T* __restrict__ out, si
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const cx<T> v = f[i];
-        out[i] = v.x * v.x + v.y * v.y;
+        if constexpr (sizeof(T) == 8)
+            out[i] = __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y));  // std::norm, uncontracted
+        else
+            out[i] = v.x * v.x + v.y * v.y;
     }
 }
 

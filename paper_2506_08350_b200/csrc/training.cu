@@ -311,6 +311,15 @@ __global__ void k_f32_to_f64(const float* __restrict__ in, double* __restrict__ 
         out[i] = static_cast<double>(in[i]);
 }
 
+// |v|^2 in f64 of the fp32 replay, rounded like intensity() of the widened field
+__global__ void k_replay_intensity(const cx<float>* __restrict__ rep, double* __restrict__ out, size_t n) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const double x = rep[i].x, y = rep[i].y;
+        out[i] = __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
+    }
+}
+
 __global__ void k_f64_to_f32(const double* __restrict__ in, float* __restrict__ out, size_t n) {
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<size_t>(gridDim.x) * blockDim.x)
@@ -517,6 +526,11 @@ double opacity_term(holo_ctx* ctx, const double* logits, size_t n, double lambda
 
 void f32_to_f64(holo_ctx* ctx, const float* in, double* out, size_t n) {
     k_f32_to_f64<<<blocks_for(n), 256, 0, ctx->stream>>>(in, out, n);
+    HC_LAUNCHED(ctx);
+}
+
+void replay_intensity_f64(holo_ctx* ctx, const cx<float>* rep, double* out, size_t n) {
+    k_replay_intensity<<<blocks_for(n), 256, 0, ctx->stream>>>(rep, out, n);
     HC_LAUNCHED(ctx);
 }
 

@@ -117,3 +117,15 @@ def test_backward_needs_the_forward_state(gpu_ctx):
     gi = torch.zeros((2, 3, 32, 32), dtype=torch.float32, device="cuda")
     with pytest.raises(HoloError):  # no replayed fields in that render
         gpu_ctx.pipeline_backward(cam, cfg, None, None, gi, s.size())
+
+
+def test_backward_is_bitwise_deterministic(gpu_ctx):
+    """test_pipeline.cpp:262-288: gradients identical run to run (no float atomics
+    in the per-entry reduction; the per-Gaussian merge is in a fixed order)."""
+    cfg = desk_config(64, 3)
+    cam = front_camera(cfg)
+    scene = random_scene(300, cfg, 17)
+    gi = np.random.default_rng(2).standard_normal((3, 3, 64, 64))
+    runs = [api.pipeline_backward(scene, cam, cfg, PipelineOptions(), gi, ctx=gpu_ctx)[0] for _ in range(3)]
+    for k in runs[0]:
+        assert np.array_equal(runs[0][k], runs[1][k]) and np.array_equal(runs[0][k], runs[2][k]), k
