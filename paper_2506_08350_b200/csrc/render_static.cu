@@ -34,6 +34,10 @@ template <> struct PlanOf<1080> { using type = Radices<8, 9, 15>; };
 // HOLO_ROW1920 selects the 1920-point plan and row-pass shape (tuning).  Measured
 // row pass at C3: 1 = [16,8,15], 2 rows x 256 threads, 2 CTAs/SM: 0.451 ms;
 // 2 = [16,15,8] 1 row, 3 CTAs: 0.554; 3 = 2 rows x 512: 0.566; 4 = 4 CTAs: 0.626.
+// Splitting the pass in two kernels around S in HBM (forward + sum, then the
+// replays at higher occupancy) measured 0.465 ms at 2 + 2 CTAs/SM, 0.484 at
+// 2 + 3, 0.515 at 3 + 3 and 0.58-0.61 with 1-row replay CTAs at 4/SM, against
+// 0.435 fused: occupancy is not what limits this pass.
 #ifndef HOLO_ROW1920
 #define HOLO_ROW1920 1
 #endif
