@@ -73,11 +73,11 @@ STAGE_KERNEL = {"preprocess": "k_preprocess", "composite": "k_composite", "fft_p
 
 def ncu_traffic(stage):
     """dram read + write bytes per launch of the stage's kernel from the newest
-    committed ncu --set full summary (profiles/r*_kernels.csv), or None."""
+    committed forward-frame ncu --set full summary (profiles/rNN_kernels.csv), or None."""
     import csv
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_kernels.csv")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r[0-9][0-9]_kernels.csv")))
     prefix = STAGE_KERNEL.get(stage)
     if not files or not prefix:
         return None
