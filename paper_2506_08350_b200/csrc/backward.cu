@@ -139,7 +139,9 @@ __global__ void __launch_bounds__(TILE * TILE) k_raster_bwd(RasterBwdArgs a) {
     // ---- pass 1: the forward's accepted set -- the first n_contrib accepted
     // entries in bucket order (rasterizer.cpp:379-387)
     int k = 0, e_last = -1;
-    for (int base = 0; base < n; base += kStage) {
+    const bool replay = a.e_last == nullptr;  // else the forward recorded e_last
+    if (!replay && inside) e_last = a.e_last[static_cast<size_t>(lplane) * P + pix];
+    for (int base = 0; replay && base < n; base += kStage) {
         const int cnt = min(n - base, kStage);
         stage(base, cnt);
         __syncthreads();
@@ -171,7 +173,7 @@ __global__ void __launch_bounds__(TILE * TILE) k_raster_bwd(RasterBwdArgs a) {
     for (int bi = nb - 1; bi >= 0; --bi) {
         const int base = bi * kStage;
         const int cnt = min(n - base, kStage);
-        if (nb > 1) stage(base, cnt);  // one batch: still staged from pass 1
+        if (nb > 1 || !replay) stage(base, cnt);  // one batch: still staged from pass 1
         __syncthreads();
         float* my_part = s_part + warp * 32 * kGradVals;
         for (int c0 = ((cnt - 1) / 32) * 32; c0 >= 0; c0 -= 32) {

@@ -422,6 +422,7 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     ca.layers = buf<cx<float>>(ctx, "layers", static_cast<size_t>(nplanes) * g.C * g.P);
     ca.t_final = want_aux ? buf<float>(ctx, "t_final", static_cast<size_t>(nplanes) * g.P) : nullptr;
     ca.n_contrib = want_aux ? buf<int>(ctx, "n_contrib", static_cast<size_t>(nplanes) * g.P) : nullptr;
+    ca.e_last = want_aux ? buf<int>(ctx, "e_last", static_cast<size_t>(nplanes) * g.P) : nullptr;
     ctx->stage_begin();
     composite(ctx, ca, g.tile);
     ctx->stage_end(2);
@@ -1005,6 +1006,7 @@ void raster_backward(holo_ctx* ctx, const holo_wave& wave, const holo_raster_set
     ra.grad_layers = grad_layers;
     ra.t_final = static_cast<const float*>(ctx->buffer("t_final", 1));
     ra.n_contrib = static_cast<const int*>(ctx->buffer("n_contrib", 1));
+    ra.e_last = static_cast<const int*>(ctx->buffer("e_last", 1));
     ra.goff = goff;
     ra.rect = static_cast<const int4*>(ctx->buffer("rect", 1));
     ra.pmask = st.soft_assignment ? static_cast<const unsigned long long*>(ctx->buffer("pmask", 1)) : nullptr;

@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
     const float eps = a.term_eps;
 
     float T = 1.0f;
-    int contrib = 0;
+    int contrib = 0, elast = -1;
     cx<float> acc[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) acc[c] = mk(0.0f, 0.0f);
@@ -274,10 +274,12 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
                     unsigned long long n_eval = 0, n_any = 0, n_acc = 0;
 #endif
                     while (mask) {
-                        const Staged* e0p = &sm.st.rec[c0 + __ffs(mask) - 1];
+                        const int j0 = __ffs(mask) - 1;
+                        const Staged* e0p = &sm.st.rec[c0 + j0];
                         mask &= mask - 1;
                         const bool two = mask != 0;
-                        const Staged* e1p = &sm.st.rec[c0 + (two ? __ffs(mask) - 1 : 0)];
+                        const int j1 = two ? __ffs(mask) - 1 : 0;
+                        const Staged* e1p = &sm.st.rec[c0 + j1];
                         mask &= mask - 1;
                         float4 B0, B1;
                         const float al0 = eval_alpha(e0p, fx, fy, clamp, B0);
@@ -286,12 +288,18 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
                         const float w0 = acc0 ? al0 * T : 0.0f;
                         blend<C>(e0p, B0, w0, acc);
                         T -= w0;  // T (1 - a)
-                        if constexpr (AUX) contrib += acc0 ? 1 : 0;
+                        if constexpr (AUX) {
+                            contrib += acc0 ? 1 : 0;
+                            elast = acc0 ? base + c0 + j0 : elast;
+                        }
                         const bool acc1 = two && (al1 > thr) && (T >= eps);
                         const float w1 = acc1 ? al1 * T : 0.0f;
                         blend<C>(e1p, B1, w1, acc);
                         T -= w1;
-                        if constexpr (AUX) contrib += acc1 ? 1 : 0;
+                        if constexpr (AUX) {
+                            contrib += acc1 ? 1 : 0;
+                            elast = acc1 ? base + c0 + j1 : elast;
+                        }
 #ifdef HOLO_COUNT
                         n_eval += two ? 2 : 1;
                         n_any += (__ballot_sync(0xffffffffu, acc0) ? 1 : 0) + (__ballot_sync(0xffffffffu, acc1) ? 1 : 0);
@@ -322,7 +330,10 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
         for (int c = 0; c < C; ++c)
             a.layers[(static_cast<size_t>(lplane) * C + c) * P + pix] = acc[c];
         if (a.t_final) a.t_final[static_cast<size_t>(lplane) * P + pix] = T;
-        if constexpr (AUX) a.n_contrib[static_cast<size_t>(lplane) * P + pix] = contrib;
+        if constexpr (AUX) {
+            a.n_contrib[static_cast<size_t>(lplane) * P + pix] = contrib;
+            if (a.e_last) a.e_last[static_cast<size_t>(lplane) * P + pix] = elast;
+        }
     }
 }
 

@@ -162,6 +162,7 @@ struct CompositeArgs {
     cx<float>* layers;        // [planes][C][H][W], plane relative to plane_begin
     float* t_final;           // optional [planes][H][W]
     int* n_contrib;           // optional
+    int* e_last;              // with n_contrib: bucket-relative index of the last accepted entry (-1: none)
 };
 void composite(holo_ctx* ctx, const CompositeArgs& a, int tile);
 
@@ -186,6 +187,7 @@ struct RasterBwdArgs {
     const cx<float>* grad_layers;  // [planes][C][H][W]
     const float* t_final;          // the forward's aux outputs
     const int* n_contrib;
+    const int* e_last;  // optional: the forward's last accepted entry per pixel (skips the replay pass)
     const unsigned* goff;          // exclusive scan of the per-Gaussian entry counts
     const int4* rect;
     const unsigned long long* pmask;  // soft mode
