@@ -9,8 +9,8 @@
 //                   (the same staged records and instruction sequence as
 //                   k_composite, raster_eval.cuh), then the back-to-front sweep
 //                   recovering T and the colour behind (rasterizer.cpp:376-428);
-//                   per-entry gradients are reduced over the warp and the CTA
-//                   (shared-memory float atomics) into egrad[entry][13]
+//                   per-entry gradients are reduced over the warp, then over
+//                   the CTA's warps in warp order (deterministic) into egrad[entry][13]
 //   k_bwd_gauss     per Gaussian, f64: sums its entries' gradients in entry
 //                   (bucket) order, the reference's merge order (:435-455), then
 //                   the chain to the stored parameters (:458-525) with
@@ -27,11 +27,13 @@ enum { kGMuX = 0, kGMuY, kGI00, kGI01, kGI11, kGAlpha, kGRho, kGAmp, kGPh = kGAm
 
 constexpr float kInvScale = -1.38629436111989061883f;  // 1 / (GRec conic scale -log2(e) / 2) = -2 ln 2
 
-__global__ void k_bwd_seed(const cx<float>* __restrict__ rep, const float* __restrict__ gi, cx<float>* __restrict__ gv,
+// dL/dI as float, or as double (total_loss's f64 loss gradient, narrowed here)
+template <class G>
+__global__ void k_bwd_seed(const cx<float>* __restrict__ rep, const G* __restrict__ gi, cx<float>* __restrict__ gv,
                            size_t n) {
     for (size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; t < n;
          t += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const float s = 2.0f * gi[t];
+        const float s = 2.0f * static_cast<float>(gi[t]);
         gv[t] = scale(rep[t], s);
     }
 }
@@ -486,10 +488,14 @@ void launch_raster_bwd_tile(holo_ctx* ctx, const RasterBwdArgs& a) {
 
 }  // namespace
 
-void bwd_seed(holo_ctx* ctx, const cx<float>* rep, const float* gi, cx<float>* gv, size_t n) {
+void bwd_seed(holo_ctx* ctx, const cx<float>* rep, const float* gi, const double* gi64, cx<float>* gv, size_t n) {
     if (n == 0) return;
     const size_t blocks = (n + 255) / 256;
-    k_bwd_seed<<<static_cast<unsigned>(blocks < 8192 ? blocks : 8192), 256, 0, ctx->stream>>>(rep, gi, gv, n);
+    const unsigned nb = static_cast<unsigned>(blocks < 8192 ? blocks : 8192);
+    if (gi64)
+        k_bwd_seed<double><<<nb, 256, 0, ctx->stream>>>(rep, gi64, gv, n);
+    else
+        k_bwd_seed<float><<<nb, 256, 0, ctx->stream>>>(rep, gi, gv, n);
     HC_LAUNCHED(ctx);
 }
 

@@ -1113,7 +1113,7 @@ void render_full(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, c
 // holo_pipeline_backward's body (pipeline.cpp:63-91 without the opacity term)
 void pipeline_backward(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, const holo_raster_settings& st,
                        const holo_prop_options& po, const float* grad_intensities, const holo_scene_grads& grads,
-                       void* grad_layers_out, void* grad_hologram_out) {
+                       void* grad_layers_out, void* grad_hologram_out, const double* grad_intensities64 = nullptr) {
     check_backward_frame(ctx, cam, wave, st);
     require((ctx->f_outputs & HOLO_OUT_REPLAYED) != 0, HOLO_ERR_USAGE,
             "pipeline backward needs the last render with HOLO_OUT_REPLAYED");
@@ -1121,7 +1121,7 @@ void pipeline_backward(holo_ctx* ctx, const holo_camera& cam, const holo_wave& w
     const size_t P = static_cast<size_t>(W) * H, n = static_cast<size_t>(L) * C * P;
     const cx<float>* rep = static_cast<const cx<float>*>(ctx->buffer(out_name("replayed", ctx->out_sel), 1));
     cx<float>* gv = buf<cx<float>>(ctx, "bwd_gv", n);
-    bwd_seed(ctx, rep, grad_intensities, gv, n);
+    bwd_seed(ctx, rep, grad_intensities, grad_intensities64, gv, n);
     cx<float>* gl = grad_layers_out ? static_cast<cx<float>*>(grad_layers_out) : buf<cx<float>>(ctx, "bwd_glayers", n);
     cx<float>* gh = grad_hologram_out ? static_cast<cx<float>*>(grad_hologram_out)
                                       : buf<cx<float>>(ctx, "bwd_gholo", static_cast<size_t>(C) * P);
@@ -1444,11 +1444,7 @@ int holo_total_loss(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave
         replay_intensity_f64(ctx, rep, i64, n);
         double* gi = grads ? buf<double>(ctx, "loss_gI", n) : nullptr;
         loss_terms(ctx, i64, targets, masks, L, C, H, W, lo, true, gi, out, psnr);
-        if (grads) {
-            float* gi32 = buf<float>(ctx, "loss_gI32", n);
-            f64_to_f32(ctx, gi, gi32, n);
-            pipeline_backward(ctx, *cam, *wave, *settings, po, gi32, *grads, nullptr, nullptr);
-        }
+        if (grads) pipeline_backward(ctx, *cam, *wave, *settings, po, nullptr, *grads, nullptr, nullptr, gi);
         // opacity decay (pipeline.cpp:47-52, 82-88) on the rendered scene
         const double* opac = ctx->scene_sets[ctx->f_scene_set].a[4];
         out->opacity = opacity_term(ctx, opac, ctx->n, lo.lambda_opacity, grads ? grads->opacity_logits : nullptr);

@@ -210,7 +210,7 @@ struct GaussBwdArgs {
     double near_clip, dilation, alpha_floor, soft_tau, ste_tau;
     holo_scene_grads g;
 };
-void bwd_seed(holo_ctx* ctx, const cx<float>* rep, const float* gi, cx<float>* gv, size_t n);
+void bwd_seed(holo_ctx* ctx, const cx<float>* rep, const float* gi, const double* gi64, cx<float>* gv, size_t n);
 void bwd_prep(holo_ctx* ctx, size_t N, const double* amplitudes, const double* phases, const GRec* rec,
               BwdRec* out);
 void raster_backward_entries(holo_ctx* ctx, const RasterBwdArgs& a, int tile);
