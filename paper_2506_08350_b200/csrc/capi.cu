@@ -1586,12 +1586,16 @@ namespace {
 struct PhaseProblem {
     holo_wave wave{};
     holo_prop_options po{};
-    int w = 0, h = 0, C = 0, L = 0, pw = 0, ph = 0;
+    int w = 0, h = 0, C = 0, L = 0, pw = 0, ph = 0, oy = 0;
     bool pad = false;
     size_t n = 0, gn = 0;
     std::vector<double> z;
-    cx<double>* tf = nullptr;  // target fields [L][C][h][w]
-    double* timg = nullptr;    // target intensities
+    cx<double>* tf = nullptr;   // target fields [L][C][h][w]
+    double* timg = nullptr;     // target intensities
+    const TfChan* tfc = nullptr;
+    cx<double>* tab = nullptr;  // H_{Z_l} on the (padded) grid [L][C][ph][pw], computed once
+    const int* planes = nullptr;  // 0..L-1
+    const int* none = nullptr;    // -1
 };
 
 PhaseProblem phase_problem(holo_ctx* ctx, const cx<double>* P, const holo_wave& wave, const holo_prop_options& po) {
@@ -1606,6 +1610,7 @@ PhaseProblem phase_problem(holo_ctx* ctx, const cx<double>* P, const holo_wave& 
     p.pad = po.pad2x != 0;
     p.pw = p.pad ? 2 * p.w : p.w;
     p.ph = p.pad ? 2 * p.h : p.h;
+    p.oy = (p.ph - p.h) / 2;  // pad_center (propagation.cpp:64-72)
     p.n = static_cast<size_t>(p.C) * p.w * p.h;
     p.gn = static_cast<size_t>(p.C) * p.pw * p.ph;
     p.z = plane_positions(wave);
@@ -1615,7 +1620,32 @@ PhaseProblem phase_problem(holo_ctx* ctx, const cx<double>* P, const holo_wave& 
     p.timg = buf<double>(ctx, "po_timg", p.n * p.L);
     op_inverse_propagate<double>(ctx, P, p.tf, wave, po);  // replay_targets (phase_only.cpp:31-38)
     intensity<double>(ctx, p.tf, p.timg, p.n * p.L);
+    // the planes' transfer functions on the propagation grid, once for the whole
+    // conversion (the same values the column passes would evaluate per element)
+    p.tfc = upload_tf(ctx, "po_tfc", wave, p.z, p.pw, p.ph, po.local_band_limit);
+    p.tab = buf<cx<double>>(ctx, "po_tftab", p.gn * p.L);
+    for (int l = 0; l < p.L; ++l)
+        transfer_function<double>(ctx, p.tab + p.gn * l, p.pw, p.ph, p.C, p.tfc + l * p.C, wave.pitch);
+    std::vector<int> pl(p.L);
+    for (int l = 0; l < p.L; ++l) pl[l] = l;
+    int* d_pl = buf<int>(ctx, "po_planes", p.L);
+    upload_small(ctx, d_pl, pl.data(), sizeof(int) * p.L);
+    int* d_none = buf<int>(ctx, "po_none", 1);
+    const int m1 = -1;
+    upload_small(ctx, d_none, &m1, sizeof(int));
+    p.planes = d_pl;
+    p.none = d_none;
     return p;
+}
+
+// row FFTs of the rows [oy, oy + h) of each of `fields` (padded) grids: the other
+// rows are zero on input (forward) or never read (inverse)
+void crop_rows_fft(holo_ctx* ctx, const PhaseProblem& p, cx<double>* f, int fields, int dir) {
+    const double s = dir > 0 ? 1.0 / (static_cast<double>(p.pw) * p.ph) : 1.0;
+    for (int k = 0; k < fields; ++k) {
+        cx<double>* r = f + static_cast<size_t>(k) * p.ph * p.pw + static_cast<size_t>(p.oy) * p.pw;
+        rows_fft<double>(ctx, r, r, p.pw, p.h, dir, s);
+    }
 }
 
 // eval_loss (phase_only.cpp:48-101); grad (device, optional) = d loss / d theta
@@ -1625,11 +1655,14 @@ double phase_eval(holo_ctx* ctx, const PhaseProblem& p, const double* theta, dou
     cx<double>* rep = buf<cx<double>>(ctx, "po_rep", p.gn * L);
     double* img = buf<double>(ctx, "po_img", p.n * L);
     double* sums = buf<double>(ctx, "po_sums", 2 * static_cast<size_t>(L));
+    const ColOpts<double> band{p.tab, p.oy, p.oy + h};
+    // e^{j theta} -> spectrum (row pass pruned to the field's rows)
     phase_field(ctx, theta, cand, w, h, C, p.pad);
-    op_fft2<double>(ctx, cand, p.pw, p.ph, C, false);
-    std::vector<int> plane_of(L);
-    for (int l = 0; l < L; ++l) plane_of[l] = l;
-    replay_from_spectrum<double>(ctx, cand, rep, p.pw, p.ph, C, p.wave, p.z, plane_of, p.po.local_band_limit);
+    crop_rows_fft(ctx, p, cand, C, -1);
+    cols_fft<double>(ctx, cand, cand, p.pw, p.ph, C, -1, 1.0);
+    // replays: column IFFT with H_{-Z_l}, the cropped rows only, then their row IFFT
+    col_replay<double>(ctx, cand, rep, p.pw, p.ph, C, L, p.planes, p.tfc, p.wave.pitch, band);
+    crop_rows_fft(ctx, p, rep, L * C, +1);
     phase_match(ctx, rep, p.tf, w, h, C, L, p.pad, img, sums);
     double* gi = nullptr;
     if (grad) {
@@ -1642,11 +1675,14 @@ double phase_eval(holo_ctx* ctx, const PhaseProblem& p, const double* theta, dou
                             cudaMemcpyDeviceToHost, ctx->stream));
     const double inv_lm = 1.0 / (static_cast<double>(L) * static_cast<double>(p.n));
     if (grad) {
+        // seed over the cropped rows, one summed spectrum sum_l H_{Z_l} FFT(gv_l),
+        // one inverse transform (again pruned to the cropped rows)
         phase_seed(ctx, rep, p.tf, gi, w, h, C, L, p.pad, inv_lm);
-        spectrum_of_layers<double>(ctx, rep, rep, cand, p.pw, p.ph, C, p.wave, p.z, p.po.local_band_limit);
+        crop_rows_fft(ctx, p, rep, L * C, -1);
+        col_spectrum<double>(ctx, rep, cand, p.pw, p.ph, C, L, p.tfc, p.wave.pitch, band);
         cx<double>* acc = buf<cx<double>>(ctx, "po_acc", p.gn);
-        replay_from_spectrum<double>(ctx, cand, acc, p.pw, p.ph, C, p.wave, p.z, std::vector<int>{-1},
-                                     p.po.local_band_limit);
+        col_replay<double>(ctx, cand, acc, p.pw, p.ph, C, 1, p.none, p.tfc, p.wave.pitch, band);
+        crop_rows_fft(ctx, p, acc, C, +1);
         phase_grad(ctx, acc, theta, grad, w, h, C, p.pad);
     }
     HC_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -50,12 +50,20 @@ template <class T>
 void rows_fft(holo_ctx* ctx, const cx<T>* in, cx<T>* out, int n, long long nrows, int dir, T s);
 template <class T>
 void cols_fft(holo_ctx* ctx, const cx<T>* in, cx<T>* out, int w, int h, int batch, int dir, T s);
+// column-pass options: tftab = transfer functions precomputed [L][C][h][w]
+// (instead of evaluated per element); [row_lo, row_hi) = the rows that can be
+// nonzero on input (col_spectrum) / that are stored (col_replay); -1 = h
+template <class T>
+struct ColOpts {
+    const cx<T>* tftab = nullptr;
+    int row_lo = 0, row_hi = -1;
+};
 template <class T>
 void col_spectrum(holo_ctx* ctx, const cx<T>* layers, cx<T>* spec, int w, int h, int C, int L, const TfChan* d_tfc,
-                  double pitch);
+                  double pitch, const ColOpts<T>& opt = ColOpts<T>{});
 template <class T>
 void col_replay(holo_ctx* ctx, const cx<T>* spec, cx<T>* out, int w, int h, int C, int nout, const int* d_plane_of,
-                const TfChan* d_tfc, double pitch);
+                const TfChan* d_tfc, double pitch, const ColOpts<T>& opt = ColOpts<T>{});
 void rows_epilogue(holo_ctx* ctx, const cx<float>* in, int w, int h, int C, int nout, int has_holo, cx<float>* holo,
                    cx<float>* replayed, float* intens);
 template <class T>

@@ -95,8 +95,9 @@ __global__ void k_phase_seed(cx<double>* __restrict__ rep, const cx<double>* __r
         const int gy = static_cast<int>((j / gw) % gh);
         const int c = static_cast<int>(j / (static_cast<size_t>(gw) * gh));
         const int x = pad ? gx - (gw - w) / 2 : gx, y = pad ? gy - (gh - h) / 2 : gy;
+        if (y < 0 || y >= h) continue;  // rows outside the crop are never read (pruned transforms)
         cx<double> v = mk(0.0, 0.0);
-        if (x >= 0 && x < w && y >= 0 && y < h) {
+        if (x >= 0 && x < w) {
             const size_t k = l * n + (static_cast<size_t>(c) * h + y) * w + x;
             const cx<double> r = rep[i], t = tf[k];
             const double g = gi[k];

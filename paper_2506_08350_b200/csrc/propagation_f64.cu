@@ -5,9 +5,10 @@ namespace holo_cuda {
 #define HC_INSTANTIATE(T)                                                                                        \
     template void rows_fft<T>(holo_ctx*, const cx<T>*, cx<T>*, int, long long, int, T);                           \
     template void cols_fft<T>(holo_ctx*, const cx<T>*, cx<T>*, int, int, int, int, T);                           \
-    template void col_spectrum<T>(holo_ctx*, const cx<T>*, cx<T>*, int, int, int, int, const TfChan*, double);    \
+    template void col_spectrum<T>(holo_ctx*, const cx<T>*, cx<T>*, int, int, int, int, const TfChan*, double,     \
+                                  const ColOpts<T>&);                                                             \
     template void col_replay<T>(holo_ctx*, const cx<T>*, cx<T>*, int, int, int, int, const int*, const TfChan*,   \
-                                double);                                                                          \
+                                double, const ColOpts<T>&);                                                       \
     template void pad_field<T>(holo_ctx*, const cx<T>*, cx<T>*, int, int, int);                                   \
     template void crop_field<T>(holo_ctx*, const cx<T>*, cx<T>*, int, int, int);                                  \
     template void accumulate<T>(holo_ctx*, const cx<T>*, cx<T>*, size_t, bool);                                   \

@@ -77,11 +77,15 @@ __global__ void __launch_bounds__(256) k_cols(const cx<T>* __restrict__ in, cx<T
 // S[c] = sum_l H_{z_l, c} . colFFT(layers[l][c]) for row-transformed layers
 // [L][C][h][w].  One CTA per (strip, channel); the spectrum strip accumulates in
 // shared memory in plane order, so the sum is deterministic.
+// Optional (ColOpts): tftab = the transfer functions precomputed [L][C][h][w] (a
+// loop that applies the same planes many times: phase-only conversion), and
+// [row_lo, row_hi) = the only input rows that can be nonzero (padded fields).
 template <class T>
 __global__ void __launch_bounds__(256) k_col_spectrum(const cx<T>* __restrict__ layers, cx<T>* __restrict__ spec,
                                                       int w, int h, int C, int L, int nb, FftPlan plan,
                                                       const cx<T>* __restrict__ tw, const TfChan* __restrict__ tfc,
-                                                      const double* __restrict__ fx, const double* __restrict__ fy) {
+                                                      const double* __restrict__ fx, const double* __restrict__ fy,
+                                                      const cx<T>* __restrict__ tftab, int row_lo, int row_hi) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<T>* b0 = reinterpret_cast<cx<T>*>(smem_raw);
     cx<T>* b1 = b0 + static_cast<size_t>(h) * nb;
@@ -94,14 +98,16 @@ __global__ void __launch_bounds__(256) k_col_spectrum(const cx<T>* __restrict__ 
         const cx<T>* src = layers + (static_cast<size_t>(l) * C + c) * h * w;
         for (int t = threadIdx.x; t < tot; t += blockDim.x) {
             const int b = t % nb, i = t / nb, x = x0 + b;
-            b0[t] = x < w ? src[static_cast<size_t>(i) * w + x] : czero<T>();
+            b0[t] = (x < w && i >= row_lo && i < row_hi) ? src[static_cast<size_t>(i) * w + x] : czero<T>();
         }
         __syncthreads();
         const cx<T>* r = fft_batch<-1, T>(b0, b1, ColLayout{h, nb}, plan, tw);
         const TfChan p = tfc[l * C + c];
+        const cx<T>* tab = tftab ? tftab + (static_cast<size_t>(l) * C + c) * h * w : nullptr;
         for (int t = threadIdx.x; t < tot; t += blockDim.x) {
             const int b = t % nb, i = t / nb, x = x0 + b;
-            if (x < w) sacc[t] = sacc[t] + r[t] * tf_value<T>(p, fx[x], fy[i]);
+            if (x < w)
+                sacc[t] = sacc[t] + r[t] * (tab ? tab[static_cast<size_t>(i) * w + x] : tf_value<T>(p, fx[x], fy[i]));
         }
         __syncthreads();
     }
@@ -119,7 +125,8 @@ __global__ void __launch_bounds__(256) k_col_replay(const cx<T>* __restrict__ sp
                                                     int w, int h, int C, int nb, FftPlan plan,
                                                     const cx<T>* __restrict__ tw, const TfChan* __restrict__ tfc,
                                                     const int* __restrict__ plane_of,
-                                                    const double* __restrict__ fx, const double* __restrict__ fy) {
+                                                    const double* __restrict__ fx, const double* __restrict__ fy,
+                                                    const cx<T>* __restrict__ tftab, int row_lo, int row_hi) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<T>* b0 = reinterpret_cast<cx<T>*>(smem_raw);
     cx<T>* b1 = b0 + static_cast<size_t>(h) * nb;
@@ -131,12 +138,13 @@ __global__ void __launch_bounds__(256) k_col_replay(const cx<T>* __restrict__ sp
     const cx<T>* src = spec + static_cast<size_t>(c) * h * w;
     TfChan p;
     if (l >= 0) p = tfc[l * C + c];
+    const cx<T>* tab = (tftab && l >= 0) ? tftab + (static_cast<size_t>(l) * C + c) * h * w : nullptr;
     for (int t = threadIdx.x; t < tot; t += blockDim.x) {
         const int b = t % nb, i = t / nb, x = x0 + b;
         cx<T> v = czero<T>();
         if (x < w) {
             v = src[static_cast<size_t>(i) * w + x];
-            if (l >= 0) v = v * conj(tf_value<T>(p, fx[x], fy[i]));
+            if (l >= 0) v = v * conj(tab ? tab[static_cast<size_t>(i) * w + x] : tf_value<T>(p, fx[x], fy[i]));
         }
         b0[t] = v;
     }
@@ -145,7 +153,7 @@ __global__ void __launch_bounds__(256) k_col_replay(const cx<T>* __restrict__ sp
     cx<T>* dst = out + (static_cast<size_t>(o) * C + c) * h * w;
     for (int t = threadIdx.x; t < tot; t += blockDim.x) {
         const int b = t % nb, i = t / nb, x = x0 + b;
-        if (x < w) dst[static_cast<size_t>(i) * w + x] = r[t];
+        if (x < w && i >= row_lo && i < row_hi) dst[static_cast<size_t>(i) * w + x] = r[t];
     }
 }
 
@@ -359,20 +367,21 @@ std::vector<TfChan> make_tf_consts(const holo_wave& wave, const double* z, int L
 
 template <class T>
 void col_spectrum(holo_ctx* ctx, const cx<T>* layers, cx<T>* spec, int w, int h, int C, int L, const TfChan* d_tfc,
-                  double pitch) {
+                  double pitch, const ColOpts<T>& opt) {
     const FftPlan plan = plan_or_throw(h);
     const int nb = cols_per_strip<T>(h, 3);
     const size_t smem = 3 * static_cast<size_t>(h) * nb * sizeof(cx<T>);
     allow_smem(k_col_spectrum<T>, smem);
     const dim3 grid((w + nb - 1) / nb, C);
     k_col_spectrum<T><<<grid, kThreads, smem, ctx->stream>>>(layers, spec, w, h, C, L, nb, plan, ctx->twiddle<T>(h),
-                                                             d_tfc, ctx->freq(w, pitch), ctx->freq(h, pitch));
+                                                             d_tfc, ctx->freq(w, pitch), ctx->freq(h, pitch),
+                                                             opt.tftab, opt.row_lo, opt.row_hi < 0 ? h : opt.row_hi);
     HC_LAUNCHED(ctx);
 }
 
 template <class T>
 void col_replay(holo_ctx* ctx, const cx<T>* spec, cx<T>* out, int w, int h, int C, int nout, const int* d_plane_of,
-                const TfChan* d_tfc, double pitch) {
+                const TfChan* d_tfc, double pitch, const ColOpts<T>& opt) {
     if (nout <= 0) return;
     const FftPlan plan = plan_or_throw(h);
     const int nb = cols_per_strip<T>(h, 2);
@@ -380,7 +389,8 @@ void col_replay(holo_ctx* ctx, const cx<T>* spec, cx<T>* out, int w, int h, int 
     allow_smem(k_col_replay<T>, smem);
     const dim3 grid((w + nb - 1) / nb, C, nout);
     k_col_replay<T><<<grid, kThreads, smem, ctx->stream>>>(spec, out, w, h, C, nb, plan, ctx->twiddle<T>(h), d_tfc,
-                                                           d_plane_of, ctx->freq(w, pitch), ctx->freq(h, pitch));
+                                                           d_plane_of, ctx->freq(w, pitch), ctx->freq(h, pitch),
+                                                           opt.tftab, opt.row_lo, opt.row_hi < 0 ? h : opt.row_hi);
     HC_LAUNCHED(ctx);
 }
 
