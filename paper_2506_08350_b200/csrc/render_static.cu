@@ -37,7 +37,8 @@ template <> struct PlanOf<1080> { using type = Radices<8, 9, 15>; };
 // Splitting the pass in two kernels around S in HBM (forward + sum, then the
 // replays at higher occupancy) measured 0.465 ms at 2 + 2 CTAs/SM, 0.484 at
 // 2 + 3, 0.515 at 3 + 3 and 0.58-0.61 with 1-row replay CTAs at 4/SM, against
-// 0.435 fused: occupancy is not what limits this pass.
+// 0.435 fused: occupancy is not what limits this pass.  One row per CTA of 128
+// threads (4 or 3 CTAs/SM, same registers per thread): 0.498 ms.
 #ifndef HOLO_ROW1920
 #define HOLO_ROW1920 1
 #endif
