@@ -253,3 +253,29 @@ def test_training_loop_lowers_the_loss(gpu_ctx):
         losses.append(b.total)
         assert optim.step(g, oc)
     assert losses[-1] < 0.7 * losses[0], losses
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_self_target_full_size(gpu_ctx, name):
+    """test_pipeline.cpp:93-113 at BASELINE sizes (a size-independent property):
+    a scene rendered against its own intensities has zero reconstruction loss,
+    PSNR 99 dB and vanishing gradients."""
+    import torch
+
+    from paper_2506_08350_b200 import _lib as L
+    from paper_2506_08350_b200.scenes import CONFIGS, synthetic_scene
+
+    c = CONFIGS[name]
+    cfg, cam = c.wave(), c.cameras()[0]
+    scene = synthetic_scene(c.n, cfg, c.seed)
+    gpu_ctx.upload_scene(scene)
+    gpu_ctx.render(cam, cfg, outputs=L.OUT_REPLAYED)
+    Cn, H, W = cfg.channels(), cfg.ny, cfg.nx
+    rep = gpu_ctx.tensor(L.BUF_REPLAYED, "c8", (cfg.num_planes, Cn, H, W)).to(torch.complex128)
+    target = (rep.real ** 2 + rep.imag ** 2).contiguous()  # |replay|^2 in f64, as total_loss forms it
+    masks = torch.zeros((cfg.num_planes, H, W), dtype=torch.float64, device="cuda:0")
+    opt = PipelineOptions(lambda_opacity=0.0)
+    b, g = gpu_ctx.total_loss(cam, cfg, target, masks, opt, n=scene.size())
+    assert b.recon == 0.0 and b.psnr_mean == 99.0 and abs(b.ssim) < 1e-12
+    worst = max(float(v.abs().max()) for k, v in g.items() if k != "mu_screen")
+    assert worst < 1e-8, worst
