@@ -53,6 +53,14 @@ def training_golden(ref):
     for adam in (0, 1):
         want, applied = ref.optimizer_run(scene, steps, OPT_CFG, use_adam=bool(adam), schedule_total=3)
         out.update({f"op{adam}_applied": applied, **{f"op{adam}_{n}": want[n] for n in GROUPS}})
+    # phase-only conversion (phase_only.cpp) of a rendered 32x32 hologram
+    pcfg = WaveConfig(nx=32, ny=32, wavelengths=RGB, num_planes=2)
+    P = ref.pipeline_forward(synthetic_scene(60, pcfg, 17), front_camera(pcfg), pcfg, RenderSettings(),
+                             PropagationOptions()).hologram
+    theta = np.angle(P) + np.random.default_rng(500).uniform(-0.3, 0.3, P.shape)
+    pl, pg = ref.phase_only_loss(P, theta, pcfg)
+    pphase, ptrace = ref.convert_phase_only(P, pcfg, 12, 0.05)
+    out.update(po_P=P, po_theta=theta, po_loss=pl, po_grad=pg, po_phase=pphase, po_trace=ptrace)
     path = os.path.join(HERE, "training.npz")
     np.savez_compressed(path, **out)
     print("training", os.path.getsize(path), "bytes")

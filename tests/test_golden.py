@@ -172,3 +172,34 @@ def test_gpu_optimizer_matches_golden(gpu_ctx, adam):
     for k in GROUPS:
         assert np.allclose(np.ravel(getattr(out, k)), t[f"op{adam}_{k}"], rtol=1e-13, atol=1e-15), k
     opt.close()
+
+
+def test_reference_reproduces_training_golden(ref_oracle):
+    """CPU: the reference build regenerates the committed training fixtures bit
+    for bit (losses, optimizer runs, phase-only loss and conversion)."""
+    t = np.load(os.path.join(HERE, "golden", "training.npz"))
+    for plain in (0, 1):
+        r, s, ps, g = ref_oracle.losses(t["ls_I"], t["ls_G"], t["ls_M"], lambda_ssim=0.2, plain=bool(plain))
+        assert r == float(t[f"ls{plain}_recon"]) and s == float(t[f"ls{plain}_ssim"])
+        assert np.array_equal(ps, t[f"ls{plain}_psnr"]) and np.array_equal(g, t[f"ls{plain}_grad"])
+    cfg = WaveConfig(nx=32, ny=32, num_planes=2)
+    pl, pg = ref_oracle.phase_only_loss(t["po_P"], t["po_theta"], cfg)
+    assert pl == float(t["po_loss"]) and np.array_equal(pg, t["po_grad"])
+    phase, trace = ref_oracle.convert_phase_only(t["po_P"], cfg, 12, 0.05)
+    assert np.array_equal(trace, t["po_trace"]) and np.array_equal(phase, t["po_phase"])
+
+
+@pytest.mark.gpu
+def test_gpu_phase_only_matches_golden(gpu_ctx):
+    # phase_only.cpp of the reference, stored: f64 on the GPU -> loss and gradient
+    # within 1e-10, a 12-iteration conversion trace within 1e-8
+    from paper_2506_08350_b200 import api
+
+    t = np.load(os.path.join(HERE, "golden", "training.npz"))
+    cfg = WaveConfig(nx=32, ny=32, num_planes=2)
+    loss, g = api.phase_only_loss(t["po_P"], t["po_theta"], cfg, want_grad=True, ctx=gpu_ctx)
+    assert abs(loss - float(t["po_loss"])) <= 1e-10 * abs(float(t["po_loss"]))
+    assert rel_l2(g, t["po_grad"]) <= 1e-10
+    res = api.convert_phase_only(t["po_P"], cfg, 12, 0.05, ctx=gpu_ctx)
+    assert np.allclose(res.trace, t["po_trace"], rtol=1e-8, atol=0)
+    assert np.max(np.abs(res.hologram.phase - t["po_phase"])) <= 1e-7
