@@ -20,8 +20,13 @@
 // first stage of the reversed inverse plan [Rk..R1] touch the same (q, r, b, i)
 // per thread, which lets a spectrum stay in registers between them.
 //
-// Shared-memory layout: element i of transform b at [i * NB + b] (batch index
-// fastest); a warp then touches 32 / NB consecutive rows of NB complex values.
+// Shared-memory layout (PadLayout): element i of transform b at
+// [(i + (i / R1) * pad) * NB + b], R1 = the plan's first radix (batch index
+// fastest; a warp touches 32 / NB consecutive rows of NB complex values).
+// Every index a stage forms is a butterfly base plus a compile-time multiple of
+// R1 (or, in the first stage, R1 j + r with r < R1), so each shared-memory access
+// is one base register plus an immediate offset; pad is the smallest that
+// spreads the first stage's stride-R1 writes evenly over the banks.
 #pragma once
 
 #include "fft.cuh"
@@ -51,18 +56,56 @@ struct RevPlan<Radices<R, Rs...>> {
 template <int N, int NB, int NT>
 struct Batch {
     static constexpr int kN = N, kNB = NB, kNT = NT;
-    // one pad slot per 32 complex values: the stride-R writes of early Stockham
-    // stages (i = R j + r) would otherwise land 32 lanes on one bank pair
-    static constexpr int kSmemElems = ((N * NB + (N * NB) / 32 + 1) + 1) & ~1;  // even: 16-byte multiple
-    static __device__ __forceinline__ int at(int b, int i) {
-        const int c = i * NB + b;
-        return c + (c >> 5);
+};
+
+template <class P>
+struct FirstRadix;
+template <int R, int... Rs>
+struct FirstRadix<Radices<R, Rs...>> {
+    static constexpr int value = R;
+};
+
+// smallest pad for which one warp's first-stage writes (lanes b = t % NB,
+// j = t / NB, element R1 j, 8-byte complex = two 4-byte banks) hit no bank more
+// than the two times a 256-byte access needs anyway
+constexpr int pick_pad(int R1, int NB) {
+    for (int p = 0; p < 64; ++p) {
+        int cnt[32] = {};
+        int worst = 0;
+        for (int t = 0; t < 32; ++t) {
+            const int b = t % NB, j = t / NB;
+            const int word = 2 * ((R1 + p) * j * NB + b);
+            for (int k = 0; k < 2; ++k) {
+                const int c = ++cnt[(word + k) % 32];
+                worst = c > worst ? c : worst;
+            }
+        }
+        if (worst <= 2) return p;
     }
+    return 0;
+}
+
+template <int N, int NB, int R1>
+struct PadLayout {
+    static constexpr int kPad = pick_pad(R1, NB);
+    static constexpr int kElems = (NB * (N + (N / R1) * kPad) + 1) & ~1;  // even: 16-byte multiple
+    static constexpr int kR1 = R1;
+    static __device__ __forceinline__ int at(int b, int i) { return (i + (i / R1) * kPad) * NB + b; }
+    // at(b, i + d) - at(b, i) for d a multiple of R1
+    static constexpr int off(int d) { return (d + (d / R1) * kPad) * NB; }
+};
+
+// shared-memory elements of batch B for plan P and its reverse (the inverse)
+template <class B, class P>
+struct FftSmem {
+    static constexpr int kF = PadLayout<B::kN, B::kNB, FirstRadix<P>::value>::kElems;
+    static constexpr int kI = PadLayout<B::kN, B::kNB, FirstRadix<typename RevPlan<P>::type>::value>::kElems;
+    static constexpr int kElems = kF > kI ? kF : kI;
 };
 
 // One stage: radix R, ns = product of the earlier radices; FIRST/LAST select the
 // functor paths.
-template <class T, int DIR, class B, int R, int NS, bool FIRST, bool LAST>
+template <class T, int DIR, class B, class Lay, int R, int NS, bool FIRST, bool LAST>
 struct Stage {
     static constexpr int N = B::kN, NB = B::kNB, NT = B::kNT;
     static constexpr int M = N / R;
@@ -95,24 +138,32 @@ struct Stage {
                 if (TOT % NT == 0 || t < TOT) {
                     const int b = t % NB, j = t / NB;
                     cx<T> v[R];
+                    if constexpr (!FIRST) {
+                        static_assert(M % Lay::kR1 == 0, "stage reads must step by multiples of R1");
+                    }
+                    const int a0 = FIRST ? 0 : Lay::at(b, j);
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         const int i = j + r * M;
                         if constexpr (FIRST)
                             v[r] = load(q, r, b, i);
                         else
-                            v[r] = sm[B::at(b, i)];
+                            v[r] = sm[a0 + Lay::off(r * M)];
                     }
                     butterfly(v, j, tw);
                     const int k = j % NS;
                     const int base = (j - k) * R + k;
+                    if constexpr (!LAST) {
+                        static_assert(NS == 1 && R == Lay::kR1, "a streaming write stage is the plan's first");
+                    }
+                    const int aw = LAST ? 0 : Lay::at(b, base);
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         const int i = base + r * NS;
                         if constexpr (LAST)
                             store(q, r, b, i, v[r]);
                         else
-                            sm[B::at(b, i)] = v[r];
+                            sm[aw + r * NB] = v[r];  // base = R1 j, r < R1
                     }
                 }
             }
@@ -120,17 +171,23 @@ struct Stage {
             // before the caller (or its next transform) writes sm again
             if constexpr (!(FIRST && LAST)) __syncthreads();
             if constexpr (FIRST) hook();  // every load of the first stage has completed
-            return;
+        } else {
+            run_middle(sm, tw);
         }
-        // Middle stage, in place: hold all of this thread's butterflies, barrier, write.
+    }
+
+    // Middle stage, in place: hold all of this thread's butterflies, barrier, write.
+    static __device__ __forceinline__ void run_middle(cx<T>* sm, const cx<T>* __restrict__ tw) {
         cx<T> v[BPT][R];
 #pragma unroll
         for (int q = 0; q < BPT; ++q) {
             const int t = threadIdx.x + q * NT;
             if (TOT % NT == 0 || t < TOT) {
                 const int b = t % NB, j = t / NB;
+                static_assert(M % Lay::kR1 == 0 && NS % Lay::kR1 == 0, "middle stages step by multiples of R1");
+                const int a0 = Lay::at(b, j);
 #pragma unroll
-                for (int r = 0; r < R; ++r) v[q][r] = sm[B::at(b, j + r * M)];
+                for (int r = 0; r < R; ++r) v[q][r] = sm[a0 + Lay::off(r * M)];
             }
         }
         __syncthreads();  // every read of sm done before any write
@@ -142,31 +199,32 @@ struct Stage {
                 butterfly(v[q], j, tw);
                 const int k = j % NS;
                 const int base = (j - k) * R + k;
+                const int aw = Lay::at(b, base);
 #pragma unroll
-                for (int r = 0; r < R; ++r) sm[B::at(b, base + r * NS)] = v[q][r];
+                for (int r = 0; r < R; ++r) sm[aw + Lay::off(r * NS)] = v[q][r];
             }
         }
         __syncthreads();
     }
 };
 
-template <class T, int DIR, class B, int NS, bool FIRST, class P>
+template <class T, int DIR, class B, class Lay, int NS, bool FIRST, class P>
 struct Stages;
 
-template <class T, int DIR, class B, int NS, bool FIRST, int R>
-struct Stages<T, DIR, B, NS, FIRST, Radices<R>> {
+template <class T, int DIR, class B, class Lay, int NS, bool FIRST, int R>
+struct Stages<T, DIR, B, Lay, NS, FIRST, Radices<R>> {
     template <class Load, class Store, class Hook>
     static __device__ __forceinline__ void run(cx<T>* sm, const cx<T>* tw, Load& load, Store& store, Hook& hook) {
-        Stage<T, DIR, B, R, NS, FIRST, true>::run(sm, tw, load, store, hook);
+        Stage<T, DIR, B, Lay, R, NS, FIRST, true>::run(sm, tw, load, store, hook);
     }
 };
 
-template <class T, int DIR, class B, int NS, bool FIRST, int R, int R2, int... Rs>
-struct Stages<T, DIR, B, NS, FIRST, Radices<R, R2, Rs...>> {
+template <class T, int DIR, class B, class Lay, int NS, bool FIRST, int R, int R2, int... Rs>
+struct Stages<T, DIR, B, Lay, NS, FIRST, Radices<R, R2, Rs...>> {
     template <class Load, class Store, class Hook>
     static __device__ __forceinline__ void run(cx<T>* sm, const cx<T>* tw, Load& load, Store& store, Hook& hook) {
-        Stage<T, DIR, B, R, NS, FIRST, false>::run(sm, tw, load, store, hook);
-        Stages<T, DIR, B, NS * R, false, Radices<R2, Rs...>>::run(sm, tw, load, store, hook);
+        Stage<T, DIR, B, Lay, R, NS, FIRST, false>::run(sm, tw, load, store, hook);
+        Stages<T, DIR, B, Lay, NS * R, false, Radices<R2, Rs...>>::run(sm, tw, load, store, hook);
     }
 };
 
@@ -178,7 +236,8 @@ struct Stages<T, DIR, B, NS, FIRST, Radices<R, R2, Rs...>> {
 template <class T, int DIR, class B, class P, class Load, class Store, class Hook>
 __device__ __forceinline__ void fft_static(cx<T>* sm, const cx<T>* __restrict__ tw, Load load, Store store,
                                            Hook hook) {
-    Stages<T, DIR, B, 1, true, P>::run(sm, tw, load, store, hook);
+    using Lay = PadLayout<B::kN, B::kNB, FirstRadix<P>::value>;
+    Stages<T, DIR, B, Lay, 1, true, P>::run(sm, tw, load, store, hook);
 }
 template <class T, int DIR, class B, class P, class Load, class Store>
 __device__ __forceinline__ void fft_static(cx<T>* sm, const cx<T>* __restrict__ tw, Load load, Store store) {

@@ -61,7 +61,8 @@ template <int H_, int NB_, int NT_, int MINB_>
 struct ColCfgT {
     static constexpr int H = H_, NB = NB_, NT = NT_, kMinBlocks = MINB_;
     using B = Batch<H, NB, NT>;
-    static constexpr size_t kSmem = sizeof(cx<float>) * (B::kSmemElems + (HOLO_COL_SMEM_TW ? H : 0));
+    static constexpr int kWorkElems = FftSmem<B, typename PlanOf<H>::type>::kElems;
+    static constexpr size_t kSmem = sizeof(cx<float>) * (kWorkElems + (HOLO_COL_SMEM_TW ? H : 0));
 };
 
 // twiddles for a column pass: staged into shared memory before the first stage
@@ -69,7 +70,7 @@ struct ColCfgT {
 template <class Cfg>
 __device__ __forceinline__ const cx<float>* col_twiddles(cx<float>* sm, const cx<float>* __restrict__ tw) {
     if constexpr (HOLO_COL_SMEM_TW) {
-        cx<float>* s_tw = sm + Cfg::B::kSmemElems;
+        cx<float>* s_tw = sm + Cfg::kWorkElems;
         for (int k = threadIdx.x; k < Cfg::H; k += Cfg::NT) s_tw[k] = tw[k];
         return s_tw;
     }
@@ -184,7 +185,7 @@ template <class Cfg, int MODE>
 struct RowSmem {
     using LS = LastStage<typename Cfg::B, typename PlanOf<Cfg::W>::type>;
     static constexpr int kRowPad = Cfg::W + 8;
-    static constexpr size_t kWork = sizeof(cx<float>) * Cfg::B::kSmemElems;
+    static constexpr size_t kWork = sizeof(cx<float>) * FftSmem<typename Cfg::B, typename PlanOf<Cfg::W>::type>::kElems;
     static constexpr size_t kPre = MODE == kModeReplay ? 0 : sizeof(cx<float>) * Cfg::NBR * kRowPad;
     static constexpr size_t kTw = sizeof(cx<float>) * Cfg::W;
     static constexpr size_t kG = sizeof(float) * LS::kBPT * LS::kR * Cfg::NT;
