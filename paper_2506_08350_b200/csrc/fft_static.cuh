@@ -112,15 +112,25 @@ struct Stage {
     static constexpr int TOT = M * NB;
     static constexpr int BPT = (TOT + NT - 1) / NT;
 
+    // Twiddles w^r, r < R: the powers of two are read from the table, the others
+    // formed as products of at most three of them (w^r = w^p w^(r-p), p the
+    // largest power of two below r) -- FMA-pipe work instead of shared-memory
+    // reads, the pass's bottleneck; error <= 3 roundings of fp32.
     static __device__ __forceinline__ void butterfly(cx<T>* v, int j, const cx<T>* __restrict__ tw) {
         const int k = j % NS;
         if constexpr (NS > 1) {
             const int step = (N / (NS * R)) * k;
+            cx<T> w[R];
 #pragma unroll
             for (int r = 1; r < R; ++r) {
-                cx<T> w = tw[r * step];
-                if (DIR > 0) w.y = -w.y;
-                v[r] = v[r] * w;
+                if ((r & (r - 1)) == 0) {
+                    w[r] = tw[r * step];
+                    if (DIR > 0) w[r].y = -w[r].y;
+                } else {
+                    const int p = 1 << (31 - __clz(r));
+                    w[r] = w[p] * w[r - p];
+                }
+                v[r] = v[r] * w[r];
             }
         }
         Dft<R, DIR, T>::run(v);
