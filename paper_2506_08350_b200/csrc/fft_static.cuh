@@ -112,10 +112,11 @@ struct Stage {
     static constexpr int TOT = M * NB;
     static constexpr int BPT = (TOT + NT - 1) / NT;
 
-    // Twiddles w^r, r < R: the powers of two are read from the table, the others
-    // formed as products of at most three of them (w^r = w^p w^(r-p), p the
-    // largest power of two below r) -- FMA-pipe work instead of shared-memory
-    // reads, the pass's bottleneck; error <= 3 roundings of fp32.
+    // Twiddles w^r, r < R: w is read from the table (consecutive k: no bank
+    // conflicts), the powers of two squared up from it and the others formed as
+    // products of them (w^r = w^p w^(r-p), p the largest power of two below r) --
+    // FMA-pipe work instead of shared-memory reads (the row pass's bottleneck),
+    // at most 6 fp32 roundings.
     static __device__ __forceinline__ void butterfly(cx<T>* v, int j, const cx<T>* __restrict__ tw) {
         const int k = j % NS;
         if constexpr (NS > 1) {
@@ -123,9 +124,11 @@ struct Stage {
             cx<T> w[R];
 #pragma unroll
             for (int r = 1; r < R; ++r) {
-                if ((r & (r - 1)) == 0) {
-                    w[r] = tw[r * step];
-                    if (DIR > 0) w[r].y = -w[r].y;
+                if (r == 1) {
+                    w[1] = tw[step];
+                    if (DIR > 0) w[1].y = -w[1].y;
+                } else if ((r & (r - 1)) == 0) {
+                    w[r] = w[r / 2] * w[r / 2];
                 } else {
                     const int p = 1 << (31 - __clz(r));
                     w[r] = w[p] * w[r - p];
