@@ -71,6 +71,21 @@ STAGE_KERNEL = {"preprocess": "k_preprocess", "composite": "k_composite", "fft_p
                 "fft_pass2": "k_row_fused", "fft_pass3": "k_row_fused", "fft_pass4": "k_col_inv_epi"}
 
 
+def ncu_metric(stage, metric):
+    """One column of the newest forward-frame ncu summary for the stage's kernel."""
+    import csv
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r[0-9][0-9]_kernels.csv")))
+    prefix = STAGE_KERNEL.get(stage)
+    if not files or not prefix:
+        return None
+    for row in csv.DictReader(open(files[-1])):
+        if row["kernel"].startswith(prefix) and row.get(metric):
+            return float(row[metric])
+    return None
+
+
 def ncu_traffic(stage):
     """dram read + write bytes per launch of the stage's kernel from the newest
     committed forward-frame ncu --set full summary (profiles/rNN_kernels.csv), or None."""
@@ -343,6 +358,12 @@ def main():
                 "frac": d["GBps"] / hbm_peak, "traffic": ncu_traffic(dom), "traffic_source": "profiles (ncu --set full, per launch)", "peak_kind": peak_kind,
                 "frame_bytes": sum(sb.values()), "frame_frac": sum(sb.values()) / (ms_per_step * 1e-3) / 1e9 /
                 (hbm_peak * world)}
+    if dom == "composite":
+        # compositing is FP32 / MUFU issue-bound, not HBM-bound: its
+        # roofline is instruction issue; report the measured issue utilisation too
+        ia = ncu_metric(dom, "smsp__issue_active.avg.pct_of_peak_sustained_active")
+        roofline["compute"] = {"bound": "fp32/mufu issue", "issue_active": ia / 100.0 if ia is not None else None,
+                               "source": "profiles (ncu --set full)"}
 
     # ---------------- end to end through the public API: pinned host scene in, results out
     # Every frame uploads the scene from pinned host memory and reads the hologram
