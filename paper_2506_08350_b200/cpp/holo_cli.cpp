@@ -10,9 +10,12 @@
 //               [--wavelength L ...] [--distance D] [--volume-depth V] [--focal-px F]
 //               [--pose x y z rx ry rz]
 //   holo bench [--grid N] [--n-list a,b,...] [--l-list a,b,...] [--out CSV]
+//   holo phase-only --in F.hfld --out PHASE.png [--iters N] [--bits 8|10] [--lr R]
+//                   [--lambda-ssim X] [--pixel-pitch P] [--wavelength L ...] [--no-pad]
 //
-// The reference's train / phase-only / gradcheck / stats subcommands and its run
+// The reference's train / gradcheck / stats subcommands and its run
 // configuration JSON are outside this repository's scope.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -24,7 +27,10 @@
 #include <string>
 #include <vector>
 
+#include <zlib.h>
+
 #include "holo/field_io.hpp"
+#include "holo/phase_only.hpp"
 #include "holo/pipeline.hpp"
 #include "holo/propagation.hpp"
 #include "holo/scene_io.hpp"
@@ -251,16 +257,128 @@ int cmd_bench(const Args& a) {
     return 0;
 }
 
+// ---- phase-only (holo_main.cpp:344-386) and its quantised phase PNGs (png_io.cpp:160-187)
+
+void put_be32(std::string& s, unsigned v) {
+    for (int k = 3; k >= 0; --k) s += static_cast<char>((v >> (8 * k)) & 0xff);
+}
+
+void png_chunk(std::string& out, const char* type, const std::string& data) {
+    put_be32(out, static_cast<unsigned>(data.size()));
+    const std::string td = std::string(type, 4) + data;
+    out += td;
+    put_be32(out, static_cast<unsigned>(crc32(0L, reinterpret_cast<const Bytef*>(td.data()), static_cast<uInt>(td.size()))));
+}
+
+// grayscale PNG, 8 or 16 bits per sample; `rows` holds the raw big-endian samples
+void write_gray_png(const std::string& path, int w, int h, int depth, const std::string& raw) {
+    std::string filtered;
+    const size_t row_bytes = static_cast<size_t>(w) * (depth / 8);
+    filtered.reserve((row_bytes + 1) * h);
+    for (int y = 0; y < h; ++y) {
+        filtered += '\0';  // filter type None
+        filtered.append(raw, static_cast<size_t>(y) * row_bytes, row_bytes);
+    }
+    uLongf zlen = compressBound(static_cast<uLong>(filtered.size()));
+    std::string z(zlen, '\0');
+    if (compress2(reinterpret_cast<Bytef*>(z.data()), &zlen, reinterpret_cast<const Bytef*>(filtered.data()),
+                  static_cast<uLong>(filtered.size()), 6) != Z_OK)
+        throw HoloError("io", "png: compression failed");
+    z.resize(zlen);
+    std::string ihdr;
+    put_be32(ihdr, static_cast<unsigned>(w));
+    put_be32(ihdr, static_cast<unsigned>(h));
+    ihdr += static_cast<char>(depth);
+    ihdr += std::string("\0\0\0\0", 4);  // gray, deflate, no filter method, no interlace
+    std::string png = "\x89PNG\r\n\x1a\n";
+    png_chunk(png, "IHDR", ihdr);
+    png_chunk(png, "IDAT", z);
+    png_chunk(png, "IEND", "");
+    std::ofstream o(path, std::ios::binary);
+    if (!o) throw HoloError("io", "cannot open for writing: " + path);
+    o.write(png.data(), static_cast<std::streamsize>(png.size()));
+    if (!o) throw HoloError("io", "write failed: " + path);
+}
+
+// png_io.cpp:160-187: codes lround(wrap(phi) / step) mod 2^bits; 10-bit codes
+// stored as 16-bit samples (code << 6 | code >> 4)
+void write_phase_png(const std::string& path, const double* phase, int w, int h, int bits) {
+    if (bits != 8 && bits != 10) throw HoloError("io", "png: phase bit depth must be 8 or 10");
+    const int levels = 1 << bits;
+    const double step = 2.0 * 3.14159265358979323846 / levels;
+    const size_t n = static_cast<size_t>(w) * h;
+    std::string raw;
+    raw.reserve(n * (bits == 8 ? 1 : 2));
+    for (size_t i = 0; i < n; ++i) {
+        const unsigned code = static_cast<unsigned>(std::lround(wrap_phase(phase[i]) / step) % levels);
+        if (bits == 8) {
+            raw += static_cast<char>(code);
+        } else {
+            const unsigned v = (code << 6) | (code >> 4);
+            raw += static_cast<char>((v >> 8) & 0xff);
+            raw += static_cast<char>(v & 0xff);
+        }
+    }
+    write_gray_png(path, w, h, bits == 8 ? 8 : 16, raw);
+}
+
+// png_io.cpp:217-226
+std::string channel_path(const std::string& base, int ch, int channels) {
+    if (channels == 1) return base;
+    static const char* rgb[3] = {"_r", "_g", "_b"};
+    const std::string suffix = channels == 3 ? rgb[ch] : "_c" + std::to_string(ch);
+    const size_t dot = base.find_last_of('.');
+    const size_t slash = base.find_last_of("/\\");
+    if (dot == std::string::npos || (slash != std::string::npos && dot < slash)) return base + suffix;
+    return base.substr(0, dot) + suffix + base.substr(dot);
+}
+
+int cmd_phase_only(const Args& a) {
+    a.only({"in", "out", "iters", "bits", "lr", "lambda-ssim", "pixel-pitch", "wavelength", "no-pad"});
+    a.require("in");
+    a.require("out");
+    const int bits = static_cast<int>(a.num("bits", 8));
+    if (bits != 8 && bits != 10) throw HoloError("usage", "--bits must be 8 or 10");
+    const double pitch = a.num("pixel-pitch", 3.74e-6);
+    const ComplexField P = read_field(a.str("in"), pitch);
+    WaveConfig optics;  // the run configuration's default optics
+    optics.nx = P.w;
+    optics.ny = P.h;
+    optics.pitch = pitch;
+    optics.wavelengths = wavelengths_for(a.nums("wavelength"), P.c);
+    PhaseOnlyOptions opt;
+    opt.lambda_ssim = a.num("lambda-ssim", 1.0);
+    if (a.has("no-pad")) opt.prop.pad2x = false;
+    const int iters = static_cast<int>(a.num("iters", 1000));
+    const PhaseOnlyResult res = convert_phase_only(P, optics, iters, a.num("lr", 0.02), opt);
+    std::string files = "[";
+    const std::string out = a.str("out");
+    for (int ch = 0; ch < P.c; ++ch) {
+        const std::string path = channel_path(out, ch, P.c);
+        write_phase_png(path, res.hologram.phase.data() + static_cast<size_t>(ch) * P.h * P.w, P.w, P.h, bits);
+        files += (ch ? "," : "") + jstr(path);
+    }
+    files += "]";
+    const double init = res.trace.front();
+    double best = init;
+    for (double v : res.trace) best = std::min(best, v);
+    std::cout << "{\"command\":\"phase-only\",\"iterations\":" << iters << ",\"bits\":" << bits
+              << ",\"initial_loss\":" << jnum(init) << ",\"final_loss\":" << jnum(best)
+              << ",\"ratio\":" << jnum(init > 0.0 ? best / init : 0.0) << ",\"files\":" << files << "}\n";
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
     try {
-        if (argc < 2) throw HoloError("usage", "a subcommand is required: render | propagate | bench");
+        if (argc < 2) throw HoloError("usage", "a subcommand is required: render | propagate | bench | phase-only");
         const std::string cmd = argv[1];
         const Args a(argc, argv, 2);
         if (cmd == "propagate") return cmd_propagate(a);
         if (cmd == "render") return cmd_render(a);
         if (cmd == "bench") return cmd_bench(a);
+        if (cmd == "phase-only") return cmd_phase_only(a);
         throw HoloError("usage", "unknown subcommand: " + cmd);
     } catch (const HoloError& e) {
         std::cerr << "{\"error\":{\"kind\":" << jstr(e.kind) << ",\"message\":" << jstr(e.what()) << "}}\n";

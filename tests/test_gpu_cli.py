@@ -86,3 +86,60 @@ def test_bench_writes_csv(tmp_path):
     assert lines[0] == "n,l,raster_seconds,record_seconds,total_seconds"
     assert [ln.split(",")[:2] for ln in lines[1:]] == [["0", "1"], ["50", "1"]]
     assert all(float(ln.split(",")[4]) > 0 for ln in lines[1:])
+
+
+def read_gray_png(path):
+    """Minimal PNG reader for the grayscale 8 / 16-bit, filter-0 files `holo` writes."""
+    import struct
+    import zlib
+
+    data = open(path, "rb").read()
+    assert data[:8] == b"\x89PNG\r\n\x1a\n"
+    pos, idat, w = 8, b"", None
+    while pos < len(data):
+        n = struct.unpack(">I", data[pos:pos + 4])[0]
+        typ, body = data[pos + 4:pos + 8], data[pos + 8:pos + 8 + n]
+        assert zlib.crc32(typ + body) == struct.unpack(">I", data[pos + 8 + n:pos + 12 + n])[0]
+        if typ == b"IHDR":
+            w, h, depth, color = struct.unpack(">IIBB", body[:10])
+            assert color == 0
+        elif typ == b"IDAT":
+            idat += body
+        pos += 12 + n
+    raw = zlib.decompress(idat)
+    bpp = depth // 8
+    rows = [raw[y * (w * bpp + 1):(y + 1) * (w * bpp + 1)] for y in range(h)]
+    assert all(r[0] == 0 for r in rows)
+    a = np.frombuffer(b"".join(r[1:] for r in rows), dtype=">u2" if depth == 16 else "u1").reshape(h, w)
+    return a.astype(np.int64), depth
+
+
+def test_phase_only_emits_quantized_phase_planes(tmp_path, gpu_ctx):
+    """test_cli.cpp:220-245: single-channel hologram, 5 iterations, 10-bit phase PNG."""
+    rng = np.random.default_rng(4)
+    P = rng.uniform(0.2, 1.0, (1, 32, 32)) * np.exp(1j * rng.uniform(0.0, 2 * np.pi, (1, 32, 32)))
+    write_field(tmp_path / "holo.hfld", P)
+    r = run("phase-only", "--in", str(tmp_path / "holo.hfld"), "--out", str(tmp_path / "phase.png"), "--iters", "5",
+            "--bits", "10", "--wavelength", "532e-9")
+    assert r.returncode == 0, r.stderr
+    rep = json.loads(r.stdout)
+    assert rep["final_loss"] <= rep["initial_loss"]
+    assert rep["files"] == [str(tmp_path / "phase.png")]  # one channel keeps the base name
+    codes, depth = read_gray_png(tmp_path / "phase.png")
+    assert codes.shape == (32, 32) and depth == 16
+    phase = (codes >> 6) * (2 * np.pi / 1024)  # read_phase_png (png_io.cpp:189-200)
+    assert np.all((phase >= 0.0) & (phase < 2 * np.pi))
+    # the quantised planes are the conversion's own phases: same GPU conversion in process
+    cfg = WaveConfig(nx=32, ny=32, wavelengths=(532e-9,), num_planes=2)
+    res = api.convert_phase_only(P, cfg, 5, ctx=gpu_ctx)
+    want = np.round(np.mod(res.hologram.phase[0], 2 * np.pi) / (2 * np.pi / 1024)).astype(np.int64) % 1024
+    assert np.array_equal(codes >> 6, want)
+    # three channels: _r / _g / _b files; bad bit depth: usage error, exit 2
+    P3 = np.concatenate([P, P, P])
+    write_field(tmp_path / "h3.hfld", P3)
+    r = run("phase-only", "--in", str(tmp_path / "h3.hfld"), "--out", str(tmp_path / "p.png"), "--iters", "2")
+    assert r.returncode == 0, r.stderr
+    assert json.loads(r.stdout)["files"] == [str(tmp_path / f"p_{c}.png") for c in "rgb"]
+    assert read_gray_png(tmp_path / "p_g.png")[1] == 8
+    bad = run("phase-only", "--in", str(tmp_path / "holo.hfld"), "--out", str(tmp_path / "x.png"), "--bits", "12")
+    assert bad.returncode == 2 and json.loads(bad.stderr)["error"]["kind"] == "usage"
