@@ -71,16 +71,17 @@ __device__ __forceinline__ void reduce_scatter_step(float (&w)[16], int lane) {
 template <int TILE, int C>
 __global__ void __launch_bounds__(TILE * TILE) k_raster_bwd(RasterBwdArgs a) {
     constexpr int NT = TILE * TILE;
-    constexpr int kStage = 128;  // with the per-warp partials: 4 CTAs of 256 threads per SM
+    constexpr int kStage = TILE == 32 ? 32 : 128;  // entries per batch (per-warp partials: 53 KB at 16x16)
     constexpr int kBlocksX = TILE / 8;
     __shared__ Staged s_rec[kStage];
     __shared__ float4 s_box[kStage];
     __shared__ int s_g[kStage];
     __shared__ BwdRec s_brec[kStage];  // pad[0] carries rho
     __shared__ float s_acc[kStage * kGradVals];
-    // per-warp partials of the current 32-entry chunk, summed over the warps in a
-    // fixed order (deterministic: no float atomics)
-    extern __shared__ float s_part[];  // [NT / 32][32][kGradVals]
+    // per-warp partials of the batch's entries, summed over the warps in a fixed
+    // order once per batch (deterministic: no float atomics, one barrier pair per
+    // batch rather than per 32-entry chunk)
+    extern __shared__ float s_part[];  // [NT / 32][kStage][kGradVals]
     constexpr int NW = NT / 32;
 
     const int tx = blockIdx.x, ty = blockIdx.y, lplane = blockIdx.z;
@@ -177,10 +178,10 @@ __global__ void __launch_bounds__(TILE * TILE) k_raster_bwd(RasterBwdArgs a) {
         const int cnt = min(n - base, kStage);
         if (nb > 1 || !replay) stage(base, cnt);  // one batch: still staged from pass 1
         __syncthreads();
-        float* my_part = s_part + warp * 32 * kGradVals;
+        float* my_part = s_part + warp * kStage * kGradVals;
+        for (int i = lane; i < cnt * kGradVals; i += 32) my_part[i] = 0.0f;
+        __syncwarp();
         for (int c0 = ((cnt - 1) / 32) * 32; c0 >= 0; c0 -= 32) {
-            for (int i = lane; i < 32 * kGradVals; i += 32) my_part[i] = 0.0f;
-            __syncwarp();
             const bool live = active && e_last >= base + c0;
             if (__any_sync(0xffffffffu, live)) {
                 const bool hit = c0 + lane < cnt && box_hits(s_box[c0 + lane], bxlo, bxhi, bylo, byhi);
@@ -246,20 +247,19 @@ __global__ void __launch_bounds__(TILE * TILE) k_raster_bwd(RasterBwdArgs a) {
                     reduce_scatter_step<2, 1>(w, lane);
                     w[0] += __shfl_xor_sync(0xffffffffu, w[0], 1);
                     const int q = (lane >> 1) & 15;
-                    if ((lane & 1) == 0 && q < kGradVals) my_part[j * kGradVals + q] = w[0];
+                    if ((lane & 1) == 0 && q < kGradVals) my_part[(c0 + j) * kGradVals + q] = w[0];
                 }
             }
-            __syncthreads();
-            // the chunk's entries: warp partials summed in warp order
-            const int nc = min(32, cnt - c0);
-            for (int i = tid; i < nc * kGradVals; i += NT) {
-                float sum = 0.0f;
-#pragma unroll
-                for (int wi = 0; wi < NW; ++wi) sum += s_part[wi * 32 * kGradVals + i];
-                s_acc[c0 * kGradVals + i] = sum;
-            }
-            __syncthreads();
         }
+        __syncthreads();
+        // the batch's entries: warp partials summed in warp order
+        for (int i = tid; i < cnt * kGradVals; i += NT) {
+            float sum = 0.0f;
+#pragma unroll
+            for (int wi = 0; wi < NW; ++wi) sum += s_part[wi * kStage * kGradVals + i];
+            s_acc[i] = sum;
+        }
+        __syncthreads();
         // egrad is ordered per Gaussian: its k-th entry (bucket order: plane, then
         // tile row, then tile column) at goff[g] + k, so the merge reads it in the
         // reference's order without searching the buckets
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(256) k_bwd_gauss(GaussBwdArgs a) {
 
 template <int TILE, int C>
 void launch_bwd_c(holo_ctx* ctx, const RasterBwdArgs& a, dim3 grid) {
-    constexpr size_t kPart = sizeof(float) * (TILE * TILE / 32) * 32 * kGradVals;
+    constexpr size_t kPart = sizeof(float) * (TILE * TILE / 32) * (TILE == 32 ? 32 : 128) * kGradVals;
     static bool attr = false;
     if (!attr) {
         HC_CUDA(cudaFuncSetAttribute(k_raster_bwd<TILE, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
