@@ -149,6 +149,10 @@ __global__ void __launch_bounds__(256) k_bucket_emit(PreOut pre, size_t N, int L
                                                      unsigned capacity, unsigned* __restrict__ flags) {
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     if (i >= N) return;
+    // every per-Gaussian load issued up front (one round trip instead of a chain)
+    const unsigned cnt_i = pre.count[i];
+    const int plane_i = soft ? 0 : pre.plane[i];
+    const int4 rect_i = pre.rect[i];
     const unsigned long long key = static_cast<unsigned long long>(__double_as_longlong(pre.zc[i]));
     bool over = false;
     // entries beyond the reserved capacity (asynchronous frames) are dropped and flagged
@@ -162,17 +166,34 @@ __global__ void __launch_bounds__(256) k_bucket_emit(PreOut pre, size_t N, int L
         egidx[e] = static_cast<int>(i);
     };
     if (!soft) {
-        if (pre.count[i] == 0) return;
-        const int l = pre.plane[i];
+        if (cnt_i == 0) return;
+        const int l = plane_i;
         if (l < pb || l >= pe) return;
-        const int4 r = pre.rect[i];
+        const int4 r = rect_i;
         const int w = r.y - r.x, n = w * (r.w - r.z);
         const int b0 = (l - pb) * num_tiles + r.z * tiles_x + r.x;
         if (pre.slots && n <= kSlots) {
-            // slots taken in preprocess: no atomics
+            // slots taken in preprocess: no atomics; all slot and bucket-start
+            // loads in flight before the first store
+            unsigned st[kSlots];
+            int bk[kSlots];
 #pragma unroll
             for (int k = 0; k < kSlots; ++k)
-                if (k < n) put(b0 + (k / w) * tiles_x + k % w, pre.slots[static_cast<size_t>(k) * N + i]);
+                if (k < n) {
+                    bk[k] = b0 + (k / w) * tiles_x + k % w;
+                    st[k] = bstart[bk[k]] + pre.slots[static_cast<size_t>(k) * N + i];
+                }
+#pragma unroll
+            for (int k = 0; k < kSlots; ++k)
+                if (k < n) {
+                    const unsigned e = st[k];
+                    if (e >= capacity) {
+                        over = true;
+                    } else {
+                        ekey[e] = key;
+                        egidx[e] = static_cast<int>(i);
+                    }
+                }
             if (over) atomicOr(flags, kFlagOverflow);
             return;
         }
