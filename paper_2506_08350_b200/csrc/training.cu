@@ -141,22 +141,42 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_ssim_row_sums(const double* 
 }
 
 // out[t] = mul * (sum of v[t * len .. t * len + len) in order) / div, one warp per
-// segment: coalesced 32-value chunks, lane 0 adds them in order via shuffles
-__global__ void k_fold_seg(const double* __restrict__ v, int nseg, int len, double mul, double div,
-                           double* __restrict__ out) {
-    const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-    if (t >= nseg) return;
-    const double* p = v + static_cast<size_t>(t) * len;
+// segment: the warp stages 256-value chunks in shared memory (coalesced) and lane 0
+// adds them in order -- loads run ahead, only the f64 add chain is serial.  Two
+// independent jobs (v0 / v1) can share a launch: warps t >= nseg take the second.
+struct FoldJob {
+    const double* v;
+    double mul, div;
+    double* out;
+};
+constexpr int kFoldChunk = 256;
+__global__ void __launch_bounds__(128) k_fold_seg(FoldJob j0, FoldJob j1, int nseg, int len) {
+    __shared__ double buf[4][kFoldChunk];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int t = blockIdx.x * 4 + warp;
+    if (t >= 2 * nseg || (t >= nseg && j1.v == nullptr)) return;
+    const FoldJob& job = t < nseg ? j0 : j1;
+    if (t >= nseg) t -= nseg;
+    const double* p = job.v + static_cast<size_t>(t) * len;
+    double* sb = buf[warp];
     double acc = 0.0;
-    for (int c0 = 0; c0 < len; c0 += 32) {
-        const int nc = min(32, len - c0);
-        const double x = lane < nc ? p[c0 + lane] : 0.0;
-        for (int k = 0; k < nc; ++k) {
-            const double y = __shfl_sync(0xffffffffu, x, k);
-            acc += y;
+    for (int c0 = 0; c0 < len; c0 += kFoldChunk) {
+        const int nc = min(kFoldChunk, len - c0);
+        for (int k = lane; k < nc; k += 32) sb[k] = p[c0 + k];
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll 16
+            for (int k = 0; k < nc; ++k) acc += sb[k];
         }
+        __syncwarp();
     }
-    if (lane == 0) out[t] = mul * acc / div;
+    if (lane == 0) job.out[t] = job.mul * acc / job.div;
+}
+
+void fold(holo_ctx* ctx, int nseg, int len, const FoldJob& a, const FoldJob& b = FoldJob{nullptr, 1.0, 1.0, nullptr}) {
+    const int warps = b.v ? 2 * nseg : nseg;
+    k_fold_seg<<<(warps + 3) / 4, 128, 0, ctx->stream>>>(a, b, nseg, len);
+    HC_LAUNCHED(ctx);
 }
 
 __global__ void k_fill(double* p, int n, double v) {
@@ -501,13 +521,9 @@ void losses_gpu(holo_ctx* ctx, const double* I, const double* G, const double* m
         k_loss_row_sums<false><<<rb, 32 * kRowWarps, 0, ctx->stream>>>(I, G, masks, C, H, W, rows_n, gscale, grad,
                                                                        rows, prow);
     HC_LAUNCHED(ctx);
-    const unsigned lb = (L + 3) / 4;  // 4 warps (segments) per block
-    k_fold_seg<<<lb, 128, 0, ctx->stream>>>(rows, L, C * H, inv_l * inv_n, 1.0, lsum);
-    HC_LAUNCHED(ctx);
-    k_fold_seg<<<lb, 128, 0, ctx->stream>>>(prow, L, C * H, 1.0, static_cast<double>(n), d_out + 1 + L);
-    HC_LAUNCHED(ctx);
-    k_fold_seg<<<1, 32, 0, ctx->stream>>>(lsum, 1, L, 1.0, 1.0, d_out);
-    HC_LAUNCHED(ctx);
+    // per plane: the recon rows (times inv_l inv_n) and the psnr rows (over n), one launch
+    fold(ctx, L, C * H, FoldJob{rows, inv_l * inv_n, 1.0, lsum}, FoldJob{prow, 1.0, static_cast<double>(n), d_out + 1 + L});
+    fold(ctx, 1, L, FoldJob{lsum, 1.0, 1.0, d_out});
 
     if (!with_ssim) {  // the SSIM term left out: mean SSIM 1 contributes 0
         k_fill<<<1, 32, 0, ctx->stream>>>(d_out + 1, L, 1.0);
@@ -551,10 +567,8 @@ void ssim_gpu(holo_ctx* ctx, const double* I, const double* G, int L, int C, int
                       ctx->stream>>>(smap, W, H, vrows, srows_n, srows);
     HC_LAUNCHED(ctx);
     // per (plane, channel) the rows in order; per plane the channels in order, / n_valid
-    k_fold_seg<<<(L * C + 3) / 4, 128, 0, ctx->stream>>>(srows, L * C, vrows, 1.0, 1.0, ssum);
-    HC_LAUNCHED(ctx);
-    k_fold_seg<<<(L + 3) / 4, 128, 0, ctx->stream>>>(ssum, L, C, 1.0, static_cast<double>(n_valid), d_mean);
-    HC_LAUNCHED(ctx);
+    fold(ctx, L * C, vrows, FoldJob{srows, 1.0, 1.0, ssum});
+    fold(ctx, L, C, FoldJob{ssum, 1.0, static_cast<double>(n_valid), d_mean});
 }
 
 double opacity_term(holo_ctx* ctx, const double* logits, size_t n, double lambda, double* gopac) {
