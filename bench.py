@@ -247,6 +247,12 @@ def main():
         raise SystemExit(f"{Lp} planes do not split over {world} ranks")
     pb, pe = rank * Lp // world, (rank + 1) * Lp // world
     scene = synthetic_scene(c.n, wave, c.seed)
+    if world > 1:
+        # hard plane assignment: each rank holds only its planes' Gaussians
+        # (sharding.plane_subset; the rendered layers are unchanged)
+        from paper_2506_08350_b200.sharding import plane_subset
+
+        scene = plane_subset(scene, pb, pe)
 
     ctx = Context(local)
     ctx.upload_scene(scene)
@@ -344,7 +350,7 @@ def main():
     st = ctx.stage_times()
     ctx.enable_timing(False)
     hbm_peak, peak_kind = load_peaks()
-    sb = stage_bytes(c.n, Lp, Cn, P, E, pe - pb, world > 1, rank == 0)
+    sb = stage_bytes(scene.size(), Lp, Cn, P, E, pe - pb, world > 1, rank == 0)
     stages = {}
     for name in STAGE_NAMES:
         tot_ms, calls = st[name]
@@ -392,7 +398,7 @@ def main():
         def e2e_step(i):
             cx_ = ectxs[i % len(ectxs)]
             holo_h, int_h = bufs[i % len(ectxs)]
-            cx_.upload_scene_pointers(c.n, Lp, ptrs, device=False)
+            cx_.upload_scene_pointers(scene.size(), Lp, ptrs, device=False)
             if world == 1:
                 cx_.render(cam, wave, None, None, outputs=outs)
             else:

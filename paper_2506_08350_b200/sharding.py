@@ -30,6 +30,26 @@ def plane_ranges(num_planes: int, world: int) -> List[Tuple[int, int]]:
     return out
 
 
+def plane_subset(scene, pb: int, pe: int):
+    """The Gaussians whose hard plane assignment (argmax of the plane logits, ties
+    to the lowest index: ste_assign, scene.cpp:132-152) falls in [pb, pe), in
+    their original order.  Under hard assignment a Gaussian contributes to its
+    plane only, and the per-bucket order (depth, then index) is unchanged by an
+    order-preserving subset, so a rank that uploads only this subset renders
+    exactly the layers of the full scene for its planes -- with preprocessing
+    and binning over ~N / world Gaussians instead of N."""
+    import numpy as np
+
+    from .holotypes import GaussianScene
+
+    plane = np.argmax(np.asarray(scene.plane_logits).reshape(scene.size(), scene.num_planes), axis=1)
+    keep = (plane >= pb) & (plane < pe)
+    sub = GaussianScene(num_planes=scene.num_planes)
+    for k in ("positions", "rotations", "log_scales", "amplitudes", "opacity_logits", "phases", "plane_logits"):
+        setattr(sub, k, np.ascontiguousarray(np.asarray(getattr(scene, k))[keep]))
+    return sub
+
+
 def view_ranges(num_views: int, world: int) -> List[Tuple[int, int]]:
     return plane_ranges(num_views, world)
 

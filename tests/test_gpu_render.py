@@ -402,3 +402,28 @@ def test_baseline_config_parity(gpu_ctx, oracle, name):
         assert abs(psnr(ints[l], t) - psnr(r.intensities[l], t)) <= 0.01
     assert np.array_equal(g.raster.bucket_start, r.raster.bucket_start)
     assert np.array_equal(g.raster.entries["gidx"], r.raster.entry_gidx)
+
+
+def test_plane_subset_shards_render_the_same_layers(gpu_ctx):
+    """sharding.plane_subset: a rank holding only its planes' Gaussians renders the
+    full scene's partial spectrum for those planes bit for bit (hard assignment:
+    one plane per Gaussian; an order-preserving subset keeps every bucket's order)."""
+    import torch
+
+    from paper_2506_08350_b200.sharding import plane_ranges, plane_subset
+
+    cfg = WaveConfig(nx=256, ny=256, wavelengths=RGB, num_planes=4)
+    s = synthetic_scene(20000, cfg, 31)
+    cam = wide_camera(cfg)
+    C, H, W = 3, 256, 256
+    for pb, pe in plane_ranges(4, 2):
+        full_part = torch.empty((C, H, W, 2), dtype=torch.float32, device="cuda")
+        gpu_ctx.upload_scene(s)
+        gpu_ctx.render_begin(cam, cfg, None, None, pb, pe, full_part.data_ptr(), 0)
+        sub = plane_subset(s, pb, pe)
+        assert 0 < sub.size() < s.size()
+        sub_part = torch.empty_like(full_part)
+        gpu_ctx.upload_scene(sub)
+        gpu_ctx.render_begin(cam, cfg, None, None, pb, pe, sub_part.data_ptr(), 0)
+        torch.cuda.synchronize()
+        assert torch.equal(full_part, sub_part)

@@ -1,6 +1,7 @@
 """One rank's share of a plane-sharded C3 frame, timed on one GPU (no collective):
 holo_render_begin for planes [0, L/N) and holo_render_end with the hologram and
-those planes' intensities.  Estimates how the per-rank compute shrinks with N; the
+those planes' intensities, the rank holding only its planes' Gaussians
+(sharding.plane_subset, as bench.py's sharded runs do).  Estimates how the per-rank compute shrinks with N; the
 all-reduce of the 49.8 MB spectrum comes on top at N > 1."""
 import json
 import sys
@@ -21,9 +22,12 @@ Cn, H, W, Lp = wave.channels(), wave.ny, wave.nx, wave.num_planes
 spec = torch.zeros((Cn, H, W, 2), dtype=torch.float32, device="cuda")
 s = torch.cuda.current_stream()
 res = {}
+from paper_2506_08350_b200.sharding import plane_subset  # noqa: E402
+
 for N in (1, 2, 4, 8):
     pe = Lp // N
     outs = L.OUT_INTENSITY | L.OUT_HOLOGRAM
+    ctx.upload_scene(plane_subset(scene, 0, pe) if N > 1 else scene)
 
     def frame():
         ctx.render_begin(cam, wave, None, None, 0, pe, spec.data_ptr(), 0)
