@@ -464,11 +464,13 @@ __global__ void __launch_bounds__(256) k_bwd_gauss(GaussBwdArgs a) {
 template <int TILE, int C>
 void launch_bwd_c(holo_ctx* ctx, const RasterBwdArgs& a, dim3 grid) {
     constexpr size_t kPart = sizeof(float) * (TILE * TILE / 32) * (TILE == 32 ? 32 : 128) * kGradVals;
-    static bool attr = false;
-    if (!attr) {
+    static bool done[256] = {};  // function attributes are per device
+    int dev = 0;
+    HC_CUDA(cudaGetDevice(&dev));
+    if (!done[dev & 255]) {
         HC_CUDA(cudaFuncSetAttribute(k_raster_bwd<TILE, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kPart)));
-        attr = true;
+        done[dev & 255] = true;
     }
     k_raster_bwd<TILE, C><<<grid, TILE * TILE, kPart, ctx->stream>>>(a);
 }

@@ -479,7 +479,11 @@ unsigned blocks_for(size_t n, unsigned cap = 8192) {
 // d_out[0] = recon, d_out[1 + l] = mean SSIM of plane l, d_out[1 + L + l] =
 // the mse of plane l; the host finishes the scalar algebra.
 void ssim_setup() {
-    static bool win_set = false;
+    // per device: constant memory and function attributes belong to a device
+    static bool done[256] = {};
+    int dev = 0;
+    HC_CUDA(cudaGetDevice(&dev));
+    bool& win_set = done[dev & 255];
     if (!win_set) {  // ssim.cpp:16-26
         double w[kWin], sum = 0.0;
         for (int i = 0; i < kWin; ++i) {
