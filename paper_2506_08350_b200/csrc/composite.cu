@@ -133,10 +133,10 @@ __device__ __forceinline__ void blend(const Staged* e, const float4& B, float w,
     }
 }
 
-// 16x16 tiles: 6 CTAs (48 warps) per SM, 40 registers -- measured faster than 5
-// (48 registers) and 8 (32 registers, spills)
+// 16x16 tiles: 7 CTAs (56 warps) per SM, 36 registers -- measured faster than 6 (40 registers,
+// -1.3 %), 5 (48 registers) and 8 (32 registers, spills)
 #ifndef HOLO_COMP_MINB
-#define HOLO_COMP_MINB 6
+#define HOLO_COMP_MINB 7
 #endif
 
 // AUX: count contributions for n_contrib (HOLO_OUT_AUX); compiled out otherwise
