@@ -28,6 +28,28 @@ def test_plane_ranges_cover_and_balance():
     assert view_ranges(64, 8) == [(8 * i, 8 * i + 8) for i in range(8)]
 
 
+def test_plane_subsets_partition_the_scene_in_order():
+    """sharding.plane_subset: the per-rank subsets partition the Gaussians by their
+    hard plane (argmax of the logits, ties to the lowest plane) and keep the
+    original relative order (which keeps every bucket's (depth, index) order)."""
+    from paper_2506_08350_b200.holotypes import WaveConfig
+    from paper_2506_08350_b200.scenes import synthetic_scene
+    from paper_2506_08350_b200.sharding import plane_subset
+
+    cfg = WaveConfig(nx=64, ny=64, num_planes=8)
+    s = synthetic_scene(3000, cfg, 5)
+    s.plane_logits[7, :] = 1.0  # an exact tie: goes to plane 0
+    plane = np.argmax(s.plane_logits, axis=1)
+    assert plane[7] == 0
+    for world in (1, 2, 4, 8):
+        parts = [plane_subset(s, pb, pe) for pb, pe in plane_ranges(8, world)]
+        assert sum(p.size() for p in parts) == s.size()
+        for (pb, pe), p in zip(plane_ranges(8, world), parts):
+            idx = np.nonzero((plane >= pb) & (plane < pe))[0]
+            assert np.array_equal(p.positions, s.positions[idx])  # same rows, same order
+            assert np.array_equal(p.plane_logits, s.plane_logits[idx])
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
