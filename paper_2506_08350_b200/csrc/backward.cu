@@ -326,8 +326,12 @@ __global__ void __launch_bounds__(256) k_bwd_gauss(GaussBwdArgs a) {
         for (int l = 0; l < Lg; ++l) dot += exp((lg[l] - top) / tau) / denom * rho_grad[l];
     if (a.g.plane_logits)
         for (int l = 0; l < L; ++l) {
-            const double w = exp((lg[l] - top) / tau) / denom;
             const double rg = l < 64 ? rho_grad[l] : 0.0;
+            if (!a.soft && rg == 0.0) {  // rg * w = 0 exactly: skip the exponential
+                a.g.plane_logits[i * L + l] = 0.0;
+                continue;
+            }
+            const double w = exp((lg[l] - top) / tau) / denom;
             a.g.plane_logits[i * L + l] = a.soft ? w * (rg - dot) / a.soft_tau : rg * w;
         }
 
