@@ -279,3 +279,31 @@ def test_self_target_full_size(gpu_ctx, name):
     assert b.recon == 0.0 and b.psnr_mean == 99.0 and abs(b.ssim) < 1e-12
     worst = max(float(v.abs().max()) for k, v in g.items() if k != "mu_screen")
     assert worst < 1e-8, worst
+
+
+def test_optimizer_rejects_a_resized_scene(gpu_ctx):
+    """optimizer.cpp:105-108: moment buffers sized for one scene do not take another
+    (densification: create a fresh optimizer state)."""
+    cfg = desk_config(32, 2)
+    a, b = random_scene(20, cfg, 1), random_scene(30, cfg, 2)
+    gpu_ctx.upload_scene(a)
+    opt = api.Optimizer(gpu_ctx)
+    assert opt.step({k: torch_dev(np.zeros(np.shape(getattr(a, k)))) for k in GROUPS})
+    gpu_ctx.upload_scene(b)
+    with pytest.raises(HoloError) as e:
+        opt.step({k: torch_dev(np.zeros(np.shape(getattr(b, k)))) for k in GROUPS})
+    assert e.value.kind == "config"
+    fresh = api.Optimizer(gpu_ctx)
+    assert fresh.step({k: torch_dev(np.zeros(np.shape(getattr(b, k)))) for k in GROUPS})
+    assert fresh.counts() == (1, 0)
+
+
+def test_total_loss_rejects_bad_inputs(gpu_ctx):
+    cfg, cam, scene, opt, targets, masks = loss_case("default")
+    with pytest.raises(HoloError):  # masks required unless plain MSE
+        api.total_loss(scene, cam, cfg, targets, None, opt, ctx=gpu_ctx)
+    small = desk_config(8, 2)  # SSIM needs >= 11 pixels (ssim.cpp:71-72)
+    with pytest.raises(HoloError) as e:
+        api.total_loss(random_scene(5, small, 3), front_camera(small), small, np.zeros((2, 3, 8, 8)),
+                       np.zeros((2, 8, 8)), opt, ctx=gpu_ctx)
+    assert e.value.kind == "config"
