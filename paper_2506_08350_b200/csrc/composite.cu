@@ -152,12 +152,13 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
             int gid[kSortCap];
         } sort;
         struct {
-            Staged rec[kStage];
-            float4 box[kStage];  // xlo, xhi, ylo, yhi of the accept ellipse, tile-relative
+            Staged rec[kStage + 1];  // [kStage]: a record that never accepts (pads odd hit counts)
+            float4 box[kStage];      // xlo, xhi, ylo, yhi of the accept ellipse, tile-relative
         } st;
     };
     __shared__ Smem sm;
     __shared__ int s_ord[kSortCap];
+    __shared__ __align__(8) int s_hit[G::kThreads / 32][34];  // per warp: byte offsets of the chunk's hit records
 
     const int tx = blockIdx.x, ty = blockIdx.y, lplane = blockIdx.z;  // grid = (tiles_x, tiles_y, planes)
     const int lb = (lplane * gridDim.y + ty) * gridDim.x + tx;        // local bucket
@@ -258,29 +259,39 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
                     alpha = static_cast<float>(static_cast<double>(r.alpha) * a.rho[static_cast<size_t>(g) * a.L + plane]);
                 stage_entry(r, px0, py0, alpha, sm.st.rec[t], sm.st.box[t]);
             }
+            if (tid == 0) {  // a = 2^-inf = 0: never accepted, and its blend adds exact zeros
+                Staged& z = sm.st.rec[kStage];
+                z.a = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                z.b = make_float4(0.0f, -INFINITY, 0.0f, 0.0f);
+                z.c = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            }
             __syncthreads();
             if (!__all_sync(0xffffffffu, done)) {
                 // 32 entries at a time: each lane tests one entry's accept box against
-                // this warp's 8x4 block of pixel centres; the warp walks the hits in
-                // order, two per step, branch-free per lane (predicated accept).
+                // this warp's 8x4 block of pixel centres; the hits are compacted (byte
+                // offsets, padded to an even count with the never-accepting record) and
+                // the warp walks them in order, two per step, branch-free per lane
+                // (predicated accept).
+                const char* recs = reinterpret_cast<const char*>(sm.st.rec);
+                int* hits = s_hit[warp];
                 for (int c0 = 0; c0 < cnt; c0 += 32) {
                     bool hit = false;
                     if (c0 + lane < cnt) {
                         const float4 bb = sm.st.box[c0 + lane];
                         hit = box_hits(bb, bxlo, bxhi, bylo, byhi);
                     }
-                    unsigned mask = __ballot_sync(0xffffffffu, hit);
+                    const unsigned mask = __ballot_sync(0xffffffffu, hit);
+                    const int nh = __popc(mask);
+                    if (hit) hits[__popc(mask & ((1u << lane) - 1u))] = (c0 + lane) * static_cast<int>(sizeof(Staged));
+                    if (lane == 0) hits[nh] = kStage * static_cast<int>(sizeof(Staged));
+                    __syncwarp();
 #ifdef HOLO_COUNT
                     unsigned long long n_eval = 0, n_any = 0, n_acc = 0;
 #endif
-                    while (mask) {
-                        const int j0 = __ffs(mask) - 1;
-                        const Staged* e0p = &sm.st.rec[c0 + j0];
-                        mask &= mask - 1;
-                        const bool two = mask != 0;
-                        const int j1 = two ? __ffs(mask) - 1 : 0;
-                        const Staged* e1p = &sm.st.rec[c0 + j1];
-                        mask &= mask - 1;
+                    for (int k = 0; k < nh; k += 2) {
+                        const int2 off = *reinterpret_cast<const int2*>(hits + k);
+                        const Staged* e0p = reinterpret_cast<const Staged*>(recs + off.x);
+                        const Staged* e1p = reinterpret_cast<const Staged*>(recs + off.y);
                         float4 B0, B1;
                         const float al0 = eval_alpha(e0p, fx, fy, clamp, B0);
                         const float al1 = eval_alpha(e1p, fx, fy, clamp, B1);
@@ -290,22 +301,23 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
                         T -= w0;  // T (1 - a)
                         if constexpr (AUX) {
                             contrib += acc0 ? 1 : 0;
-                            elast = acc0 ? base + c0 + j0 : elast;
+                            elast = acc0 ? base + off.x / static_cast<int>(sizeof(Staged)) : elast;
                         }
-                        const bool acc1 = two && (al1 > thr) && (T >= eps);
+                        const bool acc1 = (al1 > thr) && (T >= eps);
                         const float w1 = acc1 ? al1 * T : 0.0f;
                         blend<C>(e1p, B1, w1, acc);
                         T -= w1;
                         if constexpr (AUX) {
                             contrib += acc1 ? 1 : 0;
-                            elast = acc1 ? base + c0 + j1 : elast;
+                            elast = acc1 ? base + off.y / static_cast<int>(sizeof(Staged)) : elast;
                         }
 #ifdef HOLO_COUNT
-                        n_eval += two ? 2 : 1;
+                        n_eval += (k + 1 < nh) ? 2 : 1;
                         n_any += (__ballot_sync(0xffffffffu, acc0) ? 1 : 0) + (__ballot_sync(0xffffffffu, acc1) ? 1 : 0);
                         n_acc += __popc(__ballot_sync(0xffffffffu, acc0)) + __popc(__ballot_sync(0xffffffffu, acc1));
 #endif
                     }
+                    __syncwarp();  // the next chunk rewrites hits[]
 #ifdef HOLO_COUNT
                     if (lane == 0) {
                         atomicAdd(&g_counts[0], n_eval);

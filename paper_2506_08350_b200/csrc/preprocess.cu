@@ -51,6 +51,7 @@ struct PreArgs {
     int L;
     CameraConsts cam;
     double near_clip, dilation, alpha_floor, radius_form_cap, plane_eps, soft_tau;
+    double inv_tile;  // 1 / tile when the tile is a power of two (exact), else 0
     int soft, tile, tiles_x, tiles_y;
 };
 
@@ -253,11 +254,15 @@ __global__ void __launch_bounds__(256, PROJ ? 1 : HOLO_PRE_MINB) k_preprocess(Pr
             r.col[2 * c + 1] = static_cast<float>(p.amp[c] * s);
         }
         // tile_span (rasterizer.cpp:106-113)
-        const int tile = a.tile;
-        int x0 = static_cast<int>(floor((p.mu_x - radius) / tile));
-        int x1 = static_cast<int>(floor((p.mu_x + radius) / tile)) + 1;
-        int y0 = static_cast<int>(floor((p.mu_y - radius) / tile));
-        int y1 = static_cast<int>(floor((p.mu_y + radius) / tile)) + 1;
+        // the tile is a power of two, so x / tile == x * (1 / tile) exactly, and
+        // floor-then-convert is one rounding conversion (both saturate alike):
+        // bit-identical spans with fewer XU-pipe instructions (the kernel's limiter)
+        const double it = a.inv_tile;
+        const auto span = [&](double v) { return __double2int_rd(it > 0.0 ? v * it : v / a.tile); };
+        int x0 = span(p.mu_x - radius);
+        int x1 = span(p.mu_x + radius) + 1;
+        int y0 = span(p.mu_y - radius);
+        int y1 = span(p.mu_y + radius) + 1;
         x0 = x0 > 0 ? x0 : 0;
         y0 = y0 > 0 ? y0 : 0;
         x1 = x1 < a.tiles_x ? x1 : a.tiles_x;
@@ -317,6 +322,7 @@ void preprocess(holo_ctx* ctx, const CameraConsts& cc, const holo_raster_setting
     a.soft_tau = st.soft_tau;
     a.soft = st.soft_assignment;
     a.tile = st.tile;
+    a.inv_tile = (st.tile > 0 && (st.tile & (st.tile - 1)) == 0) ? 1.0 / st.tile : 0.0;
     a.tiles_x = tiles_x;
     a.tiles_y = tiles_y;
     const unsigned grid = static_cast<unsigned>((ctx->n + 255) / 256);
