@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
     };
     __shared__ Smem sm;
     __shared__ int s_ord[kSortCap];
-    __shared__ __align__(8) int s_hit[G::kThreads / 32][34];  // per warp: byte offsets of the chunk's hit records
+    __shared__ __align__(8) int s_hit[G::kThreads / 32][66];  // per warp: byte offsets of the chunk's hit records
 
     const int tx = blockIdx.x, ty = blockIdx.y, lplane = blockIdx.z;  // grid = (tiles_x, tiles_y, planes)
     const int lb = (lplane * gridDim.y + ty) * gridDim.x + tx;        // local bucket
@@ -267,22 +267,23 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
             }
             __syncthreads();
             if (!__all_sync(0xffffffffu, done)) {
-                // 32 entries at a time: each lane tests one entry's accept box against
+                // 64 entries at a time: each lane tests two entries' accept boxes against
                 // this warp's 8x4 block of pixel centres; the hits are compacted (byte
                 // offsets, padded to an even count with the never-accepting record) and
                 // the warp walks them in order, two per step, branch-free per lane
                 // (predicated accept).
                 const char* recs = reinterpret_cast<const char*>(sm.st.rec);
                 int* hits = s_hit[warp];
-                for (int c0 = 0; c0 < cnt; c0 += 32) {
-                    bool hit = false;
-                    if (c0 + lane < cnt) {
-                        const float4 bb = sm.st.box[c0 + lane];
-                        hit = box_hits(bb, bxlo, bxhi, bylo, byhi);
-                    }
-                    const unsigned mask = __ballot_sync(0xffffffffu, hit);
-                    const int nh = __popc(mask);
-                    if (hit) hits[__popc(mask & ((1u << lane) - 1u))] = (c0 + lane) * static_cast<int>(sizeof(Staged));
+                for (int c0 = 0; c0 < cnt; c0 += 64) {
+                    bool hit0 = false, hit1 = false;
+                    if (c0 + lane < cnt) hit0 = box_hits(sm.st.box[c0 + lane], bxlo, bxhi, bylo, byhi);
+                    if (c0 + 32 + lane < cnt) hit1 = box_hits(sm.st.box[c0 + 32 + lane], bxlo, bxhi, bylo, byhi);
+                    const unsigned mask0 = __ballot_sync(0xffffffffu, hit0);
+                    const unsigned mask1 = __ballot_sync(0xffffffffu, hit1);
+                    const unsigned below = (1u << lane) - 1u;
+                    const int n0 = __popc(mask0), nh = n0 + __popc(mask1);
+                    if (hit0) hits[__popc(mask0 & below)] = (c0 + lane) * static_cast<int>(sizeof(Staged));
+                    if (hit1) hits[n0 + __popc(mask1 & below)] = (c0 + 32 + lane) * static_cast<int>(sizeof(Staged));
                     if (lane == 0) hits[nh] = kStage * static_cast<int>(sizeof(Staged));
                     __syncwarp();
 #ifdef HOLO_COUNT
