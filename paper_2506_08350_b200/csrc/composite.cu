@@ -135,6 +135,9 @@ __device__ __forceinline__ void blend(const Staged* e, const float4& B, float w,
 
 // 16x16 tiles: 7 CTAs (56 warps) per SM, 36 registers -- measured faster than 6 (40 registers,
 // -1.3 %), 5 (48 registers) and 8 (32 registers, spills)
+#ifndef HOLO_COMP_TEST
+#define HOLO_COMP_TEST 2
+#endif
 #ifndef HOLO_COMP_MINB
 #define HOLO_COMP_MINB 7
 #endif
@@ -144,6 +147,7 @@ template <int TILE, int C, bool AUX>
 __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) k_composite(CompositeArgs a) {
     using G = TileGeom<TILE>;
     constexpr int kStage = 256;  // records staged per batch
+    constexpr int kTest = HOLO_COMP_TEST;  // box tests per lane per ballot round
     // the mid-size sort's arrays share storage with the staging arrays (the sort
     // finishes, behind a barrier, before the first staging write)
     union Smem {
@@ -158,7 +162,7 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
     };
     __shared__ Smem sm;
     __shared__ int s_ord[kSortCap];
-    __shared__ __align__(8) int s_hit[G::kThreads / 32][66];  // per warp: byte offsets of the chunk's hit records
+    __shared__ __align__(8) int s_hit[G::kThreads / 32][32 * kTest + 2];  // per warp: byte offsets of the chunk's hit records
 
     const int tx = blockIdx.x, ty = blockIdx.y, lplane = blockIdx.z;  // grid = (tiles_x, tiles_y, planes)
     const int lb = (lplane * gridDim.y + ty) * gridDim.x + tx;        // local bucket
@@ -267,23 +271,24 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
             }
             __syncthreads();
             if (!__all_sync(0xffffffffu, done)) {
-                // 64 entries at a time: each lane tests two entries' accept boxes against
+                // 32 kTest entries at a time: each lane tests kTest accept boxes against
                 // this warp's 8x4 block of pixel centres; the hits are compacted (byte
                 // offsets, padded to an even count with the never-accepting record) and
                 // the warp walks them in order, two per step, branch-free per lane
                 // (predicated accept).
                 const char* recs = reinterpret_cast<const char*>(sm.st.rec);
                 int* hits = s_hit[warp];
-                for (int c0 = 0; c0 < cnt; c0 += 64) {
-                    bool hit0 = false, hit1 = false;
-                    if (c0 + lane < cnt) hit0 = box_hits(sm.st.box[c0 + lane], bxlo, bxhi, bylo, byhi);
-                    if (c0 + 32 + lane < cnt) hit1 = box_hits(sm.st.box[c0 + 32 + lane], bxlo, bxhi, bylo, byhi);
-                    const unsigned mask0 = __ballot_sync(0xffffffffu, hit0);
-                    const unsigned mask1 = __ballot_sync(0xffffffffu, hit1);
+                for (int c0 = 0; c0 < cnt; c0 += 32 * kTest) {
                     const unsigned below = (1u << lane) - 1u;
-                    const int n0 = __popc(mask0), nh = n0 + __popc(mask1);
-                    if (hit0) hits[__popc(mask0 & below)] = (c0 + lane) * static_cast<int>(sizeof(Staged));
-                    if (hit1) hits[n0 + __popc(mask1 & below)] = (c0 + 32 + lane) * static_cast<int>(sizeof(Staged));
+                    int nh = 0;
+#pragma unroll
+                    for (int q = 0; q < kTest; ++q) {
+                        const int j = c0 + 32 * q + lane;
+                        const bool h = j < cnt && box_hits(sm.st.box[j], bxlo, bxhi, bylo, byhi);
+                        const unsigned m = __ballot_sync(0xffffffffu, h);
+                        if (h) hits[nh + __popc(m & below)] = j * static_cast<int>(sizeof(Staged));
+                        nh += __popc(m);
+                    }
                     if (lane == 0) hits[nh] = kStage * static_cast<int>(sizeof(Staged));
                     __syncwarp();
 #ifdef HOLO_COUNT
