@@ -56,10 +56,11 @@ def stage_bytes(N, L, C, P, E, planes_local, sharded, has_holo):
     return {
         # f64 scene read + 64-B compositing record + 33 B of binning metadata per Gaussian
         "preprocess": N * (8 * (17 + L) + 64 + 33),
-        # rect/count/plane re-read twice, bucket atomics, 12-B (key, gidx) entries
-        "binning": N * 2 * 24 + E * (4 + 12),
-        # entry list + 64-B record gather per entry, layers written once
-        "composite": E * (12 + 64) + Lr * f,
+        # rect/count/plane re-read twice, bucket atomics, 4-B gidx entries written,
+        # then sorted with their 8-B depth keys gathered
+        "binning": N * 2 * 24 + E * (4 + 4 + 8),
+        # sorted gidx list + 64-B record gather per entry, layers written once
+        "composite": E * (4 + 64) + Lr * f,
         "fft_pass1": 2 * Lr * f,                                   # column FFT, in place
         "fft_pass2": Lr * f + (f if sharded else O * f),           # rows: read planes, write S or outputs
         "fft_pass3": f + O * f,                                    # rows from S (sharded only)

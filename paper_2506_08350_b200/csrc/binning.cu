@@ -144,8 +144,7 @@ __global__ void __launch_bounds__(256) k_bucket_count(PreOut pre, size_t N, int 
 
 __global__ void __launch_bounds__(256) k_bucket_emit(PreOut pre, size_t N, int L, int pb, int pe, int tiles_x,
                                                      int num_tiles, int soft, const unsigned* __restrict__ bstart,
-                                                     unsigned* __restrict__ cursor,
-                                                     unsigned long long* __restrict__ ekey, int* __restrict__ egidx,
+                                                     unsigned* __restrict__ cursor, int* __restrict__ egidx,
                                                      unsigned capacity, unsigned* __restrict__ flags) {
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     if (i >= N) return;
@@ -153,7 +152,6 @@ __global__ void __launch_bounds__(256) k_bucket_emit(PreOut pre, size_t N, int L
     const unsigned cnt_i = pre.count[i];
     const int plane_i = soft ? 0 : pre.plane[i];
     const int4 rect_i = pre.rect[i];
-    const unsigned long long key = static_cast<unsigned long long>(__double_as_longlong(pre.zc[i]));
     bool over = false;
     // entries beyond the reserved capacity (asynchronous frames) are dropped and flagged
     auto put = [&](int b, unsigned slot) {
@@ -162,7 +160,6 @@ __global__ void __launch_bounds__(256) k_bucket_emit(PreOut pre, size_t N, int L
             over = true;
             return;
         }
-        ekey[e] = key;
         egidx[e] = static_cast<int>(i);
     };
     if (!soft) {
@@ -190,7 +187,6 @@ __global__ void __launch_bounds__(256) k_bucket_emit(PreOut pre, size_t N, int L
                     if (e >= capacity) {
                         over = true;
                     } else {
-                        ekey[e] = key;
                         egidx[e] = static_cast<int>(i);
                     }
                 }
@@ -234,7 +230,8 @@ __global__ void k_find_large(const unsigned* __restrict__ bstart, long long B, i
 __global__ void __launch_bounds__(1024) k_sort_large_dev(const int* __restrict__ list,
                                                          const unsigned* __restrict__ nlist,
                                                          const unsigned* __restrict__ bstart, unsigned capacity,
-                                                         unsigned long long* __restrict__ ekey, int* __restrict__ egidx,
+                                                         const unsigned long long* __restrict__ zkey,
+                                                         int* __restrict__ egidx,
                                                          unsigned long long* __restrict__ tkey, int* __restrict__ tg) {
     const unsigned count = *nlist;
     for (unsigned w = blockIdx.x; w < count; w += gridDim.x) {
@@ -248,8 +245,9 @@ __global__ void __launch_bounds__(1024) k_sort_large_dev(const int* __restrict__
         unsigned long long* K = tkey + 2 * static_cast<size_t>(s);
         int* G = tg + 2 * static_cast<size_t>(s);
         for (unsigned t = threadIdx.x; t < P; t += blockDim.x) {
-            K[t] = t < n ? ekey[s + t] : ~0ull;
-            G[t] = t < n ? egidx[s + t] : 0x7fffffff;
+            const int g = t < n ? egidx[s + t] : 0x7fffffff;
+            K[t] = t < n ? zkey[g] : ~0ull;
+            G[t] = g;
         }
         __syncthreads();
         for (unsigned k = 2; k <= P; k <<= 1) {
@@ -272,10 +270,7 @@ __global__ void __launch_bounds__(1024) k_sort_large_dev(const int* __restrict__
                 __syncthreads();
             }
         }
-        for (unsigned t = threadIdx.x; t < n; t += blockDim.x) {
-            ekey[s + t] = K[t];
-            egidx[s + t] = G[t];
-        }
+        for (unsigned t = threadIdx.x; t < n; t += blockDim.x) egidx[s + t] = G[t];
         __syncthreads();
     }
 }
@@ -313,16 +308,16 @@ void bucket_count(holo_ctx* ctx, const PreOut& pre, size_t N, int L, int pb, int
 }
 
 void bucket_emit(holo_ctx* ctx, const PreOut& pre, size_t N, int L, int pb, int pe, int tiles_x, int num_tiles,
-                 int soft, const unsigned* bstart, unsigned* cursor, unsigned long long* ekey, int* egidx,
-                 unsigned capacity, unsigned* flags) {
+                 int soft, const unsigned* bstart, unsigned* cursor, int* egidx, unsigned capacity,
+                 unsigned* flags) {
     if (N == 0) return;
     k_bucket_emit<<<static_cast<unsigned>((N + 255) / 256), 256, 0, ctx->stream>>>(
-        pre, N, L, pb, pe, tiles_x, num_tiles, soft, bstart, cursor, ekey, egidx, capacity, flags);
+        pre, N, L, pb, pe, tiles_x, num_tiles, soft, bstart, cursor, egidx, capacity, flags);
     HC_LAUNCHED(ctx);
 }
 
 void sort_large_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsigned capacity,
-                        unsigned long long* ekey, int* egidx, unsigned* d_nlist) {
+                        const unsigned long long* zkey, int* egidx, unsigned* d_nlist) {
     // list buffer sized for the worst case: at most capacity / (kSortCap + 1) buckets can exceed the cap
     const size_t max_list = capacity / (kSortCap + 1) + 1;
     int* list = static_cast<int*>(ctx->buffer("large_list", sizeof(int) * max_list));
@@ -332,7 +327,7 @@ void sort_large_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsi
     k_find_large<<<static_cast<unsigned>(blocks < 4096 ? (blocks > 0 ? blocks : 1) : 4096), 256, 0, ctx->stream>>>(
         bstart, B, kSortCap, list, d_nlist);
     HC_LAUNCHED(ctx);
-    k_sort_large_dev<<<ctx->sm_count, 1024, 0, ctx->stream>>>(list, d_nlist, bstart, capacity, ekey, egidx, tkey, tg);
+    k_sort_large_dev<<<ctx->sm_count, 1024, 0, ctx->stream>>>(list, d_nlist, bstart, capacity, zkey, egidx, tkey, tg);
     HC_LAUNCHED(ctx);
 }
 

@@ -383,16 +383,18 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
         if (ctx->e_cap == 0) config_error("asynchronous rendering needs holo_ctx_reserve_entries or a synchronous frame first");
         capacity = static_cast<unsigned>(std::min<size_t>(ctx->e_cap, 0xffffffffu));
     }
-    auto* ekey = buf<unsigned long long>(ctx, "ekey", capacity);
+    // sort keys are the Gaussians' depth bits, gathered by gidx from the 8 MB zc
+    // array (L2-resident) instead of being scattered into a per-entry copy
+    const auto* zkey = reinterpret_cast<const unsigned long long*>(pre.zc);
     int* egidx = buf<int>(ctx, "egidx", capacity);
     // emission cursors: soft mode counts again from zero in bcount; hard mode keeps
     // bcount (the small Gaussians' slot counts) and counts the large ones in bbig
     unsigned* cursor = hard ? bbig : bcount;
     HC_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned) * (B + 1), ctx->stream));
-    bucket_emit(ctx, pre, N, L, pb, pe, g.tiles_x, g.num_tiles, st.soft_assignment, bstart, cursor, ekey, egidx,
+    bucket_emit(ctx, pre, N, L, pb, pe, g.tiles_x, g.num_tiles, st.soft_assignment, bstart, cursor, egidx,
                 capacity, misc);
-    sort_large_buckets(ctx, bstart, B, capacity, ekey, egidx, misc + 3);
-    sort_small_buckets(ctx, bstart, B, capacity, ekey, egidx);
+    sort_large_buckets(ctx, bstart, B, capacity, zkey, egidx, misc + 3);
+    sort_small_buckets(ctx, bstart, B, capacity, zkey, egidx);
     ctx->stage_end(1);
 
     // composite into [nplanes][C][H][W]
@@ -400,7 +402,7 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     const bool want_lists = (outputs & HOLO_OUT_LISTS) != 0;
     CompositeArgs ca{};
     ca.bstart = bstart;
-    ca.ekey = ekey;
+    ca.zkey = zkey;
     ca.egidx = egidx;
     ca.rec = pre.rec;
     ca.rho = pre.rho;

@@ -79,15 +79,16 @@ __device__ __forceinline__ void warp_bitonic(KeyG (&v)[NE], int lane) {
 
 // Sort one bucket (n <= 32 NE entries) in a warp and write its gidx back in order.
 template <int NE>
-__device__ __forceinline__ void warp_sort_bucket(const unsigned long long* __restrict__ ekey, int* __restrict__ egidx,
+__device__ __forceinline__ void warp_sort_bucket(const unsigned long long* __restrict__ zkey, int* __restrict__ egidx,
                                                  unsigned e0, int n, int lane) {
     KeyG v[NE];
 #pragma unroll
     for (int s = 0; s < NE; ++s) {
         const int i = lane + 32 * s;
-        v[s].k = i < n ? ekey[e0 + i] : ~0ull;
         v[s].g = i < n ? egidx[e0 + i] : 0x7fffffff;
     }
+#pragma unroll
+    for (int s = 0; s < NE; ++s) v[s].k = lane + 32 * s < n ? zkey[v[s].g] : ~0ull;
     warp_bitonic<NE>(v, lane);
 #pragma unroll
     for (int s = 0; s < NE; ++s) {
@@ -98,7 +99,7 @@ __device__ __forceinline__ void warp_sort_bucket(const unsigned long long* __res
 
 // One warp per bucket of 2..kWarpSortCap entries.
 __global__ void __launch_bounds__(256) k_sort_small(const unsigned* __restrict__ bstart, long long B,
-                                                    unsigned capacity, const unsigned long long* __restrict__ ekey,
+                                                    unsigned capacity, const unsigned long long* __restrict__ zkey,
                                                     int* __restrict__ egidx) {
     const long long b = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
     if (b >= B) return;
@@ -107,11 +108,11 @@ __global__ void __launch_bounds__(256) k_sort_small(const unsigned* __restrict__
     const int n = static_cast<int>(min(bstart[b + 1], capacity) - e0);
     if (n < 2 || n > kWarpSortCap) return;  // warp-uniform
     if (n <= 32)
-        warp_sort_bucket<1>(ekey, egidx, e0, n, lane);
+        warp_sort_bucket<1>(zkey, egidx, e0, n, lane);
     else if (n <= 64)
-        warp_sort_bucket<2>(ekey, egidx, e0, n, lane);
+        warp_sort_bucket<2>(zkey, egidx, e0, n, lane);
     else
-        warp_sort_bucket<4>(ekey, egidx, e0, n, lane);
+        warp_sort_bucket<4>(zkey, egidx, e0, n, lane);
 }
 
 #ifdef HOLO_COUNT
@@ -192,8 +193,9 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
         const bool presorted = n <= kWarpSortCap || n > kSortCap;
         if (!presorted) {
             for (int t = tid; t < n; t += G::kThreads) {
-                sm.sort.key[t] = a.ekey[e0 + t];
-                sm.sort.gid[t] = a.egidx[e0 + t];
+                const int g = a.egidx[e0 + t];
+                sm.sort.key[t] = a.zkey[g];
+                sm.sort.gid[t] = g;
             }
             __syncthreads();
             if (n <= G::kThreads) {
@@ -387,9 +389,9 @@ void launch_tile(holo_ctx* ctx, const CompositeArgs& a) {
 }  // namespace
 
 void sort_small_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsigned capacity,
-                        const unsigned long long* ekey, int* egidx) {
+                        const unsigned long long* zkey, int* egidx) {
     if (B <= 0) return;
-    k_sort_small<<<static_cast<unsigned>((B + 7) / 8), 256, 0, ctx->stream>>>(bstart, B, capacity, ekey, egidx);
+    k_sort_small<<<static_cast<unsigned>((B + 7) / 8), 256, 0, ctx->stream>>>(bstart, B, capacity, zkey, egidx);
     HC_LAUNCHED(ctx);
 }
 

@@ -136,10 +136,10 @@ void bucket_count(holo_ctx* ctx, const PreOut& pre, size_t N, int L, int plane_b
 constexpr unsigned kFlagDegenerateQuat = 1u, kFlagNegativeAmp = 2u, kFlagOverflow = 4u;
 void bucket_emit(holo_ctx* ctx, const PreOut& pre, size_t N, int L, int plane_begin, int plane_end, int tiles_x,
                  int num_tiles, int soft, const unsigned* bstart, unsigned* cursor,
-                 unsigned long long* ekey, int* egidx, unsigned capacity, unsigned* flags);
+                 int* egidx, unsigned capacity, unsigned* flags);
 // device-driven: buckets above kSortCap are found and sorted without a host round trip
 void sort_large_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsigned capacity,
-                        unsigned long long* ekey, int* egidx, unsigned* d_nlist);
+                        const unsigned long long* zkey, int* egidx, unsigned* d_nlist);
 void entry_depths(holo_ctx* ctx, const int* egidx, const double* zc, double* edepth, const unsigned* d_E,
                   unsigned capacity);
 // host[0..2] = misc[0..2] (flags, num_valid, max bucket), host[4] = *total (E); host is pinned
@@ -158,7 +158,7 @@ void static_row(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spe
 // ---- composite.cu
 struct CompositeArgs {
     const unsigned* bstart;   // bucket_start for the rendered planes, indexed by local bucket
-    unsigned long long* ekey; // depth bits per entry (unsorted for small buckets)
+    const unsigned long long* zkey;  // depth bits per Gaussian (the IEEE bits of zc)
     int* egidx;               // gidx per entry
     const GRec* rec;
     const double* rho;        // soft mode weights or null
@@ -225,7 +225,7 @@ void raster_backward_entries(holo_ctx* ctx, const RasterBwdArgs& a, int tile);
 void gauss_backward(holo_ctx* ctx, const GaussBwdArgs& a);
 // (zc, gidx) order for buckets of 2..kWarpSortCap entries, written back to egidx
 void sort_small_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsigned capacity,
-                        const unsigned long long* ekey, int* egidx);
+                        const unsigned long long* zkey, int* egidx);
 
 // ---- training step (training.cu): losses, opacity decay, optimizer
 void losses_gpu(holo_ctx* ctx, const double* I, const double* G, const double* masks, int L, int C, int H, int W,
