@@ -185,6 +185,27 @@ def test_equal_depth_tie_by_index(gpu_ctx):
     assert list(r.entries["gidx"][r.entries["bucket"] == first_bucket]) == [0, 1]
 
 
+@pytest.mark.parametrize("n", [20, 50, 100])
+def test_depths_equal_in_fp32_sort_by_f64_depth(gpu_ctx, n):
+    """Bucket order is (zc, gidx) (rasterizer.cpp:221-224) even where distinct f64
+    depths round to one fp32 value (the warp sort's fast key) and gidx runs against
+    depth: warp-sorted bucket sizes of <= 32, <= 64 and <= 128 entries."""
+    cfg = desk_config(32, 1)
+    s = single_scene(n, 1)
+    s.positions = np.array([[0.0, 0.0, 0.3 + 1e-12 * (n - i)] for i in range(n)])
+    s.log_scales = np.full((n, 3), np.log(0.005))
+    s.amplitudes = np.ones((n, 3))
+    r = api.raster_forward(s, front_camera(cfg), cfg, ctx=gpu_ctx)
+    first_bucket = r.entries["bucket"][0]
+    sel = r.entries["bucket"] == first_bucket
+    depth, gidx = r.entries["depth"][sel], r.entries["gidx"][sel]
+    assert len(gidx) == n
+    assert len(np.unique(np.float32(depth))) < n  # the fp32 keys do collide
+    order = sorted(range(n), key=lambda k: (depth[k], gidx[k]))
+    assert list(order) == list(range(n))
+    assert list(gidx) == sorted(gidx, key=lambda g: (r.projected["zc"][g], g))
+
+
 def test_culling_and_clamp(gpu_ctx):
     cfg = desk_config(32, 1)
     s = single_scene(2, 1)
