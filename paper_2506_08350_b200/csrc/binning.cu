@@ -217,23 +217,31 @@ __global__ void __launch_bounds__(256) k_bucket_emit(PreOut pre, size_t N, int L
 }
 
 // Buckets above the in-CTA sort capacity, compacted into a device list.
-__global__ void k_find_large(const unsigned* __restrict__ bstart, long long B, int cap, int* __restrict__ list,
-                             unsigned* __restrict__ nlist) {
+// Bucket bounds are clamped to the reserved entry capacity (an overflowed
+// asynchronous frame has bstart[B] > capacity), so at most capacity / (cap + 1)
+// buckets qualify; the list index is bounded by max_list all the same.
+__global__ void k_find_large(const unsigned* __restrict__ bstart, long long B, int cap, unsigned capacity,
+                             int* __restrict__ list, unsigned max_list, unsigned* __restrict__ nlist) {
     for (long long b = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; b < B;
-         b += static_cast<long long>(gridDim.x) * blockDim.x)
-        if (bstart[b + 1] - bstart[b] > static_cast<unsigned>(cap)) list[atomicAdd(nlist, 1u)] = static_cast<int>(b);
+         b += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const unsigned s = min(bstart[b], capacity), e = min(bstart[b + 1], capacity);
+        if (e - s > static_cast<unsigned>(cap)) {
+            const unsigned k = atomicAdd(nlist, 1u);
+            if (k < max_list) list[k] = static_cast<int>(b);
+        }
+    }
 }
 
 // Persistent CTAs sort the listed buckets by (zc, gidx) with a bitonic network in
 // global scratch; bucket b uses the scratch range [2 bstart[b], 2 bstart[b] + pow2(n)),
 // which never overlaps another bucket's since pow2(n) < 2 n.
 __global__ void __launch_bounds__(1024) k_sort_large_dev(const int* __restrict__ list,
-                                                         const unsigned* __restrict__ nlist,
+                                                         const unsigned* __restrict__ nlist, unsigned max_list,
                                                          const unsigned* __restrict__ bstart, unsigned capacity,
                                                          const unsigned long long* __restrict__ zkey,
                                                          int* __restrict__ egidx,
                                                          unsigned long long* __restrict__ tkey, int* __restrict__ tg) {
-    const unsigned count = *nlist;
+    const unsigned count = min(*nlist, max_list);
     for (unsigned w = blockIdx.x; w < count; w += gridDim.x) {
         const int bk = list[w];
         const unsigned s = bstart[bk];
@@ -325,9 +333,10 @@ void sort_large_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsi
     auto* tg = static_cast<int*>(ctx->buffer("large_tg", sizeof(int) * 2 * (capacity + 1)));
     const long long blocks = (B + 255) / 256;
     k_find_large<<<static_cast<unsigned>(blocks < 4096 ? (blocks > 0 ? blocks : 1) : 4096), 256, 0, ctx->stream>>>(
-        bstart, B, kSortCap, list, d_nlist);
+        bstart, B, kSortCap, capacity, list, static_cast<unsigned>(max_list), d_nlist);
     HC_LAUNCHED(ctx);
-    k_sort_large_dev<<<ctx->sm_count, 1024, 0, ctx->stream>>>(list, d_nlist, bstart, capacity, zkey, egidx, tkey, tg);
+    k_sort_large_dev<<<ctx->sm_count, 1024, 0, ctx->stream>>>(list, d_nlist, static_cast<unsigned>(max_list), bstart,
+                                                             capacity, zkey, egidx, tkey, tg);
     HC_LAUNCHED(ctx);
 }
 

@@ -972,6 +972,12 @@ void check_backward_frame(holo_ctx* ctx, const holo_camera& cam, const holo_wave
 void raster_backward(holo_ctx* ctx, const holo_wave& wave, const holo_raster_settings& st,
                      const cx<float>* grad_layers, const holo_scene_grads& grads) {
     consume_status(ctx, true);  // E of an asynchronous frame
+    // an overflowed asynchronous frame has truncated lists, and the per-Gaussian
+    // entry offsets (the scan of the unclamped counts) would run past egrad
+    require(ctx->f_E <= ctx->f_cap && !(ctx->sticky_flags & kFlagOverflow), HOLO_ERR_USAGE,
+            ("backward: the last frame overflowed its entry capacity (" + std::to_string(ctx->f_E) + " > " +
+             std::to_string(ctx->f_cap) + "); render it again before the backward")
+                .c_str());
     const size_t N = ctx->n;
     const int L = wave.num_planes, C = wave.channels;
     const unsigned capacity = ctx->f_cap;

@@ -30,6 +30,23 @@ def plane_ranges(num_planes: int, world: int) -> List[Tuple[int, int]]:
     return out
 
 
+def hard_planes(scene):
+    """Hard plane of every Gaussian with the device's strict '>' scan
+    (preprocess.cu, ste_assign scene.cpp:132-152): ties and NaN logits keep the
+    lower index, so every rank agrees with the kernel on who owns a Gaussian
+    (np.argmax would return the first NaN instead)."""
+    import numpy as np
+
+    lg = np.asarray(scene.plane_logits, dtype=np.float64).reshape(scene.size(), scene.num_planes)
+    best = np.zeros(lg.shape[0], dtype=np.int64)
+    top = lg[:, 0].copy() if lg.shape[1] else np.zeros(0)
+    for l in range(1, lg.shape[1]):
+        take = lg[:, l] > top
+        best[take] = l
+        top[take] = lg[take, l]
+    return best
+
+
 def plane_subset(scene, pb: int, pe: int):
     """The Gaussians whose hard plane assignment (argmax of the plane logits, ties
     to the lowest index: ste_assign, scene.cpp:132-152) falls in [pb, pe), in
@@ -42,7 +59,7 @@ def plane_subset(scene, pb: int, pe: int):
 
     from .holotypes import GaussianScene
 
-    plane = np.argmax(np.asarray(scene.plane_logits).reshape(scene.size(), scene.num_planes), axis=1)
+    plane = hard_planes(scene)
     keep = (plane >= pb) & (plane < pe)
     sub = GaussianScene(num_planes=scene.num_planes)
     for k in ("positions", "rotations", "log_scales", "amplitudes", "opacity_logits", "phases", "plane_logits"):

@@ -313,6 +313,40 @@ def test_async_capacity_and_validation_reported_by_frame_status():
     ctx.close()
 
 
+def test_async_overflow_with_large_buckets_and_backward_rejected():
+    # a heavily overflowed asynchronous frame: many buckets above the in-CTA sort
+    # capacity (1024) while only 100 entries are reserved.  The large-bucket list
+    # is bounded by the clamped capacity, and a backward on the truncated lists
+    # is refused instead of running past its per-entry gradient buffer.
+    import torch
+
+    cfg = WaveConfig(nx=64, ny=64, wavelengths=RGB, num_planes=2)
+    s = overlapping_scene(40000, cfg, 45)
+    s.positions[:, :2] *= 0.2  # every Gaussian covers most of the 16 tiles
+    cam = wide_camera(cfg)
+    ctx = api.Context(0, use_torch_stream=False)
+    ctx.upload_scene(s)
+    info = ctx.render(cam, cfg, outputs=L.OUT_HOLOGRAM | L.OUT_INTENSITY | L.OUT_AUX)
+    assert info.max_bucket > 1024 and info.num_entries > 20 * 1025
+    ref = _frame(ctx, 3, 64, 64, 2)
+    ctx.set_async(True)
+    ctx.reserve_entries(100)
+    ctx.render(cam, cfg, outputs=L.OUT_HOLOGRAM | L.OUT_INTENSITY | L.OUT_AUX)
+    gl = torch.zeros((2, 3, 64, 64), dtype=torch.complex64, device="cuda:0")
+    with pytest.raises(HoloError) as e:
+        ctx.raster_backward(cam, cfg, None, gl, s.size())
+    assert "overflowed" in str(e.value)
+    with pytest.raises(HoloError) as e:
+        ctx.frame_status()
+    assert e.value.kind == "numeric" and "reserve" in str(e.value)
+    ctx.render(cam, cfg, outputs=L.OUT_HOLOGRAM | L.OUT_INTENSITY | L.OUT_AUX)  # the reservation grew
+    assert ctx.frame_status().num_entries == info.num_entries
+    got = _frame(ctx, 3, 64, 64, 2)
+    assert np.array_equal(got[0], ref[0])
+    ctx.raster_backward(cam, cfg, None, gl, s.size())
+    ctx.close()
+
+
 def test_async_upload_render_download_pipeline():
     # scene uploads on the copy-in stream into the set the running frame does not
     # read, downloads on the copy-out stream: several frames enqueued back to back

@@ -50,6 +50,23 @@ def test_plane_subsets_partition_the_scene_in_order():
             assert np.array_equal(p.plane_logits, s.plane_logits[idx])
 
 
+def test_hard_planes_follow_the_kernels_strict_scan():
+    """NaN logits never win the device's strict '>' scan (preprocess.cu), so a
+    NaN in front keeps plane 0 and a NaN later is skipped; ties keep the lower
+    plane.  np.argmax would send the first row to plane 1."""
+    from paper_2506_08350_b200.holotypes import GaussianScene
+    from paper_2506_08350_b200.sharding import hard_planes
+
+    s = GaussianScene(num_planes=4)
+    s.resize(5)
+    s.plane_logits = np.array([[0.0, np.nan, 1.0, 0.5],
+                               [np.nan, 2.0, 3.0, 1.0],
+                               [1.0, 1.0, 1.0, 1.0],
+                               [0.0, 0.0, 0.0, 5.0],
+                               [np.nan, np.nan, np.nan, np.nan]])
+    assert hard_planes(s).tolist() == [2, 0, 0, 3, 0]
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
