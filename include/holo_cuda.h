@@ -213,6 +213,98 @@ int holo_render_begin(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wa
 int holo_render_end(holo_ctx* ctx, const holo_wave* wave, const holo_prop_options* prop, int plane_begin,
                     int plane_end, const void* spectrum, unsigned outputs);
 
+/* ---- multi-GPU groups: planes, views, planes x views ----
+ * The reference has no distributed code.  The unit that is split is
+ * one pipeline_forward frame (pipeline.cpp:20-29):
+ *   planes  forward_record's sum over planes (propagation.cpp:103-114) is linear,
+ *           and hard assignment puts each Gaussian in one plane (rasterizer.cpp:
+ *           91-96): a rank renders planes [plane_begin, plane_end) of its plane
+ *           group, the partial spectra are summed channel by channel (the sum of
+ *           channel c overlaps the row pass of channel c + 1), and the rank forms
+ *           its planes' replays / intensities and the hologram channels c with
+ *           c mod plane_split == its plane rank.
+ *   views   independent frames of one resident scene, as train iterates views
+ *           (trainer.cpp:118-133; holo_main.cpp:241-258 --view-index): no
+ *           per-frame collective.
+ *   both    world = view_groups x plane_split; the sum runs inside each plane
+ *           group (ranks r with equal r / plane_split).
+ * Mesh: plane_split = ranks per plane group (1 = views only, world = planes only).
+ * Views [view_begin, view_end) of a num_views batch go to view group r / plane_split.
+ * Transports: NCCL (one process per GPU from a shared unique id, or one process
+ * driving several devices), or a caller callback that sums `count` floats of a
+ * device buffer over the plane group, ordered on `stream` (tests, custom fabrics). */
+typedef struct holo_group holo_group;
+#define HOLO_GROUP_ID_BYTES 128
+
+typedef struct {
+    int world, rank;
+    int plane_split;             /* ranks per plane group */
+    int view_groups;             /* world / plane_split */
+    int plane_rank, view_group;  /* this rank's coordinates */
+    int plane_begin, plane_end;  /* planes this rank renders */
+    int view_begin, view_end;    /* views of the batch this rank renders */
+    unsigned holo_channels;      /* bit c: this rank forms hologram channel c */
+} holo_mesh;
+
+/* Pure host arithmetic (no device): the coordinates above for (world, rank). */
+int holo_mesh_layout(int world, int rank, int plane_split, int num_planes, int num_views, int channels,
+                     holo_mesh* out);
+
+typedef int (*holo_allreduce_fn)(void* user, float* device_buffer, size_t count, void* cuda_stream);
+
+int holo_group_unique_id(unsigned char id[HOLO_GROUP_ID_BYTES]);
+/* one process per GPU: every rank passes the same id (rank 0's, broadcast by the
+ * caller); ctx stays the caller's. */
+int holo_group_init_rank(holo_ctx* ctx, const unsigned char id[HOLO_GROUP_ID_BYTES], int world, int rank,
+                         int plane_split, holo_group** out);
+int holo_group_init_callback(holo_ctx* ctx, int world, int rank, int plane_split, holo_allreduce_fn fn, void* user,
+                             holo_group** out);
+/* one process, n devices (ncclCommInitAll); the group creates and owns a context per device */
+int holo_group_create(const int* devices, int n, int plane_split, holo_group** out);
+int holo_group_destroy(holo_group* g);
+/* local ranks of this process (1, or n for holo_group_create) and their contexts */
+int holo_group_local_count(const holo_group* g);
+int holo_group_context(holo_group* g, int local, holo_ctx** ctx);
+/* frames in flight per local rank (each lane: its own stream and scene copy; default 1) */
+int holo_group_set_lanes(holo_group* g, int lanes);
+/* upload the full scene on every local rank; a rank of a plane-sharded group keeps
+ * its planes' Gaussians only (device-side stable subset). */
+int holo_group_upload_scene(holo_group* g, const holo_scene_arrays* host);
+
+/* caller-owned device destinations of one view on one local rank (NULL members:
+ * the lane's context buffers).  hologram [C][H][W] complex64 (channels this rank
+ * forms); replayed [np][C][H][W] complex64 and intensities [np][C][H][W] float32
+ * for the rank's planes. */
+typedef struct {
+    void* hologram;
+    void* replayed;
+    void* intensities;
+} holo_view_outputs;
+
+enum {
+    HOLO_GROUP_GATHER_HOLOGRAM = 1u << 0, /* every rank of a plane group gets all hologram channels */
+    HOLO_GROUP_SHARDED_PATH = 1u << 1     /* run the plane-sharded pipeline even for plane groups of one (tests) */
+};
+
+/* Render views [view_begin, view_end) of cams[0..num_views) on every local rank.
+ * outs / infos: NULL or num_views x local_count entries, index v * local_count + local
+ * (only the entries of views a rank renders are used / written). */
+int holo_group_render(holo_group* g, const holo_camera* cams, int num_views, const holo_wave* wave,
+                      const holo_raster_settings* settings, const holo_prop_options* prop, unsigned outputs,
+                      unsigned flags, const holo_view_outputs* outs, holo_frame_info* infos);
+int holo_group_synchronize(holo_group* g);
+/* holo_ctx_set_async on every lane (the lanes share the largest reservation) */
+int holo_group_set_async(holo_group* g, int enable);
+/* holo_ctx_frame_status over every lane: the first failure is returned */
+int holo_group_frame_status(holo_group* g);
+/* make `stream` (a cudaStream_t on local rank's device) wait for all of that
+ * rank's work enqueued so far (its lanes and collectives) */
+int holo_group_join(holo_group* g, int local, void* stream);
+/* kernel launches of all lanes of all local ranks */
+uint64_t holo_group_launch_count(const holo_group* g);
+/* local rank's mesh coordinates for a batch of num_views views of the wave's planes */
+int holo_group_mesh(const holo_group* g, int local, int num_planes, int num_views, int channels, holo_mesh* out);
+
 /* ---- gradients (rasterizer.hpp:79-81 raster_backward; pipeline.cpp:63-91) ----
  * Scene-shaped gradient arrays, device f64 (SceneGradients, scene.hpp:40-46;
  * mu_screen is N x 2).  NULL members are not written; the others are overwritten. */

@@ -110,6 +110,22 @@ class FrameInfo(C.Structure):
                 ("pad_", C.c_int32)]
 
 
+class Mesh(C.Structure):
+    """holo_mesh: a rank's coordinates in the (view groups x plane split) mesh."""
+    _fields_ = [("world", C.c_int), ("rank", C.c_int), ("plane_split", C.c_int), ("view_groups", C.c_int),
+                ("plane_rank", C.c_int), ("view_group", C.c_int), ("plane_begin", C.c_int), ("plane_end", C.c_int),
+                ("view_begin", C.c_int), ("view_end", C.c_int), ("holo_channels", C.c_uint)]
+
+
+class ViewOutputs(C.Structure):
+    _fields_ = [("hologram", C.c_void_p), ("replayed", C.c_void_p), ("intensities", C.c_void_p)]
+
+
+GROUP_ID_BYTES = 128
+GROUP_GATHER_HOLOGRAM, GROUP_SHARDED_PATH = 1, 2
+# int fn(void* user, float* device_buffer, size_t count, void* cuda_stream)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
 _LIB = None
 
 
@@ -169,6 +185,24 @@ def lib() -> C.CDLL:
         "holo_forward_record": (i, [vp, vp, i, vp, P(Wave), P(PropOptions), i]),
         "holo_inverse_propagate": (i, [vp, vp, vp, P(Wave), P(PropOptions), i]),
         "holo_intensity": (i, [vp, vp, vp, sz, i]),
+        "holo_mesh_layout": (i, [i, i, i, i, i, i, P(Mesh)]),
+        "holo_group_unique_id": (i, [C.c_char_p]),
+        "holo_group_init_rank": (i, [vp, C.c_char_p, i, i, i, P(vp)]),
+        "holo_group_init_callback": (i, [vp, i, i, i, ALLREDUCE_FN, vp, P(vp)]),
+        "holo_group_create": (i, [P(i), i, i, P(vp)]),
+        "holo_group_destroy": (i, [vp]),
+        "holo_group_local_count": (i, [vp]),
+        "holo_group_context": (i, [vp, i, P(vp)]),
+        "holo_group_mesh": (i, [vp, i, i, i, i, P(Mesh)]),
+        "holo_group_set_lanes": (i, [vp, i]),
+        "holo_group_upload_scene": (i, [vp, P(SceneArrays)]),
+        "holo_group_render": (i, [vp, P(Camera), i, P(Wave), P(RasterSettings), P(PropOptions), u, u,
+                                  P(ViewOutputs), P(FrameInfo)]),
+        "holo_group_synchronize": (i, [vp]),
+        "holo_group_set_async": (i, [vp, i]),
+        "holo_group_frame_status": (i, [vp]),
+        "holo_group_join": (i, [vp, i, vp]),
+        "holo_group_launch_count": (C.c_uint64, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -487,6 +487,164 @@ class Optimizer:
 _DEFAULT: dict = {}
 
 
+def _scene_arrays(scene: GaussianScene):
+    n = scene.size()
+    arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in
+            (scene.positions, scene.rotations, scene.log_scales, scene.amplitudes, scene.opacity_logits,
+             scene.phases, scene.plane_logits)]
+    if [a.size for a in arrs] != [3 * n, 4 * n, 3 * n, 3 * n, n, 3 * n, n * scene.num_planes]:
+        raise HoloError("config", "scene arrays have inconsistent sizes")
+    s = L.SceneArrays()
+    s.n, s.num_planes = n, int(scene.num_planes)
+    for name, a in zip(("positions", "rotations", "log_scales", "amplitudes", "opacity_logits", "phases",
+                        "plane_logits"), arrs):
+        setattr(s, name, a.ctypes.data)
+    return s, arrs
+
+
+def mesh_layout(world: int, rank: int, plane_split: int, num_planes: int, num_views: int = 1,
+                channels: int = 3) -> L.Mesh:
+    """holo_mesh_layout: pure host arithmetic of the (view groups x plane split) mesh."""
+    m = L.Mesh()
+    L.check(L.lib().holo_mesh_layout(int(world), int(rank), int(plane_split), int(num_planes), int(num_views),
+                                     int(channels), C.byref(m)))
+    return m
+
+
+def gloo_allreduce(group=None):
+    """An all-reduce callback for Group(transport=callback) that sums through a
+    torch.distributed process group on host memory (gloo): the transport the
+    world-2/4 tests use when every rank shares one GPU (NCCL refuses two ranks on
+    one device).  Blocking; production groups use NCCL."""
+    torch = _torch()
+    import torch.distributed as dist
+
+    def fn(user, buf, count, stream):
+        try:
+            torch.cuda.ExternalStream(int(stream or 0)).synchronize()
+            dev = torch.as_tensor(L._CudaArray(int(buf), (int(count),), "<f4"), device="cuda")
+            host = dev.cpu()
+            dist.all_reduce(host, group=group)
+            dev.copy_(host)
+            torch.cuda.synchronize()
+            return 0
+        except Exception as e:  # noqa: BLE001 - reported as a status code to the library
+            print(f"gloo_allreduce: {e!r}")
+            return 1
+
+    return fn
+
+
+class Group:
+    """holo_group (include/holo_cuda.h): this process's ranks of a multi-GPU render
+    -- plane sharding (C3), view sharding (C4) or planes x views (C5).
+
+    ``ctx``: this rank's Context (one process per GPU).  ``plane_split``: ranks per
+    plane group (default: world, planes only; 1: views only).  Transport: NCCL from
+    ``unique_id`` (rank 0's ``Group.unique_id()``, shared by the caller), or
+    ``allreduce`` = a Python callable (see gloo_allreduce)."""
+
+    def __init__(self, ctx: Context, world: int = 1, rank: int = 0, plane_split: Optional[int] = None,
+                 unique_id: Optional[bytes] = None, allreduce=None):
+        self.lib = L.lib()
+        self.ctx, self.world, self.rank = ctx, int(world), int(rank)
+        self.plane_split = int(world if plane_split is None else plane_split)
+        h = C.c_void_p()
+        self._cb = None
+        if allreduce is not None:
+            self._cb = L.ALLREDUCE_FN(allreduce)
+            L.check(self.lib.holo_group_init_callback(ctx.h, self.world, self.rank, self.plane_split, self._cb, None,
+                                                      C.byref(h)))
+        else:
+            uid = unique_id if unique_id is not None else (Group.unique_id() if self.world == 1 else None)
+            if uid is None or len(uid) != L.GROUP_ID_BYTES:
+                raise HoloError("usage", "Group: NCCL transport needs rank 0's 128-byte unique id")
+            L.check(self.lib.holo_group_init_rank(ctx.h, bytes(uid), self.world, self.rank, self.plane_split,
+                                                  C.byref(h)))
+        self.h = h
+        self._keep = []
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(L.GROUP_ID_BYTES)
+        L.check(L.lib().holo_group_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_torch(cls, ctx: Context, plane_split: Optional[int] = None, group=None):
+        """NCCL group over the ranks of a torch.distributed process group (the
+        unique id is broadcast from rank 0 through it)."""
+        import torch.distributed as dist
+
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        obj = [Group.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(ctx, world, rank, plane_split, unique_id=obj[0])
+
+    def close(self):
+        if getattr(self, "h", None):
+            L.check(self.lib.holo_group_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def mesh(self, num_planes: int, num_views: int = 1, channels: int = 3) -> L.Mesh:
+        m = L.Mesh()
+        L.check(self.lib.holo_group_mesh(self.h, 0, int(num_planes), int(num_views), int(channels), C.byref(m)))
+        return m
+
+    def set_lanes(self, lanes: int) -> None:
+        """Frames in flight on this rank (each lane: own stream and scene copy)."""
+        L.check(self.lib.holo_group_set_lanes(self.h, int(lanes)))
+
+    def upload_scene(self, scene: GaussianScene) -> None:
+        """The full scene; a plane-sharded rank keeps its planes' Gaussians (on the device)."""
+        s, arrs = _scene_arrays(scene)
+        L.check(self.lib.holo_group_upload_scene(self.h, C.byref(s)))
+        self._keep = arrs
+
+    def render(self, cams: Sequence[CameraView], cfg: WaveConfig, settings: Optional[RenderSettings] = None,
+               prop: Optional[PropagationOptions] = None, outputs: int = L.OUT_HOLOGRAM | L.OUT_INTENSITY,
+               flags: int = 0, view_outputs: Optional[dict] = None) -> List[L.FrameInfo]:
+        """Render this rank's share of the views ``cams``.  view_outputs: {view:
+        (hologram, replayed, intensities)} caller device tensors (None members: the
+        context's buffers).  Returns the FrameInfo of every view (zeros for views
+        rendered elsewhere, and for asynchronous frames)."""
+        V = len(cams)
+        cam_arr = (L.Camera * V)(*[_camera(c) for c in cams])
+        infos = (L.FrameInfo * V)()
+        outs = None
+        if view_outputs:
+            outs = (L.ViewOutputs * V)()
+            for v, (hh, rr, ii) in view_outputs.items():
+                outs[v].hologram = hh.data_ptr() if hh is not None else None
+                outs[v].replayed = rr.data_ptr() if rr is not None else None
+                outs[v].intensities = ii.data_ptr() if ii is not None else None
+        L.check(self.lib.holo_group_render(self.h, cam_arr, V, C.byref(_wave(cfg)), C.byref(_settings(settings)),
+                                           C.byref(_prop(prop)), int(outputs), int(flags), outs, infos))
+        return list(infos)
+
+    def synchronize(self) -> None:
+        L.check(self.lib.holo_group_synchronize(self.h))
+
+    def set_async(self, on: bool = True) -> None:
+        L.check(self.lib.holo_group_set_async(self.h, int(on)))
+
+    def frame_status(self) -> None:
+        L.check(self.lib.holo_group_frame_status(self.h))
+
+    def join(self, stream: int) -> None:
+        """Make CUDA stream `stream` wait for all of this rank's enqueued work."""
+        L.check(self.lib.holo_group_join(self.h, 0, C.c_void_p(int(stream) or None)))
+
+    def launch_count(self) -> int:
+        return int(self.lib.holo_group_launch_count(self.h))
+
+
 def default_context(device: int = 0) -> Context:
     ctx = _DEFAULT.get(device)
     if ctx is None:

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "render.h"
 
 using namespace holo_cuda;
 
@@ -33,9 +34,6 @@ int guarded(F&& f) {
     }
 }
 
-void require(bool ok, int code, const char* msg) {
-    if (!ok) throw Error(code, msg);
-}
 
 // WaveConfig::validate (wave_config.cpp:5-16), same messages
 void validate_wave(const holo_wave& w) {
@@ -623,6 +621,10 @@ int holo_ctx_destroy(holo_ctx* ctx) {
         }
         cudaEventDestroy(ctx->ev_out_src);
         for (auto e : ctx->ev_out_done) cudaEventDestroy(e);
+        for (int c = 0; c < HOLO_MAX_CHANNELS; ++c) {
+            if (ctx->ev_chan_ready[c]) cudaEventDestroy(ctx->ev_chan_ready[c]);
+            if (ctx->ev_chan_done[c]) cudaEventDestroy(ctx->ev_chan_done[c]);
+        }
         cudaStreamDestroy(ctx->copy_in);
         cudaStreamDestroy(ctx->copy_out);
         if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
@@ -822,11 +824,15 @@ OutBufs output_buffers(holo_ctx* ctx, unsigned outputs, int np, int C, size_t P)
     OutBufs o;
     const int k = ctx->out_sel;
     if (outputs & HOLO_OUT_HOLOGRAM)
-        o.holo = buf<cx<float>>(ctx, out_name("hologram", k).c_str(), static_cast<size_t>(C) * P);
+        o.holo = ctx->out_dest[0] ? static_cast<cx<float>*>(ctx->out_dest[0])
+                                  : buf<cx<float>>(ctx, out_name("hologram", k).c_str(), static_cast<size_t>(C) * P);
     if (outputs & HOLO_OUT_REPLAYED)
-        o.rep = buf<cx<float>>(ctx, out_name("replayed", k).c_str(), static_cast<size_t>(np) * C * P);
+        o.rep = ctx->out_dest[1]
+                    ? static_cast<cx<float>*>(ctx->out_dest[1])
+                    : buf<cx<float>>(ctx, out_name("replayed", k).c_str(), static_cast<size_t>(np) * C * P);
     if (outputs & HOLO_OUT_INTENSITY)
-        o.ints = buf<float>(ctx, out_name("intensity", k).c_str(), static_cast<size_t>(np) * C * P);
+        o.ints = ctx->out_dest[2] ? static_cast<float*>(ctx->out_dest[2])
+                                  : buf<float>(ctx, out_name("intensity", k).c_str(), static_cast<size_t>(np) * C * P);
     return o;
 }
 
@@ -1107,13 +1113,20 @@ void render_full(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, c
     if (!(outputs & (HOLO_OUT_HOLOGRAM | HOLO_OUT_REPLAYED | HOLO_OUT_INTENSITY))) return;
     const cx<float>* layers = static_cast<const cx<float>*>(ctx->buffer("layers", 1));
     const int k = ctx->out_sel;
-    cx<float>* d_holo = buf<cx<float>>(ctx, out_name("hologram", k).c_str(), static_cast<size_t>(C) * P);
+    cx<float>* d_holo = (ctx->out_dest[0] && (outputs & HOLO_OUT_HOLOGRAM))
+                            ? static_cast<cx<float>*>(ctx->out_dest[0])
+                            : buf<cx<float>>(ctx, out_name("hologram", k).c_str(), static_cast<size_t>(C) * P);
     op_forward_record<float>(ctx, layers, L, d_holo, wave, po);
     if (outputs & (HOLO_OUT_REPLAYED | HOLO_OUT_INTENSITY)) {
-        cx<float>* d_rep = buf<cx<float>>(ctx, out_name("replayed", k).c_str(), static_cast<size_t>(L) * C * P);
+        cx<float>* d_rep = (ctx->out_dest[1] && (outputs & HOLO_OUT_REPLAYED))
+                               ? static_cast<cx<float>*>(ctx->out_dest[1])
+                               : buf<cx<float>>(ctx, out_name("replayed", k).c_str(), static_cast<size_t>(L) * C * P);
         op_inverse_propagate<float>(ctx, d_holo, d_rep, wave, po);
         if (outputs & HOLO_OUT_INTENSITY)
-            intensity<float>(ctx, d_rep, buf<float>(ctx, out_name("intensity", k).c_str(), static_cast<size_t>(L) * C * P),
+            intensity<float>(ctx, d_rep,
+                             ctx->out_dest[2] ? static_cast<float*>(ctx->out_dest[2])
+                                              : buf<float>(ctx, out_name("intensity", k).c_str(),
+                                                           static_cast<size_t>(L) * C * P),
                              static_cast<size_t>(L) * C * P);
     }
 }
@@ -1138,6 +1151,223 @@ void pipeline_backward(holo_ctx* ctx, const holo_camera& cam, const holo_wave& w
 }
 
 }  // namespace
+
+// ---------------------------------------------------------------- plane-sharded frames, channel by channel
+// (the group renderer in group.cu; declared in render.h)
+namespace holo_cuda {
+
+void render_whole(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, const holo_raster_settings& st,
+                  const holo_prop_options& po, unsigned outputs, holo_frame_info* info) {
+    render_full(ctx, cam, wave, st, po, outputs, info);
+}
+
+void chan_events(holo_ctx* ctx) {
+    for (int c = 0; c < HOLO_MAX_CHANNELS; ++c) {
+        if (!ctx->ev_chan_ready[c]) HC_CUDA(cudaEventCreateWithFlags(&ctx->ev_chan_ready[c], cudaEventDisableTiming));
+        if (!ctx->ev_chan_done[c]) HC_CUDA(cudaEventCreateWithFlags(&ctx->ev_chan_done[c], cudaEventDisableTiming));
+    }
+}
+
+// Raster planes [pb, pe), then the partial spectrum S_g channel by channel into
+// spec ([C][H][W]); ev_chan_ready[c] marks channel c complete on the context
+// stream, so the sum over the plane group can start on channel c while the
+// row pass of channel c + 1 runs.
+void shard_front(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, const holo_raster_settings& st,
+                 const holo_prop_options& po, int pb, int pe, unsigned outputs, cx<float>* spec,
+                 holo_frame_info* info) {
+    const FrameGeom g = check_render(ctx, cam, wave, st);
+    require(pb >= 0 && pe <= g.L && pb <= pe, HOLO_ERR_USAGE, "plane range outside [0, num_planes]");
+    require(!po.pad2x, HOLO_ERR_CONFIG, "plane-sharded rendering does not support pad2x");
+    chan_events(ctx);
+    ctx->out_sel ^= 1;
+    wait_downloads(ctx, -1, ~kLateBufs);
+    ctx->f_L = g.L;
+    ctx->f_C = g.C;
+    ctx->f_W = g.W;
+    ctx->f_H = g.H;
+    ctx->f_tiles = g.num_tiles;
+    ctx->f_outputs = outputs;
+    ctx->f_plane_begin = pb;
+    ctx->f_plane_end = pe;
+    ctx->f_cam = cam;
+    ctx->f_st = st;
+    raster_planes(ctx, cam, wave, st, g, pb, pe, outputs, info);
+    const int np = pe - pb;
+    auto all_ready = [&] {
+        HC_CUDA(cudaEventRecord(ctx->ev_chan_ready[0], ctx->stream));
+        for (int c = 1; c < g.C; ++c) HC_CUDA(cudaEventRecord(ctx->ev_chan_ready[c], ctx->stream));
+    };
+    if (np == 0) {
+        HC_CUDA(cudaMemsetAsync(spec, 0, sizeof(cx<float>) * g.C * g.P, ctx->stream));
+        all_ready();
+        return;
+    }
+    const std::vector<double> zall = plane_positions(wave);
+    const std::vector<double> z(zall.begin() + pb, zall.begin() + pe);
+    const TfChan* tfc = upload_tf(ctx, "tf_render", wave, z, g.W, g.H, po.local_band_limit);
+    cx<float>* layers = static_cast<cx<float>*>(ctx->buffer("layers", 1));
+    const size_t nlay = static_cast<size_t>(np) * g.C * g.P;
+    if (static_render_supported(g.W, g.H)) {
+        cx<float>* work = layers;
+        if (outputs & HOLO_OUT_LAYERS) {
+            work = buf<cx<float>>(ctx, "colwork", nlay);
+            HC_CUDA(cudaMemcpyAsync(work, layers, sizeof(cx<float>) * nlay, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+        ctx->stage_begin();
+        static_col_fwd(ctx, work, g.W, g.H, np * g.C);
+        ctx->stage_end(3);
+        for (int c = 0; c < g.C; ++c) {
+            ctx->stage_begin();
+            static_row(ctx, kModeSpec, work, spec, nullptr, g.W, g.H, g.C, np, 0, 0, tfc, wave.pitch,
+                       po.local_band_limit != 0, c, 1);
+            ctx->stage_end(4);
+            HC_CUDA(cudaEventRecord(ctx->ev_chan_ready[c], ctx->stream));
+        }
+        return;
+    }
+    cx<float>* work = (outputs & HOLO_OUT_LAYERS) ? buf<cx<float>>(ctx, "rowwork", nlay) : layers;
+    ctx->stage_begin();
+    rows_fft<float>(ctx, layers, work, g.W, static_cast<long long>(np) * g.C * g.H, -1, 1.0f);
+    ctx->stage_end(3);
+    ctx->stage_begin();
+    col_spectrum<float>(ctx, work, spec, g.W, g.H, g.C, np, tfc, wave.pitch);
+    ctx->stage_end(4);
+    all_ready();
+}
+
+// From the summed spectrum: for each channel (after ev_chan_done[c]) the replay of
+// planes [pb, pe) and, for the channels in holo_mask, the hologram channel.
+void shard_back(holo_ctx* ctx, const holo_wave& wave, const holo_prop_options& po, int pb, int pe,
+                const cx<float>* spec, unsigned outputs, unsigned holo_mask) {
+    const int W = wave.nx, H = wave.ny, C = wave.channels;
+    const size_t P = static_cast<size_t>(W) * H;
+    const int np = pe - pb;
+    if (!(outputs & HOLO_OUT_HOLOGRAM)) holo_mask = 0;
+    holo_mask &= (C >= 32 ? ~0u : ((1u << C) - 1u));
+    const unsigned outs = (outputs & ~HOLO_OUT_HOLOGRAM) | (holo_mask ? HOLO_OUT_HOLOGRAM : 0u);
+    const std::vector<int> plane_of = output_planes(outs, np);
+    ctx->f_outputs |= outs;
+    if (plane_of.empty()) {
+        for (int c = 0; c < C; ++c) HC_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_chan_done[c], 0));
+        return;
+    }
+    const std::vector<double> zall = plane_positions(wave);
+    std::vector<double> z(zall.begin() + pb, zall.begin() + pe);
+    if (z.empty()) z.push_back(0.0);
+    const int O = static_cast<int>(plane_of.size());
+    const int hh = holo_mask ? 1 : 0;  // stage slot 0 holds the hologram when any channel is formed here
+    const int nrep = O - hh;
+    const TfChan* tfc = upload_tf(ctx, "tf_replay", wave, z, W, H, po.local_band_limit);
+    cx<float>* stage = buf<cx<float>>(ctx, "replay_stage", static_cast<size_t>(O) * C * P);
+    const OutBufs ob = output_buffers(ctx, outs, np, C, P);
+    if (static_render_supported(W, H)) {
+        for (int c = 0; c < C; ++c) {
+            HC_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_chan_done[c], 0));
+            const int own = (holo_mask >> c) & 1u;
+            // a channel whose hologram is formed elsewhere skips stage slot 0
+            cx<float>* st_c = stage + static_cast<size_t>(hh && !own ? 1 : 0) * C * P;
+            ctx->stage_begin();
+            static_row(ctx, kModeReplay, nullptr, const_cast<cx<float>*>(spec), st_c, W, H, C, np, own, nrep, tfc,
+                       wave.pitch, po.local_band_limit != 0, c, 1);
+            ctx->stage_end(5);
+        }
+        wait_downloads(ctx, ctx->out_sel, ~0u);
+        for (int c = 0; c < C; ++c) {
+            const int own = (holo_mask >> c) & 1u;
+            const cx<float>* st_c = stage + static_cast<size_t>(hh && !own ? 1 : 0) * C * P;
+            ctx->stage_begin();
+            static_col_inv(ctx, st_c, W, H, C, nrep + own, own, ob.holo, ob.rep, ob.ints, c, 1);
+            ctx->stage_end(6);
+        }
+        return;
+    }
+    for (int c = 0; c < C; ++c) HC_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_chan_done[c], 0));
+    int* d_plane_of = buf<int>(ctx, "plane_of_replay", O);
+    upload_small(ctx, d_plane_of, plane_of.data(), sizeof(int) * O);
+    ctx->stage_begin();
+    col_replay<float>(ctx, spec, stage, W, H, C, O, d_plane_of, tfc, wave.pitch);
+    ctx->stage_end(5);
+    wait_downloads(ctx, ctx->out_sel, ~0u);
+    ctx->stage_begin();
+    rows_epilogue(ctx, stage, W, H, C, O, hh, ob.holo, ob.rep, ob.ints);
+    ctx->stage_end(6);
+}
+
+// Keep only the Gaussians whose hard plane lies in [pb, pe) (scene_ops.cu), in
+// order: the subset goes to the other scene set, which becomes current.
+void scene_restrict_planes(holo_ctx* ctx, int pb, int pe) {
+    const int src_k = ctx->scene_cur, dst_k = src_k ^ 1;
+    holo_ctx::SceneSet& src = ctx->scene_sets[src_k];
+    holo_ctx::SceneSet& dst = ctx->scene_sets[dst_k];
+    const size_t n = ctx->n;
+    const int L = ctx->scene_planes;
+    if (ctx->scene_wait[src_k]) {  // a host upload into the source set may be in flight
+        HC_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_scene_ready[src_k], 0));
+        ctx->scene_wait[src_k] = false;
+    }
+    if (ctx->scene_wait[dst_k]) {
+        HC_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_scene_ready[dst_k], 0));
+        ctx->scene_wait[dst_k] = false;
+    }
+    const size_t count[7] = {3 * n, 4 * n, 3 * n, 3 * n, n, 3 * n, n * static_cast<size_t>(L)};
+    for (int a = 0; a < 7; ++a)
+        if (count[a] > dst.cap[a] || !dst.a[a]) {
+            HC_CUDA(cudaStreamSynchronize(ctx->stream));
+            cudaFree(dst.a[a]);
+            dst.a[a] = nullptr;
+            HC_CUDA(cudaMalloc(&dst.a[a], sizeof(double) * (count[a] ? count[a] : 1)));
+            dst.cap[a] = count[a];
+        }
+    const double* sp[7];
+    double* dp[7];
+    for (int a = 0; a < 7; ++a) {
+        sp[a] = src.a[a];
+        dp[a] = dst.a[a];
+    }
+    const size_t kept = scene_keep_planes(ctx, sp, dp, n, L, pb, pe);
+    ctx->scene_cur = dst_k;
+    double** cur[7] = {&ctx->d_positions, &ctx->d_rotations, &ctx->d_log_scales, &ctx->d_amplitudes,
+                       &ctx->d_opacity, &ctx->d_phases, &ctx->d_plane_logits};
+    for (int a = 0; a < 7; ++a) *cur[a] = dst.a[a];
+    ctx->n = kept;
+}
+
+void set_last_error(const char* msg) { g_last_error = msg; }
+
+// destination of the current frame's hologram (the caller's or the context set)
+cx<float>* frame_hologram(holo_ctx* ctx, int C, size_t P) {
+    if (ctx->out_dest[0]) return static_cast<cx<float>*>(ctx->out_dest[0]);
+    return buf<cx<float>>(ctx, out_name("hologram", ctx->out_sel).c_str(), static_cast<size_t>(C) * P);
+}
+
+// The current scene of `from` (same device) copied into `to`, ordered after
+// everything enqueued on from's stream.
+void scene_replicate(holo_ctx* from, holo_ctx* to) {
+    cudaEvent_t ev = nullptr;
+    HC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    const int k = from->scene_cur;
+    if (from->scene_wait[k]) {
+        HC_CUDA(cudaStreamWaitEvent(from->stream, from->ev_scene_ready[k], 0));
+        from->scene_wait[k] = false;
+    }
+    HC_CUDA(cudaEventRecord(ev, from->stream));
+    HC_CUDA(cudaStreamWaitEvent(to->stream, ev, 0));
+    HC_CUDA(cudaEventDestroy(ev));
+    const holo_ctx::SceneSet& s = from->scene_sets[k];
+    holo_scene_arrays arr{};
+    arr.n = from->n;
+    arr.num_planes = from->scene_planes;
+    arr.positions = s.a[0];
+    arr.rotations = s.a[1];
+    arr.log_scales = s.a[2];
+    arr.amplitudes = s.a[3];
+    arr.opacity_logits = s.a[4];
+    arr.phases = s.a[5];
+    arr.plane_logits = s.a[6];
+    if (holo_scene_upload_device(to, &arr) != HOLO_OK) throw Error(HOLO_ERR_CUDA, holo_last_error());
+}
+
+}  // namespace holo_cuda
 
 extern "C" {
 

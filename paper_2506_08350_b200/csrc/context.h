@@ -83,6 +83,13 @@ struct holo_ctx {
     cudaEvent_t ev_out_src = nullptr;       // frame work enqueued before an async download
     cudaEvent_t ev_out_done[2] = {};        // async downloads from set k complete (copy_out)
     unsigned out_pending[2] = {};           // buffer ids (bit per HOLO_BUF_*) with downloads in flight, per set
+    // caller-owned destinations of the final outputs (a multi-view group render
+    // writes each view straight into its own buffers); null = the context's sets
+    void* out_dest[3] = {};                 // hologram, replayed, intensities
+    // per-channel events of a plane-sharded frame: partial spectrum of channel c
+    // written (stream) / its sum over the plane group complete (comm stream)
+    cudaEvent_t ev_chan_ready[HOLO_MAX_CHANNELS] = {};
+    cudaEvent_t ev_chan_done[HOLO_MAX_CHANNELS] = {};
 
     // last frame
     int f_L = 0, f_C = 0, f_W = 0, f_H = 0, f_tiles = 0;

@@ -145,15 +145,23 @@ void entry_depths(holo_ctx* ctx, const int* egidx, const double* zc, double* ede
 // host[0..2] = misc[0..2] (flags, num_valid, max bucket), host[4] = *total (E); host is pinned
 void publish_status(holo_ctx* ctx, const unsigned* misc, const unsigned* total, unsigned* host_pinned);
 
+// ---- scene_ops.cu: stable subset of the Gaussians whose hard plane is in [pb, pe)
+// (src/dst: positions, rotations, log_scales, amplitudes, opacity, phases, plane
+// logits); returns the subset size (synchronises the context stream)
+size_t scene_keep_planes(holo_ctx* ctx, const double* const src[7], double* const dst[7], size_t n, int L, int pb,
+                         int pe);
+
 // ---- render_static.cu (compile-time FFT plans for the common grid sizes)
 enum { kModeFull = 0, kModeSpec = 1, kModeReplay = 2 };
 bool static_render_supported(int W, int H);
 void static_col_fwd(holo_ctx* ctx, cx<float>* data, int W, int H, int nfields);
+// [c0, c0 + nc) restricts a launch to those channels (nc < 0: through C - 1)
 void static_col_inv(holo_ctx* ctx, const cx<float>* in, int W, int H, int C, int nout, int has_holo,
-                    cx<float>* holo, cx<float>* rep, float* intens);
+                    cx<float>* holo, cx<float>* rep, float* intens, int c0 = 0, int nc = -1);
 // outputs of modes FULL / REPLAY: [hologram if has_holo] then planes 0..nrep-1
 void static_row(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spec, cx<float>* out, int W, int H,
-                int C, int Lloc, int has_holo, int nrep, const TfChan* tfc, double pitch, bool local);
+                int C, int Lloc, int has_holo, int nrep, const TfChan* tfc, double pitch, bool local, int c0 = 0,
+                int nc = -1);
 
 // ---- composite.cu
 struct CompositeArgs {

@@ -100,12 +100,6 @@ template <> struct RowCfgSel<1920> { using type = RowCfgT<1920, 1, 256, 4>; };
 template <int W>
 using RowCfg = typename RowCfgSel<W>::type;
 
-// Shape variants for tuning at the C3 sizes (HOLO_COL_VARIANT / HOLO_ROW_VARIANT).
-int env_variant(const char* name) {
-    const char* v = getenv(name);
-    return v ? atoi(v) : 0;
-}
-
 __device__ __forceinline__ cx<float> czf() { return mk(0.0f, 0.0f); }
 
 // e^{i theta} for |theta| up to a few thousand rad: two-constant reduction into
@@ -199,7 +193,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
     cx<float>* __restrict__ spec,          // [C][H][W]: written (SPEC) or read (REPLAY)
     cx<float>* __restrict__ out,           // [O][C][H][W] row-inverse-transformed outputs (FULL, REPLAY)
     int H, int C, int Lloc, int has_holo, int nrep, const TfChan* __restrict__ tfc,
-    const double* __restrict__ fx, const double* __restrict__ fy, const cx<float>* __restrict__ tw) {
+    const double* __restrict__ fx, const double* __restrict__ fy, const cx<float>* __restrict__ tw, int row_base) {
     constexpr int W = Cfg::W;
     constexpr int NBR = Cfg::NBR;
     using B = typename Cfg::B;
@@ -215,7 +209,10 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
     float2* s_tf = reinterpret_cast<float2*>(smem_raw + SM::kTf);  // (phase0, 2 pi z) per plane
     __shared__ unsigned long long s_bar;
 
-    const int row0 = blockIdx.x * NBR;  // row = c * H + y; a CTA never spans two channels
+    // row = c * H + y; a CTA never spans two channels.  row_base = c0 * H restricts a
+    // launch to the channels [c0, c0 + gridDim.x * NBR / H) (per-channel pipelines
+    // of a plane-sharded frame).
+    const int row0 = row_base + blockIdx.x * NBR;
     const int c = row0 / H;
     const size_t plane_stride = static_cast<size_t>(C) * H * W;
     const int nplanes = MODE == kModeReplay ? nrep : Lloc;
@@ -358,12 +355,12 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_col_inv_epi(const 
                                                                           const cx<float>* __restrict__ tw,
                                                                           cx<float>* __restrict__ holo,
                                                                           cx<float>* __restrict__ replayed,
-                                                                          float* __restrict__ intens) {
+                                                                          float* __restrict__ intens, int c_base) {
     constexpr int H = Cfg::H;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<float>* sm = reinterpret_cast<cx<float>*>(smem_raw);
     const int x0 = blockIdx.x * Cfg::NB;
-    const int c = blockIdx.y, o = blockIdx.z;
+    const int c = c_base + blockIdx.y, o = blockIdx.z;
     const size_t P = static_cast<size_t>(H) * W;
     const cx<float>* src = in + (static_cast<size_t>(o) * C + c) * P;
     const bool is_holo = has_holo && o == 0;
@@ -404,35 +401,35 @@ void launch_col_fwd_cfg(holo_ctx* ctx, cx<float>* data, int W, int nfields) {
 
 template <class Cfg>
 void launch_col_inv_cfg(holo_ctx* ctx, const cx<float>* in, int W, int C, int nout, int has_holo, cx<float>* holo,
-                        cx<float>* rep, float* intens) {
+                        cx<float>* rep, float* intens, int c0, int nc) {
     smem_attr(k_col_inv_epi<Cfg>, Cfg::kSmem);
-    const dim3 grid((W + Cfg::NB - 1) / Cfg::NB, C, nout);
+    const dim3 grid((W + Cfg::NB - 1) / Cfg::NB, nc, nout);
     const float s = static_cast<float>(1.0 / (static_cast<double>(W) * Cfg::H));
     k_col_inv_epi<Cfg><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(in, W, C, has_holo, s,
-                                                                   ctx->twiddle<float>(Cfg::H), holo, rep, intens);
+                                                                   ctx->twiddle<float>(Cfg::H), holo, rep, intens, c0);
     HC_LAUNCHED(ctx);
 }
 
 template <class Cfg, int MODE, bool LOCAL>
 void launch_row_mode(holo_ctx* ctx, const cx<float>* layers, cx<float>* spec, cx<float>* out, int H, int C, int Lloc,
-                     int has_holo, int nrep, const TfChan* tfc, const double* fx, const double* fy) {
-    const dim3 grid(C * H / Cfg::NBR);
+                     int has_holo, int nrep, const TfChan* tfc, const double* fx, const double* fy, int c0, int nc) {
+    const dim3 grid(nc * H / Cfg::NBR);
     const int nplanes = MODE == kModeReplay ? nrep : Lloc;
     const size_t smem = RowSmem<Cfg, MODE>::bytes(nplanes);
     HC_CUDA(cudaFuncSetAttribute(k_row_fused<Cfg, MODE, LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
     k_row_fused<Cfg, MODE, LOCAL><<<grid, Cfg::NT, smem, ctx->stream>>>(
-        layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, ctx->twiddle<float>(Cfg::W));
+        layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, ctx->twiddle<float>(Cfg::W), c0 * H);
     HC_LAUNCHED(ctx);
 }
 
 template <class Cfg>
 void launch_row_cfg(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spec, cx<float>* out, int H, int C,
                     int Lloc, int has_holo, int nrep, const TfChan* tfc, const double* fx, const double* fy,
-                    bool local) {
-#define HC_ROW_MODE(M)                                                                                      \
-    (local ? launch_row_mode<Cfg, M, true>(ctx, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy) \
-           : launch_row_mode<Cfg, M, false>(ctx, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy))
+                    bool local, int c0, int nc) {
+#define HC_ROW_MODE(M)                                                                                              \
+    (local ? launch_row_mode<Cfg, M, true>(ctx, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, c0, nc) \
+           : launch_row_mode<Cfg, M, false>(ctx, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, c0, nc))
     switch (mode) {
         case kModeFull: HC_ROW_MODE(kModeFull); break;
         case kModeSpec: HC_ROW_MODE(kModeSpec); break;
@@ -443,35 +440,20 @@ void launch_row_cfg(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>*
 
 template <int H>
 void launch_col_fwd(holo_ctx* ctx, cx<float>* data, int W, int nfields) {
-    if constexpr (H == 1080) {
-        switch (env_variant("HOLO_COL_VARIANT")) {
-            case 1: return launch_col_fwd_cfg<ColCfgT<H, 4, 256, 4>>(ctx, data, W, nfields);
-            case 2: return launch_col_fwd_cfg<ColCfgT<H, 16, 512, 1>>(ctx, data, W, nfields);
-            case 3: return launch_col_fwd_cfg<ColCfgT<H, 8, 256, 3>>(ctx, data, W, nfields);
-            default: break;
-        }
-    }
     launch_col_fwd_cfg<ColCfg<H>>(ctx, data, W, nfields);
 }
 
 template <int H>
 void launch_col_inv(holo_ctx* ctx, const cx<float>* in, int W, int C, int nout, int has_holo, cx<float>* holo,
-                    cx<float>* rep, float* intens) {
-    if constexpr (H == 1080) {
-        switch (env_variant("HOLO_COL_VARIANT")) {
-            case 1: return launch_col_inv_cfg<ColCfgT<H, 4, 256, 4>>(ctx, in, W, C, nout, has_holo, holo, rep, intens);
-            case 2: return launch_col_inv_cfg<ColCfgT<H, 16, 512, 1>>(ctx, in, W, C, nout, has_holo, holo, rep, intens);
-            case 3: return launch_col_inv_cfg<ColCfgT<H, 8, 256, 3>>(ctx, in, W, C, nout, has_holo, holo, rep, intens);
-            default: break;
-        }
-    }
-    launch_col_inv_cfg<ColCfg<H>>(ctx, in, W, C, nout, has_holo, holo, rep, intens);
+                    cx<float>* rep, float* intens, int c0, int nc) {
+    launch_col_inv_cfg<ColCfg<H>>(ctx, in, W, C, nout, has_holo, holo, rep, intens, c0, nc);
 }
 
 template <int W>
 void launch_row(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spec, cx<float>* out, int H, int C,
-                int Lloc, int has_holo, int nrep, const TfChan* tfc, const double* fx, const double* fy, bool local) {
-    launch_row_cfg<RowCfg<W>>(ctx, mode, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, local);
+                int Lloc, int has_holo, int nrep, const TfChan* tfc, const double* fx, const double* fy, bool local,
+                int c0, int nc) {
+    launch_row_cfg<RowCfg<W>>(ctx, mode, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, local, c0, nc);
 }
 
 #define HC_SIZES(X) X(48) X(64) X(128) X(256) X(512) X(1024) X(1080) X(1920) X(2048) X(2160) X(3840)
@@ -520,11 +502,12 @@ void static_col_fwd(holo_ctx* ctx, cx<float>* data, int W, int H, int nfields) {
 }
 
 void static_col_inv(holo_ctx* ctx, const cx<float>* in, int W, int H, int C, int nout, int has_holo,
-                    cx<float>* holo, cx<float>* rep, float* intens) {
-    if (nout <= 0) return;
-#define HC_CASE(N)                                                          \
-    case N:                                                                 \
-        launch_col_inv<N>(ctx, in, W, C, nout, has_holo, holo, rep, intens); \
+                    cx<float>* holo, cx<float>* rep, float* intens, int c0, int nc) {
+    if (nc < 0) nc = C - c0;
+    if (nout <= 0 || nc <= 0) return;
+#define HC_CASE(N)                                                                  \
+    case N:                                                                         \
+        launch_col_inv<N>(ctx, in, W, C, nout, has_holo, holo, rep, intens, c0, nc); \
         return;
     switch (H) {
         HC_SIZES(HC_CASE)
@@ -535,12 +518,14 @@ void static_col_inv(holo_ctx* ctx, const cx<float>* in, int W, int H, int C, int
 }
 
 void static_row(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spec, cx<float>* out, int W, int H,
-                int C, int Lloc, int has_holo, int nrep, const TfChan* tfc, double pitch, bool local) {
+                int C, int Lloc, int has_holo, int nrep, const TfChan* tfc, double pitch, bool local, int c0, int nc) {
+    if (nc < 0) nc = C - c0;
+    if (nc <= 0) return;
     const double* fx = ctx->freq(W, pitch);
     const double* fy = ctx->freq(H, pitch);
-#define HC_CASE(N)                                                                               \
-    case N:                                                                                      \
-        launch_row<N>(ctx, mode, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, local); \
+#define HC_CASE(N)                                                                                       \
+    case N:                                                                                              \
+        launch_row<N>(ctx, mode, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, local, c0, nc); \
         return;
     switch (W) {
         HC_SIZES(HC_CASE)

@@ -99,6 +99,7 @@ class BenchConfig:
     wavelengths: Tuple[float, ...]
     seed: int
     views: int = 1
+    shard: str = "planes"  # multi-GPU split: "planes", "views" or "planes_views" (bench.py)
 
     def wave(self) -> WaveConfig:
         return WaveConfig(nx=self.nx, ny=self.ny, pitch=3.74e-6, wavelengths=tuple(self.wavelengths),
@@ -116,8 +117,10 @@ CONFIGS = {
     "C1": BenchConfig("C1", 10_000, 256, 256, 3, (515e-9,), 1),
     "C2": BenchConfig("C2", 100_000, 1024, 1024, 6, RGB, 2),
     "C3": BenchConfig("C3", 1_000_000, 1920, 1080, 8, RGB, 3),
-    "C4": BenchConfig("C4", 1_000_000, 1024, 1024, 6, RGB, 4, views=64),
-    "C5": BenchConfig("C5", 3_000_000, 3840, 2160, 16, RGB, 5),
+    "C4": BenchConfig("C4", 1_000_000, 1024, 1024, 6, RGB, 4, views=64, shard="views"),
+    # BASELINE names planes x views for C5 without a view count: a batch of 8 views
+    # (yaw -0.1 .. +0.1 rad), 2 plane ranks x 4 view groups on 8 GPUs
+    "C5": BenchConfig("C5", 3_000_000, 3840, 2160, 16, RGB, 5, views=8, shard="planes_views"),
 }
 
 

@@ -3,14 +3,17 @@
 Plane sharding (BASELINE C3 at 1/2/4/8 GPUs): the hard plane assignment makes
 every Gaussian belong to one depth plane (rasterizer.cpp:91-96), so rank g
 rasterises planes [pb, pe) only, transforms them and forms its partial spectrum
-S_g = sum_{l in g} H_{Z_l} FFT2(U_l).  Because forward_record is linear
-(propagation.cpp:103-114), one all-reduce (sum) of S_g gives S, from which each
-rank replays its own planes and rank 0 forms the hologram IFFT2(S)
-(holo_render_begin / holo_render_end, include/holo_cuda.h).  Cost: C*H*W*8 bytes
-per frame over NVLink (49.8 MB at C3).
+S_g = sum_{l in g} H_{Z_l} FFT2(U_l) channel by channel.  Because forward_record
+is linear (propagation.cpp:103-114), the sum of S_g over the plane group gives S;
+channel c is summed while the row pass of channel c + 1 runs, then each rank
+replays its own planes and forms the hologram channels c with c mod plane_split
+== its plane rank (holo_group_render, include/holo_cuda.h; the lower-level
+holo_render_begin / _end split one frame around a caller's collective).  Cost:
+C*H*W*8 bytes per frame over NVLink (49.8 MB at C3).
 
 View sharding (C4): frames are independent; each rank renders its slice of the
-views with no per-frame collective.
+views with no per-frame collective.  Planes x views (C5): world = view groups x
+plane split, the sum inside each plane group.
 """
 from __future__ import annotations
 
@@ -71,27 +74,79 @@ def view_ranges(num_views: int, world: int) -> List[Tuple[int, int]]:
     return plane_ranges(num_views, world)
 
 
+def mesh(world: int, rank: int, plane_split: int, num_planes: int, num_views: int = 1, channels: int = 3) -> dict:
+    """Python statement of holo_mesh_layout (group.cu): world = view_groups x
+    plane_split; rank r is plane rank r % plane_split of view group r // plane_split;
+    it renders its plane group's share of the planes and its view group's share of
+    the views, and forms hologram channel c when c % plane_split is its plane rank."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("rank outside [0, world)")
+    if plane_split < 1 or world % plane_split:
+        raise ValueError("plane_split must divide the world size")
+    vg = world // plane_split
+    pr, v = rank % plane_split, rank // plane_split
+    pb, pe = plane_ranges(num_planes, plane_split)[pr]
+    vb, ve = view_ranges(num_views, vg)[v]
+    holo = sum(1 << c for c in range(channels) if c % plane_split == pr)
+    return {"world": world, "rank": rank, "plane_split": plane_split, "view_groups": vg, "plane_rank": pr,
+            "view_group": v, "plane_begin": pb, "plane_end": pe, "view_begin": vb, "view_end": ve,
+            "holo_channels": holo}
+
+
+def plane_groups(world: int, plane_split: int):
+    """Rank lists of the plane groups (the all-reduce groups of the spectrum)."""
+    return [list(range(g * plane_split, (g + 1) * plane_split)) for g in range(world // plane_split)]
+
+
+def torch_plane_group(plane_split: int):
+    """This rank's torch.distributed plane group (every rank creates all of them,
+    as new_group requires); None for plane groups of one."""
+    import torch.distributed as dist
+
+    world, rank = dist.get_world_size(), dist.get_rank()
+    mine = None
+    for ranks in plane_groups(world, plane_split):
+        pg = dist.new_group(ranks)
+        if rank in ranks:
+            mine = pg
+    return mine
+
+
 class ShardedRenderer:
-    """Plane-sharded frame: render_begin -> all_reduce(S) -> render_end.
+    """A frame split over the ranks of a torch.distributed job through the C-ABI
+    group (holo_group_*): planes (plane_split = world), views (plane_split = 1) or
+    planes x views.  transport "nccl" builds the library's own NCCL communicators
+    (unique id broadcast from rank 0); "gloo" sums the spectrum through torch's
+    gloo plane group (every rank may share one GPU -- the tests)."""
 
-    ``ctx`` is a paper_2506_08350_b200.api.Context on this rank's GPU with the scene
-    uploaded; ``group`` a torch.distributed process group (NCCL on GPUs)."""
-
-    def __init__(self, ctx, cfg, rank: int, world: int, group=None, outputs: int = None):
-        import torch
-
-        from . import _lib as L
-
-        self.ctx, self.cfg, self.rank, self.world, self.group = ctx, cfg, rank, world, group
-        self.pb, self.pe = plane_ranges(cfg.num_planes, world)[rank]
-        self.outputs = outputs if outputs is not None else (L.OUT_INTENSITY | (L.OUT_HOLOGRAM if rank == 0 else 0))
-        C, H, W = cfg.channels(), cfg.ny, cfg.nx
-        self.spec = torch.empty((C, H, W, 2), dtype=torch.float32, device=f"cuda:{ctx.device}")
-
-    def frame(self, cam, settings=None, prop=None) -> None:
+    def __init__(self, ctx, cfg, plane_split: int = None, transport: str = "nccl", lanes: int = 1):
         import torch.distributed as dist
 
-        self.ctx.render_begin(cam, self.cfg, settings, prop, self.pb, self.pe, self.spec.data_ptr(), 0)
-        if self.world > 1:
-            dist.all_reduce(self.spec, group=self.group)
-        self.ctx.render_end(self.cfg, prop, self.pb, self.pe, self.spec.data_ptr(), self.outputs)
+        from .api import Group, gloo_allreduce
+
+        self.ctx, self.cfg = ctx, cfg
+        self.world, self.rank = dist.get_world_size(), dist.get_rank()
+        self.plane_split = self.world if plane_split is None else plane_split
+        if transport == "nccl":
+            self.group = Group.from_torch(ctx, self.plane_split)
+        else:
+            pg = torch_plane_group(self.plane_split)
+            self.group = Group(ctx, self.world, self.rank, self.plane_split, allreduce=gloo_allreduce(pg))
+        if lanes > 1:
+            self.group.set_lanes(lanes)
+
+    def upload_scene(self, scene) -> None:
+        self.group.upload_scene(scene)
+
+    def mesh(self, num_views: int = 1):
+        return self.group.mesh(self.cfg.num_planes, num_views, self.cfg.channels())
+
+    def frame(self, cams, settings=None, prop=None, outputs: int = None, flags: int = 0, view_outputs=None):
+        from . import _lib as L
+
+        cams = cams if isinstance(cams, (list, tuple)) else [cams]
+        outs = L.OUT_HOLOGRAM | L.OUT_INTENSITY if outputs is None else outputs
+        return self.group.render(cams, self.cfg, settings, prop, outs, flags, view_outputs)
+
+    def close(self):
+        self.group.close()

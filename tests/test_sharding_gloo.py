@@ -124,3 +124,66 @@ def test_gloo_two_rank_plane_sharding():
     assert sum(out[r][2] for r in range(2)) == 4
     for r in range(2):
         assert out[r][0] < 1e-12 and out[r][1] < 1e-12
+
+
+def test_mesh_layout_library_equals_python_statement():
+    """holo_mesh_layout (group.cu, pure host arithmetic through the C-ABI) against
+    sharding.mesh for every small mesh: plane and view ranges, plane rank, view
+    group and hologram channel owners."""
+    from paper_2506_08350_b200.api import mesh_layout
+    from paper_2506_08350_b200.sharding import mesh
+
+    for world in range(1, 9):
+        for ps in [d for d in range(1, world + 1) if world % d == 0]:
+            for L in (1, 3, 6, 8, 16):
+                for V in (1, 5, 64):
+                    for C in (1, 3):
+                        for r in range(world):
+                            m = mesh_layout(world, r, ps, L, V, C)
+                            want = mesh(world, r, ps, L, V, C)
+                            got = {k: getattr(m, k) for k, _ in m._fields_}
+                            assert got == want, (world, ps, L, V, C, r)
+    with pytest.raises(Exception):
+        mesh_layout(6, 0, 4, 8)  # plane split must divide the world
+
+
+def _mesh_worker(rank, world, ps, port, out):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    from paper_2506_08350_b200.api import mesh_layout
+    from paper_2506_08350_b200.sharding import torch_plane_group
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    pg = torch_plane_group(ps)
+    m = mesh_layout(world, rank, ps, 16, 64, 3)
+    # the plane group sums exactly the ranks sharing this rank's view group, and
+    # their plane ranges tile [0, 16)
+    t = torch.tensor([float(rank), float(m.plane_end - m.plane_begin), float(m.view_group)])
+    dist.all_reduce(t, group=pg)
+    members = list(range(m.view_group * ps, (m.view_group + 1) * ps))
+    out[rank] = (t[0].item() == sum(members), t[1].item() == 16, t[2].item() == m.view_group * ps,
+                 m.view_end - m.view_begin)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,ps", [(2, 2), (2, 1), (4, 2)])
+def test_gloo_mesh_plane_groups(world, ps):
+    """The planes x views mesh of the C-ABI group under torch.distributed (gloo):
+    plane groups from sharding.torch_plane_group agree with holo_mesh_layout."""
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_mesh_worker, args=(r, world, ps, port, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert out[r][:3] == (True, True, True)
+    assert sum(out[r][3] for r in range(0, world, ps)) == 64
