@@ -522,7 +522,7 @@ def gloo_allreduce(group=None):
     def fn(user, buf, count, stream):
         try:
             torch.cuda.ExternalStream(int(stream or 0)).synchronize()
-            dev = torch.as_tensor(L._CudaArray(int(buf), (int(count),), "<f4"), device="cuda")
+            dev = torch.as_tensor(_CudaArray(int(buf), (int(count),), "<f4"), device="cuda")
             host = dev.cpu()
             dist.all_reduce(host, group=group)
             dev.copy_(host)
