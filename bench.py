@@ -90,12 +90,17 @@ def _newest_profile():
     return files[-1] if files else None
 
 
+PROFILED_CONFIG = "C3"  # the configuration the committed forward-frame ncu summaries capture
+_CONFIG = {"name": "C3"}
+
+
 def ncu_metric(stage, metric):
-    """One column of the newest forward-frame ncu summary for the stage's kernel."""
+    """One column of the newest forward-frame ncu summary for the stage's kernel
+    (C3 captures: None for the other configurations)."""
     import csv
 
     path, prefix = _newest_profile(), STAGE_KERNEL.get(stage)
-    if not path or not prefix:
+    if not path or not prefix or _CONFIG["name"] != PROFILED_CONFIG:
         return None
     for row in csv.DictReader(open(path)):
         if row["kernel"].startswith(prefix) and row.get(metric):
@@ -253,6 +258,7 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--plane-split", type=int, default=0, help="ranks per plane group (0: the config's policy)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dropin", action="store_true", help="skip the C++ drop-in API leg (e2e_dropin)")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
     ap.add_argument("--inflight", type=int, default=2, help="frames in flight (contexts / lanes) per GPU")
     ap.add_argument("--e2e-inflight", type=int, default=1, help="frames in flight in the end-to-end run at N=1")
@@ -275,6 +281,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     c = CONFIGS[args.config]
+    _CONFIG["name"] = args.config
     if c.views == 1 and world == 1:
         res = run_single(args, c, local)
     else:
@@ -284,9 +291,41 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(args.config)
         res["cpu_baseline"] = cpu
+        if world == 1 and c.views == 1 and not args.no_dropin:
+            res["e2e_dropin"] = dropin_leg(c)
         print(json.dumps(res), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def dropin_leg(c):
+    """holo::pipeline_forward through the C++ drop-in (libholo.so), timed by
+    paper_2506_08350_b200/lib/dropin_bench with steady_clock as the reference times
+    its own API (holo_main.cpp:507-514): scene in from host memory, the whole
+    PipelineForward (f64 raster layers and lists, hologram, replayed fields,
+    intensities) back in host memory, every call."""
+    exe = os.path.join(ROOT, "paper_2506_08350_b200", "lib", "dropin_bench")
+    if not os.path.exists(exe):
+        return {"unavailable": "dropin_bench not built"}
+    try:
+        import tempfile
+
+        from paper_2506_08350_b200.scenes import synthetic_scene, write_scene
+
+        wave = c.wave()
+        with tempfile.TemporaryDirectory() as d:
+            path = os.path.join(d, "scene.holoscene")
+            write_scene(path, synthetic_scene(c.n, wave, c.seed))
+            cmd = [exe, path, "--nx", str(wave.nx), "--ny", str(wave.ny), "--planes", str(wave.num_planes),
+                   "--wavelengths", ",".join(repr(x) for x in wave.wavelengths), "--frames", "5", "--warmup", "1"]
+            out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+        if out.returncode != 0:
+            return {"unavailable": out.stderr.strip()[-300:]}
+        r = json.loads(out.stdout.strip().splitlines()[-1])
+        r["unit"] = "frames/s"
+        return r
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": repr(e)}
 
 
 def cpu_baseline(cfgname):

@@ -459,6 +459,10 @@ int holo_inverse_propagate(holo_ctx* ctx, const void* hologram, void* replayed, 
                            const holo_prop_options* prop, int dtype);
 /* intensity (field.cpp:5-14): |u|^2 per sample; out is float for F32, double for F64. */
 int holo_intensity(holo_ctx* ctx, const void* field, void* out, size_t samples, int dtype);
+/* f64 intensity of complex64 device samples widened to f64: bitwise the f64 operator
+ * applied to the widened field (the drop-in's pipeline_forward intensities equal
+ * intensity(replayed) of its returned fields, pipeline.cpp:26-27, test_pipeline.cpp:50-53) */
+int holo_intensity_widened(holo_ctx* ctx, const void* field, double* out, size_t samples);
 
 /* Supported FFT lengths: every n whose prime factors are <= 31. */
 int holo_fft_supported(int n);

@@ -677,8 +677,21 @@ PipelineForward pipeline_forward(const GaussianScene& scene, const CameraView& c
         f.replayed.push_back(std::move(r));
     }
     // intensities = intensity(replayed) of the returned fields, literally as
-    // pipeline.cpp:26-27 (f64 squares of the widened fp32 replay)
-    for (int l = 0; l < L; ++l) f.intensities.push_back(intensity(f.replayed[l]));
+    // pipeline.cpp:26-27 (f64 squares of the widened fp32 replay), formed on the
+    // device from the resident replay: no re-upload of the returned fields
+    {
+        void* drep = nullptr;
+        size_t bytes = 0;
+        check(holo_frame_buffer(ctx(), HOLO_BUF_REPLAYED, &drep, &bytes));
+        const size_t total = static_cast<size_t>(L) * n;
+        DevMem dint(sizeof(double) * total);
+        check(holo_intensity_widened(ctx(), drep, static_cast<double*>(dint.p), total));
+        for (int l = 0; l < L; ++l) {
+            IntensityImage im(cfg.nx, cfg.ny, C);
+            d2h(im.data.data(), static_cast<const double*>(dint.p) + static_cast<size_t>(l) * n, sizeof(double) * n);
+            f.intensities.push_back(std::move(im));
+        }
+    }
     return f;
 }
 

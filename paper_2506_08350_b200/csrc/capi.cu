@@ -17,6 +17,17 @@ namespace {
 
 thread_local std::string g_last_error;
 
+// intensity (field.cpp:5-14) of complex64 samples widened to f64: the same
+// uncontracted std::norm as the f64 operator (k_intensity), so it equals the f64
+// intensity of the downloaded, widened field bit for bit
+__global__ void k_intensity_widened(const cx<float>* __restrict__ f, double* __restrict__ out, size_t n) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const double re = f[i].x, im = f[i].y;
+        out[i] = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+    }
+}
+
 template <class F>
 int guarded(F&& f) {
     try {
@@ -1570,6 +1581,16 @@ int holo_inverse_propagate(holo_ctx* ctx, const void* hologram, void* replayed, 
         else
             op_inverse_propagate<double>(ctx, static_cast<const cx<double>*>(hologram),
                                          static_cast<cx<double>*>(replayed), *wave, po);
+    });
+}
+
+int holo_intensity_widened(holo_ctx* ctx, const void* field, double* out, size_t samples) {
+    return guarded([&] {
+        require(ctx && field && out, HOLO_ERR_USAGE, "null argument");
+        if (samples == 0) return;
+        const unsigned blocks = static_cast<unsigned>(std::min<size_t>((samples + 255) / 256, 16 * 148));
+        k_intensity_widened<<<blocks, 256, 0, ctx->stream>>>(static_cast<const cx<float>*>(field), out, samples);
+        HC_LAUNCHED(ctx);
     });
 }
 
