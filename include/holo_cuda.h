@@ -170,6 +170,11 @@ int holo_ctx_stage_times(holo_ctx* ctx, double* ms_out, int* launches_out, int m
 int holo_ctx_reset_timing(holo_ctx* ctx);
 /* Kernel launches issued by this context since creation. */
 uint64_t holo_ctx_launch_count(holo_ctx* ctx);
+/* Guard mode (also HOLO_GUARD=1 at creation; set before the first render): scratch
+ * buffers get their exact size plus a 4 KB guard band; holo_ctx_check_guards
+ * synchronises and reports any band overwritten (HOLO_ERR_NUMERIC, buffer names). */
+int holo_ctx_set_guard(holo_ctx* ctx, int enable);
+int holo_ctx_check_guards(holo_ctx* ctx);
 /* Asynchronous frames.  By default a render makes one host round trip (entry
  * count + scene validation) and returns with its outputs complete, like the
  * reference.  With async enabled a render only enqueues work: the entry buffers

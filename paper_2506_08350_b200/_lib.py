@@ -154,6 +154,8 @@ def lib() -> C.CDLL:
         "holo_ctx_stage_times": (i, [vp, P(d), P(i), i]),
         "holo_ctx_reset_timing": (i, [vp]),
         "holo_ctx_launch_count": (C.c_uint64, [vp]),
+        "holo_ctx_set_guard": (i, [vp, i]),
+        "holo_ctx_check_guards": (i, [vp]),
         "holo_ctx_set_async": (i, [vp, i]),
         "holo_ctx_reserve_entries": (i, [vp, C.c_uint64]),
         "holo_ctx_frame_status": (i, [vp, P(FrameInfo)]),

@@ -185,6 +185,14 @@ class Context:
     def launch_count(self) -> int:
         return int(self.lib.holo_ctx_launch_count(self.h))
 
+    def set_guard(self, on: bool = True) -> None:
+        """Guard bands after every scratch buffer (set before the first render)."""
+        L.check(self.lib.holo_ctx_set_guard(self.h, int(on)))
+
+    def check_guards(self) -> None:
+        """Raise HoloError naming any scratch buffer whose guard band was overwritten."""
+        L.check(self.lib.holo_ctx_check_guards(self.h))
+
     def set_async(self, on: bool = True) -> None:
         """Asynchronous frames: render() only enqueues; frame_status() reports (holo_cuda.h)."""
         L.check(self.lib.holo_ctx_set_async(self.h, int(on)))

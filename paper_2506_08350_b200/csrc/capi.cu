@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -92,19 +93,43 @@ T* buf(holo_ctx* ctx, const char* name, size_t count) {
 
 // ---------------------------------------------------------------- holo_ctx methods
 
+namespace {
+
+// the guard band of b intact? (synchronises the stream)
+bool guard_intact(holo_ctx* ctx, const DevBuf& b) {
+    std::vector<unsigned char> h(kGuardBytes);
+    HC_CUDA(cudaStreamSynchronize(ctx->stream));
+    HC_CUDA(cudaMemcpy(h.data(), static_cast<const unsigned char*>(b.p) + b.guard_at, kGuardBytes,
+                       cudaMemcpyDeviceToHost));
+    for (unsigned char v : h)
+        if (v != kGuardByte) return false;
+    return true;
+}
+
+}  // namespace
+
 void* holo_ctx::buffer(const std::string& name, size_t bytes) {
     DevBuf& b = scratch[name];
     if (b.bytes < bytes) {
         if (b.p) {
             HC_CUDA(cudaStreamSynchronize(stream));
+            if (guard && !guard_intact(this, b))
+                throw Error(HOLO_ERR_NUMERIC, "guard band overwritten past scratch buffer '" + name + "'");
             HC_CUDA(cudaFree(b.p));
             b.p = nullptr;
             b.bytes = 0;
             small_cache.clear();  // a freed address may come back for another buffer
         }
-        const size_t want = bytes + bytes / 8;  // headroom for frame-to-frame growth
-        HC_CUDA(cudaMalloc(&b.p, want));
-        b.bytes = want;
+        if (guard) {  // exact size, then the guard band
+            HC_CUDA(cudaMalloc(&b.p, bytes + kGuardBytes));
+            HC_CUDA(cudaMemsetAsync(static_cast<unsigned char*>(b.p) + bytes, kGuardByte, kGuardBytes, stream));
+            b.bytes = bytes;
+            b.guard_at = bytes;
+        } else {
+            const size_t want = bytes + bytes / 8;  // headroom for frame-to-frame growth
+            HC_CUDA(cudaMalloc(&b.p, want));
+            b.bytes = want;
+        }
     }
     return b.p;
 }
@@ -596,6 +621,7 @@ int holo_ctx_create(int device, holo_ctx** out) {
         auto* ctx = new holo_ctx();
         ctx->device = device;
         HC_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
+        if (const char* gv = std::getenv("HOLO_GUARD")) ctx->guard = gv[0] == '1';
         HC_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
         ctx->stream = ctx->own_stream;
         HC_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->host_status),
@@ -750,6 +776,27 @@ int holo_ctx_reset_timing(holo_ctx* ctx) {
 }
 
 uint64_t holo_ctx_launch_count(holo_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int holo_ctx_set_guard(holo_ctx* ctx, int enable) {
+    return guarded([&] {
+        require(ctx != nullptr, HOLO_ERR_USAGE, "null context");
+        require(ctx->scratch.empty() || (enable != 0) == ctx->guard, HOLO_ERR_USAGE,
+                "holo_ctx_set_guard: set guard mode before the first render");
+        ctx->guard = enable != 0;
+    });
+}
+
+int holo_ctx_check_guards(holo_ctx* ctx) {
+    return guarded([&] {
+        require(ctx != nullptr, HOLO_ERR_USAGE, "null context");
+        require(ctx->guard, HOLO_ERR_USAGE, "holo_ctx_check_guards: guard mode is off");
+        HC_CUDA(cudaSetDevice(ctx->device));
+        std::string bad;
+        for (const auto& kv : ctx->scratch)
+            if (kv.second.p && !guard_intact(ctx, kv.second)) bad += (bad.empty() ? "" : ", ") + kv.first;
+        if (!bad.empty()) throw Error(HOLO_ERR_NUMERIC, "guard band overwritten past scratch buffer(s): " + bad);
+    });
+}
 
 static int scene_upload(holo_ctx* ctx, const holo_scene_arrays* s, cudaMemcpyKind kind) {
     return guarded([&] {

@@ -18,7 +18,16 @@ namespace holo_cuda {
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    size_t guard_at = 0;  // guard mode: offset of the guard band (the requested size)
 };
+
+// Guard mode (HOLO_GUARD=1 at context creation, or holo_ctx_set_guard): every
+// scratch buffer is allocated at its exact requested size followed by a band of
+// kGuardBytes set to kGuardByte; holo_ctx_check_guards (and every reallocation)
+// verifies the bands -- an out-of-bounds write past any buffer is reported by
+// name.  The substitute for compute-sanitizer memcheck, which this pool disables.
+constexpr size_t kGuardBytes = 4096;
+constexpr unsigned char kGuardByte = 0xA5;
 
 // Per-(plane, channel) transfer-function constants, see tf_value() in kernels.cuh.
 struct TfChan {
@@ -49,6 +58,7 @@ struct holo_ctx {
     int stage_calls[holo_cuda::kNumStages] = {};
 
     std::map<std::string, holo_cuda::DevBuf> scratch;
+    bool guard = false;
     std::map<std::pair<int, int>, void*> twiddles;      // (n, sizeof(T)) -> exp(-2 pi i q/n)
     std::map<std::pair<int, uint64_t>, double*> freqs;  // (n, pitch bits) -> freq_at(i, n, pitch)
     void* host_pinned = nullptr;
