@@ -2,6 +2,7 @@
 // members -- gradients, init, densification -- are out of scope for this build).
 #pragma once
 
+#include <Eigen/Dense>
 #include <vector>
 
 #include "holo/camera.hpp"
@@ -37,11 +38,11 @@ struct SceneGradients {
     void clear();
 };
 
-// Sigma = R diag(e^s)^2 R^T for the normalised quaternion
-Mat3 covariance_3d(const double* quat, const double* log_scales);
+// Sigma = R diag(e^s)^2 R^T for the normalised quaternion (scene.hpp:49)
+Eigen::Matrix3d covariance_3d(const double* quat, const double* log_scales);
 
 namespace detail {
-Mat3 quat_to_rot(const double* q);
+Eigen::Matrix3d quat_to_rot(const double* q);  // scene.hpp:53
 }
 
 // argmax plane (ties -> lowest index); backward weights softmax(logits / tau)

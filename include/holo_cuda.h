@@ -205,6 +205,15 @@ int holo_scene_upload_device(holo_ctx* ctx, const holo_scene_arrays* dev);
 int holo_render(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave, const holo_raster_settings* settings,
                 const holo_prop_options* prop, unsigned outputs, holo_frame_info* info);
 
+/* brute_force_forward (rasterizer.hpp:85-86, rasterizer.cpp:265-315): the same
+ * per-pixel math as holo_render's tiled raster with no tiles, no support-radius
+ * culling and no early termination (every valid Gaussian of a plane, global
+ * (depth, index) order, at every pixel) -- the reference's equivalence oracle.
+ * Writes HOLO_BUF_LAYERS (the frame's other buffers are those of a raster-only
+ * holo_render with HOLO_OUT_PROJECTED). */
+int holo_brute_force_forward(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave,
+                             const holo_raster_settings* settings);
+
 /* Plane-sharded halves of holo_render (one process per GPU).  begin: rasterise
  * planes [plane_begin, plane_end) and write their partial spectrum
  * S_g = sum_{l in g} H_{Z_l} FFT2(U_l) (float2 [C][H][W]) to spectrum_out

@@ -165,6 +165,7 @@ def lib() -> C.CDLL:
         "holo_render_begin": (i, [vp, P(Camera), P(Wave), P(RasterSettings), P(PropOptions), i, i, vp, u,
                                   P(FrameInfo)]),
         "holo_render_end": (i, [vp, P(Wave), P(PropOptions), i, i, vp, u]),
+        "holo_brute_force_forward": (i, [vp, P(Camera), P(Wave), P(RasterSettings)]),
         "holo_frame_buffer": (i, [vp, i, P(vp), P(sz)]),
         "holo_frame_download": (i, [vp, i, vp, sz]),
         "holo_frame_download_async": (i, [vp, i, vp, sz]),

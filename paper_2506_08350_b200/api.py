@@ -718,6 +718,20 @@ def raster_forward(scene: GaussianScene, cam: CameraView, cfg: WaveConfig,
     return _collect_raster(ctx, scene, cfg3, C_, info)
 
 
+def brute_force_forward(scene: GaussianScene, cam: CameraView, cfg: WaveConfig,
+                        settings: Optional[RenderSettings] = None, ctx: Optional[Context] = None) -> List[np.ndarray]:
+    """holo::brute_force_forward (rasterizer.cpp:265-315) on the GPU: every valid
+    Gaussian of a plane at every pixel in the global (depth, index) order, no
+    tiles, no radius culling, no early termination.  Layers [C, H, W] per plane."""
+    _check_shapes(scene, cam, cfg)
+    ctx = ctx or default_context()
+    ctx.upload_scene(scene)
+    L.check(ctx.lib.holo_brute_force_forward(ctx.h, C.byref(_camera(cam)), C.byref(_wave(cfg)),
+                                             C.byref(_settings(settings))))
+    lay = ctx.download(L.BUF_LAYERS, np.complex64, (cfg.num_planes, cfg.channels(), cfg.ny, cfg.nx))
+    return [lay[l].astype(np.complex128) for l in range(cfg.num_planes)]
+
+
 def pipeline_forward(scene: GaussianScene, cam: CameraView, cfg: WaveConfig,
                      opt: Optional[PipelineOptions] = None, ctx: Optional[Context] = None,
                      raster: bool = True, replayed: bool = True) -> PipelineForward:

@@ -349,41 +349,21 @@ ComplexField point_source_field(const WaveConfig& cfg, const std::vector<PointSo
 
 // ------------------------------------------------------------------ camera (camera.cpp)
 
-Mat3 Mat3::transpose() const {
-    Mat3 t;
-    for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c) t(c, r) = (*this)(r, c);
-    return t;
-}
-
-Mat3 Mat3::operator*(const Mat3& o) const {
-    Mat3 t;
-    for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c) t(r, c) = ((*this)(r, 0) * o(0, c) + (*this)(r, 1) * o(1, c)) + (*this)(r, 2) * o(2, c);
-    return t;
-}
-
-Vec3 Mat3::operator*(const Vec3& x) const {
-    Vec3 y;
-    for (int r = 0; r < 3; ++r) y[r] = ((*this)(r, 0) * x[0] + (*this)(r, 1) * x[1]) + (*this)(r, 2) * x[2];
-    return y;
-}
-
-Mat3 CameraView::rot_cam_to_world() const {
+Eigen::Matrix3d CameraView::rot_cam_to_world() const {
     const double ca = std::cos(pose[3]), sa = std::sin(pose[3]);
     const double cb = std::cos(pose[4]), sb = std::sin(pose[4]);
     const double cg = std::cos(pose[5]), sg = std::sin(pose[5]);
-    Mat3 rx, ry, rz;
-    rx.m[0] = 1; rx.m[4] = ca; rx.m[5] = -sa; rx.m[7] = sa; rx.m[8] = ca;
-    ry.m[0] = cb; ry.m[2] = sb; ry.m[4] = 1; ry.m[6] = -sb; ry.m[8] = cb;
-    rz.m[0] = cg; rz.m[1] = -sg; rz.m[3] = sg; rz.m[4] = cg; rz.m[8] = 1;
-    return (rz * ry) * rx;
+    Eigen::Matrix3d rx, ry, rz;
+    rx << 1, 0, 0, 0, ca, -sa, 0, sa, ca;
+    ry << cb, 0, sb, 0, 1, 0, -sb, 0, cb;
+    rz << cg, -sg, 0, sg, cg, 0, 0, 0, 1;
+    return rz * ry * rx;
 }
 
-Mat3 CameraView::rot_world_to_cam() const { return rot_cam_to_world().transpose(); }
+Eigen::Matrix3d CameraView::rot_world_to_cam() const { return rot_cam_to_world().transpose(); }
 
-Vec3 CameraView::world_to_camera(const Vec3& p) const {
-    return rot_world_to_cam() * Vec3(p[0] - pose[0], p[1] - pose[1], p[2] - pose[2]);
+Eigen::Vector3d CameraView::world_to_camera(const Eigen::Vector3d& p) const {
+    return rot_world_to_cam() * (p - position());
 }
 
 void CameraView::validate() const {
@@ -435,20 +415,20 @@ void GaussianScene::renormalize() {
 }
 
 namespace detail {
-Mat3 quat_to_rot(const double* q) {
+Eigen::Matrix3d quat_to_rot(const double* q) {
     const double n = quat_norm(q);
     const double w = q[0] / n, x = q[1] / n, y = q[2] / n, z = q[3] / n;
-    Mat3 r;
-    r.m[0] = 1 - 2 * (y * y + z * z); r.m[1] = 2 * (x * y - w * z);     r.m[2] = 2 * (x * z + w * y);
-    r.m[3] = 2 * (x * y + w * z);     r.m[4] = 1 - 2 * (x * x + z * z); r.m[5] = 2 * (y * z - w * x);
-    r.m[6] = 2 * (x * z - w * y);     r.m[7] = 2 * (y * z + w * x);     r.m[8] = 1 - 2 * (x * x + y * y);
+    Eigen::Matrix3d r;
+    r << 1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+         2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+         2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y);
     return r;
 }
 }  // namespace detail
 
-Mat3 covariance_3d(const double* quat, const double* log_scales) {
-    const Mat3 R = detail::quat_to_rot(quat);
-    Mat3 M = R;
+Eigen::Matrix3d covariance_3d(const double* quat, const double* log_scales) {
+    const Eigen::Matrix3d R = detail::quat_to_rot(quat);
+    Eigen::Matrix3d M = R;
     for (int k = 0; k < 3; ++k) {
         const double e = std::exp(log_scales[k]);
         for (int r = 0; r < 3; ++r) M(r, k) = R(r, k) * e;
@@ -500,13 +480,33 @@ std::vector<T> download_buf(int which) {
     return h;
 }
 
-RasterForward collect_raster(const GaussianScene& scene, const WaveConfig& cfg, int C, const holo_frame_info& info) {
-    RasterForward r;
+detail::Projected to_projected(const holo_projected& q) {
+    detail::Projected p;
+    p.valid = q.valid != 0;
+    p.n = q.n;
+    p.mu_x = q.mu_x;
+    p.mu_y = q.mu_y;
+    p.inv00 = q.inv00;
+    p.inv01 = q.inv01;
+    p.inv11 = q.inv11;
+    p.radius = q.radius;
+    p.xc = q.xc;
+    p.yc = q.yc;
+    p.zc = q.zc;
+    p.alpha_sig = q.alpha_sig;
+    for (int c = 0; c < 3; ++c) {
+        p.amp[c] = q.amp[c];
+        p.phase[c] = q.phase[c];
+    }
+    p.plane = q.plane;
+    return p;
+}
+
+std::vector<ComplexField> download_layers(const WaveConfig& cfg, int C) {
     const int L = cfg.num_planes, W = cfg.nx, H = cfg.ny;
-    const size_t P = static_cast<size_t>(W) * H, N = scene.size();
-    r.tiles_x = info.tiles_x;
-    r.tiles_y = info.tiles_y;
+    const size_t P = static_cast<size_t>(W) * H;
     const std::vector<std::complex<float>> lay = download_buf<std::complex<float>>(HOLO_BUF_LAYERS);
+    std::vector<ComplexField> out;
     for (int l = 0; l < L; ++l) {
         ComplexField f(W, H, GaussianScene::kChannels, cfg.pitch);
         for (int c = 0; c < C; ++c)
@@ -514,35 +514,25 @@ RasterForward collect_raster(const GaussianScene& scene, const WaveConfig& cfg, 
                 const std::complex<float> v = lay[(static_cast<size_t>(l) * C + c) * P + i];
                 f.data[static_cast<size_t>(c) * P + i] = c64(v.real(), v.imag());
             }
-        r.layers.push_back(std::move(f));
+        out.push_back(std::move(f));
     }
+    return out;
+}
+
+RasterForward collect_raster(const GaussianScene& scene, const WaveConfig& cfg, int C, const holo_frame_info& info) {
+    RasterForward r;
+    const int L = cfg.num_planes, W = cfg.nx, H = cfg.ny;
+    const size_t P = static_cast<size_t>(W) * H, N = scene.size();
+    r.tiles_x = info.tiles_x;
+    r.tiles_y = info.tiles_y;
+    r.layers = download_layers(cfg, C);
     const std::vector<float> tf = download_buf<float>(HOLO_BUF_T_FINAL);
     r.t_final.assign(tf.begin(), tf.begin() + static_cast<long>(L * P));
     r.n_contrib = download_buf<std::int32_t>(HOLO_BUF_N_CONTRIB);
     r.n_contrib.resize(L * P);
     const std::vector<holo_projected> proj = download_buf<holo_projected>(HOLO_BUF_PROJECTED);
     r.projected.resize(N);
-    for (size_t i = 0; i < N; ++i) {
-        const holo_projected& q = proj[i];
-        detail::Projected& p = r.projected[i];
-        p.valid = q.valid != 0;
-        p.n = q.n;
-        p.mu_x = q.mu_x;
-        p.mu_y = q.mu_y;
-        p.inv00 = q.inv00;
-        p.inv01 = q.inv01;
-        p.inv11 = q.inv11;
-        p.radius = q.radius;
-        p.xc = q.xc;
-        p.yc = q.yc;
-        p.zc = q.zc;
-        p.alpha_sig = q.alpha_sig;
-        for (int c = 0; c < 3; ++c) {
-            p.amp[c] = q.amp[c];
-            p.phase[c] = q.phase[c];
-        }
-        p.plane = q.plane;
-    }
+    for (size_t i = 0; i < N; ++i) r.projected[i] = to_projected(proj[i]);
     r.rho = download_buf<double>(HOLO_BUF_RHO);
     r.rho.resize(N * L);
     r.touched = download_buf<std::uint8_t>(HOLO_BUF_TOUCHED);
@@ -580,6 +570,66 @@ RasterForward raster_forward(const GaussianScene& scene, const CameraView& cam, 
     check(holo_render(ctx(), &c, &w, &st, &po, kRasterOutputs, &info));
     return collect_raster(scene, cfg, GaussianScene::kChannels, info);
 }
+
+// rasterizer.cpp:265-315 on the GPU (holo_brute_force_forward): same per-pixel math,
+// global depth order, no tiles, no radius culling, no early termination
+std::vector<ComplexField> brute_force_forward(const GaussianScene& scene, const CameraView& cam, const WaveConfig& cfg,
+                                              const RenderSettings& settings) {
+    check_raster_inputs(scene, cam, cfg);
+    const holo_scene_arrays sa = scene_arrays(scene);
+    check(holo_scene_upload(ctx(), &sa));
+    holo_wave w = to_c(cfg);
+    w.channels = GaussianScene::kChannels;
+    for (int c = cfg.channels(); c < w.channels; ++c) w.wavelengths[c] = cfg.wavelengths.back();
+    const holo_camera c = to_c(cam);
+    const holo_raster_settings st = to_c(settings);
+    check(holo_brute_force_forward(ctx(), &c, &w, &st));
+    return download_layers(cfg, GaussianScene::kChannels);
+}
+
+namespace detail {
+// rasterizer.cpp:10-70 for Gaussian n: the device projection of a one-Gaussian
+// frame (f64, the same kernel as raster_forward's).  The device forms the
+// rotation from the camera, so world_to_cam must be cam.rot_world_to_cam().
+Projected project_gaussian(const GaussianScene& scene, size_t n, const CameraView& cam,
+                           const Eigen::Matrix3d& world_to_cam, const WaveConfig& cfg, const RenderSettings& settings) {
+    if (n >= scene.size()) throw HoloError("usage", "project_gaussian: index out of range");
+    const Eigen::Matrix3d r = cam.rot_world_to_cam();
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            if (r(i, j) != world_to_cam(i, j))
+                throw HoloError("usage", "project_gaussian: world_to_cam must be cam.rot_world_to_cam()");
+    GaussianScene one;
+    one.num_planes = scene.num_planes;
+    one.resize(1);
+    auto take = [n](const std::vector<double>& from, std::vector<double>& to, size_t k) {
+        std::copy(from.begin() + static_cast<long>(n * k), from.begin() + static_cast<long>((n + 1) * k), to.begin());
+    };
+    take(scene.positions, one.positions, 3);
+    take(scene.rotations, one.rotations, 4);
+    take(scene.log_scales, one.log_scales, 3);
+    take(scene.amplitudes, one.amplitudes, 3);
+    take(scene.opacity_logits, one.opacity_logits, 1);
+    take(scene.phases, one.phases, 3);
+    take(scene.plane_logits, one.plane_logits, static_cast<size_t>(scene.num_planes));
+    CameraView c = cam;
+    c.width = cfg.nx;
+    c.height = cfg.ny;
+    const holo_scene_arrays sa = scene_arrays(one);
+    check(holo_scene_upload(ctx(), &sa));
+    holo_wave w = to_c(cfg);
+    w.channels = GaussianScene::kChannels;
+    for (int k = cfg.channels(); k < w.channels; ++k) w.wavelengths[k] = cfg.wavelengths.back();
+    const holo_camera hc = to_c(c);
+    const holo_raster_settings st = to_c(settings);
+    const holo_prop_options po{0, 0};
+    holo_frame_info info{};
+    check(holo_render(ctx(), &hc, &w, &st, &po, HOLO_OUT_PROJECTED, &info));
+    Projected p = to_projected(download_buf<holo_projected>(HOLO_BUF_PROJECTED).at(0));
+    p.n = static_cast<int>(n);
+    return p;
+}
+}  // namespace detail
 
 void SceneGradients::resize_like(const GaussianScene& s) {
     const size_t n = s.size();

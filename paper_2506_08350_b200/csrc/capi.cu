@@ -1452,6 +1452,46 @@ int holo_pipeline_backward(holo_ctx* ctx, const holo_camera* cam, const holo_wav
     });
 }
 
+int holo_brute_force_forward(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave,
+                             const holo_raster_settings* settings) {
+    return guarded([&] {
+        require(ctx && cam && wave && settings, HOLO_ERR_USAGE, "null argument");
+        HC_CUDA(cudaSetDevice(ctx->device));
+        const holo_prop_options po{0, 0};
+        // the tiled raster supplies the projections, records and plane weights
+        render_full(ctx, *cam, *wave, *settings, po, HOLO_OUT_LAYERS | HOLO_OUT_PROJECTED, nullptr);
+        const size_t N = ctx->n;
+        const int L = wave->num_planes, C = wave->channels;
+        std::vector<holo_projected> proj(N);
+        if (N) {
+            HC_CUDA(cudaMemcpyAsync(proj.data(), ctx->buffer("projected", 1), sizeof(holo_projected) * N,
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+            HC_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
+        // global front-to-back order over every valid Gaussian (rasterizer.cpp:280-288)
+        std::vector<int> order;
+        for (size_t i = 0; i < N; ++i)
+            if (proj[i].valid) order.push_back(static_cast<int>(i));
+        std::sort(order.begin(), order.end(), [&](int a, int b) {
+            if (proj[a].zc != proj[b].zc) return proj[a].zc < proj[b].zc;
+            return a < b;
+        });
+        int* d_order = buf<int>(ctx, "brute_order", order.size() + 1);
+        if (!order.empty())
+            HC_CUDA(cudaMemcpyAsync(d_order, order.data(), sizeof(int) * order.size(), cudaMemcpyHostToDevice,
+                                    ctx->stream));
+        const size_t P = static_cast<size_t>(wave->nx) * wave->ny;
+        cx<float>* layers = buf<cx<float>>(ctx, "layers", static_cast<size_t>(L) * C * P);
+        brute_force(ctx, static_cast<const GRec*>(ctx->buffer("rec", 1)), d_order, static_cast<int>(order.size()),
+                    static_cast<const int*>(ctx->buffer("plane", 1)),
+                    settings->soft_assignment ? static_cast<const double*>(ctx->buffer("rho", 1)) : nullptr, L, C,
+                    wave->nx, wave->ny, settings->tile, settings->soft_assignment != 0, 1.0 > settings->plane_eps,
+                    static_cast<float>(settings->alpha_floor), settings->alpha_floor > 0.0,
+                    static_cast<float>(settings->alpha_clamp), layers);
+        HC_CUDA(cudaStreamSynchronize(ctx->stream));  // order lives on the host stack
+    });
+}
+
 int holo_render_begin(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave,
                       const holo_raster_settings* settings, const holo_prop_options* prop, int plane_begin,
                       int plane_end, void* spectrum_out, unsigned outputs, holo_frame_info* info) {

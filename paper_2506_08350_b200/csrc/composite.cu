@@ -189,21 +189,6 @@ __global__ void __launch_bounds__(256) k_sort_small(const unsigned* __restrict__
 __device__ unsigned long long g_counts[4];
 #endif
 
-// acc_c += w * (amp_c cos phi_c, amp_c sin phi_c): one FFMA2 per channel
-__device__ __forceinline__ cx<float> axpy(float w, float re, float im, cx<float> acc) {
-    return f32x2::unpack(f32x2::fma(f32x2::pack(w, w), f32x2::pack(re, im), f32x2::pack(acc.x, acc.y)));
-}
-
-template <int C>
-__device__ __forceinline__ void blend(const Staged* e, const float4& B, float w, cx<float> (&acc)[C]) {
-    acc[0] = axpy(w, B.z, B.w, acc[0]);
-    if constexpr (C > 1) {
-        const float4 Cc = e->c;
-        acc[1 % C] = axpy(w, Cc.x, Cc.y, acc[1 % C]);
-        if constexpr (C > 2) acc[2 % C] = axpy(w, Cc.z, Cc.w, acc[2 % C]);
-    }
-}
-
 // 16x16 tiles: 7 CTAs (56 warps) per SM, 36 registers -- measured faster than 6 (40 registers,
 // -1.3 %), 5 (48 registers) and 8 (32 registers, spills)
 #ifndef HOLO_COMP_TEST

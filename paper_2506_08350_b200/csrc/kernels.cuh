@@ -182,6 +182,11 @@ struct CompositeArgs {
 };
 void composite(holo_ctx* ctx, const CompositeArgs& a, int tile);
 
+// ---- brute.cu: brute_force_forward (rasterizer.cpp:265-315), layers [L][C][H][W]
+void brute_force(holo_ctx* ctx, const GRec* rec, const int* order, int n_order, const int* plane_of,
+                 const double* rho, int L, int C, int W, int H, int tile, bool soft, bool gate_open,
+                 float alpha_floor, bool floor_positive, float clamp, cx<float>* layers);
+
 // ---- backward.cu
 struct alignas(16) BwdRec {  // per Gaussian: cos / sin of the phases, amplitudes, sigmoid(opacity)
     float cs[6];

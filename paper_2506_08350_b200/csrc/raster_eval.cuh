@@ -49,6 +49,22 @@ __device__ __forceinline__ float eval_alpha(const Staged* e, float fx, float fy,
     return fminf(ex2_approx(q), clamp);
 }
 
+// acc_c += w * (amp_c cos phi_c, amp_c sin phi_c): one FFMA2 per channel
+__device__ __forceinline__ cx<float> axpy(float w, float re, float im, cx<float> acc) {
+    return f32x2::unpack(f32x2::fma(f32x2::pack(w, w), f32x2::pack(re, im), f32x2::pack(acc.x, acc.y)));
+}
+
+// acc[c] += w * amp_c e^{i phi_c}
+template <int C>
+__device__ __forceinline__ void blend(const Staged* e, const float4& B, float w, cx<float> (&acc)[C]) {
+    acc[0] = axpy(w, B.z, B.w, acc[0]);
+    if constexpr (C > 1) {
+        const float4 Cc = e->c;
+        acc[1 % C] = axpy(w, Cc.x, Cc.y, acc[1 % C]);
+        if constexpr (C > 2) acc[2 % C] = axpy(w, Cc.z, Cc.w, acc[2 % C]);
+    }
+}
+
 // does the accept box meet the warp's block of pixel centres [bxlo, bxhi] x [bylo, byhi]?
 __device__ __forceinline__ bool box_hits(const float4& bb, float bxlo, float bxhi, float bylo, float byhi) {
     return !(bb.y < bxlo || bb.x > bxhi || bb.w < bylo || bb.z > byhi);

@@ -5,7 +5,8 @@ by paper_2506_08350_b200/cpp/Makefile where /root/reference exists -- the
 reference's OWN unit tests test_field.cpp, test_propagation.cpp,
 test_losses.cpp, test_optimizer.cpp and test_phase_only.cpp, unmodified, at the
 reference's tolerances (f64 operators, losses, optimizer and phase-only
-conversion on the GPU).
+conversion on the GPU), and test_pipeline.cpp / test_rasterizer.cpp with the
+cases an fp32 render cannot meet allow-listed below, each with its reason.
 CPU: libholo.so exports the reference API symbols."""
 import os
 import subprocess
@@ -26,7 +27,7 @@ def test_libholo_exports_reference_api():
                  "holo::intensity(", "holo::plane_positions(", "holo::read_field(", "holo::write_field(",
                  "holo::total_loss(", "holo::loss_recon(", "holo::loss_ssim(", "holo::ssim_mean(", "holo::psnr(",
                  "holo::optimizer_step(", "holo::convert_phase_only(", "holo::phase_only_loss(",
-                 "holo::make_target_from_scene("):
+                 "holo::make_target_from_scene(", "holo::brute_force_forward(", "holo::detail::project_gaussian("):
         assert name in syms, name
 
 
@@ -38,20 +39,22 @@ def test_libholo_exports_reference_api():
 EXPECTED_FAILURES = {
     "ref_test_pipeline": {"end-to-end gradients match finite differences",
                           "soft assignment exposes plane logit gradients to finite differences"},
+    "ref_test_rasterizer": set(),
 }
 
 
 @pytest.mark.gpu
-def test_reference_pipeline_suite(tmp_path):
-    path = os.path.join(LIB, "ref_test_pipeline")
+@pytest.mark.parametrize("binary,cases", [("ref_test_pipeline", 11), ("ref_test_rasterizer", 11)])
+def test_reference_suite_with_fp32_allowlist(binary, cases, tmp_path):
+    path = os.path.join(LIB, binary)
     if not os.path.exists(path):
-        pytest.skip("ref_test_pipeline not built (needs /root/reference at build time)")
+        pytest.skip(f"{binary} not built (needs /root/reference at build time)")
     r = subprocess.run([path], capture_output=True, text=True, cwd=tmp_path, timeout=900)
     failed = {line.split("test case FAILED:", 1)[1].strip() for line in r.stdout.splitlines()
               if "test case FAILED:" in line}
-    print(r.stdout[-3000:])
-    assert failed <= EXPECTED_FAILURES["ref_test_pipeline"], failed
-    assert "test cases: 11" in r.stdout
+    print(r.stdout[-6000:])
+    assert failed <= EXPECTED_FAILURES[binary], failed
+    assert f"test cases: {cases}" in r.stdout
 
 
 @pytest.mark.gpu

@@ -134,6 +134,35 @@ def test_large_buckets_sorted_globally(gpu_ctx, oracle):
     assert int(np.diff(r.raster.bucket_start.astype(np.int64)).max()) > 1024
 
 
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
+def test_tiled_equals_brute_force_bitwise_without_termination(gpu_ctx, oracle, seed):
+    """test_rasterizer.cpp:244-255 on the GPU: with term_eps = 0 the tiled raster
+    (bucket lists, accept-box culling) equals the untiled brute force bit for bit;
+    the brute force itself matches the reference's (rasterizer.cpp:265-315)."""
+    cfg = desk_config(48, 2)
+    cam = front_camera(cfg)
+    st = RenderSettings(term_eps=0.0)
+    s = random_scene(30, cfg, seed)
+    tiled = api.raster_forward(s, cam, cfg, st, ctx=gpu_ctx).layers
+    brute = api.brute_force_forward(s, cam, cfg, st, ctx=gpu_ctx)
+    for l in range(cfg.num_planes):
+        assert np.array_equal(np.asarray(tiled[l]), brute[l])
+    ref = oracle.brute_force_forward(s, cam, cfg, st)
+    assert rel_l2(np.stack(brute), ref[:, :cfg.channels()]) <= 1e-5
+
+
+def test_brute_force_soft_assignment_and_dense_overlap(gpu_ctx, oracle):
+    cfg = WaveConfig(nx=64, ny=48, wavelengths=RGB, num_planes=3)
+    for st, s in ((RenderSettings(term_eps=0.0, soft_assignment=True, soft_tau=1.0), synthetic_scene(300, cfg, 33)),
+                  (RenderSettings(term_eps=0.0), overlapping_scene(200, cfg, 34))):
+        cam = wide_camera(cfg) if st.soft_assignment else front_camera(cfg)
+        tiled = api.raster_forward(s, cam, cfg, st, ctx=gpu_ctx).layers
+        brute = api.brute_force_forward(s, cam, cfg, st, ctx=gpu_ctx)
+        assert np.array_equal(np.stack(tiled), np.stack(brute))
+        ref = oracle.brute_force_forward(s, cam, cfg, st)
+        assert rel_l2(np.stack(brute), ref[:, :cfg.channels()]) <= 1e-5
+
+
 def test_render_is_deterministic(gpu_ctx):
     cfg = WaveConfig(nx=256, ny=192, wavelengths=RGB, num_planes=4)
     s = synthetic_scene(30000, cfg, 27)
