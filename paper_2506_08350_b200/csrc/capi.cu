@@ -18,6 +18,15 @@ namespace {
 
 thread_local std::string g_last_error;
 
+// The largest float not above x: the fp32 alpha clamp never exceeds the
+// reference's f64 one (a = min(alpha g, alpha_clamp) <= alpha_clamp and
+// T = 1 - a >= 1 - alpha_clamp hold as in test_rasterizer.cpp:327-344).
+float float_not_above(double x) {
+    float f = static_cast<float>(x);
+    if (static_cast<double>(f) > x) f = std::nextafter(f, -INFINITY);
+    return f;
+}
+
 // intensity (field.cpp:5-14) of complex64 samples widened to f64: the same
 // uncontracted std::norm as the f64 operator (k_intensity), so it equals the f64
 // intensity of the downloaded, widened field bit for bit
@@ -453,7 +462,7 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     ca.capacity = capacity;
     ca.term_eps = static_cast<float>(st.term_eps);
     ca.alpha_floor = static_cast<float>(st.alpha_floor);
-    ca.alpha_clamp = static_cast<float>(st.alpha_clamp);
+    ca.alpha_clamp = float_not_above(st.alpha_clamp);
     ca.floor_positive = st.alpha_floor > 0.0 ? 1 : 0;
     ca.layers = buf<cx<float>>(ctx, "layers", static_cast<size_t>(nplanes) * g.C * g.P);
     ca.t_final = want_aux ? buf<float>(ctx, "t_final", static_cast<size_t>(nplanes) * g.P) : nullptr;
@@ -1073,7 +1082,7 @@ void raster_backward(holo_ctx* ctx, const holo_wave& wave, const holo_raster_set
     ra.soft = st.soft_assignment;
     ra.capacity = capacity;
     ra.alpha_floor = static_cast<float>(st.alpha_floor);
-    ra.alpha_clamp = static_cast<float>(st.alpha_clamp);
+    ra.alpha_clamp = float_not_above(st.alpha_clamp);
     ra.floor_positive = st.alpha_floor > 0.0 ? 1 : 0;
     ra.grad_layers = grad_layers;
     ra.t_final = static_cast<const float*>(ctx->buffer("t_final", 1));
@@ -1487,7 +1496,7 @@ int holo_brute_force_forward(holo_ctx* ctx, const holo_camera* cam, const holo_w
                     settings->soft_assignment ? static_cast<const double*>(ctx->buffer("rho", 1)) : nullptr, L, C,
                     wave->nx, wave->ny, settings->tile, settings->soft_assignment != 0, 1.0 > settings->plane_eps,
                     static_cast<float>(settings->alpha_floor), settings->alpha_floor > 0.0,
-                    static_cast<float>(settings->alpha_clamp), layers);
+                    float_not_above(settings->alpha_clamp), layers);
         HC_CUDA(cudaStreamSynchronize(ctx->stream));  // order lives on the host stack
     });
 }
