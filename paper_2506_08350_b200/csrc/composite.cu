@@ -189,6 +189,65 @@ __global__ void __launch_bounds__(256) k_sort_small(const unsigned* __restrict__
 __device__ unsigned long long g_counts[4];
 #endif
 
+// Buckets of kWarpSortCap + 1 .. kSortCap entries: sorted by the compositing CTA in
+// shared memory on (zc, gidx) (rank sort up to 256 entries, bitonic above) into
+// s_ord; the sorted gidx are written back so the lists stay in reference order
+// for the frame's other consumers (HOLO_BUF_ENTRY_*, the backward pass).
+template <int NT>
+__device__ __forceinline__ void sort_bucket_cta(const CompositeArgs& a, unsigned e0, int n, int tid,
+                                                unsigned long long* key, int* gid, int* s_ord) {
+    for (int t = tid; t < n; t += NT) {
+        const int g = a.egidx[e0 + t];
+        key[t] = a.zkey[g];
+        gid[t] = g;
+    }
+    __syncthreads();
+    if (n <= 256) {
+        for (int t = tid; t < n; t += NT) {
+            const unsigned long long k = key[t];
+            const int g = gid[t];
+            int rank = 0;
+            for (int j = 0; j < n; ++j) {
+                const unsigned long long kj = key[j];
+                rank += (kj < k || (kj == k && gid[j] < g)) ? 1 : 0;
+            }
+            s_ord[rank] = g;
+        }
+    } else {
+        int P = 1;
+        while (P < n) P <<= 1;
+        for (int t = n + tid; t < P; t += NT) {
+            key[t] = ~0ull;
+            gid[t] = 0x7fffffff;
+        }
+        __syncthreads();
+        for (int k = 2; k <= P; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int t = tid; t < P; t += NT) {
+                    const int u = t ^ j;
+                    if (u > t) {
+                        const bool up = (t & k) == 0;
+                        const unsigned long long ka = key[t], kb = key[u];
+                        const int ga = gid[t], gb = gid[u];
+                        const bool b_less = kb < ka || (kb == ka && gb < ga);
+                        const bool a_less = ka < kb || (ka == kb && ga < gb);
+                        if (up ? b_less : a_less) {
+                            key[t] = kb;
+                            key[u] = ka;
+                            gid[t] = gb;
+                            gid[u] = ga;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (int t = tid; t < n; t += NT) s_ord[t] = gid[t];
+    }
+    __syncthreads();
+    for (int t = tid; t < n; t += NT) a.egidx[e0 + t] = s_ord[t];
+}
+
 // 16x16 tiles: 7 CTAs (56 warps) per SM, 36 registers -- measured faster than 6 (40 registers,
 // -1.3 %), 5 (48 registers) and 8 (32 registers, spills)
 #ifndef HOLO_COMP_TEST
@@ -196,6 +255,13 @@ __device__ unsigned long long g_counts[4];
 #endif
 #ifndef HOLO_COMP_MINB
 #define HOLO_COMP_MINB 7
+#endif
+// k_composite2 (two pixels per thread) for 16x16 tiles; HOLO_COMP2=0 selects k_composite
+#ifndef HOLO_COMP2
+#define HOLO_COMP2 1
+#endif
+#ifndef HOLO_COMP2_MINB
+#define HOLO_COMP2_MINB 8
 #endif
 
 // AUX: count contributions for n_contrib (HOLO_OUT_AUX); compiled out otherwise
@@ -246,60 +312,7 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
 
     if (n > 0) {
         const bool presorted = n <= kWarpSortCap || n > kSortCap;
-        if (!presorted) {
-            for (int t = tid; t < n; t += G::kThreads) {
-                const int g = a.egidx[e0 + t];
-                sm.sort.key[t] = a.zkey[g];
-                sm.sort.gid[t] = g;
-            }
-            __syncthreads();
-            if (n <= G::kThreads) {
-                if (tid < n) {
-                    const unsigned long long k = sm.sort.key[tid];
-                    const int g = sm.sort.gid[tid];
-                    int rank = 0;
-                    for (int j = 0; j < n; ++j) {
-                        const unsigned long long kj = sm.sort.key[j];
-                        rank += (kj < k || (kj == k && sm.sort.gid[j] < g)) ? 1 : 0;
-                    }
-                    s_ord[rank] = g;
-                }
-            } else {
-                int P = 1;
-                while (P < n) P <<= 1;
-                for (int t = n + tid; t < P; t += G::kThreads) {
-                    sm.sort.key[t] = ~0ull;
-                    sm.sort.gid[t] = 0x7fffffff;
-                }
-                __syncthreads();
-                for (int k = 2; k <= P; k <<= 1) {
-                    for (int j = k >> 1; j > 0; j >>= 1) {
-                        for (int t = tid; t < P; t += G::kThreads) {
-                            const int u = t ^ j;
-                            if (u > t) {
-                                const bool up = (t & k) == 0;
-                                const unsigned long long ka = sm.sort.key[t], kb = sm.sort.key[u];
-                                const int ga = sm.sort.gid[t], gb = sm.sort.gid[u];
-                                const bool b_less = kb < ka || (kb == ka && gb < ga);
-                                const bool a_less = ka < kb || (ka == kb && ga < gb);
-                                if (up ? b_less : a_less) {
-                                    sm.sort.key[t] = kb;
-                                    sm.sort.key[u] = ka;
-                                    sm.sort.gid[t] = gb;
-                                    sm.sort.gid[u] = ga;
-                                }
-                            }
-                        }
-                        __syncthreads();
-                    }
-                }
-                for (int t = tid; t < n; t += G::kThreads) s_ord[t] = sm.sort.gid[t];
-            }
-            __syncthreads();
-            // the lists stay in reference order for the frame's other consumers
-            // (HOLO_BUF_ENTRY_*, the backward pass)
-            for (int t = tid; t < n; t += G::kThreads) a.egidx[e0 + t] = s_ord[t];
-        }
+        if (!presorted) sort_bucket_cta<G::kThreads>(a, e0, n, tid, sm.sort.key, sm.sort.gid, s_ord);
 
         const float fx = static_cast<float>(lx) + 0.5f, fy = static_cast<float>(ly) + 0.5f;
         const float bxlo = static_cast<float>(bx) + 0.5f, bxhi = static_cast<float>(bx) + 7.5f;
@@ -412,6 +425,158 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
     }
 }
 
+// 16x16 tiles, two pixels per thread: 128 threads, each warp an 8 x 8 block, each
+// lane the pixels (x, y) and (x, y + 4).  A hit entry's staged record is read once
+// for both pixels, and the two quadratic forms are evaluated with packed fp32x2
+// arithmetic; every packed operation rounds per element exactly as the scalar one
+// of eval_alpha, so each pixel's alpha -- hence every accept decision -- is the
+// one k_composite, the backward and the brute force compute.
+template <int C, bool AUX>
+__global__ void __launch_bounds__(128, HOLO_COMP2_MINB) k_composite2(CompositeArgs a) {
+    constexpr int TILE = 16, NT = 128;
+    constexpr int kStage = 256;
+    constexpr int kTest = HOLO_COMP_TEST;
+    union Smem {
+        struct {
+            unsigned long long key[kSortCap];
+            int gid[kSortCap];
+        } sort;
+        struct {
+            Staged rec[kStage + 1];
+            float4 box[kStage];
+        } st;
+    };
+    __shared__ Smem sm;
+    __shared__ int s_ord[kSortCap];
+    __shared__ __align__(8) int s_hit[NT / 32][32 * kTest + 2];
+
+    const int tx = blockIdx.x, ty = blockIdx.y, lplane = blockIdx.z;
+    const int lb = (lplane * gridDim.y + ty) * gridDim.x + tx;
+    const int px0 = tx * TILE, py0 = ty * TILE;
+    const unsigned e0 = min(a.bstart[lb], a.capacity);
+    const int n = static_cast<int>(min(a.bstart[lb + 1], a.capacity) - e0);
+    const int plane = a.plane_begin + lplane;
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int bx = (warp & 1) * 8, by = (warp >> 1) * 8;
+    const int lx = bx + (lane & 7), ly = by + (lane >> 3);  // pixels (lx, ly) and (lx, ly + 4)
+    const int px = px0 + lx, py = py0 + ly;
+    const bool in0 = px < a.W && py < a.H, in1 = px < a.W && py + 4 < a.H;
+    const float eps = a.term_eps;
+
+    float T0 = 1.0f, T1 = 1.0f;
+    int contrib0 = 0, contrib1 = 0, elast0 = -1, elast1 = -1;
+    cx<float> acc0[C], acc1[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc0[c] = acc1[c] = mk(0.0f, 0.0f);
+    bool done = !(in0 && 1.0f >= eps) && !(in1 && 1.0f >= eps);
+
+    if (n > 0) {
+        const bool presorted = n <= kWarpSortCap || n > kSortCap;
+        if (!presorted) sort_bucket_cta<NT>(a, e0, n, tid, sm.sort.key, sm.sort.gid, s_ord);
+
+        const float fx = static_cast<float>(lx) + 0.5f;
+        const unsigned long long fy01 = f32x2::pack(static_cast<float>(ly) + 0.5f, static_cast<float>(ly) + 4.5f);
+        const float bxlo = static_cast<float>(bx) + 0.5f, bxhi = static_cast<float>(bx) + 7.5f;
+        const float bylo = static_cast<float>(by) + 0.5f, byhi = static_cast<float>(by) + 7.5f;
+        const float thr = a.floor_positive ? a.alpha_floor : 0.0f;
+        const float clamp = a.alpha_clamp;
+        // a pixel outside the image is parked with T = -1: never accepts, never written
+        if (!in0) T0 = -1.0f;
+        if (!in1) T1 = -1.0f;
+
+        for (int base = 0; base < n; base += kStage) {
+            const int cnt = (n - base) < kStage ? (n - base) : kStage;
+            for (int t = tid; t < cnt; t += NT) {
+                const int g = presorted ? a.egidx[e0 + base + t] : s_ord[base + t];
+                const GRec r = a.rec[g];
+                float alpha = r.alpha;
+                if (a.soft)
+                    alpha = static_cast<float>(static_cast<double>(r.alpha) * a.rho[static_cast<size_t>(g) * a.L + plane]);
+                stage_entry(r, px0, py0, alpha, sm.st.rec[t], sm.st.box[t]);
+            }
+            if (tid == 0) {
+                Staged& z = sm.st.rec[kStage];
+                z.a = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                z.b = make_float4(0.0f, -INFINITY, 0.0f, 0.0f);
+                z.c = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            }
+            __syncthreads();
+            if (!__all_sync(0xffffffffu, done)) {
+                const char* recs = reinterpret_cast<const char*>(sm.st.rec);
+                int* hits = s_hit[warp];
+                for (int c0 = 0; c0 < cnt; c0 += 32 * kTest) {
+                    const unsigned below = (1u << lane) - 1u;
+                    int nh = 0;
+#pragma unroll
+                    for (int q = 0; q < kTest; ++q) {
+                        const int j = c0 + 32 * q + lane;
+                        const bool h = j < cnt && box_hits(sm.st.box[j], bxlo, bxhi, bylo, byhi);
+                        const unsigned m = __ballot_sync(0xffffffffu, h);
+                        if (h) hits[nh + __popc(m & below)] = j * static_cast<int>(sizeof(Staged));
+                        nh += __popc(m);
+                    }
+                    __syncwarp();
+                    for (int k = 0; k < nh; ++k) {
+                        const int off = hits[k];
+                        const Staged* e = reinterpret_cast<const Staged*>(recs + off);
+                        const float4 A = e->a, B = e->b;
+                        // eval_alpha for both pixels: d = centre - mu (dx shared), then
+                        // t = fma(cb, dy, ca dx), u = fma(dx, t, log2 alpha),
+                        // q = fma(cc dy, dy, u), a = min(2^q, clamp)
+                        const float dx = fx - A.x;
+                        const unsigned long long dy = f32x2::sub(fy01, f32x2::pack(A.y, A.y));
+                        const float cadx = A.z * dx;
+                        const unsigned long long t = f32x2::fma(f32x2::pack(A.w, A.w), dy, f32x2::pack(cadx, cadx));
+                        const unsigned long long u = f32x2::fma(f32x2::pack(dx, dx), t, f32x2::pack(B.y, B.y));
+                        const unsigned long long ccdy = f32x2::mul(f32x2::pack(B.x, B.x), dy);
+                        const cx<float> qq = f32x2::unpack(f32x2::fma(ccdy, dy, u));
+                        const float al0 = fminf(ex2_approx(qq.x), clamp);
+                        const float al1 = fminf(ex2_approx(qq.y), clamp);
+                        const bool a0 = (al0 > thr) && (T0 >= eps);
+                        const bool a1 = (al1 > thr) && (T1 >= eps);
+                        const cx<float> wt = f32x2::unpack(f32x2::mul(f32x2::pack(al0, al1), f32x2::pack(T0, T1)));
+                        const float w0 = a0 ? wt.x : 0.0f, w1 = a1 ? wt.y : 0.0f;
+                        blend<C>(e, B, w0, acc0);
+                        blend<C>(e, B, w1, acc1);
+                        const cx<float> Tn = f32x2::unpack(f32x2::sub(f32x2::pack(T0, T1), f32x2::pack(w0, w1)));
+                        T0 = Tn.x;
+                        T1 = Tn.y;
+                        if constexpr (AUX) {
+                            const int ei = base + off / static_cast<int>(sizeof(Staged));
+                            contrib0 += a0 ? 1 : 0;
+                            contrib1 += a1 ? 1 : 0;
+                            elast0 = a0 ? ei : elast0;
+                            elast1 = a1 ? ei : elast1;
+                        }
+                    }
+                    __syncwarp();
+                    done = !(T0 >= eps) && !(T1 >= eps);
+                    if (__all_sync(0xffffffffu, done)) break;
+                }
+            }
+            if (base + kStage >= n) break;
+            if (__syncthreads_count(done ? 1 : 0) == NT) break;
+        }
+    }
+
+    const size_t P = static_cast<size_t>(a.W) * a.H;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if (!(h ? in1 : in0)) continue;
+        const size_t pix = static_cast<size_t>(py + 4 * h) * a.W + px;
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+            a.layers[(static_cast<size_t>(lplane) * C + c) * P + pix] = h ? acc1[c] : acc0[c];
+        if (a.t_final) a.t_final[static_cast<size_t>(lplane) * P + pix] = h ? T1 : T0;
+        if constexpr (AUX) {
+            a.n_contrib[static_cast<size_t>(lplane) * P + pix] = h ? contrib1 : contrib0;
+            if (a.e_last) a.e_last[static_cast<size_t>(lplane) * P + pix] = h ? elast1 : elast0;
+        }
+    }
+}
+
 #ifdef HOLO_COUNT
 __global__ void k_print_counts() {
     printf("composite counts: warp-evals %llu, with any accept %llu, accepted lanes %llu, chunks %llu\n",
@@ -425,6 +590,22 @@ void launch_tile(holo_ctx* ctx, const CompositeArgs& a) {
     if (a.num_buckets <= 0) return;
     const int tiles_y = a.num_tiles / a.tiles_x;
     const dim3 grid(a.tiles_x, tiles_y, a.num_buckets / a.num_tiles);
+    if constexpr (TILE == 16) {
+        if (HOLO_COMP2) {
+            switch (a.C) {
+#define HC_COMP2(CC)                                                                     \
+    (a.n_contrib ? k_composite2<CC, true><<<grid, 128, 0, ctx->stream>>>(a)             \
+                 : k_composite2<CC, false><<<grid, 128, 0, ctx->stream>>>(a))
+                case 1: HC_COMP2(1); break;
+                case 2: HC_COMP2(2); break;
+                case 3: HC_COMP2(3); break;
+#undef HC_COMP2
+                default: throw Error(HOLO_ERR_CONFIG, "render supports 1 to 3 wavelength channels");
+            }
+            HC_LAUNCHED(ctx);
+            return;
+        }
+    }
     switch (a.C) {
 #define HC_COMP(CC)                                                                   \
     (a.n_contrib ? k_composite<TILE, CC, true><<<grid, TILE * TILE, 0, ctx->stream>>>(a) \
