@@ -55,7 +55,11 @@ template <> struct PlanOf<3840> { using type = Radices<16, 16, 15>; };
 // The twiddle table is copied to shared memory behind the FFT work area
 // (HOLO_COL_SMEM_TW=0 reads it from global memory instead).
 #ifndef HOLO_COL_SMEM_TW
-#define HOLO_COL_SMEM_TW 1
+#define HOLO_COL_SMEM_TW 0  // measured: global (L1) twiddles 0.211 -> 0.197 ms (col fwd, C3)
+#endif
+// the row pass's twiddles: shared-memory copy (1) or global / L1 (0)
+#ifndef HOLO_ROW_SMEM_TW
+#define HOLO_ROW_SMEM_TW 1
 #endif
 template <int H_, int NB_, int NT_, int MINB_>
 struct ColCfgT {
@@ -77,8 +81,19 @@ __device__ __forceinline__ const cx<float>* col_twiddles(cx<float>* sm, const cx
     return tw;
 }
 // default: 8-column strips (64-byte row segments); 2 CTAs per SM while 64 registers suffice
+// (HOLO_COL_NB / _NT / _MINB override the shape, for measurement)
+#ifndef HOLO_COL_NB
+#define HOLO_COL_NB 8
+#endif
+#ifndef HOLO_COL_NT
+#define HOLO_COL_NT 0
+#endif
+#ifndef HOLO_COL_MINB
+#define HOLO_COL_MINB 0
+#endif
 template <int H>
-using ColCfg = ColCfgT<H, 8, (H >= 1024 ? 512 : 256), (H <= 1280 ? 2 : 1)>;
+using ColCfg = ColCfgT<H, HOLO_COL_NB, (HOLO_COL_NT ? HOLO_COL_NT : (H >= 1024 ? 512 : 256)),
+                       (HOLO_COL_MINB ? HOLO_COL_MINB : (H <= 1280 ? 2 : 1))>;
 
 // row pass: NBR rows of one channel per CTA
 template <int W_, int NBR_, int NT_, int MINB_>
@@ -181,7 +196,7 @@ struct RowSmem {
     static constexpr int kRowPad = Cfg::W + 8;
     static constexpr size_t kWork = sizeof(cx<float>) * FftSmem<typename Cfg::B, typename PlanOf<Cfg::W>::type>::kElems;
     static constexpr size_t kPre = MODE == kModeReplay ? 0 : sizeof(cx<float>) * Cfg::NBR * kRowPad;
-    static constexpr size_t kTw = sizeof(cx<float>) * Cfg::W;
+    static constexpr size_t kTw = HOLO_ROW_SMEM_TW ? sizeof(cx<float>) * Cfg::W : 0;
     static constexpr size_t kG = sizeof(float) * LS::kBPT * LS::kR * Cfg::NT;
     static constexpr size_t kTf = kWork + kPre + kTw + kG;  // offset of the per-plane constants
     static size_t bytes(int Lloc) { return kTf + sizeof(float2) * (Lloc > 0 ? Lloc : 1); }
@@ -204,7 +219,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<float>* sm = reinterpret_cast<cx<float>*>(smem_raw);
     cx<float>* pre = reinterpret_cast<cx<float>*>(smem_raw + SM::kWork);
-    cx<float>* s_tw = reinterpret_cast<cx<float>*>(smem_raw + SM::kWork + SM::kPre);
+    const cx<float>* s_tw = HOLO_ROW_SMEM_TW ? reinterpret_cast<cx<float>*>(smem_raw + SM::kWork + SM::kPre) : tw;
     float* s_G = reinterpret_cast<float*>(smem_raw + SM::kWork + SM::kPre + SM::kTw);
     float2* s_tf = reinterpret_cast<float2*>(smem_raw + SM::kTf);  // (phase0, 2 pi z) per plane
     __shared__ unsigned long long s_bar;
@@ -217,7 +232,8 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
     const size_t plane_stride = static_cast<size_t>(C) * H * W;
     const int nplanes = MODE == kModeReplay ? nrep : Lloc;
     for (int l = threadIdx.x; l < nplanes; l += Cfg::NT) s_tf[l] = make_float2(tfc[l * C + c].phase0, tfc[l * C + c].two_pi_z_f);
-    for (int k = threadIdx.x; k < W; k += Cfg::NT) s_tw[k] = tw[k];
+    if constexpr (HOLO_ROW_SMEM_TW)
+        for (int k = threadIdx.x; k < W; k += Cfg::NT) const_cast<cx<float>*>(s_tw)[k] = tw[k];
 
     // prefetch of plane l's NBR rows (one thread issues; the buffer is free once
     // every thread has finished the previous plane's first FFT stage)
