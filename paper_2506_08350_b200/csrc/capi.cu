@@ -498,6 +498,17 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     if (info) *info = holo_frame_info{};  // known after holo_ctx_frame_status
 }
 
+// The row pass evaluates every plane's transfer function directly (instead of the
+// plane-to-plane recurrence) for local band limits or unevenly spaced planes.
+bool tf_direct(const std::vector<double>& z, int local) {
+    if (local) return true;
+    for (size_t l = 2; l < z.size(); ++l) {
+        const double d0 = z[1] - z[0], d = z[l] - z[l - 1];
+        if (std::fabs(d - d0) > 1e-12 * std::fabs(d0)) return true;
+    }
+    return false;
+}
+
 TfChan* upload_tf(holo_ctx* ctx, const char* name, const holo_wave& wave, const std::vector<double>& z, int w, int h,
                   int local) {
     const std::vector<TfChan> t = make_tf_consts(wave, z.data(), static_cast<int>(z.size()), w, h, local);
@@ -927,7 +938,7 @@ void render_back(holo_ctx* ctx, const holo_wave& wave, const holo_prop_options& 
     if (static_render_supported(W, H)) {
         ctx->stage_begin();
         static_row(ctx, kModeReplay, nullptr, const_cast<cx<float>*>(spec), stage, W, H, C, np, has_holo,
-                   O - has_holo, tfc, wave.pitch, po.local_band_limit != 0);
+                   O - has_holo, tfc, wave.pitch, tf_direct(z, po.local_band_limit));
         ctx->stage_end(5);
         wait_downloads(ctx, ctx->out_sel, ~0u);
         ctx->stage_begin();
@@ -995,7 +1006,7 @@ void render_front(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, 
         if (!full) {
             ctx->stage_begin();
             static_row(ctx, kModeSpec, work, spec, nullptr, g.W, g.H, g.C, np, 0, 0, tfc, wave.pitch,
-                       po.local_band_limit != 0);
+                       tf_direct(z, po.local_band_limit));
             ctx->stage_end(4);
             return;
         }
@@ -1005,7 +1016,7 @@ void render_front(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, 
         const OutBufs ob = output_buffers(ctx, outputs, np, g.C, g.P);
         ctx->stage_begin();
         static_row(ctx, kModeFull, work, nullptr, stage, g.W, g.H, g.C, np, has_holo, O - has_holo, tfc, wave.pitch,
-                   po.local_band_limit != 0);
+                   tf_direct(z, po.local_band_limit));
         ctx->stage_end(4);
         wait_downloads(ctx, ctx->out_sel, ~0u);
         ctx->stage_begin();
@@ -1153,7 +1164,8 @@ void adjoint_propagation(holo_ctx* ctx, const holo_wave& wave, const holo_prop_o
     cx<float>* stage = buf<cx<float>>(ctx, "bwd_stage", static_cast<size_t>(O) * C * P);
     if (static_render_supported(W, H)) {
         static_col_fwd(ctx, gv, W, H, L * C);
-        static_row(ctx, kModeFull, gv, nullptr, stage, W, H, C, L, 1, L, tfc, wave.pitch, po.local_band_limit != 0);
+        static_row(ctx, kModeFull, gv, nullptr, stage, W, H, C, L, 1, L, tfc, wave.pitch,
+                   tf_direct(z, po.local_band_limit));
         static_col_inv(ctx, stage, W, H, C, O, 1, gholo, glayers, nullptr);
         return;
     }
@@ -1286,7 +1298,7 @@ void shard_front(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, c
         for (int c = 0; c < g.C; ++c) {
             ctx->stage_begin();
             static_row(ctx, kModeSpec, work, spec, nullptr, g.W, g.H, g.C, np, 0, 0, tfc, wave.pitch,
-                       po.local_band_limit != 0, c, 1);
+                       tf_direct(z, po.local_band_limit), c, 1);
             ctx->stage_end(4);
             HC_CUDA(cudaEventRecord(ctx->ev_chan_ready[c], ctx->stream));
         }
@@ -1335,7 +1347,7 @@ void shard_back(holo_ctx* ctx, const holo_wave& wave, const holo_prop_options& p
             cx<float>* st_c = stage + static_cast<size_t>(hh && !own ? 1 : 0) * C * P;
             ctx->stage_begin();
             static_row(ctx, kModeReplay, nullptr, const_cast<cx<float>*>(spec), st_c, W, H, C, np, own, nrep, tfc,
-                       wave.pitch, po.local_band_limit != 0, c, 1);
+                       wave.pitch, tf_direct(z, po.local_band_limit), c, 1);
             ctx->stage_end(5);
         }
         wait_downloads(ctx, ctx->out_sel, ~0u);

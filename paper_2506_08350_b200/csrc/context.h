@@ -38,6 +38,10 @@ struct TfChan {
     float two_pi_z_f;   // 2 pi z
     float phase0;       // (2 pi z / lambda) mod 2 pi
     int local;          // local band limit active (opt && z != 0)
+    // step to the next plane (the row pass's plane recurrence, render_static.cu):
+    // (2 pi dz / lambda) mod 2 pi and 2 pi dz, dz = z_{l+1} - z_l (f64, then fp32)
+    float step_phase;
+    float step_2piz;
 };
 
 constexpr int kNumStages = 8;

@@ -359,6 +359,11 @@ std::vector<TfChan> make_tf_consts(const holo_wave& wave, const double* z, int L
             double ph = std::fmod(p.two_pi_z * inv_l, two_pi);
             if (ph < 0) ph += two_pi;
             p.phase0 = static_cast<float>(ph);
+            const double dz2 = l + 1 < L ? two_pi * (z[l + 1] - z[l]) : 0.0;
+            double dph = std::fmod(dz2 * inv_l, two_pi);
+            if (dph < 0) dph += two_pi;
+            p.step_phase = static_cast<float>(dph);
+            p.step_2piz = static_cast<float>(dz2);
         }
     }
     return v;

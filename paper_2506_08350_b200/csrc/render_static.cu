@@ -188,21 +188,31 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 
 // Row-pass shared memory: FFT work area; the prefetch buffer for the next plane's
 // NBR rows (each row padded by 8 complex = 16 banks; FULL / SPEC); the twiddle
-// table; the plane-independent TF factor G of every owned spectral sample
-// ([slot][thread], conflict-free); per-plane TF constants.
-template <class Cfg, int MODE>
+// table; per owned spectral sample ([slot][thread], conflict-free) either the
+// plane-independent TF factor G (DIRECT) or the plane-to-plane TF ratio Q; the
+// per-plane TF constants.
+template <class Cfg, int MODE, bool DIRECT>
 struct RowSmem {
     using LS = LastStage<typename Cfg::B, typename PlanOf<Cfg::W>::type>;
     static constexpr int kRowPad = Cfg::W + 8;
     static constexpr size_t kWork = sizeof(cx<float>) * FftSmem<typename Cfg::B, typename PlanOf<Cfg::W>::type>::kElems;
     static constexpr size_t kPre = MODE == kModeReplay ? 0 : sizeof(cx<float>) * Cfg::NBR * kRowPad;
     static constexpr size_t kTw = HOLO_ROW_SMEM_TW ? sizeof(cx<float>) * Cfg::W : 0;
-    static constexpr size_t kG = sizeof(float) * LS::kBPT * LS::kR * Cfg::NT;
+    static constexpr size_t kG = (DIRECT ? sizeof(float) : sizeof(cx<float>)) * LS::kBPT * LS::kR * Cfg::NT;
     static constexpr size_t kTf = kWork + kPre + kTw + kG;  // offset of the per-plane constants
     static size_t bytes(int Lloc) { return kTf + sizeof(float2) * (Lloc > 0 ? Lloc : 1); }
 };
 
-template <class Cfg, int MODE, bool LOCAL>
+// The planes are evenly spaced (plane_positions, wave_config.cpp:18-30), so the
+// transfer functions of consecutive planes differ by one per-sample factor:
+//   H_l = A Q^l,  A = e^{i (phase0_0 - 2 pi z_0 g)},  Q = e^{i (dphase - 2 pi dz g)}
+// (g = f^2 / (1/l + sqrt(1/l^2 - f^2)) as in tf_value<float>; dphase = 2 pi dz / lambda
+// reduced mod 2 pi in f64 on the host).  The forward sum is evaluated by Horner over
+// the planes in reverse order, S' = X_{L-1}, S' = Q S' + X_l, S = A S' -- one complex
+// FMA per plane and sample instead of a range-reduced sin / cos -- and the replays
+// take S conj(H_l) = S' conj(Q)^l, stepping S' by conj(Q) after each plane.  DIRECT
+// evaluates every H_l itself (local band limits, unevenly spaced planes).
+template <class Cfg, int MODE, bool DIRECT>
 __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
     const cx<float>* __restrict__ layers,  // [Lloc][C][H][W], column-transformed (FULL, SPEC)
     cx<float>* __restrict__ spec,          // [C][H][W]: written (SPEC) or read (REPLAY)
@@ -215,12 +225,12 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
     using P = typename PlanOf<W>::type;
     using Pinv = typename RevPlan<P>::type;
     using LS = LastStage<B, P>;
-    using SM = RowSmem<Cfg, MODE>;
+    using SM = RowSmem<Cfg, MODE, DIRECT>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<float>* sm = reinterpret_cast<cx<float>*>(smem_raw);
     cx<float>* pre = reinterpret_cast<cx<float>*>(smem_raw + SM::kWork);
     const cx<float>* s_tw = HOLO_ROW_SMEM_TW ? reinterpret_cast<cx<float>*>(smem_raw + SM::kWork + SM::kPre) : tw;
-    float* s_G = reinterpret_cast<float*>(smem_raw + SM::kWork + SM::kPre + SM::kTw);
+    unsigned char* s_slot = smem_raw + SM::kWork + SM::kPre + SM::kTw;
     float2* s_tf = reinterpret_cast<float2*>(smem_raw + SM::kTf);  // (phase0, 2 pi z) per plane
     __shared__ unsigned long long s_bar;
 
@@ -246,13 +256,15 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
             bulk_g2s(pre + b * SM::kRowPad, src + static_cast<size_t>(b) * W,
                      W * static_cast<unsigned>(sizeof(cx<float>)), &s_bar);
     };
+    // forward planes in the order the sum needs them: Horner runs from the last plane
+    auto fwd_plane = [&](int it) { return DIRECT ? it : Lloc - 1 - it; };
     if constexpr (MODE != kModeReplay) {
         if (threadIdx.x == 0) {
             mbar_init(&s_bar, 1);
             mbar_init_fence();
         }
         __syncthreads();
-        if (threadIdx.x == 0 && Lloc > 0) issue(0);
+        if (threadIdx.x == 0 && Lloc > 0) issue(fwd_plane(0));
     } else {
         __syncthreads();
     }
@@ -265,43 +277,56 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
         i = t / B::kNB + r * M;
         return t < M * B::kNB;
     };
+    // g = f^2 / (1/l + sqrt(1/l^2 - f^2)) at owned sample (q, r), or -1 outside the
+    // propagating band (band test in f64, reference order)
+    const TfChan p0 = tfc[c];  // 1/l^2, 1/l depend on the channel only
+    auto g_at = [&](int q, int r) -> float {
+        int b, i;
+        float g = -1.0f;
+        if (owner(q, r, b, i)) {
+            const double fxv = fx[i], fyv = fy[(row0 + b) - c * H];
+            const double fx2 = __dmul_rn(fxv, fxv), fy2 = __dmul_rn(fyv, fyv);
+            const double arg = __dsub_rn(__dsub_rn(p0.inv_l2, fx2), fy2);
+            if (!(arg < 0.0)) g = static_cast<float>(__dadd_rn(fx2, fy2)) / (p0.inv_l + sqrtf(static_cast<float>(arg)));
+        }
+        return g;
+    };
+    // A = H_{plane 0} (for the Horner form)
+    auto a_at = [&](int q, int r) -> cx<float> {
+        const float2 t = s_tf[0];
+        return phasor_reduced(t.x - t.y * g_at(q, r));
+    };
 
     cx<float> S[LS::kBPT][LS::kR];
-    // Plane-independent part of the transfer-function phase for each owned spectral
-    // sample: g = f^2 / (1/l + sqrt(1/l^2 - f^2)), or -1 outside the propagating
-    // band (band test in f64, reference order).  Per plane the phase is then
-    // phase0 - 2 pi z g (see tf_value<float>).  Kept in shared memory, one slot
-    // per (q, r) and thread (registers go to the FFT).
-    auto G = [&](int q, int r) -> float& { return s_G[(q * LS::kR + r) * Cfg::NT + threadIdx.x]; };
+    // DIRECT: G per slot; otherwise Q per slot (0 outside the band)
+    auto G = [&](int q, int r) -> float& {
+        return reinterpret_cast<float*>(s_slot)[(q * LS::kR + r) * Cfg::NT + threadIdx.x];
+    };
+    auto Qs = [&](int q, int r) -> cx<float>& {
+        return reinterpret_cast<cx<float>*>(s_slot)[(q * LS::kR + r) * Cfg::NT + threadIdx.x];
+    };
     {
-        const TfChan p0 = tfc[c];  // 1/l^2, 1/l depend on the channel only
+        const float dph = p0.step_phase, dz2 = p0.step_2piz;
 #pragma unroll
         for (int q = 0; q < LS::kBPT; ++q)
 #pragma unroll
             for (int r = 0; r < LS::kR; ++r) {
                 S[q][r] = czf();
-                float g = -1.0f;
-                int b, i;
-                if (owner(q, r, b, i)) {
-                    const double fxv = fx[i], fyv = fy[(row0 + b) - c * H];
-                    const double fx2 = __dmul_rn(fxv, fxv), fy2 = __dmul_rn(fyv, fyv);
-                    const double arg = __dsub_rn(__dsub_rn(p0.inv_l2, fx2), fy2);
-                    if (!(arg < 0.0))
-                        g = static_cast<float>(__dadd_rn(fx2, fy2)) / (p0.inv_l + sqrtf(static_cast<float>(arg)));
-                }
-                G(q, r) = g;
+                const float g = g_at(q, r);
+                if constexpr (DIRECT)
+                    G(q, r) = g;
+                else
+                    Qs(q, r) = g < 0.0f ? czf() : phasor_reduced(dph - dz2 * g);
             }
     }
-    // H_{Z_l} at owned sample (q, r) inside the propagating band: the
+    // DIRECT: H_{Z_l} at owned sample (q, r) inside the propagating band: the
     // plane-independent part G and the plane's (phase0, 2 pi z); local band limits
     // (rare) take the full f64 path.  The band mask (H = 0 outside, for every plane)
     // is applied once to S instead of per plane: S = sum_l H_l X_l vanishes there,
     // and so does every S . conj(H_l).
     auto tf = [&](int l, int q, int r, int b, int i) -> cx<float> {
-        if constexpr (LOCAL) {
-            const TfChan p = tfc[l * C + c];
-            if (p.local) return tf_value<float>(p, fx[i], fy[(row0 + b) - c * H]);
-        }
+        const TfChan p = tfc[l * C + c];
+        if (p.local) return tf_value<float>(p, fx[i], fy[(row0 + b) - c * H]);
         const float2 t = s_tf[l];
         return phasor_reduced(t.x - t.y * G(q, r));
     };
@@ -309,18 +334,30 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
 #pragma unroll
         for (int q = 0; q < LS::kBPT; ++q)
 #pragma unroll
-            for (int r = 0; r < LS::kR; ++r)
-                if (G(q, r) < 0.0f) S[q][r] = czf();
+            for (int r = 0; r < LS::kR; ++r) {
+                if constexpr (DIRECT) {
+                    if (G(q, r) < 0.0f) S[q][r] = czf();
+                } else {
+                    const cx<float> Q = Qs(q, r);
+                    if (Q.x == 0.0f && Q.y == 0.0f) S[q][r] = czf();
+                }
+            }
     };
 
     if constexpr (MODE != kModeReplay) {
-        for (int l = 0; l < Lloc; ++l) {
-            mbar_wait(&s_bar, l & 1);
+        for (int it = 0; it < Lloc; ++it) {
+            const int l = fwd_plane(it);
+            mbar_wait(&s_bar, it & 1);
             auto load = [&](int, int, int b, int i) -> cx<float> { return pre[b * SM::kRowPad + i]; };
-            auto store = [&](int q, int r, int b, int i, cx<float> v) { S[q][r] = cfma(v, tf(l, q, r, b, i), S[q][r]); };
+            auto store = [&](int q, int r, int b, int i, cx<float> v) {
+                if constexpr (DIRECT)
+                    S[q][r] = cfma(v, tf(l, q, r, b, i), S[q][r]);
+                else
+                    S[q][r] = cfma(S[q][r], Qs(q, r), v);  // S' = Q S' + X_l
+            };
             // once the first stage has read the buffer, start loading the next plane
             auto hook = [&] {
-                if (threadIdx.x == 0 && l + 1 < Lloc) issue(l + 1);
+                if (threadIdx.x == 0 && it + 1 < Lloc) issue(fwd_plane(it + 1));
             };
             fft_static<float, -1, B, P>(sm, s_tw, load, store, hook);
         }
@@ -333,31 +370,44 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
 #pragma unroll
             for (int r = 0; r < LS::kR; ++r) {
                 int b, i;
-                if (owner(q, r, b, i)) dst[static_cast<size_t>(b) * W + i] = S[q][r];
+                if (owner(q, r, b, i)) dst[static_cast<size_t>(b) * W + i] = DIRECT ? S[q][r] : S[q][r] * a_at(q, r);
             }
         return;
     }
     if constexpr (MODE == kModeReplay) {
+        // S' = S conj(A) (the replayed planes start at plane 0 of the range)
         const cx<float>* srcs = spec + static_cast<size_t>(row0) * W;
 #pragma unroll
         for (int q = 0; q < LS::kBPT; ++q)
 #pragma unroll
             for (int r = 0; r < LS::kR; ++r) {
                 int b, i;
-                if (owner(q, r, b, i)) S[q][r] = srcs[static_cast<size_t>(b) * W + i];
+                if (owner(q, r, b, i)) {
+                    const cx<float> v = srcs[static_cast<size_t>(b) * W + i];
+                    S[q][r] = DIRECT || nrep == 0 ? v : v * conj(a_at(q, r));
+                }
             }
         band_mask();
     }
     // outputs: [hologram] then planes 0..nrep-1 (output_planes in capi.cu)
     if (has_holo) {
         cx<float>* dst = out + static_cast<size_t>(row0) * W;
-        auto load = [&](int q, int r, int, int) -> cx<float> { return S[q][r]; };
+        const bool plain = DIRECT || (MODE == kModeReplay && nrep == 0);  // S itself
+        auto load = [&](int q, int r, int, int) -> cx<float> { return plain ? S[q][r] : S[q][r] * a_at(q, r); };
         auto store = [&](int, int, int b, int i, cx<float> v) { dst[static_cast<size_t>(b) * W + i] = v; };
         fft_static<float, +1, B, Pinv>(sm, s_tw, load, store);
     }
     for (int l = 0; l < nrep; ++l) {
         cx<float>* dst = out + (static_cast<size_t>(l + has_holo) * C * H + row0) * W;
-        auto load = [&](int q, int r, int b, int i) -> cx<float> { return S[q][r] * conj(tf(l, q, r, b, i)); };
+        auto load = [&](int q, int r, int b, int i) -> cx<float> {
+            if constexpr (DIRECT) {
+                return S[q][r] * conj(tf(l, q, r, b, i));
+            } else {
+                const cx<float> v = S[q][r];  // S' conj(Q)^l
+                S[q][r] = v * conj(Qs(q, r));
+                return v;
+            }
+        };
         auto store = [&](int, int, int b, int i, cx<float> v) { dst[static_cast<size_t>(b) * W + i] = v; };
         fft_static<float, +1, B, Pinv>(sm, s_tw, load, store);
     }
@@ -431,7 +481,7 @@ void launch_row_mode(holo_ctx* ctx, const cx<float>* layers, cx<float>* spec, cx
                      int has_holo, int nrep, const TfChan* tfc, const double* fx, const double* fy, int c0, int nc) {
     const dim3 grid(nc * H / Cfg::NBR);
     const int nplanes = MODE == kModeReplay ? nrep : Lloc;
-    const size_t smem = RowSmem<Cfg, MODE>::bytes(nplanes);
+    const size_t smem = RowSmem<Cfg, MODE, LOCAL>::bytes(nplanes);
     HC_CUDA(cudaFuncSetAttribute(k_row_fused<Cfg, MODE, LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
     k_row_fused<Cfg, MODE, LOCAL><<<grid, Cfg::NT, smem, ctx->stream>>>(
