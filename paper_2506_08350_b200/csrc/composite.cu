@@ -263,6 +263,13 @@ __device__ __forceinline__ void sort_bucket_cta(const CompositeArgs& a, unsigned
 #ifndef HOLO_COMP2_MINB
 #define HOLO_COMP2_MINB 8
 #endif
+// pixels per thread of k_composite2 (2: 128 threads per tile, 4: 64)
+#ifndef HOLO_COMP_PPT
+#define HOLO_COMP_PPT 2
+#endif
+#ifndef HOLO_COMP4_MINB
+#define HOLO_COMP4_MINB 12
+#endif
 
 // AUX: count contributions for n_contrib (HOLO_OUT_AUX); compiled out otherwise
 template <int TILE, int C, bool AUX>
@@ -425,17 +432,19 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
     }
 }
 
-// 16x16 tiles, two pixels per thread: 128 threads, each warp an 8 x 8 block, each
-// lane the pixels (x, y) and (x, y + 4).  A hit entry's staged record is read once
-// for both pixels, and the two quadratic forms are evaluated with packed fp32x2
-// arithmetic; every packed operation rounds per element exactly as the scalar one
-// of eval_alpha, so each pixel's alpha -- hence every accept decision -- is the
-// one k_composite, the backward and the brute force compute.
-template <int C, bool AUX>
-__global__ void __launch_bounds__(128, HOLO_COMP2_MINB) k_composite2(CompositeArgs a) {
-    constexpr int TILE = 16, NT = 128;
+// 16x16 tiles, PPT (2 or 4) pixels per thread: 256 / PPT threads, each warp an
+// 8 x 4 PPT block, each lane the pixels (x, y + 4 k), k < PPT.  A hit entry's staged
+// record is read once for all of a lane's pixels, and the quadratic forms of pixel
+// pairs are evaluated with packed fp32x2 arithmetic; every packed operation rounds
+// per element exactly as the scalar one of eval_alpha, so each pixel's alpha --
+// hence every accept decision -- is the one k_composite, the backward and the
+// brute force compute.
+template <int C, bool AUX, int PPT>
+__global__ void __launch_bounds__(256 / PPT, PPT == 2 ? HOLO_COMP2_MINB : HOLO_COMP4_MINB) k_composite2(CompositeArgs a) {
+    constexpr int TILE = 16, NT = 256 / PPT;
     constexpr int kStage = 256;
     constexpr int kTest = HOLO_COMP_TEST;
+    static_assert(PPT % 2 == 0, "pixels are evaluated in pairs");
     union Smem {
         struct {
             unsigned long long key[kSortCap];
@@ -459,32 +468,44 @@ __global__ void __launch_bounds__(128, HOLO_COMP2_MINB) k_composite2(CompositeAr
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
-    const int bx = (warp & 1) * 8, by = (warp >> 1) * 8;
-    const int lx = bx + (lane & 7), ly = by + (lane >> 3);  // pixels (lx, ly) and (lx, ly + 4)
+    const int bx = (warp & 1) * 8, by = (warp >> 1) * (4 * PPT);
+    const int lx = bx + (lane & 7), ly = by + (lane >> 3);  // pixels (lx, ly + 4 k)
     const int px = px0 + lx, py = py0 + ly;
-    const bool in0 = px < a.W && py < a.H, in1 = px < a.W && py + 4 < a.H;
     const float eps = a.term_eps;
 
-    float T0 = 1.0f, T1 = 1.0f;
-    int contrib0 = 0, contrib1 = 0, elast0 = -1, elast1 = -1;
-    cx<float> acc0[C], acc1[C];
+    bool in[PPT];
+    float T[PPT];
+    int contrib[PPT], elast[PPT];
+    cx<float> acc[PPT][C];
+    bool done = true;
 #pragma unroll
-    for (int c = 0; c < C; ++c) acc0[c] = acc1[c] = mk(0.0f, 0.0f);
-    bool done = !(in0 && 1.0f >= eps) && !(in1 && 1.0f >= eps);
+    for (int k = 0; k < PPT; ++k) {
+        in[k] = px < a.W && py + 4 * k < a.H;
+        T[k] = 1.0f;
+        contrib[k] = 0;
+        elast[k] = -1;
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[k][c] = mk(0.0f, 0.0f);
+        done = done && !(in[k] && 1.0f >= eps);
+    }
 
     if (n > 0) {
         const bool presorted = n <= kWarpSortCap || n > kSortCap;
         if (!presorted) sort_bucket_cta<NT>(a, e0, n, tid, sm.sort.key, sm.sort.gid, s_ord);
 
         const float fx = static_cast<float>(lx) + 0.5f;
-        const unsigned long long fy01 = f32x2::pack(static_cast<float>(ly) + 0.5f, static_cast<float>(ly) + 4.5f);
+        unsigned long long fy2[PPT / 2];
+#pragma unroll
+        for (int j = 0; j < PPT / 2; ++j)
+            fy2[j] = f32x2::pack(static_cast<float>(ly + 8 * j) + 0.5f, static_cast<float>(ly + 8 * j + 4) + 0.5f);
         const float bxlo = static_cast<float>(bx) + 0.5f, bxhi = static_cast<float>(bx) + 7.5f;
-        const float bylo = static_cast<float>(by) + 0.5f, byhi = static_cast<float>(by) + 7.5f;
+        const float bylo = static_cast<float>(by) + 0.5f, byhi = static_cast<float>(by + 4 * PPT - 1) + 0.5f;
         const float thr = a.floor_positive ? a.alpha_floor : 0.0f;
         const float clamp = a.alpha_clamp;
         // a pixel outside the image is parked with T = -1: never accepts, never written
-        if (!in0) T0 = -1.0f;
-        if (!in1) T1 = -1.0f;
+#pragma unroll
+        for (int k = 0; k < PPT; ++k)
+            if (!in[k]) T[k] = -1.0f;
 
         for (int base = 0; base < n; base += kStage) {
             const int cnt = (n - base) < kStage ? (n - base) : kStage;
@@ -518,41 +539,50 @@ __global__ void __launch_bounds__(128, HOLO_COMP2_MINB) k_composite2(CompositeAr
                         nh += __popc(m);
                     }
                     __syncwarp();
-                    for (int k = 0; k < nh; ++k) {
-                        const int off = hits[k];
+                    for (int kh = 0; kh < nh; ++kh) {
+                        const int off = hits[kh];
                         const Staged* e = reinterpret_cast<const Staged*>(recs + off);
                         const float4 A = e->a, B = e->b;
-                        // eval_alpha for both pixels: d = centre - mu (dx shared), then
+                        // eval_alpha per pixel: d = centre - mu (dx shared), then
                         // t = fma(cb, dy, ca dx), u = fma(dx, t, log2 alpha),
                         // q = fma(cc dy, dy, u), a = min(2^q, clamp)
                         const float dx = fx - A.x;
-                        const unsigned long long dy = f32x2::sub(fy01, f32x2::pack(A.y, A.y));
                         const float cadx = A.z * dx;
-                        const unsigned long long t = f32x2::fma(f32x2::pack(A.w, A.w), dy, f32x2::pack(cadx, cadx));
-                        const unsigned long long u = f32x2::fma(f32x2::pack(dx, dx), t, f32x2::pack(B.y, B.y));
-                        const unsigned long long ccdy = f32x2::mul(f32x2::pack(B.x, B.x), dy);
-                        const cx<float> qq = f32x2::unpack(f32x2::fma(ccdy, dy, u));
-                        const float al0 = fminf(ex2_approx(qq.x), clamp);
-                        const float al1 = fminf(ex2_approx(qq.y), clamp);
-                        const bool a0 = (al0 > thr) && (T0 >= eps);
-                        const bool a1 = (al1 > thr) && (T1 >= eps);
-                        const cx<float> wt = f32x2::unpack(f32x2::mul(f32x2::pack(al0, al1), f32x2::pack(T0, T1)));
-                        const float w0 = a0 ? wt.x : 0.0f, w1 = a1 ? wt.y : 0.0f;
-                        blend<C>(e, B, w0, acc0);
-                        blend<C>(e, B, w1, acc1);
-                        const cx<float> Tn = f32x2::unpack(f32x2::sub(f32x2::pack(T0, T1), f32x2::pack(w0, w1)));
-                        T0 = Tn.x;
-                        T1 = Tn.y;
-                        if constexpr (AUX) {
-                            const int ei = base + off / static_cast<int>(sizeof(Staged));
-                            contrib0 += a0 ? 1 : 0;
-                            contrib1 += a1 ? 1 : 0;
-                            elast0 = a0 ? ei : elast0;
-                            elast1 = a1 ? ei : elast1;
+                        const unsigned long long my2 = f32x2::pack(A.y, A.y), cb2 = f32x2::pack(A.w, A.w);
+                        const unsigned long long cadx2 = f32x2::pack(cadx, cadx), dx2 = f32x2::pack(dx, dx);
+                        const unsigned long long la2 = f32x2::pack(B.y, B.y), cc2 = f32x2::pack(B.x, B.x);
+                        const int ei = base + off / static_cast<int>(sizeof(Staged));
+#pragma unroll
+                        for (int j = 0; j < PPT / 2; ++j) {
+                            const unsigned long long dy = f32x2::sub(fy2[j], my2);
+                            const unsigned long long t = f32x2::fma(cb2, dy, cadx2);
+                            const unsigned long long u = f32x2::fma(dx2, t, la2);
+                            const cx<float> qq = f32x2::unpack(f32x2::fma(f32x2::mul(cc2, dy), dy, u));
+                            const float al0 = fminf(ex2_approx(qq.x), clamp);
+                            const float al1 = fminf(ex2_approx(qq.y), clamp);
+                            float& Ta = T[2 * j];
+                            float& Tb = T[2 * j + 1];
+                            const bool a0 = (al0 > thr) && (Ta >= eps);
+                            const bool a1 = (al1 > thr) && (Tb >= eps);
+                            const cx<float> wt = f32x2::unpack(f32x2::mul(f32x2::pack(al0, al1), f32x2::pack(Ta, Tb)));
+                            const float w0 = a0 ? wt.x : 0.0f, w1 = a1 ? wt.y : 0.0f;
+                            blend<C>(e, B, w0, acc[2 * j]);
+                            blend<C>(e, B, w1, acc[2 * j + 1]);
+                            const cx<float> Tn = f32x2::unpack(f32x2::sub(f32x2::pack(Ta, Tb), f32x2::pack(w0, w1)));
+                            Ta = Tn.x;
+                            Tb = Tn.y;
+                            if constexpr (AUX) {
+                                contrib[2 * j] += a0 ? 1 : 0;
+                                contrib[2 * j + 1] += a1 ? 1 : 0;
+                                elast[2 * j] = a0 ? ei : elast[2 * j];
+                                elast[2 * j + 1] = a1 ? ei : elast[2 * j + 1];
+                            }
                         }
                     }
                     __syncwarp();
-                    done = !(T0 >= eps) && !(T1 >= eps);
+                    done = true;
+#pragma unroll
+                    for (int k = 0; k < PPT; ++k) done = done && !(T[k] >= eps);
                     if (__all_sync(0xffffffffu, done)) break;
                 }
             }
@@ -563,16 +593,15 @@ __global__ void __launch_bounds__(128, HOLO_COMP2_MINB) k_composite2(CompositeAr
 
     const size_t P = static_cast<size_t>(a.W) * a.H;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        if (!(h ? in1 : in0)) continue;
-        const size_t pix = static_cast<size_t>(py + 4 * h) * a.W + px;
+    for (int k = 0; k < PPT; ++k) {
+        if (!in[k]) continue;
+        const size_t pix = static_cast<size_t>(py + 4 * k) * a.W + px;
 #pragma unroll
-        for (int c = 0; c < C; ++c)
-            a.layers[(static_cast<size_t>(lplane) * C + c) * P + pix] = h ? acc1[c] : acc0[c];
-        if (a.t_final) a.t_final[static_cast<size_t>(lplane) * P + pix] = h ? T1 : T0;
+        for (int c = 0; c < C; ++c) a.layers[(static_cast<size_t>(lplane) * C + c) * P + pix] = acc[k][c];
+        if (a.t_final) a.t_final[static_cast<size_t>(lplane) * P + pix] = T[k];
         if constexpr (AUX) {
-            a.n_contrib[static_cast<size_t>(lplane) * P + pix] = h ? contrib1 : contrib0;
-            if (a.e_last) a.e_last[static_cast<size_t>(lplane) * P + pix] = h ? elast1 : elast0;
+            a.n_contrib[static_cast<size_t>(lplane) * P + pix] = contrib[k];
+            if (a.e_last) a.e_last[static_cast<size_t>(lplane) * P + pix] = elast[k];
         }
     }
 }
@@ -593,9 +622,9 @@ void launch_tile(holo_ctx* ctx, const CompositeArgs& a) {
     if constexpr (TILE == 16) {
         if (HOLO_COMP2) {
             switch (a.C) {
-#define HC_COMP2(CC)                                                                     \
-    (a.n_contrib ? k_composite2<CC, true><<<grid, 128, 0, ctx->stream>>>(a)             \
-                 : k_composite2<CC, false><<<grid, 128, 0, ctx->stream>>>(a))
+#define HC_COMP2(CC)                                                                                          \
+    (a.n_contrib ? k_composite2<CC, true, HOLO_COMP_PPT><<<grid, 256 / HOLO_COMP_PPT, 0, ctx->stream>>>(a)      \
+                 : k_composite2<CC, false, HOLO_COMP_PPT><<<grid, 256 / HOLO_COMP_PPT, 0, ctx->stream>>>(a))
                 case 1: HC_COMP2(1); break;
                 case 2: HC_COMP2(2); break;
                 case 3: HC_COMP2(3); break;
