@@ -349,10 +349,8 @@ FrameGeom check_render(holo_ctx* ctx, const holo_camera& cam, const holo_wave& w
 }
 
 // raster stage for planes [pb, pe): preprocess, binning, composite -> "layers"
-// strip: composite the layers in the column-strip layout (kStripW; the static
-// propagation path's input) instead of the planar [planes][C][H][W]
 void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, const holo_raster_settings& st,
-                   const FrameGeom& g, int pb, int pe, unsigned outputs, holo_frame_info* info, bool strip = false) {
+                   const FrameGeom& g, int pb, int pe, unsigned outputs, holo_frame_info* info) {
     const size_t N = ctx->n;
     const int L = g.L;
     const int nplanes = pe - pb;
@@ -466,7 +464,6 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     ca.alpha_floor = static_cast<float>(st.alpha_floor);
     ca.alpha_clamp = float_not_above(st.alpha_clamp);
     ca.floor_positive = st.alpha_floor > 0.0 ? 1 : 0;
-    ca.strip = strip ? 1 : 0;
     ca.layers = buf<cx<float>>(ctx, "layers", static_cast<size_t>(nplanes) * g.C * g.P);
     ca.t_final = want_aux ? buf<float>(ctx, "t_final", static_cast<size_t>(nplanes) * g.P) : nullptr;
     ca.n_contrib = want_aux ? buf<int>(ctx, "n_contrib", static_cast<size_t>(nplanes) * g.P) : nullptr;
@@ -980,14 +977,11 @@ void render_front(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, 
     ctx->f_plane_end = pe;
     ctx->f_cam = cam;
     ctx->f_st = st;
+    raster_planes(ctx, cam, wave, st, g, pb, pe, outputs, info);
+    if (po.pad2x) return;  // holo_render runs the padded operators on the spatial layers
     const int np = pe - pb;
     const std::vector<int> plane_of = output_planes(outputs, np);
-    const bool propagate = !po.pad2x && !(full && plane_of.empty());
-    // the static path composites straight into the column-strip layout unless the
-    // planar layers are an output
-    const bool strip = propagate && static_render_supported(g.W, g.H) && !(outputs & HOLO_OUT_LAYERS);
-    raster_planes(ctx, cam, wave, st, g, pb, pe, outputs, info, strip);
-    if (!propagate) return;  // pad2x: holo_render runs the padded operators on the spatial layers
+    if (full && plane_of.empty()) return;
     cx<float>* spec = (!full && spectrum_out) ? static_cast<cx<float>*>(spectrum_out)
                                               : buf<cx<float>>(ctx, "spectrum", static_cast<size_t>(g.C) * g.P);
     if (np == 0) {
@@ -1001,11 +995,13 @@ void render_front(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, 
     cx<float>* layers = static_cast<cx<float>*>(ctx->buffer("layers", 1));
     const size_t nlay = static_cast<size_t>(np) * g.C * g.P;
     if (static_render_supported(g.W, g.H)) {
-        // column FFT into the strip layout: in place, or from the planar layers
-        // (kept as an output) into a separate stack
-        cx<float>* work = strip ? layers : buf<cx<float>>(ctx, "colwork", nlay);
+        cx<float>* work = layers;
+        if (outputs & HOLO_OUT_LAYERS) {  // keep the spatial layers: transform a copy
+            work = buf<cx<float>>(ctx, "colwork", nlay);
+            HC_CUDA(cudaMemcpyAsync(work, layers, sizeof(cx<float>) * nlay, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
         ctx->stage_begin();
-        static_col_fwd(ctx, layers, work, g.W, g.H, np * g.C, strip);
+        static_col_fwd(ctx, work, g.W, g.H, np * g.C);
         ctx->stage_end(3);
         if (!full) {
             ctx->stage_begin();
@@ -1167,9 +1163,8 @@ void adjoint_propagation(holo_ctx* ctx, const holo_wave& wave, const holo_prop_o
     const int O = L + 1;  // the hologram, then every plane
     cx<float>* stage = buf<cx<float>>(ctx, "bwd_stage", static_cast<size_t>(O) * C * P);
     if (static_render_supported(W, H)) {
-        cx<float>* gs = buf<cx<float>>(ctx, "bwd_colwork", static_cast<size_t>(L) * C * P);  // strip layout
-        static_col_fwd(ctx, gv, gs, W, H, L * C, false);
-        static_row(ctx, kModeFull, gs, nullptr, stage, W, H, C, L, 1, L, tfc, wave.pitch,
+        static_col_fwd(ctx, gv, W, H, L * C);
+        static_row(ctx, kModeFull, gv, nullptr, stage, W, H, C, L, 1, L, tfc, wave.pitch,
                    tf_direct(z, po.local_band_limit));
         static_col_inv(ctx, stage, W, H, C, O, 1, gholo, glayers, nullptr);
         return;
@@ -1275,9 +1270,8 @@ void shard_front(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, c
     ctx->f_plane_end = pe;
     ctx->f_cam = cam;
     ctx->f_st = st;
+    raster_planes(ctx, cam, wave, st, g, pb, pe, outputs, info);
     const int np = pe - pb;
-    const bool strip = static_render_supported(g.W, g.H) && !(outputs & HOLO_OUT_LAYERS);
-    raster_planes(ctx, cam, wave, st, g, pb, pe, outputs, info, strip);
     auto all_ready = [&] {
         HC_CUDA(cudaEventRecord(ctx->ev_chan_ready[0], ctx->stream));
         for (int c = 1; c < g.C; ++c) HC_CUDA(cudaEventRecord(ctx->ev_chan_ready[c], ctx->stream));
@@ -1293,9 +1287,13 @@ void shard_front(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave, c
     cx<float>* layers = static_cast<cx<float>*>(ctx->buffer("layers", 1));
     const size_t nlay = static_cast<size_t>(np) * g.C * g.P;
     if (static_render_supported(g.W, g.H)) {
-        cx<float>* work = strip ? layers : buf<cx<float>>(ctx, "colwork", nlay);
+        cx<float>* work = layers;
+        if (outputs & HOLO_OUT_LAYERS) {
+            work = buf<cx<float>>(ctx, "colwork", nlay);
+            HC_CUDA(cudaMemcpyAsync(work, layers, sizeof(cx<float>) * nlay, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
         ctx->stage_begin();
-        static_col_fwd(ctx, layers, work, g.W, g.H, np * g.C, strip);
+        static_col_fwd(ctx, work, g.W, g.H, np * g.C);
         ctx->stage_end(3);
         for (int c = 0; c < g.C; ++c) {
             ctx->stage_begin();

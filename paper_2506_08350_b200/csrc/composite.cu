@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
         const size_t pix = static_cast<size_t>(py) * a.W + px;
 #pragma unroll
         for (int c = 0; c < C; ++c)
-            a.layers[(static_cast<size_t>(lplane) * C + c) * P + (a.strip ? strip_at(a.W, a.H, py, px) : pix)] = acc[c];
+            a.layers[(static_cast<size_t>(lplane) * C + c) * P + pix] = acc[c];
         if (a.t_final) a.t_final[static_cast<size_t>(lplane) * P + pix] = T;
         if constexpr (AUX) {
             a.n_contrib[static_cast<size_t>(lplane) * P + pix] = contrib;
@@ -596,9 +596,8 @@ __global__ void __launch_bounds__(256 / PPT, PPT == 2 ? HOLO_COMP2_MINB : HOLO_C
     for (int k = 0; k < PPT; ++k) {
         if (!in[k]) continue;
         const size_t pix = static_cast<size_t>(py + 4 * k) * a.W + px;
-        const size_t at = a.strip ? strip_at(a.W, a.H, py + 4 * k, px) : pix;
 #pragma unroll
-        for (int c = 0; c < C; ++c) a.layers[(static_cast<size_t>(lplane) * C + c) * P + at] = acc[k][c];
+        for (int c = 0; c < C; ++c) a.layers[(static_cast<size_t>(lplane) * C + c) * P + pix] = acc[k][c];
         if (a.t_final) a.t_final[static_cast<size_t>(lplane) * P + pix] = T[k];
         if constexpr (AUX) {
             a.n_contrib[static_cast<size_t>(lplane) * P + pix] = contrib[k];

@@ -154,12 +154,7 @@ size_t scene_keep_planes(holo_ctx* ctx, const double* const src[7], double* cons
 // ---- render_static.cu (compile-time FFT plans for the common grid sizes)
 enum { kModeFull = 0, kModeSpec = 1, kModeReplay = 2 };
 bool static_render_supported(int W, int H);
-// column FFT of nfields H x W fields from in (strip layout if in_strip, else planar)
-// into out (strip layout); in == out is allowed for a strip input
-void static_col_fwd(holo_ctx* ctx, const cx<float>* in, cx<float>* out, int W, int H, int nfields, bool in_strip);
-// The row pass reads the column-transformed planes (FULL / SPEC) and writes its
-// outputs (FULL / REPLAY) in the strip layout; the spectrum (SPEC / REPLAY) is
-// planar.  The column IFFT reads the strip layout and writes planar outputs.
+void static_col_fwd(holo_ctx* ctx, cx<float>* data, int W, int H, int nfields);
 // [c0, c0 + nc) restricts a launch to those channels (nc < 0: through C - 1)
 void static_col_inv(holo_ctx* ctx, const cx<float>* in, int W, int H, int C, int nout, int has_holo,
                     cx<float>* holo, cx<float>* rep, float* intens, int c0 = 0, int nc = -1);
@@ -167,15 +162,6 @@ void static_col_inv(holo_ctx* ctx, const cx<float>* in, int W, int H, int C, int
 void static_row(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spec, cx<float>* out, int W, int H,
                 int C, int Lloc, int has_holo, int nrep, const TfChan* tfc, double pitch, bool local, int c0 = 0,
                 int nc = -1);
-
-// Column-strip layout of a field stack (the render path's intermediates between
-// compositing, the column passes and the row pass): each H x W field is stored as
-// [W / kStripW][H][kStripW], so a column pass reads and writes one strip as a
-// contiguous block and a row pair is kStripW * 2 complex (128 B) per strip.
-constexpr int kStripW = 8;
-__host__ __device__ __forceinline__ size_t strip_at(int W, int H, int y, int x) {
-    return (static_cast<size_t>(x / kStripW) * H + y) * kStripW + (x % kStripW);
-}
 
 // ---- composite.cu
 struct CompositeArgs {
@@ -189,7 +175,6 @@ struct CompositeArgs {
     unsigned capacity;        // entry-buffer size: bucket ranges are clamped to it (overflowed async frames)
     float term_eps, alpha_floor, alpha_clamp;
     int floor_positive;
-    int strip;                // layers in the column-strip layout (kStripW) instead of planar
     cx<float>* layers;        // [planes][C][H][W], plane relative to plane_begin
     float* t_final;           // optional [planes][H][W]
     int* n_contrib;           // optional

@@ -130,28 +130,61 @@ __device__ __forceinline__ cx<float> phasor_reduced(float theta) {
 
 // ---------------------------------------------------------------- 1. column FFT (forward, in place)
 
-// One strip of kStripW columns per CTA, read from the strip layout (a contiguous
-// block; in place) or from planar fields, written to the strip layout.
-template <class Cfg, bool IN_STRIP>
-__global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_col_fwd(const cx<float>* in, cx<float>* out, int W,
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_col_fwd(cx<float>* __restrict__ data, int W,
                                                                       const cx<float>* __restrict__ tw) {
     constexpr int H = Cfg::H;
-    static_assert(Cfg::NB == kStripW, "column strips are the strip layout's");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<float>* sm = reinterpret_cast<cx<float>*>(smem_raw);
     const int x0 = blockIdx.x * Cfg::NB;
-    const size_t field = static_cast<size_t>(blockIdx.y) * H * W;
-    const size_t strip = field + static_cast<size_t>(blockIdx.x) * H * kStripW;
+    cx<float>* base = data + static_cast<size_t>(blockIdx.y) * H * W;
     auto load = [&](int, int, int b, int i) -> cx<float> {
-        if constexpr (IN_STRIP) return in[strip + static_cast<size_t>(i) * kStripW + b];
         const int x = x0 + b;
-        return x < W ? in[field + static_cast<size_t>(i) * W + x] : czf();
+        return x < W ? base[static_cast<size_t>(i) * W + x] : czf();
     };
-    auto store = [&](int, int, int b, int i, cx<float> v) { out[strip + static_cast<size_t>(i) * kStripW + b] = v; };
+    auto store = [&](int, int, int b, int i, cx<float> v) {
+        const int x = x0 + b;
+        if (x < W) base[static_cast<size_t>(i) * W + x] = v;
+    };
     fft_static<float, -1, typename Cfg::B, typename PlanOf<H>::type>(sm, col_twiddles<Cfg>(sm, tw), load, store);
 }
 
 // ---------------------------------------------------------------- 2. row pass with the spectrum in registers
+
+// Bulk (TMA) copies global -> shared completing on an mbarrier.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
 
 // Row-pass shared memory: FFT work area; the prefetch buffer for the next plane's
 // NBR rows (each row padded by 8 complex = 16 banks; FULL / SPEC); the twiddle
@@ -199,38 +232,42 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
     const cx<float>* s_tw = HOLO_ROW_SMEM_TW ? reinterpret_cast<cx<float>*>(smem_raw + SM::kWork + SM::kPre) : tw;
     unsigned char* s_slot = smem_raw + SM::kWork + SM::kPre + SM::kTw;
     float2* s_tf = reinterpret_cast<float2*>(smem_raw + SM::kTf);  // (phase0, 2 pi z) per plane
+    __shared__ unsigned long long s_bar;
 
     // row = c * H + y; a CTA never spans two channels.  row_base = c0 * H restricts a
     // launch to the channels [c0, c0 + gridDim.x * NBR / H) (per-channel pipelines
     // of a plane-sharded frame).
     const int row0 = row_base + blockIdx.x * NBR;
     const int c = row0 / H;
+    const size_t plane_stride = static_cast<size_t>(C) * H * W;
     const int nplanes = MODE == kModeReplay ? nrep : Lloc;
     for (int l = threadIdx.x; l < nplanes; l += Cfg::NT) s_tf[l] = make_float2(tfc[l * C + c].phase0, tfc[l * C + c].two_pi_z_f);
     if constexpr (HOLO_ROW_SMEM_TW)
         for (int k = threadIdx.x; k < W; k += Cfg::NT) const_cast<cx<float>*>(s_tw)[k] = tw[k];
 
-    // the rows' position in the strip layout: row y of strip s of a field starts at
-    // (s H + y) kStripW, and the NBR rows of this CTA are one NBR * kStripW block
-    const int y0 = row0 - c * H;
-    // prefetch of plane l's NBR rows: 16-byte cp.async pieces, a warp covering four
-    // strips' 128-byte row blocks per instruction (the buffer is free once every
-    // thread has finished the previous plane's first FFT stage)
+    // prefetch of plane l's NBR rows (one thread issues; the buffer is free once
+    // every thread has finished the previous plane's first FFT stage)
     auto issue = [&](int l) {
-        const cx<float>* src = layers + (static_cast<size_t>(l) * C + c) * H * W + static_cast<size_t>(y0) * kStripW;
-        constexpr int kPer = NBR * kStripW / 2;  // 16-byte pieces per strip block
-        for (int k = threadIdx.x; k < NBR * W / 2; k += Cfg::NT) {
-            const int st = k / kPer, p = k % kPer, b = p / (kStripW / 2), x = st * kStripW + (p % (kStripW / 2)) * 2;
-            cp_async16(pre + b * SM::kRowPad + x, src + static_cast<size_t>(st) * H * kStripW + 2 * p);
-        }
-        cp_async_commit();
+        const cx<float>* src = layers + l * plane_stride + static_cast<size_t>(row0) * W;
+        fence_proxy_async_smem();  // the buffer's previous generic reads precede the async writes
+        mbar_expect_tx(&s_bar, NBR * W * static_cast<unsigned>(sizeof(cx<float>)));
+#pragma unroll
+        for (int b = 0; b < NBR; ++b)
+            bulk_g2s(pre + b * SM::kRowPad, src + static_cast<size_t>(b) * W,
+                     W * static_cast<unsigned>(sizeof(cx<float>)), &s_bar);
     };
     // forward planes in the order the sum needs them: Horner runs from the last plane
     auto fwd_plane = [&](int it) { return DIRECT ? it : Lloc - 1 - it; };
     if constexpr (MODE != kModeReplay) {
-        if (Lloc > 0) issue(fwd_plane(0));
+        if (threadIdx.x == 0) {
+            mbar_init(&s_bar, 1);
+            mbar_init_fence();
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && Lloc > 0) issue(fwd_plane(0));
+    } else {
+        __syncthreads();
     }
-    __syncthreads();
 
     // (q, r) <-> (b, i) of the last forward stage = first inverse stage
     auto owner = [&](int q, int r, int& b, int& i) -> bool {
@@ -310,8 +347,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
     if constexpr (MODE != kModeReplay) {
         for (int it = 0; it < Lloc; ++it) {
             const int l = fwd_plane(it);
-            cp_async_wait<0>();
-            __syncthreads();  // every thread's pieces of plane l have landed
+            mbar_wait(&s_bar, it & 1);
             auto load = [&](int, int, int b, int i) -> cx<float> { return pre[b * SM::kRowPad + i]; };
             auto store = [&](int q, int r, int b, int i, cx<float> v) {
                 if constexpr (DIRECT)
@@ -321,7 +357,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
             };
             // once the first stage has read the buffer, start loading the next plane
             auto hook = [&] {
-                if (it + 1 < Lloc) issue(fwd_plane(it + 1));
+                if (threadIdx.x == 0 && it + 1 < Lloc) issue(fwd_plane(it + 1));
             };
             fft_static<float, -1, B, P>(sm, s_tw, load, store, hook);
         }
@@ -353,19 +389,16 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
             }
         band_mask();
     }
-    // outputs: [hologram] then planes 0..nrep-1 (output_planes in capi.cu), each in
-    // the strip layout for the column IFFT
-    auto out_field = [&](int o) { return out + (static_cast<size_t>(o) * C + c) * H * W + static_cast<size_t>(y0) * kStripW; };
-    auto out_at = [&](int b, int i) { return (static_cast<size_t>(i / kStripW) * H + b) * kStripW + i % kStripW; };
+    // outputs: [hologram] then planes 0..nrep-1 (output_planes in capi.cu)
     if (has_holo) {
-        cx<float>* dst = out_field(0);
+        cx<float>* dst = out + static_cast<size_t>(row0) * W;
         const bool plain = DIRECT || (MODE == kModeReplay && nrep == 0);  // S itself
         auto load = [&](int q, int r, int, int) -> cx<float> { return plain ? S[q][r] : S[q][r] * a_at(q, r); };
-        auto store = [&](int, int, int b, int i, cx<float> v) { dst[out_at(b, i)] = v; };
+        auto store = [&](int, int, int b, int i, cx<float> v) { dst[static_cast<size_t>(b) * W + i] = v; };
         fft_static<float, +1, B, Pinv>(sm, s_tw, load, store);
     }
     for (int l = 0; l < nrep; ++l) {
-        cx<float>* dst = out_field(l + has_holo);
+        cx<float>* dst = out + (static_cast<size_t>(l + has_holo) * C * H + row0) * W;
         auto load = [&](int q, int r, int b, int i) -> cx<float> {
             if constexpr (DIRECT) {
                 return S[q][r] * conj(tf(l, q, r, b, i));
@@ -375,7 +408,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
                 return v;
             }
         };
-        auto store = [&](int, int, int b, int i, cx<float> v) { dst[out_at(b, i)] = v; };
+        auto store = [&](int, int, int b, int i, cx<float> v) { dst[static_cast<size_t>(b) * W + i] = v; };
         fft_static<float, +1, B, Pinv>(sm, s_tw, load, store);
     }
 }
@@ -392,15 +425,16 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_col_inv_epi(const 
     constexpr int H = Cfg::H;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<float>* sm = reinterpret_cast<cx<float>*>(smem_raw);
-    static_assert(Cfg::NB == kStripW, "column strips are the strip layout's");
     const int x0 = blockIdx.x * Cfg::NB;
     const int c = c_base + blockIdx.y, o = blockIdx.z;
     const size_t P = static_cast<size_t>(H) * W;
-    // the row pass's outputs, strip layout: this CTA's strip is one contiguous block
-    const cx<float>* src = in + (static_cast<size_t>(o) * C + c) * P + static_cast<size_t>(blockIdx.x) * H * kStripW;
+    const cx<float>* src = in + (static_cast<size_t>(o) * C + c) * P;
     const bool is_holo = has_holo && o == 0;
     const size_t obase = is_holo ? static_cast<size_t>(c) * P : (static_cast<size_t>(o - has_holo) * C + c) * P;
-    auto load = [&](int, int, int b, int i) -> cx<float> { return src[static_cast<size_t>(i) * kStripW + b]; };
+    auto load = [&](int, int, int b, int i) -> cx<float> {
+        const int x = x0 + b;
+        return x < W ? src[static_cast<size_t>(i) * W + x] : czf();
+    };
     auto store = [&](int, int, int b, int i, cx<float> v) {
         const int x = x0 + b;
         if (x >= W) return;
@@ -424,15 +458,10 @@ void smem_attr(K kernel, size_t bytes) {
 }
 
 template <class Cfg>
-void launch_col_fwd_cfg(holo_ctx* ctx, const cx<float>* in, cx<float>* out, int W, int nfields, bool in_strip) {
+void launch_col_fwd_cfg(holo_ctx* ctx, cx<float>* data, int W, int nfields) {
+    smem_attr(k_col_fwd<Cfg>, Cfg::kSmem);
     const dim3 grid((W + Cfg::NB - 1) / Cfg::NB, nfields);
-    if (in_strip) {
-        smem_attr(k_col_fwd<Cfg, true>, Cfg::kSmem);
-        k_col_fwd<Cfg, true><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(in, out, W, ctx->twiddle<float>(Cfg::H));
-    } else {
-        smem_attr(k_col_fwd<Cfg, false>, Cfg::kSmem);
-        k_col_fwd<Cfg, false><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(in, out, W, ctx->twiddle<float>(Cfg::H));
-    }
+    k_col_fwd<Cfg><<<grid, Cfg::NT, Cfg::kSmem, ctx->stream>>>(data, W, ctx->twiddle<float>(Cfg::H));
     HC_LAUNCHED(ctx);
 }
 
@@ -476,8 +505,8 @@ void launch_row_cfg(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>*
 }
 
 template <int H>
-void launch_col_fwd(holo_ctx* ctx, const cx<float>* in, cx<float>* out, int W, int nfields, bool in_strip) {
-    launch_col_fwd_cfg<ColCfg<H>>(ctx, in, out, W, nfields, in_strip);
+void launch_col_fwd(holo_ctx* ctx, cx<float>* data, int W, int nfields) {
+    launch_col_fwd_cfg<ColCfg<H>>(ctx, data, W, nfields);
 }
 
 template <int H>
@@ -521,14 +550,14 @@ int row_nbr(int W) {
 }  // namespace
 
 bool static_render_supported(int W, int H) {
-    return size_listed(W) && size_listed(H) && H % row_nbr(W) == 0 && W % kStripW == 0;
+    return size_listed(W) && size_listed(H) && H % row_nbr(W) == 0;
 }
 
-void static_col_fwd(holo_ctx* ctx, const cx<float>* in, cx<float>* out, int W, int H, int nfields, bool in_strip) {
+void static_col_fwd(holo_ctx* ctx, cx<float>* data, int W, int H, int nfields) {
     if (nfields <= 0) return;
-#define HC_CASE(N)                                                 \
-    case N:                                                        \
-        launch_col_fwd<N>(ctx, in, out, W, nfields, in_strip);     \
+#define HC_CASE(N)                                    \
+    case N:                                           \
+        launch_col_fwd<N>(ctx, data, W, nfields);     \
         return;
     switch (H) {
         HC_SIZES(HC_CASE)
