@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <omp.h>
 
 #include "holo/camera.hpp"
 #include "holo/device.hpp"
@@ -74,12 +75,105 @@ struct DevMem {
     DevMem& operator=(const DevMem&) = delete;
 };
 
-void h2d(void* d, const void* h, size_t n) {
-    cuda_check(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, stream()), "cudaMemcpyAsync H2D");
+// The value-semantics API moves large host arrays in and out every call.  Large
+// transfers go through a pinned staging pair per thread (pageable cudaMemcpy runs
+// at a fraction of PCIe bandwidth), and the host-side copy between the staging
+// buffer and the caller's memory -- including the first-touch page faults of a
+// freshly allocated result -- runs on all cores, overlapped with the next chunk's
+// DMA.
+struct Staging {
+    static constexpr size_t kChunk = size_t{32} << 20;
+    unsigned char* buf[2] = {};
+    cudaEvent_t ev[2] = {};
+    Staging() {
+        for (int k = 0; k < 2; ++k) {
+            cuda_check(cudaMallocHost(reinterpret_cast<void**>(&buf[k]), kChunk), "cudaMallocHost");
+            cuda_check(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming), "cudaEventCreate");
+        }
+    }
+    ~Staging() {
+        for (int k = 0; k < 2; ++k) {
+            if (ev[k]) cudaEventSynchronize(ev[k]), cudaEventDestroy(ev[k]);
+            if (buf[k]) cudaFreeHost(buf[k]);
+        }
+    }
+};
+Staging& staging() {
+    thread_local Staging s;
+    return s;
 }
+constexpr size_t kStagedMin = size_t{4} << 20;
+
+void par_copy(void* dst, const void* src, size_t n) {
+    constexpr size_t kBlk = size_t{1} << 20;
+    const long nb = static_cast<long>((n + kBlk - 1) / kBlk);
+#pragma omp parallel for schedule(static)
+    for (long i = 0; i < nb; ++i) {
+        const size_t o = static_cast<size_t>(i) * kBlk;
+        std::memcpy(static_cast<unsigned char*>(dst) + o, static_cast<const unsigned char*>(src) + o,
+                    std::min(kBlk, n - o));
+    }
+}
+
+void h2d(void* d, const void* h, size_t n) {
+    if (n < kStagedMin) {
+        cuda_check(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, stream()), "cudaMemcpyAsync H2D");
+        return;
+    }
+    Staging& st = staging();
+    for (size_t off = 0, i = 0; off < n; off += Staging::kChunk, ++i) {
+        const int k = static_cast<int>(i & 1);
+        const size_t len = std::min(Staging::kChunk, n - off);
+        cuda_check(cudaEventSynchronize(st.ev[k]), "cudaEventSynchronize");  // the buffer's last DMA is done
+        par_copy(st.buf[k], static_cast<const unsigned char*>(h) + off, len);
+        cuda_check(cudaMemcpyAsync(static_cast<unsigned char*>(d) + off, st.buf[k], len, cudaMemcpyHostToDevice,
+                                   stream()),
+                   "cudaMemcpyAsync H2D");
+        cuda_check(cudaEventRecord(st.ev[k], stream()), "cudaEventRecord");
+    }
+}
+
 void d2h(void* h, const void* d, size_t n) {
-    cuda_check(cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, stream()), "cudaMemcpyAsync D2H");
-    cuda_check(cudaStreamSynchronize(stream()), "cudaStreamSynchronize");
+    if (n < kStagedMin) {
+        cuda_check(cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, stream()), "cudaMemcpyAsync D2H");
+        cuda_check(cudaStreamSynchronize(stream()), "cudaStreamSynchronize");
+        return;
+    }
+    Staging& st = staging();
+    auto issue = [&](size_t i) {
+        const size_t off = i * Staging::kChunk;
+        const int k = static_cast<int>(i & 1);
+        cuda_check(cudaEventSynchronize(st.ev[k]), "cudaEventSynchronize");
+        cuda_check(cudaMemcpyAsync(st.buf[k], static_cast<const unsigned char*>(d) + off,
+                                   std::min(Staging::kChunk, n - off), cudaMemcpyDeviceToHost, stream()),
+                   "cudaMemcpyAsync D2H");
+        cuda_check(cudaEventRecord(st.ev[k], stream()), "cudaEventRecord");
+    };
+    const size_t chunks = (n + Staging::kChunk - 1) / Staging::kChunk;
+    issue(0);
+    for (size_t i = 0; i < chunks; ++i) {
+        const int k = static_cast<int>(i & 1);
+        cuda_check(cudaEventSynchronize(st.ev[k]), "cudaEventSynchronize");
+        if (i + 1 < chunks) issue(i + 1);  // the other buffer's host copy finished last iteration
+        const size_t off = i * Staging::kChunk;
+        par_copy(static_cast<unsigned char*>(h) + off, st.buf[k], std::min(Staging::kChunk, n - off));
+    }
+}
+
+// complex64 device samples -> complex<double> host samples, in staged chunks
+void d2h_widen(c64* h, const void* d, size_t n) {
+    Staging& st = staging();
+    constexpr size_t kPer = Staging::kChunk / sizeof(std::complex<float>);
+    for (size_t off = 0; off < n; off += kPer) {
+        const size_t len = std::min(kPer, n - off);
+        cuda_check(cudaMemcpyAsync(st.buf[0], static_cast<const std::complex<float>*>(d) + off,
+                                   len * sizeof(std::complex<float>), cudaMemcpyDeviceToHost, stream()),
+                   "cudaMemcpyAsync D2H");
+        cuda_check(cudaStreamSynchronize(stream()), "cudaStreamSynchronize");
+        const auto* src = reinterpret_cast<const std::complex<float>*>(st.buf[0]);
+#pragma omp parallel for schedule(static)
+        for (long i = 0; i < static_cast<long>(len); ++i) h[off + i] = c64(src[i].real(), src[i].imag());
+    }
 }
 
 holo_wave to_c(const WaveConfig& w) {
@@ -461,6 +555,46 @@ holo_scene_arrays scene_arrays(const GaussianScene& s) {
             s.plane_logits.data()};
 }
 
+// Upload a scene through a persistent pinned copy (the context's copy-in stream
+// then runs at full PCIe bandwidth, asynchronously); the copy is reused once the
+// previous upload from it has completed.
+void upload_scene(const GaussianScene& s) {
+    struct Pinned {
+        double* p = nullptr;
+        size_t cap = 0;
+        ~Pinned() {
+            if (p) cudaFreeHost(p);
+        }
+    };
+    thread_local Pinned pin;
+    const std::vector<double>* arr[7] = {&s.positions, &s.rotations, &s.log_scales, &s.amplitudes,
+                                         &s.opacity_logits, &s.phases, &s.plane_logits};
+    size_t total = 0;
+    for (auto* a : arr) total += a->size();
+    if (total * sizeof(double) < kStagedMin) {
+        const holo_scene_arrays sa = scene_arrays(s);
+        check(holo_scene_upload(ctx(), &sa));
+        return;
+    }
+    cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(holo_ctx_get_copy_stream(ctx(), 0))),
+               "cudaStreamSynchronize");  // the last upload from the pinned copy is done
+    if (pin.cap < total) {
+        if (pin.p) cudaFreeHost(pin.p);
+        pin.p = nullptr;
+        cuda_check(cudaMallocHost(reinterpret_cast<void**>(&pin.p), total * sizeof(double)), "cudaMallocHost");
+        pin.cap = total;
+    }
+    const double* at[7];
+    size_t o = 0;
+    for (int k = 0; k < 7; ++k) {
+        par_copy(pin.p + o, arr[k]->data(), arr[k]->size() * sizeof(double));
+        at[k] = pin.p + o;
+        o += arr[k]->size();
+    }
+    const holo_scene_arrays sa{s.size(), s.num_planes, at[0], at[1], at[2], at[3], at[4], at[5], at[6]};
+    check(holo_scene_upload(ctx(), &sa));
+}
+
 void check_raster_inputs(const GaussianScene& scene, const CameraView& cam, const WaveConfig& cfg) {
     scene.validate();
     cam.validate();
@@ -505,15 +639,14 @@ detail::Projected to_projected(const holo_projected& q) {
 std::vector<ComplexField> download_layers(const WaveConfig& cfg, int C) {
     const int L = cfg.num_planes, W = cfg.nx, H = cfg.ny;
     const size_t P = static_cast<size_t>(W) * H;
-    const std::vector<std::complex<float>> lay = download_buf<std::complex<float>>(HOLO_BUF_LAYERS);
+    void* d = nullptr;
+    size_t bytes = 0;
+    check(holo_frame_buffer(ctx(), HOLO_BUF_LAYERS, &d, &bytes));
     std::vector<ComplexField> out;
     for (int l = 0; l < L; ++l) {
         ComplexField f(W, H, GaussianScene::kChannels, cfg.pitch);
-        for (int c = 0; c < C; ++c)
-            for (size_t i = 0; i < P; ++i) {
-                const std::complex<float> v = lay[(static_cast<size_t>(l) * C + c) * P + i];
-                f.data[static_cast<size_t>(c) * P + i] = c64(v.real(), v.imag());
-            }
+        d2h_widen(f.data.data(), static_cast<const std::complex<float>*>(d) + static_cast<size_t>(l) * C * P,
+                  static_cast<size_t>(C) * P);
         out.push_back(std::move(f));
     }
     return out;
@@ -558,8 +691,7 @@ constexpr unsigned kRasterOutputs = HOLO_OUT_LAYERS | HOLO_OUT_AUX | HOLO_OUT_LI
 RasterForward raster_forward(const GaussianScene& scene, const CameraView& cam, const WaveConfig& cfg,
                              const RenderSettings& settings) {
     check_raster_inputs(scene, cam, cfg);
-    const holo_scene_arrays sa = scene_arrays(scene);
-    check(holo_scene_upload(ctx(), &sa));
+    upload_scene(scene);
     holo_wave w = to_c(cfg);
     w.channels = GaussianScene::kChannels;  // the rasteriser ignores wavelengths; it emits every scene channel
     for (int c = cfg.channels(); c < w.channels; ++c) w.wavelengths[c] = cfg.wavelengths.back();
@@ -701,8 +833,7 @@ PipelineForward pipeline_forward(const GaussianScene& scene, const CameraView& c
     check_raster_inputs(scene, cam, cfg);
     if (cfg.channels() != GaussianScene::kChannels)  // propagate's channel check (propagation.cpp:94-95)
         throw HoloError("config", "propagate: field does not match the configured grid");
-    const holo_scene_arrays sa = scene_arrays(scene);
-    check(holo_scene_upload(ctx(), &sa));
+    upload_scene(scene);
     const holo_wave w = to_c(cfg);
     const holo_camera c = to_c(cam);
     const holo_raster_settings st = to_c(opt.raster);
@@ -714,16 +845,16 @@ PipelineForward pipeline_forward(const GaussianScene& scene, const CameraView& c
     const int L = cfg.num_planes, C = cfg.channels();
     const size_t n = static_cast<size_t>(cfg.nx) * cfg.ny * C;
     f.raster = collect_raster(scene, cfg, C, info);
-    const std::vector<std::complex<float>> holo = download_buf<std::complex<float>>(HOLO_BUF_HOLOGRAM);
-    const std::vector<std::complex<float>> rep = download_buf<std::complex<float>>(HOLO_BUF_REPLAYED);
+    void* dholo = nullptr;
+    void* drep0 = nullptr;
+    size_t bytes0 = 0;
+    check(holo_frame_buffer(ctx(), HOLO_BUF_HOLOGRAM, &dholo, &bytes0));
+    check(holo_frame_buffer(ctx(), HOLO_BUF_REPLAYED, &drep0, &bytes0));
     f.hologram = ComplexField(cfg.nx, cfg.ny, C, cfg.pitch);
-    for (size_t i = 0; i < n; ++i) f.hologram.data[i] = c64(holo[i].real(), holo[i].imag());
+    d2h_widen(f.hologram.data.data(), dholo, n);
     for (int l = 0; l < L; ++l) {
         ComplexField r(cfg.nx, cfg.ny, C, cfg.pitch);
-        for (size_t i = 0; i < n; ++i) {
-            const std::complex<float> v = rep[static_cast<size_t>(l) * n + i];
-            r.data[i] = c64(v.real(), v.imag());
-        }
+        d2h_widen(r.data.data(), static_cast<const std::complex<float>*>(drep0) + static_cast<size_t>(l) * n, n);
         f.replayed.push_back(std::move(r));
     }
     // intensities = intensity(replayed) of the returned fields, literally as
