@@ -660,12 +660,15 @@ RasterForward collect_raster(const GaussianScene& scene, const WaveConfig& cfg, 
     r.tiles_y = info.tiles_y;
     r.layers = download_layers(cfg, C);
     const std::vector<float> tf = download_buf<float>(HOLO_BUF_T_FINAL);
-    r.t_final.assign(tf.begin(), tf.begin() + static_cast<long>(L * P));
+    r.t_final.resize(L * P);
+#pragma omp parallel for schedule(static)
+    for (long i = 0; i < static_cast<long>(L * P); ++i) r.t_final[i] = tf[i];
     r.n_contrib = download_buf<std::int32_t>(HOLO_BUF_N_CONTRIB);
     r.n_contrib.resize(L * P);
     const std::vector<holo_projected> proj = download_buf<holo_projected>(HOLO_BUF_PROJECTED);
     r.projected.resize(N);
-    for (size_t i = 0; i < N; ++i) r.projected[i] = to_projected(proj[i]);
+#pragma omp parallel for schedule(static)
+    for (long i = 0; i < static_cast<long>(N); ++i) r.projected[i] = to_projected(proj[i]);
     r.rho = download_buf<double>(HOLO_BUF_RHO);
     r.rho.resize(N * L);
     r.touched = download_buf<std::uint8_t>(HOLO_BUF_TOUCHED);
@@ -677,7 +680,8 @@ RasterForward collect_raster(const GaussianScene& scene, const WaveConfig& cfg, 
     std::vector<std::int32_t> gidx = download_buf<std::int32_t>(HOLO_BUF_ENTRY_GIDX);
     std::vector<double> depth = download_buf<double>(HOLO_BUF_ENTRY_DEPTH);
     r.entries.resize(E);
-    for (size_t b = 0; b < B; ++b)
+#pragma omp parallel for schedule(dynamic, 256)
+    for (long b = 0; b < static_cast<long>(B); ++b)
         for (std::uint32_t e = r.bucket_start[b]; e < r.bucket_start[b + 1]; ++e)
             r.entries[e] = detail::Entry{static_cast<std::int32_t>(b), gidx[e], depth[e]};
     return r;
