@@ -263,6 +263,10 @@ __device__ __forceinline__ void sort_bucket_cta(const CompositeArgs& a, unsigned
 #ifndef HOLO_COMP2_MINB
 #define HOLO_COMP2_MINB 8
 #endif
+// unroll factor of k_composite2's walk over a chunk's hits (measurement knob)
+#ifndef HOLO_COMP2_UNROLL
+#define HOLO_COMP2_UNROLL 4
+#endif
 // pixels per thread of k_composite2 (2: 128 threads per tile, 4: 64)
 #ifndef HOLO_COMP_PPT
 #define HOLO_COMP_PPT 2
@@ -442,6 +446,7 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? HOLO_COMP_MINB : 1) 
 template <int C, bool AUX, int PPT>
 __global__ void __launch_bounds__(256 / PPT, PPT == 2 ? HOLO_COMP2_MINB : HOLO_COMP4_MINB) k_composite2(CompositeArgs a) {
     constexpr int TILE = 16, NT = 256 / PPT;
+    constexpr int kUnroll = HOLO_COMP2_UNROLL;
     constexpr int kStage = 256;
     constexpr int kTest = HOLO_COMP_TEST;
     static_assert(PPT % 2 == 0, "pixels are evaluated in pairs");
@@ -539,6 +544,7 @@ __global__ void __launch_bounds__(256 / PPT, PPT == 2 ? HOLO_COMP2_MINB : HOLO_C
                         nh += __popc(m);
                     }
                     __syncwarp();
+#pragma unroll(kUnroll)
                     for (int kh = 0; kh < nh; ++kh) {
                         const int off = hits[kh];
                         const Staged* e = reinterpret_cast<const Staged*>(recs + off);
