@@ -6,7 +6,7 @@
 //   a = min(alpha * exp(-form / 2) * rho, alpha_clamp), skip unless a > alpha_floor,
 //   acc_c += a T amp_c e^{i phi_c},  T *= 1 - a,  ++n_contrib.
 // Bucket order -- ascending (zc, gidx), rasterizer.cpp:221-224 -- is restored
-// before compositing: buckets of up to kWarpSortCap entries by k_sort_small (one
+// before compositing: buckets of up to kWarpSortCap entries by k_sort_small / k_sort_mid (one
 // warp per bucket, shuffle bitonic), buckets above kSortCap by binning.cu, and the
 // ones in between by the compositing CTA itself in shared memory.
 // Compositing: one CTA per bucket, one thread per pixel.  Records are staged 256
@@ -175,14 +175,28 @@ __global__ void __launch_bounds__(256) k_sort_small(const unsigned* __restrict__
     const int lane = threadIdx.x & 31;
     const unsigned e0 = min(bstart[b], capacity);
     const int n = static_cast<int>(min(bstart[b + 1], capacity) - e0);
-    if (n < 2 || n > kWarpSortCap) return;  // warp-uniform
+    if (n < 2 || n > 128) return;  // warp-uniform
     if (n <= 32) {
         if (!warp_sort_bucket_fast<1>(zkey, egidx, e0, n, lane)) warp_sort_bucket<1>(zkey, egidx, e0, n, lane);
     } else if (n <= 64) {
         if (!warp_sort_bucket_fast<2>(zkey, egidx, e0, n, lane)) warp_sort_bucket<2>(zkey, egidx, e0, n, lane);
-    } else {
+    } else if (n <= 128) {
         if (!warp_sort_bucket_fast<4>(zkey, egidx, e0, n, lane)) warp_sort_bucket<4>(zkey, egidx, e0, n, lane);
     }
+}
+
+// One warp per bucket of 129..kWarpSortCap entries (eight keys per lane): a
+// kernel of its own so the common small buckets keep k_sort_small's registers.
+__global__ void __launch_bounds__(256) k_sort_mid(const unsigned* __restrict__ bstart, long long B, unsigned capacity,
+                                                  const unsigned long long* __restrict__ zkey,
+                                                  int* __restrict__ egidx) {
+    const long long b = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (b >= B) return;
+    const int lane = threadIdx.x & 31;
+    const unsigned e0 = min(bstart[b], capacity);
+    const int n = static_cast<int>(min(bstart[b + 1], capacity) - e0);
+    if (n <= 128 || n > kWarpSortCap) return;  // warp-uniform
+    if (!warp_sort_bucket_fast<8>(zkey, egidx, e0, n, lane)) warp_sort_bucket<8>(zkey, egidx, e0, n, lane);
 }
 
 #ifdef HOLO_COUNT
@@ -663,6 +677,8 @@ void sort_small_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsi
                         const unsigned long long* zkey, int* egidx) {
     if (B <= 0) return;
     k_sort_small<<<static_cast<unsigned>((B + 7) / 8), 256, 0, ctx->stream>>>(bstart, B, capacity, zkey, egidx);
+    HC_LAUNCHED(ctx);
+    k_sort_mid<<<static_cast<unsigned>((B + 7) / 8), 256, 0, ctx->stream>>>(bstart, B, capacity, zkey, egidx);
     HC_LAUNCHED(ctx);
 }
 

@@ -124,7 +124,7 @@ void preprocess(holo_ctx* ctx, const CameraConsts& cc, const holo_raster_setting
                 int tiles_x, int tiles_y, const PreOut& out);
 
 constexpr int kSortCap = 1024;     // largest bucket the compositing CTA sorts in shared memory
-constexpr int kWarpSortCap = 128;  // buckets up to this size are sorted one warp each (k_sort_small)
+constexpr int kWarpSortCap = 256;  // buckets up to this size are sorted one warp each (k_sort_small)
 
 // ---- binning.cu
 // out = exclusive scan of in (+ in2 when given), out[n] = total; *d_max = max element

@@ -197,8 +197,12 @@ struct RowSmem {
     static constexpr int kRowPad = Cfg::W + 8;
     static constexpr size_t kWork = sizeof(cx<float>) * FftSmem<typename Cfg::B, typename PlanOf<Cfg::W>::type>::kElems;
     static constexpr size_t kPre = MODE == kModeReplay ? 0 : sizeof(cx<float>) * Cfg::NBR * kRowPad;
-    static constexpr size_t kTw = HOLO_ROW_SMEM_TW ? sizeof(cx<float>) * Cfg::W : 0;
     static constexpr size_t kG = (DIRECT ? sizeof(float) : sizeof(cx<float>)) * LS::kBPT * LS::kR * Cfg::NT;
+    // the twiddle table is copied to shared memory only while kMinBlocks CTAs still
+    // fit an SM (227 KB); wide rows (3840) read it through L1 instead
+    static constexpr bool kTwSmem =
+        HOLO_ROW_SMEM_TW && (kWork + kPre + sizeof(cx<float>) * Cfg::W + kG + 2048) * Cfg::kMinBlocks <= 227 * 1024;
+    static constexpr size_t kTw = kTwSmem ? sizeof(cx<float>) * Cfg::W : 0;
     static constexpr size_t kTf = kWork + kPre + kTw + kG;  // offset of the per-plane constants
     static size_t bytes(int Lloc) { return kTf + sizeof(float2) * (Lloc > 0 ? Lloc : 1); }
 };
@@ -229,7 +233,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<float>* sm = reinterpret_cast<cx<float>*>(smem_raw);
     cx<float>* pre = reinterpret_cast<cx<float>*>(smem_raw + SM::kWork);
-    const cx<float>* s_tw = HOLO_ROW_SMEM_TW ? reinterpret_cast<cx<float>*>(smem_raw + SM::kWork + SM::kPre) : tw;
+    const cx<float>* s_tw = SM::kTwSmem ? reinterpret_cast<cx<float>*>(smem_raw + SM::kWork + SM::kPre) : tw;
     unsigned char* s_slot = smem_raw + SM::kWork + SM::kPre + SM::kTw;
     float2* s_tf = reinterpret_cast<float2*>(smem_raw + SM::kTf);  // (phase0, 2 pi z) per plane
     __shared__ unsigned long long s_bar;
@@ -242,7 +246,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
     const size_t plane_stride = static_cast<size_t>(C) * H * W;
     const int nplanes = MODE == kModeReplay ? nrep : Lloc;
     for (int l = threadIdx.x; l < nplanes; l += Cfg::NT) s_tf[l] = make_float2(tfc[l * C + c].phase0, tfc[l * C + c].two_pi_z_f);
-    if constexpr (HOLO_ROW_SMEM_TW)
+    if constexpr (SM::kTwSmem)
         for (int k = threadIdx.x; k < W; k += Cfg::NT) const_cast<cx<float>*>(s_tw)[k] = tw[k];
 
     // prefetch of plane l's NBR rows (one thread issues; the buffer is free once

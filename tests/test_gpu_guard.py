@@ -45,7 +45,7 @@ def test_forward_and_every_sort_path_stay_in_bounds(W, H):
     s.positions[4000:8000, :2] *= 0.4
     g = api.pipeline_forward(s, front_camera(cfg), cfg, ctx=ctx)
     sizes = np.diff(g.raster.bucket_start.astype(np.int64))
-    assert sizes.max() > 1024 and ((sizes > 128) & (sizes <= 1024)).any()
+    assert sizes.max() > 1024 and ((sizes > 256) & (sizes <= 1024)).any()
     api.pipeline_forward(synthetic_scene(800, cfg, 3), front_camera(cfg), cfg,
                          PipelineOptions(prop=PropagationOptions(pad2x=True)), ctx=ctx)
     ctx.check_guards()
