@@ -9,6 +9,7 @@
 // reference's.  Buckets above kSortCap entries are sorted here instead, by a
 // single-CTA bitonic network per bucket.
 #include "kernels.cuh"
+#include "sort_warp.cuh"
 
 namespace holo_cuda {
 
@@ -216,18 +217,24 @@ __global__ void __launch_bounds__(256) k_bucket_emit(PreOut pre, size_t N, int L
     if (over) atomicOr(flags, kFlagOverflow);
 }
 
-// Buckets above the in-CTA sort capacity, compacted into a device list.
-// Bucket bounds are clamped to the reserved entry capacity (an overflowed
-// asynchronous frame has bstart[B] > capacity), so at most capacity / (cap + 1)
-// buckets qualify; the list index is bounded by max_list all the same.
+// Buckets above the in-CTA sort capacity (list, nlist[0]) and of 129..kWarpSortCap
+// entries (mid, nlist[1]), compacted into device lists.  Bucket bounds are clamped
+// to the reserved entry capacity (an overflowed asynchronous frame has
+// bstart[B] > capacity), so at most capacity / (cap + 1) resp. capacity / 129
+// buckets qualify; the list indices are bounded by max_list / max_mid all the same.
 __global__ void k_find_large(const unsigned* __restrict__ bstart, long long B, int cap, unsigned capacity,
-                             int* __restrict__ list, unsigned max_list, unsigned* __restrict__ nlist) {
+                             int* __restrict__ list, unsigned max_list, int* __restrict__ mid, unsigned max_mid,
+                             unsigned* __restrict__ nlist) {
     for (long long b = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; b < B;
          b += static_cast<long long>(gridDim.x) * blockDim.x) {
         const unsigned s = min(bstart[b], capacity), e = min(bstart[b + 1], capacity);
-        if (e - s > static_cast<unsigned>(cap)) {
+        const unsigned n = e - s;
+        if (n > static_cast<unsigned>(cap)) {
             const unsigned k = atomicAdd(nlist, 1u);
             if (k < max_list) list[k] = static_cast<int>(b);
+        } else if (n > 128u && n <= static_cast<unsigned>(kWarpSortCap)) {
+            const unsigned k = atomicAdd(nlist + 1, 1u);
+            if (k < max_mid) mid[k] = static_cast<int>(b);
         }
     }
 }
@@ -235,12 +242,25 @@ __global__ void k_find_large(const unsigned* __restrict__ bstart, long long B, i
 // Persistent CTAs sort the listed buckets by (zc, gidx) with a bitonic network in
 // global scratch; bucket b uses the scratch range [2 bstart[b], 2 bstart[b] + pow2(n)),
 // which never overlaps another bucket's since pow2(n) < 2 n.
+// The listed mid-size buckets come first, one warp each (eight keys per lane).
 __global__ void __launch_bounds__(1024) k_sort_large_dev(const int* __restrict__ list,
                                                          const unsigned* __restrict__ nlist, unsigned max_list,
+                                                         const int* __restrict__ mid, unsigned max_mid,
                                                          const unsigned* __restrict__ bstart, unsigned capacity,
                                                          const unsigned long long* __restrict__ zkey,
                                                          int* __restrict__ egidx,
                                                          unsigned long long* __restrict__ tkey, int* __restrict__ tg) {
+    {
+        const unsigned nmid = min(nlist[1], max_mid);
+        const int lane = threadIdx.x & 31;
+        for (unsigned w = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); w < nmid; w += gridDim.x * (blockDim.x / 32)) {
+            const int bk = mid[w];
+            const unsigned e0 = min(bstart[bk], capacity);
+            const int n = static_cast<int>(min(bstart[bk + 1], capacity) - e0);
+            if (!warpsort::warp_sort_bucket_fast<8>(zkey, egidx, e0, n, lane))
+                warpsort::warp_sort_bucket<8>(zkey, egidx, e0, n, lane);
+        }
+    }
     const unsigned count = min(*nlist, max_list);
     for (unsigned w = blockIdx.x; w < count; w += gridDim.x) {
         const int bk = list[w];
@@ -328,15 +348,19 @@ void sort_large_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsi
                         const unsigned long long* zkey, int* egidx, unsigned* d_nlist) {
     // list buffer sized for the worst case: at most capacity / (kSortCap + 1) buckets can exceed the cap
     const size_t max_list = capacity / (kSortCap + 1) + 1;
+    const size_t max_mid = capacity / 129 + 1;
     int* list = static_cast<int*>(ctx->buffer("large_list", sizeof(int) * max_list));
+    int* mid = static_cast<int*>(ctx->buffer("mid_list", sizeof(int) * max_mid));
     auto* tkey = static_cast<unsigned long long*>(ctx->buffer("large_tkey", sizeof(unsigned long long) * 2 * (capacity + 1)));
     auto* tg = static_cast<int*>(ctx->buffer("large_tg", sizeof(int) * 2 * (capacity + 1)));
     const long long blocks = (B + 255) / 256;
     k_find_large<<<static_cast<unsigned>(blocks < 4096 ? (blocks > 0 ? blocks : 1) : 4096), 256, 0, ctx->stream>>>(
-        bstart, B, kSortCap, capacity, list, static_cast<unsigned>(max_list), d_nlist);
+        bstart, B, kSortCap, capacity, list, static_cast<unsigned>(max_list), mid, static_cast<unsigned>(max_mid),
+        d_nlist);
     HC_LAUNCHED(ctx);
-    k_sort_large_dev<<<ctx->sm_count, 1024, 0, ctx->stream>>>(list, d_nlist, static_cast<unsigned>(max_list), bstart,
-                                                             capacity, zkey, egidx, tkey, tg);
+    k_sort_large_dev<<<ctx->sm_count, 1024, 0, ctx->stream>>>(list, d_nlist, static_cast<unsigned>(max_list), mid,
+                                                             static_cast<unsigned>(max_mid), bstart, capacity, zkey,
+                                                             egidx, tkey, tg);
     HC_LAUNCHED(ctx);
 }
 

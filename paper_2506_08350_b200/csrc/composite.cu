@@ -6,7 +6,7 @@
 //   a = min(alpha * exp(-form / 2) * rho, alpha_clamp), skip unless a > alpha_floor,
 //   acc_c += a T amp_c e^{i phi_c},  T *= 1 - a,  ++n_contrib.
 // Bucket order -- ascending (zc, gidx), rasterizer.cpp:221-224 -- is restored
-// before compositing: buckets of up to kWarpSortCap entries by k_sort_small / k_sort_mid (one
+// before compositing: buckets of up to kWarpSortCap entries by k_sort_small / k_sort_large_dev (one
 // warp per bucket, shuffle bitonic), buckets above kSortCap by binning.cu, and the
 // ones in between by the compositing CTA itself in shared memory.
 // Compositing: one CTA per bucket, one thread per pixel.  Records are staged 256
@@ -17,10 +17,13 @@
 // with the centre offset formed in f64 per entry, so dx, dy keep full fp32
 // precision, and alpha folded into the exponent: a = 2^(q + log2 alpha).
 #include "raster_eval.cuh"
+#include "sort_warp.cuh"
 
 namespace holo_cuda {
 
 namespace {
+
+using namespace warpsort;
 
 template <int TILE>
 struct TileGeom {
@@ -29,144 +32,7 @@ struct TileGeom {
     static constexpr int kBlocksX = TILE / 8;
 };
 
-struct KeyG {
-    unsigned long long k;  // IEEE bits of zc (> 0, so they order like zc)
-    int g;                 // Gaussian index: the tie-break
-};
-
-__device__ __forceinline__ bool kg_less(const KeyG& a, const KeyG& b) {
-    return a.k < b.k || (a.k == b.k && a.g < b.g);
-}
-
-// Bitonic sort of 32 * NE (key, gidx) pairs held by one warp, element i in lane
-// i % 32, slot i / 32; ascending on (zc, gidx) -- rasterizer.cpp:221-224.
-template <int NE>
-__device__ __forceinline__ void warp_bitonic(KeyG (&v)[NE], int lane) {
-#pragma unroll
-    for (int k = 2; k <= 32 * NE; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j >= 32) {
-#pragma unroll
-                for (int s = 0; s < NE; ++s) {
-                    const int s2 = s ^ (j >> 5);
-                    if (s2 > s) {
-                        const bool up = ((lane + 32 * s) & k) == 0;
-                        const bool swap = up ? kg_less(v[s2], v[s]) : kg_less(v[s], v[s2]);
-                        if (swap) {
-                            const KeyG t = v[s];
-                            v[s] = v[s2];
-                            v[s2] = t;
-                        }
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int s = 0; s < NE; ++s) {
-                    KeyG o;
-                    o.k = __shfl_xor_sync(0xffffffffu, v[s].k, j);
-                    o.g = __shfl_xor_sync(0xffffffffu, v[s].g, j);
-                    const bool lower = (lane & j) == 0;
-                    const bool up = ((lane + 32 * s) & k) == 0;
-                    const bool take_min = lower == up;
-                    const bool o_less = kg_less(o, v[s]);
-                    if (take_min ? o_less : !o_less) v[s] = o;
-                }
-            }
-        }
-    }
-}
-
-// Sort one bucket (n <= 32 NE entries) in a warp and write its gidx back in order.
-template <int NE>
-__device__ __forceinline__ void warp_sort_bucket(const unsigned long long* __restrict__ zkey, int* __restrict__ egidx,
-                                                 unsigned e0, int n, int lane) {
-    KeyG v[NE];
-#pragma unroll
-    for (int s = 0; s < NE; ++s) {
-        const int i = lane + 32 * s;
-        v[s].g = i < n ? egidx[e0 + i] : 0x7fffffff;
-    }
-#pragma unroll
-    for (int s = 0; s < NE; ++s) v[s].k = lane + 32 * s < n ? zkey[v[s].g] : ~0ull;
-    warp_bitonic<NE>(v, lane);
-#pragma unroll
-    for (int s = 0; s < NE; ++s) {
-        const int i = lane + 32 * s;
-        if (i < n) egidx[e0 + i] = v[s].g;
-    }
-}
-
-// Bitonic sort of 32 * NE 64-bit keys held by one warp (layout as warp_bitonic).
-template <int NE>
-__device__ __forceinline__ void warp_bitonic_u64(unsigned long long (&v)[NE], int lane) {
-#pragma unroll
-    for (int k = 2; k <= 32 * NE; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j >= 32) {
-#pragma unroll
-                for (int s = 0; s < NE; ++s) {
-                    const int s2 = s ^ (j >> 5);
-                    if (s2 > s) {
-                        const bool up = ((lane + 32 * s) & k) == 0;
-                        const unsigned long long a = v[s], b = v[s2];
-                        v[s] = up ? min(a, b) : max(a, b);
-                        v[s2] = up ? max(a, b) : min(a, b);
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int s = 0; s < NE; ++s) {
-                    const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[s], j);
-                    const bool lower = (lane & j) == 0;
-                    const bool up = ((lane + 32 * s) & k) == 0;
-                    v[s] = (lower == up) ? min(v[s], o) : max(v[s], o);
-                }
-            }
-        }
-    }
-}
-
-// Fast path of warp_sort_bucket: one 64-bit key per entry, (fp32 depth bits << 32 |
-// gidx).  Rounding to fp32 is monotonic, so this order equals (zc, gidx) unless two
-// entries share an fp32 depth with different f64 depths; that (rare) case is
-// detected on the sorted sequence and the exact sort runs instead.  Returns false then.
-template <int NE>
-__device__ __forceinline__ bool warp_sort_bucket_fast(const unsigned long long* __restrict__ zkey,
-                                                      int* __restrict__ egidx, unsigned e0, int n, int lane) {
-    unsigned long long v[NE];
-#pragma unroll
-    for (int s = 0; s < NE; ++s) {
-        const int i = lane + 32 * s;
-        v[s] = i < n ? static_cast<unsigned long long>(static_cast<unsigned>(egidx[e0 + i])) : ~0ull;
-    }
-#pragma unroll
-    for (int s = 0; s < NE; ++s)
-        if (lane + 32 * s < n) {
-            const float z = __double2float_rn(__longlong_as_double(static_cast<long long>(zkey[v[s]])));
-            v[s] |= static_cast<unsigned long long>(__float_as_uint(z)) << 32;
-        }
-    warp_bitonic_u64<NE>(v, lane);
-    bool tie = false;
-#pragma unroll
-    for (int s = 0; s < NE; ++s) {
-        const unsigned long long dn = __shfl_down_sync(0xffffffffu, v[s], 1);
-        const unsigned long long wrap = __shfl_sync(0xffffffffu, v[(s + 1) % NE], 0);
-        const unsigned long long next = lane < 31 ? dn : wrap;
-        const int i = lane + 32 * s;
-        tie = tie || (i + 1 < n && (v[s] >> 32) == (next >> 32));
-    }
-    if (__any_sync(0xffffffffu, tie)) return false;
-#pragma unroll
-    for (int s = 0; s < NE; ++s) {
-        const int i = lane + 32 * s;
-        if (i < n) egidx[e0 + i] = static_cast<int>(v[s] & 0xffffffffull);
-    }
-    return true;
-}
-
-// One warp per bucket of 2..kWarpSortCap entries.
+// One warp per bucket of 2..128 entries (129..kWarpSortCap: binning.cu, with the large ones).
 __global__ void __launch_bounds__(256) k_sort_small(const unsigned* __restrict__ bstart, long long B,
                                                     unsigned capacity, const unsigned long long* __restrict__ zkey,
                                                     int* __restrict__ egidx) {
@@ -183,20 +49,6 @@ __global__ void __launch_bounds__(256) k_sort_small(const unsigned* __restrict__
     } else if (n <= 128) {
         if (!warp_sort_bucket_fast<4>(zkey, egidx, e0, n, lane)) warp_sort_bucket<4>(zkey, egidx, e0, n, lane);
     }
-}
-
-// One warp per bucket of 129..kWarpSortCap entries (eight keys per lane): a
-// kernel of its own so the common small buckets keep k_sort_small's registers.
-__global__ void __launch_bounds__(256) k_sort_mid(const unsigned* __restrict__ bstart, long long B, unsigned capacity,
-                                                  const unsigned long long* __restrict__ zkey,
-                                                  int* __restrict__ egidx) {
-    const long long b = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-    if (b >= B) return;
-    const int lane = threadIdx.x & 31;
-    const unsigned e0 = min(bstart[b], capacity);
-    const int n = static_cast<int>(min(bstart[b + 1], capacity) - e0);
-    if (n <= 128 || n > kWarpSortCap) return;  // warp-uniform
-    if (!warp_sort_bucket_fast<8>(zkey, egidx, e0, n, lane)) warp_sort_bucket<8>(zkey, egidx, e0, n, lane);
 }
 
 #ifdef HOLO_COUNT
@@ -677,8 +529,6 @@ void sort_small_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsi
                         const unsigned long long* zkey, int* egidx) {
     if (B <= 0) return;
     k_sort_small<<<static_cast<unsigned>((B + 7) / 8), 256, 0, ctx->stream>>>(bstart, B, capacity, zkey, egidx);
-    HC_LAUNCHED(ctx);
-    k_sort_mid<<<static_cast<unsigned>((B + 7) / 8), 256, 0, ctx->stream>>>(bstart, B, capacity, zkey, egidx);
     HC_LAUNCHED(ctx);
 }
 

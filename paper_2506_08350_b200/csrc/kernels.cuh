@@ -137,7 +137,8 @@ constexpr unsigned kFlagDegenerateQuat = 1u, kFlagNegativeAmp = 2u, kFlagOverflo
 void bucket_emit(holo_ctx* ctx, const PreOut& pre, size_t N, int L, int plane_begin, int plane_end, int tiles_x,
                  int num_tiles, int soft, const unsigned* bstart, unsigned* cursor,
                  int* egidx, unsigned capacity, unsigned* flags);
-// device-driven: buckets above kSortCap are found and sorted without a host round trip
+// device-driven: buckets above kSortCap (and, one warp each, those of 129..kWarpSortCap
+// entries) are found and sorted without a host round trip; d_nlist[0..1] count them
 void sort_large_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsigned capacity,
                         const unsigned long long* zkey, int* egidx, unsigned* d_nlist);
 void entry_depths(holo_ctx* ctx, const int* egidx, const double* zc, double* edepth, const unsigned* d_E,
