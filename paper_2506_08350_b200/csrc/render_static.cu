@@ -30,7 +30,13 @@ template <> struct PlanOf<128> { using type = Radices<16, 8>; };
 template <> struct PlanOf<256> { using type = Radices<16, 16>; };
 template <> struct PlanOf<512> { using type = Radices<8, 8, 8>; };
 template <> struct PlanOf<1024> { using type = Radices<16, 16, 4>; };
-template <> struct PlanOf<1080> { using type = Radices<8, 9, 15>; };
+// HOLO_P1080_{A,B,C} / HOLO_P1920_{A,B,C}: plan orderings for measurement
+#ifndef HOLO_P1080_A
+#define HOLO_P1080_A 8
+#define HOLO_P1080_B 9
+#define HOLO_P1080_C 15
+#endif
+template <> struct PlanOf<1080> { using type = Radices<HOLO_P1080_A, HOLO_P1080_B, HOLO_P1080_C>; };
 // HOLO_ROW1920 selects the 1920-point plan and row-pass shape (tuning).  Measured
 // row pass at C3: 1 = [16,8,15], 2 rows x 256 threads, 2 CTAs/SM: 0.451 ms;
 // 2 = [16,15,8] 1 row, 3 CTAs: 0.554; 3 = 2 rows x 512: 0.566; 4 = 4 CTAs: 0.626.
@@ -42,11 +48,18 @@ template <> struct PlanOf<1080> { using type = Radices<8, 9, 15>; };
 #ifndef HOLO_ROW1920
 #define HOLO_ROW1920 1
 #endif
+#ifndef HOLO_P1920_A
 #if HOLO_ROW1920 == 1
-template <> struct PlanOf<1920> { using type = Radices<16, 8, 15>; };
+#define HOLO_P1920_A 16
+#define HOLO_P1920_B 8
+#define HOLO_P1920_C 15
 #else
-template <> struct PlanOf<1920> { using type = Radices<16, 15, 8>; };
+#define HOLO_P1920_A 16
+#define HOLO_P1920_B 15
+#define HOLO_P1920_C 8
 #endif
+#endif
+template <> struct PlanOf<1920> { using type = Radices<HOLO_P1920_A, HOLO_P1920_B, HOLO_P1920_C>; };
 template <> struct PlanOf<2048> { using type = Radices<16, 16, 8>; };
 template <> struct PlanOf<2160> { using type = Radices<16, 9, 15>; };
 template <> struct PlanOf<3840> { using type = Radices<16, 16, 15>; };
