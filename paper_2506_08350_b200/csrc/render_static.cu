@@ -29,11 +29,18 @@ template <> struct PlanOf<64> { using type = Radices<16, 4>; };
 template <> struct PlanOf<128> { using type = Radices<16, 8>; };
 template <> struct PlanOf<256> { using type = Radices<16, 16>; };
 template <> struct PlanOf<512> { using type = Radices<8, 8, 8>; };
-template <> struct PlanOf<1024> { using type = Radices<16, 16, 4>; };
+#ifndef HOLO_P1024_A
+#define HOLO_P1024_A 16
+#define HOLO_P1024_B 16
+#define HOLO_P1024_C 4
+#endif
+template <> struct PlanOf<1024> { using type = Radices<HOLO_P1024_A, HOLO_P1024_B, HOLO_P1024_C>; };
 // HOLO_P1080_{A,B,C} / HOLO_P1920_{A,B,C}: plan orderings for measurement
+// measured at C3 (column FFT / IFFT, ms): [8,9,15] 0.197 / 0.208, [9,8,15] 0.185 / 0.203,
+// [12,9,10] 0.193 / 0.205, [8,15,9] 0.208 / 0.208, [15,9,8] 0.199 / 0.232
 #ifndef HOLO_P1080_A
-#define HOLO_P1080_A 8
-#define HOLO_P1080_B 9
+#define HOLO_P1080_A 9
+#define HOLO_P1080_B 8
 #define HOLO_P1080_C 15
 #endif
 template <> struct PlanOf<1080> { using type = Radices<HOLO_P1080_A, HOLO_P1080_B, HOLO_P1080_C>; };
@@ -48,11 +55,13 @@ template <> struct PlanOf<1080> { using type = Radices<HOLO_P1080_A, HOLO_P1080_
 #ifndef HOLO_ROW1920
 #define HOLO_ROW1920 1
 #endif
+// measured at C3 (row pass, ms): [16,8,15] 0.306, [8,15,16] 0.293, [8,16,15] 0.297,
+// [15,8,16] 0.318, [15,16,8] 0.314
 #ifndef HOLO_P1920_A
 #if HOLO_ROW1920 == 1
-#define HOLO_P1920_A 16
-#define HOLO_P1920_B 8
-#define HOLO_P1920_C 15
+#define HOLO_P1920_A 8
+#define HOLO_P1920_B 15
+#define HOLO_P1920_C 16
 #else
 #define HOLO_P1920_A 16
 #define HOLO_P1920_B 15
@@ -60,9 +69,24 @@ template <> struct PlanOf<1080> { using type = Radices<HOLO_P1080_A, HOLO_P1080_
 #endif
 #endif
 template <> struct PlanOf<1920> { using type = Radices<HOLO_P1920_A, HOLO_P1920_B, HOLO_P1920_C>; };
-template <> struct PlanOf<2048> { using type = Radices<16, 16, 8>; };
-template <> struct PlanOf<2160> { using type = Radices<16, 9, 15>; };
-template <> struct PlanOf<3840> { using type = Radices<16, 16, 15>; };
+#ifndef HOLO_P2048_A
+#define HOLO_P2048_A 16
+#define HOLO_P2048_B 16
+#define HOLO_P2048_C 8
+#endif
+template <> struct PlanOf<2048> { using type = Radices<HOLO_P2048_A, HOLO_P2048_B, HOLO_P2048_C>; };
+#ifndef HOLO_P2160_A
+#define HOLO_P2160_A 16
+#define HOLO_P2160_B 9
+#define HOLO_P2160_C 15
+#endif
+template <> struct PlanOf<2160> { using type = Radices<HOLO_P2160_A, HOLO_P2160_B, HOLO_P2160_C>; };
+#ifndef HOLO_P3840_A
+#define HOLO_P3840_A 16
+#define HOLO_P3840_B 16
+#define HOLO_P3840_C 15
+#endif
+template <> struct PlanOf<3840> { using type = Radices<HOLO_P3840_A, HOLO_P3840_B, HOLO_P3840_C>; };
 
 // column passes: strips of NB columns, NT threads, MINB CTAs per SM (register cap)
 // The twiddle table is copied to shared memory behind the FFT work area
