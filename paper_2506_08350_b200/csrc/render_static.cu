@@ -24,6 +24,11 @@ namespace {
 
 template <int N>
 struct PlanOf;
+// the column IFFT's plan: the forward plan reversed unless specialised (the row
+// pass needs the exact reverse to keep its spectrum in registers; the column
+// passes are separate kernels)
+template <int N>
+struct InvColPlanOf;
 template <> struct PlanOf<48> { using type = Radices<16, 3>; };
 template <> struct PlanOf<64> { using type = Radices<16, 4>; };
 template <> struct PlanOf<128> { using type = Radices<16, 8>; };
@@ -88,6 +93,13 @@ template <> struct PlanOf<2160> { using type = Radices<HOLO_P2160_A, HOLO_P2160_
 #endif
 template <> struct PlanOf<3840> { using type = Radices<HOLO_P3840_A, HOLO_P3840_B, HOLO_P3840_C>; };
 
+template <int N>
+struct InvColPlanOf {
+    using type = typename RevPlan<typename PlanOf<N>::type>::type;
+};
+// measured at C3 (column IFFT): [15,8,9] (the reverse of [9,8,15]) 0.203 ms, [10,12,9] 0.192 ms
+template <> struct InvColPlanOf<1080> { using type = Radices<10, 12, 9>; };
+
 // column passes: strips of NB columns, NT threads, MINB CTAs per SM (register cap)
 // The twiddle table is copied to shared memory behind the FFT work area
 // (HOLO_COL_SMEM_TW=0 reads it from global memory instead).
@@ -102,7 +114,9 @@ template <int H_, int NB_, int NT_, int MINB_>
 struct ColCfgT {
     static constexpr int H = H_, NB = NB_, NT = NT_, kMinBlocks = MINB_;
     using B = Batch<H, NB, NT>;
-    static constexpr int kWorkElems = FftSmem<B, typename PlanOf<H>::type>::kElems;
+    static constexpr int kWorkF = FftSmem<B, typename PlanOf<H>::type>::kElems;
+    static constexpr int kWorkI = FftSmem<B, typename InvColPlanOf<H>::type>::kElems;
+    static constexpr int kWorkElems = kWorkF > kWorkI ? kWorkF : kWorkI;
     static constexpr size_t kSmem = sizeof(cx<float>) * (kWorkElems + (HOLO_COL_SMEM_TW ? H : 0));
 };
 
@@ -488,7 +502,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_col_inv_epi(const 
             if (intens) intens[at] = v.x * v.x + v.y * v.y;
         }
     };
-    using Pinv = typename RevPlan<typename PlanOf<H>::type>::type;
+    using Pinv = typename InvColPlanOf<H>::type;
     fft_static<float, +1, typename Cfg::B, Pinv>(sm, col_twiddles<Cfg>(sm, tw), load, store);
 }
 
