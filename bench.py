@@ -269,6 +269,9 @@ def main():
         run_reference(args)
         return
 
+    # keep stdout to the one JSON line (NCCL prints a version banner at its first
+    # communicator otherwise)
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
     import torch
     import torch.distributed as dist
 
