@@ -34,10 +34,12 @@ template <> struct PlanOf<64> { using type = Radices<16, 4>; };
 template <> struct PlanOf<128> { using type = Radices<16, 8>; };
 template <> struct PlanOf<256> { using type = Radices<16, 16>; };
 template <> struct PlanOf<512> { using type = Radices<8, 8, 8>; };
+// measured at C4 (row pass / column FFT / column IFFT, ms): [16,16,4] 0.136 / 0.069 / 0.078,
+// [16,8,8] 0.112 / 0.069 / 0.076, [8,16,8] 0.125 / 0.068 / 0.078, [8,8,16] 0.142 / 0.077 / 0.076
 #ifndef HOLO_P1024_A
 #define HOLO_P1024_A 16
-#define HOLO_P1024_B 16
-#define HOLO_P1024_C 4
+#define HOLO_P1024_B 8
+#define HOLO_P1024_C 8
 #endif
 template <> struct PlanOf<1024> { using type = Radices<HOLO_P1024_A, HOLO_P1024_B, HOLO_P1024_C>; };
 // HOLO_P1080_{A,B,C} / HOLO_P1920_{A,B,C}: plan orderings for measurement
@@ -86,10 +88,11 @@ template <> struct PlanOf<2048> { using type = Radices<HOLO_P2048_A, HOLO_P2048_
 #define HOLO_P2160_C 15
 #endif
 template <> struct PlanOf<2160> { using type = Radices<HOLO_P2160_A, HOLO_P2160_B, HOLO_P2160_C>; };
+// measured at C5 (row pass, ms): [16,16,15] 2.120, [16,15,16] 2.090, [15,16,16] 2.184
 #ifndef HOLO_P3840_A
 #define HOLO_P3840_A 16
-#define HOLO_P3840_B 16
-#define HOLO_P3840_C 15
+#define HOLO_P3840_B 15
+#define HOLO_P3840_C 16
 #endif
 template <> struct PlanOf<3840> { using type = Radices<HOLO_P3840_A, HOLO_P3840_B, HOLO_P3840_C>; };
 
@@ -99,6 +102,8 @@ struct InvColPlanOf {
 };
 // measured at C3 (column IFFT): [15,8,9] (the reverse of [9,8,15]) 0.203 ms, [10,12,9] 0.192 ms
 template <> struct InvColPlanOf<1080> { using type = Radices<10, 12, 9>; };
+// measured at C5 (column FFT / IFFT, ms): [16,9,15] 1.698 / 2.141 (its reverse), inverse [16,15,9] 1.883
+template <> struct InvColPlanOf<2160> { using type = Radices<16, 15, 9>; };
 
 // column passes: strips of NB columns, NT threads, MINB CTAs per SM (register cap)
 // The twiddle table is copied to shared memory behind the FFT work area
