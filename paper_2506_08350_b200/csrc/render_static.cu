@@ -111,9 +111,10 @@ template <> struct InvColPlanOf<2160> { using type = Radices<16, 15, 9>; };
 #ifndef HOLO_COL_SMEM_TW
 #define HOLO_COL_SMEM_TW 0  // measured: global (L1) twiddles 0.211 -> 0.197 ms (col fwd, C3)
 #endif
-// the row pass's twiddles: shared-memory copy (1) or global / L1 (0)
+// the row pass's twiddles: shared-memory copy (1) or global / L1 (0); measured at
+// C3 with the [8,15,16] plan: 0.292 ms (shared) vs 0.281 ms (L1)
 #ifndef HOLO_ROW_SMEM_TW
-#define HOLO_ROW_SMEM_TW 1
+#define HOLO_ROW_SMEM_TW 0
 #endif
 template <int H_, int NB_, int NT_, int MINB_>
 struct ColCfgT {
