@@ -8,6 +8,8 @@
 // (rasterizer.cpp:221-224), so the final lists are deterministic and equal the
 // reference's.  Buckets above kSortCap entries are sorted here instead, by a
 // single-CTA bitonic network per bucket.
+#include <algorithm>
+
 #include "kernels.cuh"
 #include "sort_warp.cuh"
 
@@ -18,6 +20,9 @@ namespace {
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;
+#ifndef HOLO_SCAN_ONEPASS
+#define HOLO_SCAN_ONEPASS 1
+#endif
 
 __device__ __forceinline__ unsigned warp_incl_scan(unsigned v) {
     const int lane = threadIdx.x & 31;
@@ -108,6 +113,71 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_final(const unsigned* __r
         run += v[k];
     }
     if (blockIdx.x == nblocks - 1 && threadIdx.x == 0) out[n] = partials[nblocks];
+}
+
+// Single-pass exclusive scan with decoupled look-back: tiles are taken in launch
+// order (an atomic ticket), each tile publishes its aggregate and then its
+// inclusive prefix in a 64-bit status word (epoch:30 | flag:2 | value:32; flag 1 =
+// aggregate, 2 = inclusive), and sums its predecessors' words until it meets an
+// inclusive one.  The epoch (one per call) makes stale words of earlier calls
+// invisible without clearing the array.  Integer sums: the result is exact and
+// independent of the order.
+__global__ void __launch_bounds__(kScanThreads) k_scan_onepass(const unsigned* __restrict__ in,
+                                                              const unsigned* __restrict__ in2, long long n,
+                                                              unsigned* __restrict__ out, unsigned* __restrict__ dmax,
+                                                              unsigned long long* __restrict__ status,
+                                                              unsigned* __restrict__ ticket, unsigned epoch,
+                                                              unsigned ticket_base) {
+    __shared__ unsigned s_tile, s_prefix;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u) - ticket_base;
+    __syncthreads();
+    const int tile = static_cast<int>(s_tile);
+    const long long base = static_cast<long long>(tile) * kScanTile + static_cast<long long>(threadIdx.x) * kScanItems;
+    unsigned v[kScanItems];
+    unsigned sum = 0, m = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const long long i = base + k;
+        v[k] = i < n ? in[i] + (in2 ? in2[i] : 0u) : 0u;
+        sum += v[k];
+        m = v[k] > m ? v[k] : m;
+    }
+    unsigned total;
+    const unsigned ex = block_excl_scan(sum, &total);
+    const unsigned long long tag = static_cast<unsigned long long>(epoch & 0x3fffffffu) << 34;
+    if (threadIdx.x == 0) {
+        unsigned prefix = 0;
+        if (tile == 0) {
+            atomicExch(&status[0], tag | (2ull << 32) | total);
+        } else {
+            atomicExch(&status[tile], tag | (1ull << 32) | total);
+            for (int j = tile - 1; j >= 0;) {
+                const unsigned long long w = atomicAdd(&status[j], 0ull);
+                if ((w >> 34) != (tag >> 34) || ((w >> 32) & 3u) == 0) continue;  // not yet published
+                prefix += static_cast<unsigned>(w);
+                if (((w >> 32) & 3u) == 2) break;
+                --j;
+            }
+            atomicExch(&status[tile], tag | (2ull << 32) | (prefix + total));
+        }
+        s_prefix = prefix;
+    }
+    __syncthreads();
+    unsigned run = s_prefix + ex;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const long long i = base + k;
+        if (i < n) out[i] = run;
+        run += v[k];
+    }
+    if (base <= n && n <= base + kScanItems) out[n] = run;  // the total, by the thread that ends at n
+    if (dmax) {
+        for (int d = 16; d > 0; d >>= 1) {
+            const unsigned o = __shfl_down_sync(0xffffffffu, m, d);
+            m = o > m ? o : m;
+        }
+        if ((threadIdx.x & 31) == 0) atomicMax(dmax, m);
+    }
 }
 
 // Loop over the (plane, tile) buckets of Gaussian i restricted to planes [pb, pe).
@@ -217,28 +287,6 @@ __global__ void __launch_bounds__(256) k_bucket_emit(PreOut pre, size_t N, int L
     if (over) atomicOr(flags, kFlagOverflow);
 }
 
-// Buckets above the in-CTA sort capacity (list, nlist[0]) and of 129..kWarpSortCap
-// entries (mid, nlist[1]), compacted into device lists.  Bucket bounds are clamped
-// to the reserved entry capacity (an overflowed asynchronous frame has
-// bstart[B] > capacity), so at most capacity / (cap + 1) resp. capacity / 129
-// buckets qualify; the list indices are bounded by max_list / max_mid all the same.
-__global__ void k_find_large(const unsigned* __restrict__ bstart, long long B, int cap, unsigned capacity,
-                             int* __restrict__ list, unsigned max_list, int* __restrict__ mid, unsigned max_mid,
-                             unsigned* __restrict__ nlist) {
-    for (long long b = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; b < B;
-         b += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const unsigned s = min(bstart[b], capacity), e = min(bstart[b + 1], capacity);
-        const unsigned n = e - s;
-        if (n > static_cast<unsigned>(cap)) {
-            const unsigned k = atomicAdd(nlist, 1u);
-            if (k < max_list) list[k] = static_cast<int>(b);
-        } else if (n > 128u && n <= static_cast<unsigned>(kWarpSortCap)) {
-            const unsigned k = atomicAdd(nlist + 1, 1u);
-            if (k < max_mid) mid[k] = static_cast<int>(b);
-        }
-    }
-}
-
 // Persistent CTAs sort the listed buckets by (zc, gidx) with a bitonic network in
 // global scratch; bucket b uses the scratch range [2 bstart[b], 2 bstart[b] + pow2(n)),
 // which never overlaps another bucket's since pow2(n) < 2 n.
@@ -318,6 +366,31 @@ void exclusive_scan_u32(holo_ctx* ctx, const unsigned* in, unsigned* out, long l
                         const unsigned* in2) {
     const int nblocks = static_cast<int>((n + kScanTile - 1) / kScanTile);
     const int nb = nblocks > 0 ? nblocks : 1;
+    if (HOLO_SCAN_ONEPASS) {
+        // The status words and the ticket persist across calls: each call takes a new
+        // epoch (stale words of other calls never match it) and the ticket base it
+        // starts from (every tile of a call takes one ticket).  Growth, epoch wrap and
+        // ticket wrap start over on zeroed memory.
+        holo_ctx::ScanState& stt = ctx->scan;
+        auto* status = static_cast<unsigned long long*>(ctx->buffer("scan_status", sizeof(unsigned long long) * (nb + 64)));
+        auto* ticket = reinterpret_cast<unsigned*>(status + nb + 32);
+        if (nb > stt.cap || stt.epoch >= (1u << 30) - 1 ||
+            static_cast<unsigned long long>(stt.ticket) + static_cast<unsigned>(nb) >= 0xffffffffull) {
+            stt.cap = std::max(stt.cap, nb);
+            status = static_cast<unsigned long long*>(ctx->buffer("scan_status", sizeof(unsigned long long) * (stt.cap + 64)));
+            ticket = reinterpret_cast<unsigned*>(status + stt.cap + 32);
+            HC_CUDA(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (stt.cap + 64), ctx->stream));
+            stt.epoch = 1;
+            stt.ticket = 0;
+        }
+        ticket = reinterpret_cast<unsigned*>(status + stt.cap + 32);
+        k_scan_onepass<<<nb, kScanThreads, 0, ctx->stream>>>(in, in2, n, out, d_max, status, ticket, stt.epoch,
+                                                             stt.ticket);
+        HC_LAUNCHED(ctx);
+        ++stt.epoch;
+        stt.ticket += static_cast<unsigned>(nb);
+        return;
+    }
     unsigned* partials = static_cast<unsigned*>(ctx->buffer("scan_partials", sizeof(unsigned) * (nb + 1)));
     k_scan_partials<<<nb, kScanThreads, 0, ctx->stream>>>(in, in2, n, partials, d_max);
     HC_LAUNCHED(ctx);
@@ -344,20 +417,14 @@ void bucket_emit(holo_ctx* ctx, const PreOut& pre, size_t N, int L, int pb, int 
     HC_LAUNCHED(ctx);
 }
 
-void sort_large_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsigned capacity,
-                        const unsigned long long* zkey, int* egidx, unsigned* d_nlist) {
-    // list buffer sized for the worst case: at most capacity / (kSortCap + 1) buckets can exceed the cap
-    const size_t max_list = capacity / (kSortCap + 1) + 1;
-    const size_t max_mid = capacity / 129 + 1;
-    int* list = static_cast<int*>(ctx->buffer("large_list", sizeof(int) * max_list));
-    int* mid = static_cast<int*>(ctx->buffer("mid_list", sizeof(int) * max_mid));
+void sort_large_buckets(holo_ctx* ctx, const unsigned* bstart, unsigned capacity, const unsigned long long* zkey,
+                        int* egidx, unsigned* d_nlist) {
+    // the lists k_sort_small built (sized as there)
+    const size_t max_list = capacity / (kSortCap + 1) + 1, max_mid = capacity / 129 + 1;
+    const int* list = static_cast<const int*>(ctx->buffer("large_list", sizeof(int) * max_list));
+    const int* mid = static_cast<const int*>(ctx->buffer("mid_list", sizeof(int) * max_mid));
     auto* tkey = static_cast<unsigned long long*>(ctx->buffer("large_tkey", sizeof(unsigned long long) * 2 * (capacity + 1)));
     auto* tg = static_cast<int*>(ctx->buffer("large_tg", sizeof(int) * 2 * (capacity + 1)));
-    const long long blocks = (B + 255) / 256;
-    k_find_large<<<static_cast<unsigned>(blocks < 4096 ? (blocks > 0 ? blocks : 1) : 4096), 256, 0, ctx->stream>>>(
-        bstart, B, kSortCap, capacity, list, static_cast<unsigned>(max_list), mid, static_cast<unsigned>(max_mid),
-        d_nlist);
-    HC_LAUNCHED(ctx);
     k_sort_large_dev<<<ctx->sm_count, 1024, 0, ctx->stream>>>(list, d_nlist, static_cast<unsigned>(max_list), mid,
                                                              static_cast<unsigned>(max_mid), bstart, capacity, zkey,
                                                              egidx, tkey, tg);

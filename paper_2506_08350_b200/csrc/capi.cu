@@ -436,8 +436,10 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     HC_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned) * (B + 1), ctx->stream));
     bucket_emit(ctx, pre, N, L, pb, pe, g.tiles_x, g.num_tiles, st.soft_assignment, bstart, cursor, egidx,
                 capacity, misc);
-    sort_large_buckets(ctx, bstart, B, capacity, zkey, egidx, misc + 3);
-    sort_small_buckets(ctx, bstart, B, capacity, zkey, egidx);
+    // buckets of <= 128 entries sorted one warp each; the larger ones listed, then
+    // sorted on the device (mid-size one warp each, large ones CTA-wide)
+    sort_small_buckets(ctx, bstart, B, capacity, zkey, egidx, misc + 3);
+    sort_large_buckets(ctx, bstart, capacity, zkey, egidx, misc + 3);
     ctx->stage_end(1);
 
     // composite into [nplanes][C][H][W]

@@ -33,15 +33,34 @@ struct TileGeom {
 };
 
 // One warp per bucket of 2..128 entries (129..kWarpSortCap: binning.cu, with the large ones).
+// The warp of a larger bucket instead appends it to the device list of the
+// mid-size (129..kWarpSortCap: nlist[1], mid) or large (> kSortCap: nlist[0],
+// large) buckets that k_sort_large_dev sorts next.  Bucket bounds are clamped to
+// the reserved capacity, so at most capacity / 129 resp. capacity / (kSortCap + 1)
+// buckets qualify; the list indices are bounded all the same.
 __global__ void __launch_bounds__(256) k_sort_small(const unsigned* __restrict__ bstart, long long B,
                                                     unsigned capacity, const unsigned long long* __restrict__ zkey,
-                                                    int* __restrict__ egidx) {
+                                                    int* __restrict__ egidx, int* __restrict__ large,
+                                                    unsigned max_large, int* __restrict__ mid, unsigned max_mid,
+                                                    unsigned* __restrict__ nlist) {
     const long long b = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
     if (b >= B) return;
     const int lane = threadIdx.x & 31;
     const unsigned e0 = min(bstart[b], capacity);
     const int n = static_cast<int>(min(bstart[b + 1], capacity) - e0);
-    if (n < 2 || n > 128) return;  // warp-uniform
+    if (n > 128) {
+        if (lane == 0) {
+            if (n > kSortCap) {
+                const unsigned k = atomicAdd(nlist, 1u);
+                if (k < max_large) large[k] = static_cast<int>(b);
+            } else if (n <= kWarpSortCap) {
+                const unsigned k = atomicAdd(nlist + 1, 1u);
+                if (k < max_mid) mid[k] = static_cast<int>(b);
+            }
+        }
+        return;
+    }
+    if (n < 2) return;  // warp-uniform
     if (n <= 32) {
         if (!warp_sort_bucket_fast<1>(zkey, egidx, e0, n, lane)) warp_sort_bucket<1>(zkey, egidx, e0, n, lane);
     } else if (n <= 64) {
@@ -526,9 +545,14 @@ void launch_tile(holo_ctx* ctx, const CompositeArgs& a) {
 }  // namespace
 
 void sort_small_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsigned capacity,
-                        const unsigned long long* zkey, int* egidx) {
+                        const unsigned long long* zkey, int* egidx, unsigned* d_nlist) {
     if (B <= 0) return;
-    k_sort_small<<<static_cast<unsigned>((B + 7) / 8), 256, 0, ctx->stream>>>(bstart, B, capacity, zkey, egidx);
+    const size_t max_large = capacity / (kSortCap + 1) + 1, max_mid = capacity / 129 + 1;
+    int* large = static_cast<int*>(ctx->buffer("large_list", sizeof(int) * max_large));
+    int* mid = static_cast<int*>(ctx->buffer("mid_list", sizeof(int) * max_mid));
+    k_sort_small<<<static_cast<unsigned>((B + 7) / 8), 256, 0, ctx->stream>>>(
+        bstart, B, capacity, zkey, egidx, large, static_cast<unsigned>(max_large), mid, static_cast<unsigned>(max_mid),
+        d_nlist);
     HC_LAUNCHED(ctx);
 }
 

@@ -63,6 +63,12 @@ struct holo_ctx {
 
     std::map<std::string, holo_cuda::DevBuf> scratch;
     bool guard = false;
+    // single-pass scans (binning.cu): epoch and ticket base of the next call, and
+    // the tile capacity of the zero-initialised status words
+    struct ScanState {
+        unsigned epoch = 0, ticket = 0;
+        int cap = 0;
+    } scan;
     std::map<std::pair<int, int>, void*> twiddles;      // (n, sizeof(T)) -> exp(-2 pi i q/n)
     std::map<std::pair<int, uint64_t>, double*> freqs;  // (n, pitch bits) -> freq_at(i, n, pitch)
     void* host_pinned = nullptr;

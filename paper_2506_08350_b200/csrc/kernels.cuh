@@ -139,8 +139,8 @@ void bucket_emit(holo_ctx* ctx, const PreOut& pre, size_t N, int L, int plane_be
                  int* egidx, unsigned capacity, unsigned* flags);
 // device-driven: buckets above kSortCap (and, one warp each, those of 129..kWarpSortCap
 // entries) are found and sorted without a host round trip; d_nlist[0..1] count them
-void sort_large_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsigned capacity,
-                        const unsigned long long* zkey, int* egidx, unsigned* d_nlist);
+void sort_large_buckets(holo_ctx* ctx, const unsigned* bstart, unsigned capacity, const unsigned long long* zkey,
+                        int* egidx, unsigned* d_nlist);
 void entry_depths(holo_ctx* ctx, const int* egidx, const double* zc, double* edepth, const unsigned* d_E,
                   unsigned capacity);
 // host[0..2] = misc[0..2] (flags, num_valid, max bucket), host[4] = *total (E); host is pinned
@@ -239,7 +239,7 @@ void raster_backward_entries(holo_ctx* ctx, const RasterBwdArgs& a, int tile);
 void gauss_backward(holo_ctx* ctx, const GaussBwdArgs& a);
 // (zc, gidx) order for buckets of 2..kWarpSortCap entries, written back to egidx
 void sort_small_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsigned capacity,
-                        const unsigned long long* zkey, int* egidx);
+                        const unsigned long long* zkey, int* egidx, unsigned* d_nlist);
 
 // ---- training step (training.cu): losses, opacity decay, optimizer
 void losses_gpu(holo_ctx* ctx, const double* I, const double* G, const double* masks, int L, int C, int H, int W,
