@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libholo_cuda.so")
+# HOLO_CUDA_LIB: another build of the same library (measurement variants)
+LIB_PATH = os.environ.get("HOLO_CUDA_LIB") or os.path.join(HERE, "lib", "libholo_cuda.so")
 MAX_CH = 16
 
 OK, ERR_CONFIG, ERR_IO, ERR_USAGE, ERR_NUMERIC, ERR_CUDA, ERR_OOM, ERR_NCCL = range(8)

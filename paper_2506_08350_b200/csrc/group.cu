@@ -130,6 +130,7 @@ struct holo_group {
     struct Local {
         int rank = 0;
         int device = 0;
+        unsigned long long frames = 0;  // frames rendered: the lane of the next one rotates across calls
         ncclComm_t world_comm = nullptr;
         ncclComm_t plane_comm = nullptr;  // the plane group's (== world_comm when one group spans the world)
         std::vector<Lane> lanes;
@@ -419,7 +420,7 @@ int holo_group_render(holo_group* g, const holo_camera* cams, int num_views, con
                 const int v = mesh[i].view_begin + step;
                 if (v >= mesh[i].view_end) continue;
                 auto& l = g->locals[i];
-                lanes.push_back(&l.lanes[step % l.lanes.size()]);
+                lanes.push_back(&l.lanes[(l.frames++) % l.lanes.size()]);
                 who.push_back(i);
                 views.push_back(v);
             }
