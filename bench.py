@@ -595,7 +595,8 @@ def run_group(args, c, world, rank, local):
         step()
     g.synchronize()
     g.set_async(True)
-    step()
+    for _ in range(2 * max(1, args.inflight)):  # every lane's first asynchronous frame (buffer growth)
+        step()
     g.synchronize()
     g.frame_status()
 

@@ -42,6 +42,9 @@ def rank_ms(world, rank):
         g.render([cam], wave, outputs=outs, flags=flags)
     g.synchronize()
     g.set_async(True)
+    for _ in range(2 * max(1, args.lanes)):  # every lane's first asynchronous frame grows its buffers
+        g.render([cam], wave, outputs=outs, flags=flags)
+    g.synchronize()
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
