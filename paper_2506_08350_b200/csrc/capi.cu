@@ -503,7 +503,8 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
 // The row pass evaluates every plane's transfer function directly (instead of the
 // plane-to-plane recurrence) for local band limits or unevenly spaced planes.
 bool tf_direct(const std::vector<double>& z, int local) {
-    if (local) return true;
+    // one plane: the recurrence would cost two phasors per sample (A and Q) for one
+    if (local || z.size() <= 1) return true;
     for (size_t l = 2; l < z.size(); ++l) {
         const double d0 = z[1] - z[0], d = z[l] - z[l - 1];
         if (std::fabs(d - d0) > 1e-12 * std::fabs(d0)) return true;
