@@ -141,9 +141,6 @@ __device__ __forceinline__ void sort_bucket_cta(const CompositeArgs& a, unsigned
 #ifndef HOLO_COMP_MINB
 #define HOLO_COMP_MINB 7
 #endif
-// hit-list words of k_composite2: the record's byte offset, and which half of the
-// warp's 8 x 8 block (rows y, y + 4 of each lane) the accept box meets
-constexpr int kHalfTop = 1 << 29, kHalfBottom = 1 << 30, kHalfOffMask = kHalfTop - 1;
 // k_composite2 (two pixels per thread) for 16x16 tiles; HOLO_COMP2=0 selects k_composite
 #ifndef HOLO_COMP2
 #define HOLO_COMP2 1
@@ -426,60 +423,17 @@ __global__ void __launch_bounds__(256 / PPT, PPT == 2 ? HOLO_COMP2_MINB : HOLO_C
 #pragma unroll
                     for (int q = 0; q < kTest; ++q) {
                         const int j = c0 + 32 * q + lane;
-                        int hv = 0;
-                        if (j < cnt) {
-                            const float4 bb = sm.st.box[j];
-                            if constexpr (PPT == 2) {
-                                // which 8 x 4 half of the block (rows y / y + 4) the box meets
-                                const bool hx = !(bb.y < bxlo || bb.x > bxhi);
-                                const bool ht = hx && !(bb.w < bylo || bb.z > bylo + 3.0f);
-                                const bool hb = hx && !(bb.w < bylo + 4.0f || bb.z > byhi);
-                                hv = (ht ? kHalfTop : 0) | (hb ? kHalfBottom : 0);
-                            } else {
-                                hv = box_hits(bb, bxlo, bxhi, bylo, byhi) ? kHalfTop | kHalfBottom : 0;
-                            }
-                        }
-                        const bool h = hv != 0;
+                        const bool h = j < cnt && box_hits(sm.st.box[j], bxlo, bxhi, bylo, byhi);
                         const unsigned m = __ballot_sync(0xffffffffu, h);
-                        if (h) hits[nh + __popc(m & below)] = j * static_cast<int>(sizeof(Staged)) | hv;
+                        if (h) hits[nh + __popc(m & below)] = j * static_cast<int>(sizeof(Staged));
                         nh += __popc(m);
                     }
                     __syncwarp();
 #pragma unroll(kUnroll)
                     for (int kh = 0; kh < nh; ++kh) {
-                        const int hv = hits[kh];
-                        const int off = hv & kHalfOffMask;
+                        const int off = hits[kh];
                         const Staged* e = reinterpret_cast<const Staged*>(recs + off);
                         const float4 A = e->a, B = e->b;
-                        if constexpr (PPT == 2) {
-                            const int half = hv & (kHalfTop | kHalfBottom);
-                            if (half != (kHalfTop | kHalfBottom)) {
-                                // one half only (about half the hits at C3): one pixel, scalar,
-                                // the same operations as eval_alpha
-                                const float dx = fx - A.x;
-                                const cx<float> fyk = f32x2::unpack(fy2[0]);
-                                auto one = [&](float fy, float& Tk, cx<float>(&ak)[C], int& ck, int& lk) {
-                                    const float dy = fy - A.y;
-                                    const float t = fmaf(A.w, dy, A.z * dx);
-                                    const float u = fmaf(dx, t, B.y);
-                                    const float q = fmaf(B.x * dy, dy, u);
-                                    const float al = fminf(ex2_approx(q), clamp);
-                                    const bool ok = (al > thr) && (Tk >= eps);
-                                    const float w = ok ? al * Tk : 0.0f;
-                                    blend<C>(e, B, w, ak);
-                                    Tk -= w;
-                                    if constexpr (AUX) {
-                                        ck += ok ? 1 : 0;
-                                        lk = ok ? base + off / static_cast<int>(sizeof(Staged)) : lk;
-                                    }
-                                };
-                                if (half == kHalfTop)
-                                    one(fyk.x, T[0], acc[0], contrib[0], elast[0]);
-                                else
-                                    one(fyk.y, T[1], acc[1], contrib[1], elast[1]);
-                                continue;
-                            }
-                        }
                         // eval_alpha per pixel: d = centre - mu (dx shared), then
                         // t = fma(cb, dy, ca dx), u = fma(dx, t, log2 alpha),
                         // q = fma(cc dy, dy, u), a = min(2^q, clamp)
