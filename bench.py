@@ -280,9 +280,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # HOLO_BENCH_ONE_GPU=1 (dry runs of the N > 1 path on a one-GPU box): every rank
+    # on cuda:0, torch.distributed over gloo and the group's spectrum sums through
+    # gloo (NCCL refuses two ranks on one device); timings are then meaningless
+    one_gpu = os.environ.get("HOLO_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     c = CONFIGS[args.config]
     _CONFIG["name"] = args.config
     if c.views == 1 and world == 1:
@@ -569,7 +578,13 @@ def run_group(args, c, world, rank, local):
     scene = synthetic_scene(c.n, wave, c.seed)
     ctx = Context(local)
     if world > 1:
-        g = Group.from_torch(ctx, plane_split=ps)
+        if os.environ.get("HOLO_BENCH_ONE_GPU") == "1":
+            from paper_2506_08350_b200.api import gloo_allreduce
+            from paper_2506_08350_b200.sharding import torch_plane_group
+
+            g = Group(ctx, world, rank, ps, allreduce=gloo_allreduce(torch_plane_group(ps)))
+        else:
+            g = Group.from_torch(ctx, plane_split=ps)
     else:
         g = Group(ctx, plane_split=1)
     if args.inflight > 1:
