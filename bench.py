@@ -222,6 +222,10 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    # rank 0 alone runs the reference, on every host core: torchrun's default
+    # OMP_NUM_THREADS=1 per process would leave its OpenMP loops single-threaded
+    # (set before the reference library -- and its OpenMP runtime -- is loaded)
+    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count())
     kind, frame = reference_frame_seconds(args.config)
     cores = os.cpu_count()
     budget = args.ref_budget_s
