@@ -722,7 +722,7 @@ def run_group(args, c, world, rank, local):
     return {
         "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong" if c.views == 1 else "weak",
+        "scaling": "strong",  # the batch (1, 64 or 8 views) is fixed: total work fixed
         "vs_baseline": None, "dtype": "fp32 (f64 projection/keys)", "data": "synthetic",
         "config": {"workload": f"{c.name}: {c.n} Gaussians, {W}x{H}, {Lp} planes, {Cn} channels, "
                                f"{V} view(s) per step",
