@@ -353,6 +353,9 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
         return g;
     };
     // A = H_{plane 0} (for the Horner form)
+    // A = 1 exactly when the first plane sits at z = 0 (every unsharded frame at the
+    // paper's optics: Z_0 = 0 for L >= 2, wave_config.cpp:18-30) -- then S = S'
+    const bool a_one = s_tf[0].x == 0.0f && s_tf[0].y == 0.0f;
     auto a_at = [&](int q, int r) -> cx<float> {
         const float2 t = s_tf[0];
         return phasor_reduced(t.x - t.y * g_at(q, r));
@@ -431,7 +434,8 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
 #pragma unroll
             for (int r = 0; r < LS::kR; ++r) {
                 int b, i;
-                if (owner(q, r, b, i)) dst[static_cast<size_t>(b) * W + i] = DIRECT ? S[q][r] : S[q][r] * a_at(q, r);
+                if (owner(q, r, b, i))
+                    dst[static_cast<size_t>(b) * W + i] = DIRECT || a_one ? S[q][r] : S[q][r] * a_at(q, r);
             }
         return;
     }
@@ -445,7 +449,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
                 int b, i;
                 if (owner(q, r, b, i)) {
                     const cx<float> v = srcs[static_cast<size_t>(b) * W + i];
-                    S[q][r] = DIRECT || nrep == 0 ? v : v * conj(a_at(q, r));
+                    S[q][r] = DIRECT || nrep == 0 || a_one ? v : v * conj(a_at(q, r));
                 }
             }
         band_mask();
@@ -453,7 +457,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
     // outputs: [hologram] then planes 0..nrep-1 (output_planes in capi.cu)
     if (has_holo) {
         cx<float>* dst = out + static_cast<size_t>(row0) * W;
-        const bool plain = DIRECT || (MODE == kModeReplay && nrep == 0);  // S itself
+        const bool plain = DIRECT || a_one || (MODE == kModeReplay && nrep == 0);  // S itself
         auto load = [&](int q, int r, int, int) -> cx<float> { return plain ? S[q][r] : S[q][r] * a_at(q, r); };
         auto store = [&](int, int, int b, int i, cx<float> v) { dst[static_cast<size_t>(b) * W + i] = v; };
         fft_static<float, +1, B, Pinv>(sm, s_tw, load, store);
