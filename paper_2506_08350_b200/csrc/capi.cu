@@ -673,6 +673,7 @@ int holo_ctx_destroy(holo_ctx* ctx) {
         for (auto& kv : ctx->scratch) cudaFree(kv.second.p);
         for (auto& kv : ctx->twiddles) cudaFree(kv.second);
         for (auto& kv : ctx->freqs) cudaFree(kv.second);
+        for (auto& kv : ctx->tables) cudaFree(kv.second);
         for (auto& set : ctx->scene_sets)
             for (double* p : set.a) cudaFree(p);
         for (int k = 0; k < 2; ++k) {

@@ -71,6 +71,7 @@ struct holo_ctx {
     } scan;
     std::map<std::pair<int, int>, void*> twiddles;      // (n, sizeof(T)) -> exp(-2 pi i q/n)
     std::map<std::pair<int, uint64_t>, double*> freqs;  // (n, pitch bits) -> freq_at(i, n, pitch)
+    std::map<std::string, void*> tables;                 // frame-invariant device tables (render_static.cu)
     void* host_pinned = nullptr;
     size_t host_pinned_bytes = 0;
 

@@ -13,7 +13,9 @@
 // (modes SPEC / REPLAY of k_row_fused bracket the all-reduce of S).  The
 // identity FFT2(hologram) = S (the hologram is IFFT2(S)) removes the forward
 // transform of inverse_propagate.
+#include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "fft_static.cuh"
 #include "kernels.cuh"
@@ -279,7 +281,8 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
     cx<float>* __restrict__ spec,          // [C][H][W]: written (SPEC) or read (REPLAY)
     cx<float>* __restrict__ out,           // [O][C][H][W] row-inverse-transformed outputs (FULL, REPLAY)
     int H, int C, int Lloc, int has_holo, int nrep, const TfChan* __restrict__ tfc,
-    const double* __restrict__ fx, const double* __restrict__ fy, const cx<float>* __restrict__ tw, int row_base) {
+    const double* __restrict__ fx, const double* __restrict__ fy, const cx<float>* __restrict__ tw, int row_base,
+    const cx<float>* __restrict__ qtab) {
     constexpr int W = Cfg::W;
     constexpr int NBR = Cfg::NBR;
     using B = typename Cfg::B;
@@ -370,17 +373,18 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
         return reinterpret_cast<cx<float>*>(s_slot)[(q * LS::kR + r) * Cfg::NT + threadIdx.x];
     };
     {
-        const float dph = p0.step_phase, dz2 = p0.step_2piz;
+        // Q of the owned samples from the frame-invariant table (plane_ratio_table)
 #pragma unroll
         for (int q = 0; q < LS::kBPT; ++q)
 #pragma unroll
             for (int r = 0; r < LS::kR; ++r) {
                 S[q][r] = czf();
-                const float g = g_at(q, r);
-                if constexpr (DIRECT)
-                    G(q, r) = g;
-                else
-                    Qs(q, r) = g < 0.0f ? czf() : phasor_reduced(dph - dz2 * g);
+                if constexpr (DIRECT) {
+                    G(q, r) = g_at(q, r);
+                } else {
+                    int b, i;
+                    if (owner(q, r, b, i)) Qs(q, r) = qtab[static_cast<size_t>(row0 + b) * W + i];
+                }
             }
     }
     // DIRECT: H_{Z_l} at owned sample (q, r) inside the propagating band: the
@@ -478,6 +482,29 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_row_fused(
     }
 }
 
+// The plane-to-plane transfer-function ratio Q = e^{i (dphase - 2 pi dz g)} of every
+// spectral sample [C][H][W] (0 outside the propagating band): frame-invariant for a
+// grid, optics and plane spacing, so it is built once and cached per context; the
+// same operations as the row pass's g_at and phasor_reduced.
+__global__ void k_plane_ratio(cx<float>* __restrict__ q, int W, int H, int C, const TfChan* __restrict__ tfc,
+                              const double* __restrict__ fx, const double* __restrict__ fy) {
+    const size_t n = static_cast<size_t>(C) * H * W;
+    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int x = static_cast<int>(k % W), y = static_cast<int>((k / W) % H), c = static_cast<int>(k / (static_cast<size_t>(W) * H));
+        const TfChan p0 = tfc[c];
+        const double fxv = fx[x], fyv = fy[y];
+        const double fx2 = __dmul_rn(fxv, fxv), fy2 = __dmul_rn(fyv, fyv);
+        const double arg = __dsub_rn(__dsub_rn(p0.inv_l2, fx2), fy2);
+        cx<float> v = czf();
+        if (!(arg < 0.0)) {
+            const float g = static_cast<float>(__dadd_rn(fx2, fy2)) / (p0.inv_l + sqrtf(static_cast<float>(arg)));
+            v = phasor_reduced(p0.step_phase - p0.step_2piz * g);
+        }
+        q[k] = v;
+    }
+}
+
 // ---------------------------------------------------------------- 3. column IFFT + epilogue
 
 template <class Cfg>
@@ -543,24 +570,27 @@ void launch_col_inv_cfg(holo_ctx* ctx, const cx<float>* in, int W, int C, int no
 
 template <class Cfg, int MODE, bool LOCAL>
 void launch_row_mode(holo_ctx* ctx, const cx<float>* layers, cx<float>* spec, cx<float>* out, int H, int C, int Lloc,
-                     int has_holo, int nrep, const TfChan* tfc, const double* fx, const double* fy, int c0, int nc) {
+                     int has_holo, int nrep, const TfChan* tfc, const double* fx, const double* fy, int c0, int nc,
+                     const cx<float>* qtab) {
     const dim3 grid(nc * H / Cfg::NBR);
     const int nplanes = MODE == kModeReplay ? nrep : Lloc;
     const size_t smem = RowSmem<Cfg, MODE, LOCAL>::bytes(nplanes);
     HC_CUDA(cudaFuncSetAttribute(k_row_fused<Cfg, MODE, LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
     k_row_fused<Cfg, MODE, LOCAL><<<grid, Cfg::NT, smem, ctx->stream>>>(
-        layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, ctx->twiddle<float>(Cfg::W), c0 * H);
+        layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, ctx->twiddle<float>(Cfg::W), c0 * H, qtab);
     HC_LAUNCHED(ctx);
 }
 
 template <class Cfg>
 void launch_row_cfg(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spec, cx<float>* out, int H, int C,
                     int Lloc, int has_holo, int nrep, const TfChan* tfc, const double* fx, const double* fy,
-                    bool local, int c0, int nc) {
-#define HC_ROW_MODE(M)                                                                                              \
-    (local ? launch_row_mode<Cfg, M, true>(ctx, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, c0, nc) \
-           : launch_row_mode<Cfg, M, false>(ctx, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, c0, nc))
+                    bool local, int c0, int nc, const cx<float>* qtab) {
+#define HC_ROW_MODE(M)                                                                                        \
+    (local ? launch_row_mode<Cfg, M, true>(ctx, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, c0, \
+                                           nc, qtab)                                                          \
+           : launch_row_mode<Cfg, M, false>(ctx, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, c0, \
+                                            nc, qtab))
     switch (mode) {
         case kModeFull: HC_ROW_MODE(kModeFull); break;
         case kModeSpec: HC_ROW_MODE(kModeSpec); break;
@@ -583,8 +613,39 @@ void launch_col_inv(holo_ctx* ctx, const cx<float>* in, int W, int C, int nout, 
 template <int W>
 void launch_row(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spec, cx<float>* out, int H, int C,
                 int Lloc, int has_holo, int nrep, const TfChan* tfc, const double* fx, const double* fy, bool local,
-                int c0, int nc) {
-    launch_row_cfg<RowCfg<W>>(ctx, mode, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, local, c0, nc);
+                int c0, int nc, const cx<float>* qtab) {
+    launch_row_cfg<RowCfg<W>>(ctx, mode, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, local, c0, nc,
+                              qtab);
+}
+
+// the cached Q table of (grid, channels' wavelengths, pitch, plane step) for tfc's plane 0
+const cx<float>* plane_ratio_table(holo_ctx* ctx, int W, int H, int C, const TfChan* tfc, double pitch) {
+    // the host copy of the constants: the context's record of its last small upload
+    // to tfc (upload_tf), so no device read-back
+    const auto rec = ctx->small_cache.find(tfc);
+    if (rec == ctx->small_cache.end() || rec->second.size() < sizeof(TfChan) * C)
+        throw Error(HOLO_ERR_NUMERIC, "row pass: transfer-function constants not on record");
+    const TfChan* host = reinterpret_cast<const TfChan*>(rec->second.data());
+    std::string key = "qtab";
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "|%d|%d|%d|%a", W, H, C, pitch);
+    key += buf;
+    for (int c = 0; c < C; ++c) {
+        std::snprintf(buf, sizeof buf, "|%a|%a|%a", host[c].inv_l2, static_cast<double>(host[c].step_phase),
+                      static_cast<double>(host[c].step_2piz));
+        key += buf;
+    }
+    auto it = ctx->tables.find(key);
+    if (it != ctx->tables.end()) return static_cast<const cx<float>*>(it->second);
+    void* p = nullptr;
+    const size_t n = static_cast<size_t>(C) * H * W;
+    HC_CUDA(cudaMalloc(&p, sizeof(cx<float>) * n));
+    const unsigned blocks = static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 16 * 148));
+    k_plane_ratio<<<blocks, 256, 0, ctx->stream>>>(static_cast<cx<float>*>(p), W, H, C, tfc, ctx->freq(W, pitch),
+                                                 ctx->freq(H, pitch));
+    HC_LAUNCHED(ctx);
+    ctx->tables[key] = p;
+    return static_cast<const cx<float>*>(p);
 }
 
 #define HC_SIZES(X) X(48) X(64) X(128) X(256) X(512) X(1024) X(1080) X(1920) X(2048) X(2160) X(3840)
@@ -654,9 +715,10 @@ void static_row(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spe
     if (nc <= 0) return;
     const double* fx = ctx->freq(W, pitch);
     const double* fy = ctx->freq(H, pitch);
-#define HC_CASE(N)                                                                                       \
-    case N:                                                                                              \
-        launch_row<N>(ctx, mode, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, local, c0, nc); \
+    const cx<float>* qtab = local ? nullptr : plane_ratio_table(ctx, W, H, C, tfc, pitch);
+#define HC_CASE(N)                                                                                              \
+    case N:                                                                                                     \
+        launch_row<N>(ctx, mode, layers, spec, out, H, C, Lloc, has_holo, nrep, tfc, fx, fy, local, c0, nc, qtab); \
         return;
     switch (W) {
         HC_SIZES(HC_CASE)
