@@ -517,6 +517,7 @@ TfChan* upload_tf(holo_ctx* ctx, const char* name, const holo_wave& wave, const 
     const std::vector<TfChan> t = make_tf_consts(wave, z.data(), static_cast<int>(z.size()), w, h, local);
     TfChan* d = buf<TfChan>(ctx, name, t.size());
     upload_small(ctx, d, t.data(), sizeof(TfChan) * t.size());
+    ctx->tf_host[d] = t;  // the row pass keys its cached tables on these (render_static.cu)
     return d;
 }
 

@@ -72,6 +72,7 @@ struct holo_ctx {
     std::map<std::pair<int, int>, void*> twiddles;      // (n, sizeof(T)) -> exp(-2 pi i q/n)
     std::map<std::pair<int, uint64_t>, double*> freqs;  // (n, pitch bits) -> freq_at(i, n, pitch)
     std::map<std::string, void*> tables;                 // frame-invariant device tables (render_static.cu)
+    std::map<const void*, std::vector<holo_cuda::TfChan>> tf_host;  // host copy of each uploaded TF table
     void* host_pinned = nullptr;
     size_t host_pinned_bytes = 0;
 

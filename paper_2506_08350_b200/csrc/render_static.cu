@@ -620,12 +620,11 @@ void launch_row(holo_ctx* ctx, int mode, const cx<float>* layers, cx<float>* spe
 
 // the cached Q table of (grid, channels' wavelengths, pitch, plane step) for tfc's plane 0
 const cx<float>* plane_ratio_table(holo_ctx* ctx, int W, int H, int C, const TfChan* tfc, double pitch) {
-    // the host copy of the constants: the context's record of its last small upload
-    // to tfc (upload_tf), so no device read-back
-    const auto rec = ctx->small_cache.find(tfc);
-    if (rec == ctx->small_cache.end() || rec->second.size() < sizeof(TfChan) * C)
+    // the host copy of the constants upload_tf recorded for tfc (no device read-back)
+    const auto rec = ctx->tf_host.find(tfc);
+    if (rec == ctx->tf_host.end() || rec->second.size() < static_cast<size_t>(C))
         throw Error(HOLO_ERR_NUMERIC, "row pass: transfer-function constants not on record");
-    const TfChan* host = reinterpret_cast<const TfChan*>(rec->second.data());
+    const TfChan* host = rec->second.data();
     std::string key = "qtab";
     char buf[64];
     std::snprintf(buf, sizeof buf, "|%d|%d|%d|%a", W, H, C, pitch);
