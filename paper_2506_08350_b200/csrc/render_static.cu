@@ -17,12 +17,15 @@
 #include <cstdlib>
 #include <string>
 
+#include "bulk.cuh"
 #include "fft_static.cuh"
 #include "kernels.cuh"
 
 namespace holo_cuda {
 
 namespace {
+
+using namespace bulk;
 
 template <int N>
 struct PlanOf;
@@ -209,41 +212,6 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::kMinBlocks) k_col_fwd(cx<float>*
 }
 
 // ---------------------------------------------------------------- 2. row pass with the spectrum in registers
-
-// Bulk (TMA) copies global -> shared completing on an mbarrier.
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_init_fence() {
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-}
 
 // Row-pass shared memory: FFT work area; the prefetch buffer for the next plane's
 // NBR rows (each row padded by 8 complex = 16 banks; FULL / SPEC); the twiddle
