@@ -243,14 +243,18 @@ __global__ void __launch_bounds__(256) k_bucket_emit(PreOut pre, size_t N, int L
         if (pre.slots && n <= kSlots) {
             // slots taken in preprocess: no atomics; all slot and bucket-start
             // loads in flight before the first store
+            // the k-th tile of the span, row-major: offsets stepped, no divisions
             unsigned st[kSlots];
-            int bk[kSlots];
+            int off = 0, cx = 0;
 #pragma unroll
-            for (int k = 0; k < kSlots; ++k)
-                if (k < n) {
-                    bk[k] = b0 + (k / w) * tiles_x + k % w;
-                    st[k] = bstart[bk[k]] + pre.slots[static_cast<size_t>(k) * N + i];
+            for (int k = 0; k < kSlots; ++k) {
+                if (k < n) st[k] = bstart[b0 + off] + pre.slots[static_cast<size_t>(k) * N + i];
+                ++off;
+                if (++cx == w) {
+                    cx = 0;
+                    off += tiles_x - w;
                 }
+            }
 #pragma unroll
             for (int k = 0; k < kSlots; ++k)
                 if (k < n) {
@@ -267,13 +271,19 @@ __global__ void __launch_bounds__(256) k_bucket_emit(PreOut pre, size_t N, int L
         // the rect's tiles 4 at a time, so the slot atomics of a group are in flight
         // together instead of one round trip per entry; with preprocess slots, the
         // large Gaussians' slots follow the small ones' (bcount) in each bucket
+        int off = 0, cx = 0;
         for (int k = 0; k < n; k += 4) {
             int b[4];
             unsigned s[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int idx = k + u;
-                b[u] = b0 + (idx / w) * tiles_x + idx % w;
+                b[u] = b0 + off;
+                ++off;
+                if (++cx == w) {
+                    cx = 0;
+                    off += tiles_x - w;
+                }
                 if (idx < n) s[u] = atomicAdd(cursor + b[u], 1u) + (pre.slots ? pre.bcount[b[u]] : 0u);
             }
 #pragma unroll
@@ -305,7 +315,8 @@ __global__ void __launch_bounds__(1024) k_sort_large_dev(const int* __restrict__
             const int bk = mid[w];
             const unsigned e0 = min(bstart[bk], capacity);
             const int n = static_cast<int>(min(bstart[bk + 1], capacity) - e0);
-            if (!warpsort::warp_sort_bucket_fast<8>(zkey, egidx, e0, n, lane))
+            if (!warpsort::warp_sort_bucket_u32<8>(zkey, egidx, e0, n, lane) &&
+                !warpsort::warp_sort_bucket_fast<8>(zkey, egidx, e0, n, lane))
                 warpsort::warp_sort_bucket<8>(zkey, egidx, e0, n, lane);
         }
     }

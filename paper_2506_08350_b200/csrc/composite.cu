@@ -61,12 +61,16 @@ __global__ void __launch_bounds__(256) k_sort_small(const unsigned* __restrict__
         return;
     }
     if (n < 2) return;  // warp-uniform
+    // 32-bit keys, else 64-bit keys, else the exact (zc, gidx) pairs
     if (n <= 32) {
-        if (!warp_sort_bucket_fast<1>(zkey, egidx, e0, n, lane)) warp_sort_bucket<1>(zkey, egidx, e0, n, lane);
+        if (!warp_sort_bucket_u32<1>(zkey, egidx, e0, n, lane) && !warp_sort_bucket_fast<1>(zkey, egidx, e0, n, lane))
+            warp_sort_bucket<1>(zkey, egidx, e0, n, lane);
     } else if (n <= 64) {
-        if (!warp_sort_bucket_fast<2>(zkey, egidx, e0, n, lane)) warp_sort_bucket<2>(zkey, egidx, e0, n, lane);
+        if (!warp_sort_bucket_u32<2>(zkey, egidx, e0, n, lane) && !warp_sort_bucket_fast<2>(zkey, egidx, e0, n, lane))
+            warp_sort_bucket<2>(zkey, egidx, e0, n, lane);
     } else if (n <= 128) {
-        if (!warp_sort_bucket_fast<4>(zkey, egidx, e0, n, lane)) warp_sort_bucket<4>(zkey, egidx, e0, n, lane);
+        if (!warp_sort_bucket_u32<4>(zkey, egidx, e0, n, lane) && !warp_sort_bucket_fast<4>(zkey, egidx, e0, n, lane))
+            warp_sort_bucket<4>(zkey, egidx, e0, n, lane);
     }
 }
 

@@ -235,6 +235,28 @@ def test_depths_equal_in_fp32_sort_by_f64_depth(gpu_ctx, n):
     assert list(gidx) == sorted(gidx, key=lambda g: (r.projected["zc"][g], g))
 
 
+@pytest.mark.parametrize("n", [20, 50, 100, 200])
+def test_depths_apart_in_fp32_but_equal_in_the_short_key(gpu_ctx, n):
+    """Depths two fp32 ulps apart: distinct fp32 keys, but equal 32-bit short keys
+    (fp32 depth without its low mantissa bits), so the sort must detect the shared
+    short key and fall back; gidx runs against depth."""
+    cfg = desk_config(32, 1)
+    s = single_scene(n, 1)
+    ulp = float(np.spacing(np.float32(0.3)))
+    s.positions = np.array([[0.0, 0.0, 0.3 + 2 * ulp * (n - i)] for i in range(n)])
+    s.log_scales = np.full((n, 3), np.log(0.005))
+    s.amplitudes = np.ones((n, 3))
+    r = api.raster_forward(s, front_camera(cfg), cfg, ctx=gpu_ctx)
+    first_bucket = r.entries["bucket"][0]
+    sel = r.entries["bucket"] == first_bucket
+    gidx = r.entries["gidx"][sel]
+    assert len(gidx) == n
+    zc = r.projected["zc"]
+    assert len(np.unique(np.float32(zc[gidx]))) == n  # the fp32 keys do not collide
+    assert list(gidx) == sorted(gidx, key=lambda g: (zc[g], g))
+    assert list(gidx) == list(range(n - 1, -1, -1))
+
+
 def test_culling_and_clamp(gpu_ctx):
     cfg = desk_config(32, 1)
     s = single_scene(2, 1)
