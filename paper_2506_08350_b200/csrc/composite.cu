@@ -156,6 +156,10 @@ __device__ __forceinline__ void sort_bucket_cta(const CompositeArgs& a, unsigned
 #ifndef HOLO_COMP2_UNROLL
 #define HOLO_COMP2_UNROLL 4
 #endif
+// k_composite2's accept predicate as one setp.and + selp per pixel (measurement knob)
+#ifndef HOLO_COMP_PRED
+#define HOLO_COMP_PRED 1
+#endif
 // pixels per thread of k_composite2 (2: 128 threads per tile, 4: 64)
 #ifndef HOLO_COMP_PPT
 #define HOLO_COMP_PPT 2
@@ -433,6 +437,9 @@ __global__ void __launch_bounds__(256 / PPT, PPT == 2 ? HOLO_COMP2_MINB : HOLO_C
                         nh += __popc(m);
                     }
                     __syncwarp();
+#ifdef HOLO_COUNT
+                    unsigned long long n_any = 0;
+#endif
 #pragma unroll(kUnroll)
                     for (int kh = 0; kh < nh; ++kh) {
                         const int off = hits[kh];
@@ -457,10 +464,19 @@ __global__ void __launch_bounds__(256 / PPT, PPT == 2 ? HOLO_COMP2_MINB : HOLO_C
                             const float al1 = fminf(ex2_approx(qq.y), clamp);
                             float& Ta = T[2 * j];
                             float& Tb = T[2 * j + 1];
+                            const cx<float> wt = f32x2::unpack(f32x2::mul(f32x2::pack(al0, al1), f32x2::pack(Ta, Tb)));
+#if HOLO_COMP_PRED
+                            // accept = (a > floor) and (T >= eps): one compare folds the other's
+                            // predicate in, one select per pixel
+                            const float w0 = accept_weight(al0, thr, Ta, eps, wt.x);
+                            const float w1 = accept_weight(al1, thr, Tb, eps, wt.y);
+                            const bool a0 = (al0 > thr) && (Ta >= eps);  // AUX only
+                            const bool a1 = (al1 > thr) && (Tb >= eps);
+#else
                             const bool a0 = (al0 > thr) && (Ta >= eps);
                             const bool a1 = (al1 > thr) && (Tb >= eps);
-                            const cx<float> wt = f32x2::unpack(f32x2::mul(f32x2::pack(al0, al1), f32x2::pack(Ta, Tb)));
                             const float w0 = a0 ? wt.x : 0.0f, w1 = a1 ? wt.y : 0.0f;
+#endif
                             blend<C>(e, B, w0, acc[2 * j]);
                             blend<C>(e, B, w1, acc[2 * j + 1]);
                             const cx<float> Tn = f32x2::unpack(f32x2::sub(f32x2::pack(Ta, Tb), f32x2::pack(w0, w1)));
@@ -472,8 +488,17 @@ __global__ void __launch_bounds__(256 / PPT, PPT == 2 ? HOLO_COMP2_MINB : HOLO_C
                                 elast[2 * j] = a0 ? ei : elast[2 * j];
                                 elast[2 * j + 1] = a1 ? ei : elast[2 * j + 1];
                             }
+#ifdef HOLO_COUNT
+                            n_any += __any_sync(0xffffffffu, (al0 > thr) || (al1 > thr)) ? 1 : 0;
+#endif
                         }
                     }
+#ifdef HOLO_COUNT
+                    if (lane == 0) {
+                        atomicAdd(&g_counts[0], static_cast<unsigned long long>(nh));
+                        atomicAdd(&g_counts[1], n_any);
+                    }
+#endif
                     __syncwarp();
                     done = true;
 #pragma unroll
@@ -527,6 +552,9 @@ void launch_tile(holo_ctx* ctx, const CompositeArgs& a) {
                 default: throw Error(HOLO_ERR_CONFIG, "render supports 1 to 3 wavelength channels");
             }
             HC_LAUNCHED(ctx);
+#ifdef HOLO_COUNT
+            k_print_counts<<<1, 1, 0, ctx->stream>>>();
+#endif
             return;
         }
     }

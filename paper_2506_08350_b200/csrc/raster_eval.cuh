@@ -70,4 +70,14 @@ __device__ __forceinline__ bool box_hits(const float4& bb, float bxlo, float bxh
     return !(bb.y < bxlo || bb.x > bxhi || bb.w < bylo || bb.z > byhi);
 }
 
+// w if (a > thr) and (T >= eps), else 0: the accept decision of eval_alpha's
+// callers as one compare with the other folded in and one select
+__device__ __forceinline__ float accept_weight(float a, float thr, float T, float eps, float w) {
+    float r;
+    asm("{\n.reg .pred l, p;\nsetp.ge.f32 l, %2, %4;\nsetp.gt.and.f32 p, %1, %3, l;\nselp.f32 %0, %5, 0f00000000, p;\n}"
+        : "=f"(r)
+        : "f"(a), "f"(T), "f"(thr), "f"(eps), "f"(w));
+    return r;
+}
+
 }  // namespace holo_cuda
