@@ -423,7 +423,8 @@ __global__ void __launch_bounds__(256 / PPT, PPT == 2 ? HOLO_COMP2_MINB : HOLO_C
             }
             __syncthreads();
             if (!__all_sync(0xffffffffu, done)) {
-                const char* recs = reinterpret_cast<const char*>(sm.st.rec);
+                // hits[] holds shared-window addresses: the walk's loads use them as is
+                const unsigned recs = static_cast<unsigned>(__cvta_generic_to_shared(sm.st.rec));
                 int* hits = s_hit[warp];
                 for (int c0 = 0; c0 < cnt; c0 += 32 * kTest) {
                     const unsigned below = (1u << lane) - 1u;
@@ -433,7 +434,7 @@ __global__ void __launch_bounds__(256 / PPT, PPT == 2 ? HOLO_COMP2_MINB : HOLO_C
                         const int j = c0 + 32 * q + lane;
                         const bool h = j < cnt && box_hits(sm.st.box[j], bxlo, bxhi, bylo, byhi);
                         const unsigned m = __ballot_sync(0xffffffffu, h);
-                        if (h) hits[nh + __popc(m & below)] = j * static_cast<int>(sizeof(Staged));
+                        if (h) hits[nh + __popc(m & below)] = static_cast<int>(recs + j * sizeof(Staged));
                         nh += __popc(m);
                     }
                     __syncwarp();
@@ -442,9 +443,9 @@ __global__ void __launch_bounds__(256 / PPT, PPT == 2 ? HOLO_COMP2_MINB : HOLO_C
 #endif
 #pragma unroll(kUnroll)
                     for (int kh = 0; kh < nh; ++kh) {
-                        const int off = hits[kh];
-                        const Staged* e = reinterpret_cast<const Staged*>(recs + off);
-                        const float4 A = e->a, B = e->b;
+                        const unsigned ad = static_cast<unsigned>(hits[kh]);
+                        const float4 A = lds128(ad), B = lds128(ad + 16);
+                        const float4 Cc = C > 1 ? lds128(ad + 32) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
                         // eval_alpha per pixel: d = centre - mu (dx shared), then
                         // t = fma(cb, dy, ca dx), u = fma(dx, t, log2 alpha),
                         // q = fma(cc dy, dy, u), a = min(2^q, clamp)
@@ -453,7 +454,7 @@ __global__ void __launch_bounds__(256 / PPT, PPT == 2 ? HOLO_COMP2_MINB : HOLO_C
                         const unsigned long long my2 = f32x2::pack(A.y, A.y), cb2 = f32x2::pack(A.w, A.w);
                         const unsigned long long cadx2 = f32x2::pack(cadx, cadx), dx2 = f32x2::pack(dx, dx);
                         const unsigned long long la2 = f32x2::pack(B.y, B.y), cc2 = f32x2::pack(B.x, B.x);
-                        const int ei = base + off / static_cast<int>(sizeof(Staged));
+                        const int ei = base + static_cast<int>((ad - recs) / sizeof(Staged));
 #pragma unroll
                         for (int j = 0; j < PPT / 2; ++j) {
                             const unsigned long long dy = f32x2::sub(fy2[j], my2);
@@ -477,8 +478,8 @@ __global__ void __launch_bounds__(256 / PPT, PPT == 2 ? HOLO_COMP2_MINB : HOLO_C
                             const bool a1 = (al1 > thr) && (Tb >= eps);
                             const float w0 = a0 ? wt.x : 0.0f, w1 = a1 ? wt.y : 0.0f;
 #endif
-                            blend<C>(e, B, w0, acc[2 * j]);
-                            blend<C>(e, B, w1, acc[2 * j + 1]);
+                            blend_c<C>(B, Cc, w0, acc[2 * j]);
+                            blend_c<C>(B, Cc, w1, acc[2 * j + 1]);
                             const cx<float> Tn = f32x2::unpack(f32x2::sub(f32x2::pack(Ta, Tb), f32x2::pack(w0, w1)));
                             Ta = Tn.x;
                             Tb = Tn.y;

@@ -65,6 +65,23 @@ __device__ __forceinline__ void blend(const Staged* e, const float4& B, float w,
     }
 }
 
+// blend with the channel-1/2 phasors already loaded (Cc = the record's c)
+template <int C>
+__device__ __forceinline__ void blend_c(const float4& B, const float4& Cc, float w, cx<float> (&acc)[C]) {
+    acc[0] = axpy(w, B.z, B.w, acc[0]);
+    if constexpr (C > 1) {
+        acc[1 % C] = axpy(w, Cc.x, Cc.y, acc[1 % C]);
+        if constexpr (C > 2) acc[2 % C] = axpy(w, Cc.z, Cc.w, acc[2 % C]);
+    }
+}
+
+// 16-byte shared load from a shared-window address
+__device__ __forceinline__ float4 lds128(unsigned addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
+
 // does the accept box meet the warp's block of pixel centres [bxlo, bxhi] x [bylo, byhi]?
 __device__ __forceinline__ bool box_hits(const float4& bb, float bxlo, float bxhi, float bylo, float byhi) {
     return !(bb.y < bxlo || bb.x > bxhi || bb.w < bylo || bb.z > byhi);
