@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(256) k_bucket_emit(PreOut pre, size_t N, int L
 // which never overlaps another bucket's since pow2(n) < 2 n.
 // The listed mid-size buckets come first, one warp each (eight keys per lane).
 __global__ void __launch_bounds__(1024) k_sort_large_dev(const int* __restrict__ list,
-                                                         const unsigned* __restrict__ nlist, unsigned max_list,
+                                                         unsigned* __restrict__ nlist, unsigned max_list,
                                                          const int* __restrict__ mid, unsigned max_mid,
                                                          const unsigned* __restrict__ bstart, unsigned capacity,
                                                          const unsigned long long* __restrict__ zkey,
@@ -311,7 +311,13 @@ __global__ void __launch_bounds__(1024) k_sort_large_dev(const int* __restrict__
     {
         const unsigned nmid = min(nlist[1], max_mid);
         const int lane = threadIdx.x & 31;
-        for (unsigned w = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); w < nmid; w += gridDim.x * (blockDim.x / 32)) {
+        // buckets taken one at a time from a counter (nlist[2], zero at the frame's
+        // start): no tail of SMs idle while others finish a third round
+        while (nmid > 0) {
+            unsigned w = 0;
+            if (lane == 0) w = atomicAdd(nlist + 2, 1u);
+            w = __shfl_sync(0xffffffffu, w, 0);
+            if (w >= nmid) break;
             const int bk = mid[w];
             const unsigned e0 = min(bstart[bk], capacity);
             const int n = static_cast<int>(min(bstart[bk + 1], capacity) - e0);

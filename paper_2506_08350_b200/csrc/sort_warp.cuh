@@ -194,13 +194,46 @@ __device__ __forceinline__ bool warp_sort_bucket_u32(const unsigned long long* _
         const int i = lane + 32 * s;
         gid[s] = i < n ? egidx[e0 + i] : 0;
     }
+    if constexpr (NE < 8) {
 #pragma unroll
-    for (int s = 0; s < NE; ++s) {
-        const int i = lane + 32 * s;
-        v[s] = ~0u;
-        if (i < n) {
-            const float z = __double2float_rn(__longlong_as_double(static_cast<long long>(zkey[gid[s]])));
-            v[s] = ((__float_as_uint(z) >> (SB - 1)) << SB) | static_cast<unsigned>(i);
+        for (int s = 0; s < NE; ++s) {
+            const int i = lane + 32 * s;
+            v[s] = ~0u;
+            if (i < n) {
+                const float z = __double2float_rn(__longlong_as_double(static_cast<long long>(zkey[gid[s]])));
+                v[s] = ((__float_as_uint(z) >> (SB - 1)) << SB) | static_cast<unsigned>(i);
+            }
+        }
+    } else {
+        // 129..256 entries: 24 bits of truncated depth would collide in most
+        // buckets (birthday bound), so the depth is quantised over the bucket's own
+        // range instead, q = (z - zmin) (2^24 - 1) / (zmax - zmin) -- every step
+        // monotonic, so distinct q still give the (zc, gidx) order
+        constexpr unsigned kQMax = (1u << (32 - SB)) - 1u;
+        float z[NE];
+        float zlo = INFINITY, zhi = -INFINITY;
+#pragma unroll
+        for (int s = 0; s < NE; ++s) {
+            const int i = lane + 32 * s;
+            z[s] = 0.0f;
+            if (i < n) {
+                z[s] = __double2float_rn(__longlong_as_double(static_cast<long long>(zkey[gid[s]])));
+                zlo = fminf(zlo, z[s]);
+                zhi = fmaxf(zhi, z[s]);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            zlo = fminf(zlo, __shfl_xor_sync(0xffffffffu, zlo, o));
+            zhi = fmaxf(zhi, __shfl_xor_sync(0xffffffffu, zhi, o));
+        }
+        if (!(zhi > zlo)) return false;  // one fp32 depth for all: the 64-bit key decides
+        const float scale = static_cast<float>(kQMax) / (zhi - zlo);
+#pragma unroll
+        for (int s = 0; s < NE; ++s) {
+            const int i = lane + 32 * s;
+            v[s] = ~0u;
+            if (i < n) v[s] = (min(__float2uint_rz((z[s] - zlo) * scale), kQMax) << SB) | static_cast<unsigned>(i);
         }
     }
     warp_bitonic_u32<NE>(v, lane);
