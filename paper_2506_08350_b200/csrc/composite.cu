@@ -512,17 +512,20 @@ __global__ void __launch_bounds__(256 / PPT, PPT == 2 ? HOLO_COMP2_MINB : HOLO_C
         }
     }
 
+    // outputs: one 64-bit base per array, then 32-bit steps of 4 rows / one channel
     const size_t P = static_cast<size_t>(a.W) * a.H;
+    const size_t pix0 = static_cast<size_t>(lplane) * P + static_cast<size_t>(py) * a.W + px;
+    cx<float>* lay = a.layers + static_cast<size_t>(lplane) * (C - 1) * P + pix0;
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
         if (!in[k]) continue;
-        const size_t pix = static_cast<size_t>(py + 4 * k) * a.W + px;
+        const int dk = 4 * k * a.W;
 #pragma unroll
-        for (int c = 0; c < C; ++c) a.layers[(static_cast<size_t>(lplane) * C + c) * P + pix] = acc[k][c];
-        if (a.t_final) a.t_final[static_cast<size_t>(lplane) * P + pix] = T[k];
+        for (int c = 0; c < C; ++c) lay[static_cast<size_t>(c) * P + dk] = acc[k][c];
+        if (a.t_final) a.t_final[pix0 + dk] = T[k];
         if constexpr (AUX) {
-            a.n_contrib[static_cast<size_t>(lplane) * P + pix] = contrib[k];
-            if (a.e_last) a.e_last[static_cast<size_t>(lplane) * P + pix] = elast[k];
+            a.n_contrib[pix0 + dk] = contrib[k];
+            if (a.e_last) a.e_last[pix0 + dk] = elast[k];
         }
     }
 }
