@@ -38,7 +38,10 @@ struct TileGeom {
 // large) buckets that k_sort_large_dev sorts next.  Bucket bounds are clamped to
 // the reserved capacity, so at most capacity / 129 resp. capacity / (kSortCap + 1)
 // buckets qualify; the list indices are bounded all the same.
-__global__ void __launch_bounds__(256) k_sort_small(const unsigned* __restrict__ bstart, long long B,
+#ifndef HOLO_SORT_SMALL_MINB
+#define HOLO_SORT_SMALL_MINB 6  // 40 registers: C3 binning -4 us, C5 -37 us (8: C5 -49, C3/C4 slower)
+#endif
+__global__ void __launch_bounds__(256, HOLO_SORT_SMALL_MINB) k_sort_small(const unsigned* __restrict__ bstart, long long B,
                                                     unsigned capacity, const unsigned long long* __restrict__ zkey,
                                                     int* __restrict__ egidx, int* __restrict__ large,
                                                     unsigned max_large, int* __restrict__ mid, unsigned max_mid,
