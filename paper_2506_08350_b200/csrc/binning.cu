@@ -18,7 +18,10 @@ namespace holo_cuda {
 namespace {
 
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 16;
+#ifndef HOLO_SCAN_ITEMS
+#define HOLO_SCAN_ITEMS 4  // 1024-count tiles: C3 binning -4 us against 4096
+#endif
+constexpr int kScanItems = HOLO_SCAN_ITEMS;
 constexpr int kScanTile = kScanThreads * kScanItems;
 #ifndef HOLO_SCAN_ONEPASS
 #define HOLO_SCAN_ONEPASS 1
@@ -145,22 +148,39 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_onepass(const unsigned* _
     unsigned total;
     const unsigned ex = block_excl_scan(sum, &total);
     const unsigned long long tag = static_cast<unsigned long long>(epoch & 0x3fffffffu) << 34;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
+        // warp-parallel look-back: 32 predecessors' status words per round trip,
+        // summed up to the nearest one holding an inclusive prefix (flag 2); a
+        // window with an unpublished word (flag 0) before that point is re-read
+        const int lane = threadIdx.x;
         unsigned prefix = 0;
         if (tile == 0) {
-            atomicExch(&status[0], tag | (2ull << 32) | total);
+            if (lane == 0) atomicExch(&status[0], tag | (2ull << 32) | total);
         } else {
-            atomicExch(&status[tile], tag | (1ull << 32) | total);
+            if (lane == 0) atomicExch(&status[tile], tag | (1ull << 32) | total);
             for (int j = tile - 1; j >= 0;) {
-                const unsigned long long w = atomicAdd(&status[j], 0ull);
-                if ((w >> 34) != (tag >> 34) || ((w >> 32) & 3u) == 0) continue;  // not yet published
-                prefix += static_cast<unsigned>(w);
-                if (((w >> 32) & 3u) == 2) break;
-                --j;
+                const int idx = j - lane;
+                unsigned flag = 2, val = 0;  // before tile 0: an inclusive zero
+                if (idx >= 0) {
+                    const unsigned long long w = atomicAdd(&status[idx], 0ull);
+                    flag = (w >> 34) != (tag >> 34) ? 0u : static_cast<unsigned>((w >> 32) & 3u);
+                    val = static_cast<unsigned>(w);
+                }
+                const unsigned incl = __ballot_sync(0xffffffffu, flag == 2);
+                const unsigned zero = __ballot_sync(0xffffffffu, flag == 0);
+                const int stop = incl ? __ffs(incl) - 1 : 31;
+                const unsigned upto = stop == 31 ? 0xffffffffu : (2u << stop) - 1u;
+                if (zero & upto) continue;  // not yet published
+                unsigned v = lane <= stop ? val : 0u;
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+                prefix += v;
+                if (incl) break;
+                j -= 32;
             }
-            atomicExch(&status[tile], tag | (2ull << 32) | (prefix + total));
+            if (lane == 0) atomicExch(&status[tile], tag | (2ull << 32) | (prefix + total));
         }
-        s_prefix = prefix;
+        if (lane == 0) s_prefix = prefix;
     }
     __syncthreads();
     unsigned run = s_prefix + ex;
