@@ -279,11 +279,6 @@ __global__ void __launch_bounds__(TILE * TILE) k_raster_bwd(RasterBwdArgs a) {
 
 // ---- per-Gaussian chain (f64)
 
-__device__ __forceinline__ void mat3_mul(const double* a, const double* b, double* c) {
-    for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j) c[i * 3 + j] = (a[i * 3 + 0] * b[0 * 3 + j] + a[i * 3 + 1] * b[1 * 3 + j]) + a[i * 3 + 2] * b[2 * 3 + j];
-}
-
 __global__ void __launch_bounds__(256) k_bwd_gauss(GaussBwdArgs a) {
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     if (i >= a.n) return;
