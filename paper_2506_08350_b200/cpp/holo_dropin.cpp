@@ -11,6 +11,8 @@
 
 #include <algorithm>
 #include <bit>
+#include <chrono>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -837,7 +839,22 @@ PipelineForward pipeline_forward(const GaussianScene& scene, const CameraView& c
     check_raster_inputs(scene, cam, cfg);
     if (cfg.channels() != GaussianScene::kChannels)  // propagate's channel check (propagation.cpp:94-95)
         throw HoloError("config", "propagate: field does not match the configured grid");
+    // HOLO_DROPIN_PROFILE=1: phase times of this call on stderr (measurement aid)
+    static const bool prof = [] {
+        const char* e = std::getenv("HOLO_DROPIN_PROFILE");
+        return e && e[0] == '1';
+    }();
+    using clk = std::chrono::steady_clock;
+    auto t_last = clk::now();
+    auto lap = [&](const char* what) {
+        if (!prof) return;
+        const auto t = clk::now();
+        std::fprintf(stderr, "pipeline_forward %s %.1f ms\n", what,
+                     std::chrono::duration<double, std::milli>(t - t_last).count());
+        t_last = t;
+    };
     upload_scene(scene);
+    lap("upload_scene");
     const holo_wave w = to_c(cfg);
     const holo_camera c = to_c(cam);
     const holo_raster_settings st = to_c(opt.raster);
@@ -845,10 +862,12 @@ PipelineForward pipeline_forward(const GaussianScene& scene, const CameraView& c
     holo_frame_info info{};
     check(holo_render(ctx(), &c, &w, &st, &po,
                       kRasterOutputs | HOLO_OUT_HOLOGRAM | HOLO_OUT_REPLAYED | HOLO_OUT_INTENSITY, &info));
+    lap("render");
     PipelineForward f;
     const int L = cfg.num_planes, C = cfg.channels();
     const size_t n = static_cast<size_t>(cfg.nx) * cfg.ny * C;
     f.raster = collect_raster(scene, cfg, C, info);
+    lap("collect_raster");
     void* dholo = nullptr;
     void* drep0 = nullptr;
     size_t bytes0 = 0;
@@ -861,6 +880,7 @@ PipelineForward pipeline_forward(const GaussianScene& scene, const CameraView& c
         d2h_widen(r.data.data(), static_cast<const std::complex<float>*>(drep0) + static_cast<size_t>(l) * n, n);
         f.replayed.push_back(std::move(r));
     }
+    lap("hologram+replayed");
     // intensities = intensity(replayed) of the returned fields, literally as
     // pipeline.cpp:26-27 (f64 squares of the widened fp32 replay), formed on the
     // device from the resident replay: no re-upload of the returned fields
@@ -877,6 +897,7 @@ PipelineForward pipeline_forward(const GaussianScene& scene, const CameraView& c
             f.intensities.push_back(std::move(im));
         }
     }
+    lap("intensities");
     return f;
 }
 
