@@ -16,6 +16,8 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <thread>
+#include <type_traits>
 #include <omp.h>
 
 #include "holo/camera.hpp"
@@ -162,20 +164,47 @@ void d2h(void* h, const void* d, size_t n) {
     }
 }
 
-// complex64 device samples -> complex<double> host samples, in staged chunks
+// complex64 device samples -> complex<double> host samples, in staged chunks:
+// double-buffered, the next chunk's DMA in flight while this one is widened
 void d2h_widen(c64* h, const void* d, size_t n) {
     Staging& st = staging();
     constexpr size_t kPer = Staging::kChunk / sizeof(std::complex<float>);
-    for (size_t off = 0; off < n; off += kPer) {
-        const size_t len = std::min(kPer, n - off);
-        cuda_check(cudaMemcpyAsync(st.buf[0], static_cast<const std::complex<float>*>(d) + off,
-                                   len * sizeof(std::complex<float>), cudaMemcpyDeviceToHost, stream()),
+    const size_t chunks = (n + kPer - 1) / kPer;
+    auto issue = [&](size_t i) {
+        const int k = static_cast<int>(i & 1);
+        const size_t off = i * kPer;
+        cuda_check(cudaEventSynchronize(st.ev[k]), "cudaEventSynchronize");
+        cuda_check(cudaMemcpyAsync(st.buf[k], static_cast<const std::complex<float>*>(d) + off,
+                                   std::min(kPer, n - off) * sizeof(std::complex<float>), cudaMemcpyDeviceToHost,
+                                   stream()),
                    "cudaMemcpyAsync D2H");
-        cuda_check(cudaStreamSynchronize(stream()), "cudaStreamSynchronize");
-        const auto* src = reinterpret_cast<const std::complex<float>*>(st.buf[0]);
+        cuda_check(cudaEventRecord(st.ev[k], stream()), "cudaEventRecord");
+    };
+    if (chunks > 0) issue(0);
+    for (size_t i = 0; i < chunks; ++i) {
+        const int k = static_cast<int>(i & 1);
+        cuda_check(cudaEventSynchronize(st.ev[k]), "cudaEventSynchronize");
+        if (i + 1 < chunks) issue(i + 1);  // the other buffer was widened last iteration
+        const size_t off = i * kPer, len = std::min(kPer, n - off);
+        const auto* src = reinterpret_cast<const std::complex<float>*>(st.buf[k]);
 #pragma omp parallel for schedule(static)
-        for (long i = 0; i < static_cast<long>(len); ++i) h[off + i] = c64(src[i].real(), src[i].imag());
+        for (long j = 0; j < static_cast<long>(len); ++j) h[off + j] = c64(src[j].real(), src[j].imag());
     }
+}
+
+// count fields (or images) of one shape, allocated and zero-filled by parallel
+// threads: the first touch of fresh host pages is the cost of large results
+template <class T>
+std::vector<T> make_parallel(int count, int w, int h, int c, double pitch) {
+    std::vector<T> out(static_cast<size_t>(count));
+#pragma omp parallel for schedule(static, 1)
+    for (int l = 0; l < count; ++l) {
+        if constexpr (std::is_same_v<T, ComplexField>)
+            out[l] = T(w, h, c, pitch);
+        else
+            out[l] = T(w, h, c);
+    }
+    return out;
 }
 
 holo_wave to_c(const WaveConfig& w) {
@@ -616,6 +645,38 @@ std::vector<T> download_buf(int which) {
     return h;
 }
 
+// A frame buffer read whole into pinned host memory that is reused across calls
+// (grown on demand): the source of element-wise conversions into the result
+// arrays, without a zero-filled temporary vector and a second copy.
+template <class T>
+const T* download_pinned(int which, size_t& count, int slot) {
+    struct Pinned {
+        void* p = nullptr;
+        size_t cap = 0;
+        ~Pinned() {
+            if (p) cudaFreeHost(p);
+        }
+    };
+    thread_local Pinned pins[4];
+    Pinned& pin = pins[slot];
+    void* d = nullptr;
+    size_t bytes = 0;
+    check(holo_frame_buffer(ctx(), which, &d, &bytes));
+    if (bytes > pin.cap) {
+        if (pin.p) cudaFreeHost(pin.p);
+        pin.p = nullptr;
+        pin.cap = 0;
+        cuda_check(cudaMallocHost(&pin.p, bytes), "cudaMallocHost");
+        pin.cap = bytes;
+    }
+    if (bytes) {
+        cuda_check(cudaMemcpyAsync(pin.p, d, bytes, cudaMemcpyDeviceToHost, stream()), "cudaMemcpyAsync D2H");
+        cuda_check(cudaStreamSynchronize(stream()), "cudaStreamSynchronize");
+    }
+    count = bytes / sizeof(T);
+    return static_cast<const T*>(pin.p);
+}
+
 detail::Projected to_projected(const holo_projected& q) {
     detail::Projected p;
     p.valid = q.valid != 0;
@@ -644,13 +705,10 @@ std::vector<ComplexField> download_layers(const WaveConfig& cfg, int C) {
     void* d = nullptr;
     size_t bytes = 0;
     check(holo_frame_buffer(ctx(), HOLO_BUF_LAYERS, &d, &bytes));
-    std::vector<ComplexField> out;
-    for (int l = 0; l < L; ++l) {
-        ComplexField f(W, H, GaussianScene::kChannels, cfg.pitch);
-        d2h_widen(f.data.data(), static_cast<const std::complex<float>*>(d) + static_cast<size_t>(l) * C * P,
+    std::vector<ComplexField> out = make_parallel<ComplexField>(L, W, H, GaussianScene::kChannels, cfg.pitch);
+    for (int l = 0; l < L; ++l)
+        d2h_widen(out[l].data.data(), static_cast<const std::complex<float>*>(d) + static_cast<size_t>(l) * C * P,
                   static_cast<size_t>(C) * P);
-        out.push_back(std::move(f));
-    }
     return out;
 }
 
@@ -660,28 +718,46 @@ RasterForward collect_raster(const GaussianScene& scene, const WaveConfig& cfg, 
     const size_t P = static_cast<size_t>(W) * H, N = scene.size();
     r.tiles_x = info.tiles_x;
     r.tiles_y = info.tiles_y;
-    r.layers = download_layers(cfg, C);
-    const std::vector<float> tf = download_buf<float>(HOLO_BUF_T_FINAL);
-    r.t_final.resize(L * P);
-#pragma omp parallel for schedule(static)
-    for (long i = 0; i < static_cast<long>(L * P); ++i) r.t_final[i] = tf[i];
-    r.n_contrib = download_buf<std::int32_t>(HOLO_BUF_N_CONTRIB);
-    r.n_contrib.resize(L * P);
-    const std::vector<holo_projected> proj = download_buf<holo_projected>(HOLO_BUF_PROJECTED);
-    r.projected.resize(N);
-#pragma omp parallel for schedule(static)
-    for (long i = 0; i < static_cast<long>(N); ++i) r.projected[i] = to_projected(proj[i]);
-    r.rho = download_buf<double>(HOLO_BUF_RHO);
-    r.rho.resize(N * L);
-    r.touched = download_buf<std::uint8_t>(HOLO_BUF_TOUCHED);
-    r.touched.resize(N);
-    r.bucket_start = download_buf<std::uint32_t>(HOLO_BUF_BUCKET_START);
     const size_t B = static_cast<size_t>(L) * info.tiles_x * info.tiles_y;
-    r.bucket_start.resize(B + 1);
     const size_t E = info.num_entries;
-    std::vector<std::int32_t> gidx = download_buf<std::int32_t>(HOLO_BUF_ENTRY_GIDX);
-    std::vector<double> depth = download_buf<double>(HOLO_BUF_ENTRY_DEPTH);
-    r.entries.resize(E);
+    // the result arrays are zero-filled by their constructors: side threads size
+    // them while the main thread fills the layers (first touch of fresh pages is
+    // the cost here)
+    std::thread sizer1([&] {
+        r.t_final.resize(L * P);
+        r.projected.resize(N);
+    });
+    std::thread sizer2([&] {
+        r.entries.resize(E);
+        r.n_contrib.resize(L * P);
+        r.rho.resize(N * L);
+        r.touched.resize(N);
+        r.bucket_start.resize(B + 1);
+    });
+    r.layers = download_layers(cfg, C);
+    sizer1.join();
+    sizer2.join();
+    auto into = [&](int which, void* dst, size_t max_bytes) {
+        void* d = nullptr;
+        size_t bytes = 0;
+        check(holo_frame_buffer(ctx(), which, &d, &bytes));
+        if (bytes) d2h(dst, d, std::min(bytes, max_bytes));
+    };
+    size_t cnt = 0;
+    const float* tf = download_pinned<float>(HOLO_BUF_T_FINAL, cnt, 0);
+#pragma omp parallel for schedule(static)
+    for (long i = 0; i < static_cast<long>(std::min(cnt, L * P)); ++i) r.t_final[i] = tf[i];
+    into(HOLO_BUF_N_CONTRIB, r.n_contrib.data(), sizeof(std::int32_t) * L * P);
+    const holo_projected* proj = download_pinned<holo_projected>(HOLO_BUF_PROJECTED, cnt, 1);
+#pragma omp parallel for schedule(static)
+    for (long i = 0; i < static_cast<long>(std::min(cnt, N)); ++i) r.projected[i] = to_projected(proj[i]);
+    into(HOLO_BUF_RHO, r.rho.data(), sizeof(double) * N * L);
+    into(HOLO_BUF_TOUCHED, r.touched.data(), N);
+    into(HOLO_BUF_BUCKET_START, r.bucket_start.data(), sizeof(std::uint32_t) * (B + 1));
+    size_t ng = 0, nd = 0;
+    const std::int32_t* gidx = download_pinned<std::int32_t>(HOLO_BUF_ENTRY_GIDX, ng, 2);
+    const double* depth = download_pinned<double>(HOLO_BUF_ENTRY_DEPTH, nd, 3);
+    if (ng < E || nd < E) throw HoloError("numeric", "raster_forward: entry buffers shorter than the entry count");
 #pragma omp parallel for schedule(dynamic, 256)
     for (long b = 0; b < static_cast<long>(B); ++b)
         for (std::uint32_t e = r.bucket_start[b]; e < r.bucket_start[b + 1]; ++e)
@@ -875,11 +951,10 @@ PipelineForward pipeline_forward(const GaussianScene& scene, const CameraView& c
     check(holo_frame_buffer(ctx(), HOLO_BUF_REPLAYED, &drep0, &bytes0));
     f.hologram = ComplexField(cfg.nx, cfg.ny, C, cfg.pitch);
     d2h_widen(f.hologram.data.data(), dholo, n);
-    for (int l = 0; l < L; ++l) {
-        ComplexField r(cfg.nx, cfg.ny, C, cfg.pitch);
-        d2h_widen(r.data.data(), static_cast<const std::complex<float>*>(drep0) + static_cast<size_t>(l) * n, n);
-        f.replayed.push_back(std::move(r));
-    }
+    f.replayed = make_parallel<ComplexField>(L, cfg.nx, cfg.ny, C, cfg.pitch);
+    for (int l = 0; l < L; ++l)
+        d2h_widen(f.replayed[l].data.data(), static_cast<const std::complex<float>*>(drep0) + static_cast<size_t>(l) * n,
+                  n);
     lap("hologram+replayed");
     // intensities = intensity(replayed) of the returned fields, literally as
     // pipeline.cpp:26-27 (f64 squares of the widened fp32 replay), formed on the
@@ -891,11 +966,10 @@ PipelineForward pipeline_forward(const GaussianScene& scene, const CameraView& c
         const size_t total = static_cast<size_t>(L) * n;
         DevMem dint(sizeof(double) * total);
         check(holo_intensity_widened(ctx(), drep, static_cast<double*>(dint.p), total));
-        for (int l = 0; l < L; ++l) {
-            IntensityImage im(cfg.nx, cfg.ny, C);
-            d2h(im.data.data(), static_cast<const double*>(dint.p) + static_cast<size_t>(l) * n, sizeof(double) * n);
-            f.intensities.push_back(std::move(im));
-        }
+        f.intensities = make_parallel<IntensityImage>(L, cfg.nx, cfg.ny, C, 0.0);
+        for (int l = 0; l < L; ++l)
+            d2h(f.intensities[l].data.data(), static_cast<const double*>(dint.p) + static_cast<size_t>(l) * n,
+                sizeof(double) * n);
     }
     lap("intensities");
     return f;
