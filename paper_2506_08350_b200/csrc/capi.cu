@@ -375,7 +375,7 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     pre.rho = (st.soft_assignment || want_proj) ? buf<double>(ctx, "rho", N * L) : nullptr;
     pre.touched = buf<unsigned char>(ctx, "touched", N);
     pre.projected = want_proj ? buf<holo_projected>(ctx, "projected", N) : nullptr;
-    // flags, num_valid, max bucket, large / mid bucket counts, mid work counter
+    // flags, num_valid, max bucket, large / mid bucket counts
     unsigned* misc = buf<unsigned>(ctx, "misc", 8);
     pre.flags = misc;
     pre.num_valid = misc + 1;
