@@ -71,7 +71,7 @@ __device__ __forceinline__ double sigmoid_ref(double x) {
 // PROJ: also fill the full f64 detail::Projected record (HOLO_OUT_PROJECTED); the
 // render path compiles it out, which keeps the kernel at 64 registers.
 #ifndef HOLO_PRE_NT
-#define HOLO_PRE_NT 128
+#define HOLO_PRE_NT 64  // 12 CTAs of 64 per SM: C3 0.091 -> 0.089 ms, C5 0.465 -> 0.442 ms against 6 of 128
 #endif
 #ifndef HOLO_PRE_MINB
 #define HOLO_PRE_MINB (768 / HOLO_PRE_NT)  // 80 registers: no spills (measured best)
