@@ -38,15 +38,18 @@ struct TileGeom {
 // large) buckets that k_sort_large_dev sorts next.  Bucket bounds are clamped to
 // the reserved capacity, so at most capacity / 129 resp. capacity / (kSortCap + 1)
 // buckets qualify; the list indices are bounded all the same.
+#ifndef HOLO_SORT_SMALL_WARPS
+#define HOLO_SORT_SMALL_WARPS 8  // warps (buckets) per CTA
+#endif
 #ifndef HOLO_SORT_SMALL_MINB
 #define HOLO_SORT_SMALL_MINB 6  // 40 registers: C3 binning -4 us, C5 -37 us (8: C5 -49, C3/C4 slower)
 #endif
-__global__ void __launch_bounds__(256, HOLO_SORT_SMALL_MINB) k_sort_small(const unsigned* __restrict__ bstart, long long B,
+__global__ void __launch_bounds__(32 * HOLO_SORT_SMALL_WARPS, HOLO_SORT_SMALL_MINB * 8 / HOLO_SORT_SMALL_WARPS) k_sort_small(const unsigned* __restrict__ bstart, long long B,
                                                     unsigned capacity, const unsigned long long* __restrict__ zkey,
                                                     int* __restrict__ egidx, int* __restrict__ large,
                                                     unsigned max_large, int* __restrict__ mid, unsigned max_mid,
                                                     unsigned* __restrict__ nlist) {
-    const long long b = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    const long long b = static_cast<long long>(blockIdx.x) * HOLO_SORT_SMALL_WARPS + (threadIdx.x >> 5);
     if (b >= B) return;
     const int lane = threadIdx.x & 31;
     const unsigned e0 = min(bstart[b], capacity);
@@ -589,7 +592,8 @@ void sort_small_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsi
     const size_t max_large = capacity / (kSortCap + 1) + 1, max_mid = capacity / 129 + 1;
     int* large = static_cast<int*>(ctx->buffer("large_list", sizeof(int) * max_large));
     int* mid = static_cast<int*>(ctx->buffer("mid_list", sizeof(int) * max_mid));
-    k_sort_small<<<static_cast<unsigned>((B + 7) / 8), 256, 0, ctx->stream>>>(
+    k_sort_small<<<static_cast<unsigned>((B + HOLO_SORT_SMALL_WARPS - 1) / HOLO_SORT_SMALL_WARPS), 32 * HOLO_SORT_SMALL_WARPS, 0,
+                   ctx->stream>>>(
         bstart, B, capacity, zkey, egidx, large, static_cast<unsigned>(max_large), mid, static_cast<unsigned>(max_mid),
         d_nlist);
     HC_LAUNCHED(ctx);
