@@ -324,7 +324,13 @@ __global__ void __launch_bounds__(HOLO_EMIT_NT) k_bucket_emit(PreOut pre, size_t
 // global scratch; bucket b uses the scratch range [2 bstart[b], 2 bstart[b] + pow2(n)),
 // which never overlaps another bucket's since pow2(n) < 2 n.
 // The listed mid-size buckets come first, one warp each (eight keys per lane).
-__global__ void __launch_bounds__(1024) k_sort_large_dev(const int* __restrict__ list,
+#ifndef HOLO_LARGE_NT
+#define HOLO_LARGE_NT 256  // small CTAs: a frame without listed buckets does not hold whole SMs
+#endif
+#ifndef HOLO_LARGE_CTAS_PER_SM
+#define HOLO_LARGE_CTAS_PER_SM 4
+#endif
+__global__ void __launch_bounds__(HOLO_LARGE_NT) k_sort_large_dev(const int* __restrict__ list,
                                                          const unsigned* __restrict__ nlist, unsigned max_list,
                                                          const int* __restrict__ mid, unsigned max_mid,
                                                          const unsigned* __restrict__ bstart, unsigned capacity,
@@ -471,7 +477,7 @@ void sort_large_buckets(holo_ctx* ctx, const unsigned* bstart, unsigned capacity
     const int* mid = static_cast<const int*>(ctx->buffer("mid_list", sizeof(int) * max_mid));
     auto* tkey = static_cast<unsigned long long*>(ctx->buffer("large_tkey", sizeof(unsigned long long) * 2 * (capacity + 1)));
     auto* tg = static_cast<int*>(ctx->buffer("large_tg", sizeof(int) * 2 * (capacity + 1)));
-    k_sort_large_dev<<<ctx->sm_count, 1024, 0, ctx->stream>>>(list, d_nlist, static_cast<unsigned>(max_list), mid,
+    k_sort_large_dev<<<ctx->sm_count * HOLO_LARGE_CTAS_PER_SM, HOLO_LARGE_NT, 0, ctx->stream>>>(list, d_nlist, static_cast<unsigned>(max_list), mid,
                                                              static_cast<unsigned>(max_mid), bstart, capacity, zkey,
                                                              egidx, tkey, tg);
     HC_LAUNCHED(ctx);
