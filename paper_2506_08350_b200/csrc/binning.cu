@@ -469,15 +469,20 @@ void bucket_emit(holo_ctx* ctx, const PreOut& pre, size_t N, int L, int pb, int 
     HC_LAUNCHED(ctx);
 }
 
-void sort_large_buckets(holo_ctx* ctx, const unsigned* bstart, unsigned capacity, const unsigned long long* zkey,
-                        int* egidx, unsigned* d_nlist) {
+void sort_large_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsigned capacity,
+                        const unsigned long long* zkey, int* egidx, unsigned* d_nlist) {
     // the lists k_sort_small built (sized as there)
     const size_t max_list = capacity / (kSortCap + 1) + 1, max_mid = capacity / 129 + 1;
     const int* list = static_cast<const int*>(ctx->buffer("large_list", sizeof(int) * max_list));
     const int* mid = static_cast<const int*>(ctx->buffer("mid_list", sizeof(int) * max_mid));
     auto* tkey = static_cast<unsigned long long*>(ctx->buffer("large_tkey", sizeof(unsigned long long) * 2 * (capacity + 1)));
     auto* tg = static_cast<int*>(ctx->buffer("large_tg", sizeof(int) * 2 * (capacity + 1)));
-    k_sort_large_dev<<<ctx->sm_count * HOLO_LARGE_CTAS_PER_SM, HOLO_LARGE_NT, 0, ctx->stream>>>(list, d_nlist, static_cast<unsigned>(max_list), mid,
+    // the lists are on the device: size the grid by the mean bucket (entry capacity
+    // over buckets) -- one CTA per SM where listed buckets are unlikely, so an empty
+    // pass costs the other frame in flight little
+    const double mean = B > 0 ? static_cast<double>(capacity) / static_cast<double>(B) : 0.0;
+    const int per_sm = mean > 96.0 ? HOLO_LARGE_CTAS_PER_SM : 1;
+    k_sort_large_dev<<<ctx->sm_count * per_sm, HOLO_LARGE_NT, 0, ctx->stream>>>(list, d_nlist, static_cast<unsigned>(max_list), mid,
                                                              static_cast<unsigned>(max_mid), bstart, capacity, zkey,
                                                              egidx, tkey, tg);
     HC_LAUNCHED(ctx);

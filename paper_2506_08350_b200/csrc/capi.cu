@@ -439,7 +439,7 @@ void raster_planes(holo_ctx* ctx, const holo_camera& cam, const holo_wave& wave,
     // buckets of <= 128 entries sorted one warp each; the larger ones listed, then
     // sorted on the device (mid-size one warp each, large ones CTA-wide)
     sort_small_buckets(ctx, bstart, B, capacity, zkey, egidx, misc + 3);
-    sort_large_buckets(ctx, bstart, capacity, zkey, egidx, misc + 3);
+    sort_large_buckets(ctx, bstart, B, capacity, zkey, egidx, misc + 3);
     ctx->stage_end(1);
 
     // composite into [nplanes][C][H][W]
