@@ -264,7 +264,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dropin", action="store_true", help="skip the C++ drop-in API leg (e2e_dropin)")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
-    ap.add_argument("--inflight", type=int, default=2, help="frames in flight (contexts / lanes) per GPU")
+    ap.add_argument("--inflight", type=int, default=3, help="frames in flight (contexts / lanes) per GPU")
     ap.add_argument("--e2e-inflight", type=int, default=1, help="frames in flight in the end-to-end run at N=1")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
