@@ -395,6 +395,13 @@ int holo_total_loss(holo_ctx* ctx, const holo_camera* cam, const holo_wave* wave
 int holo_ssim(holo_ctx* ctx, const double* x, const double* y, int L, int C, int H, int W, double* mean_ssim,
               double* grad);
 
+/* make_target_from_scene's masks (pipeline.cpp:106-124) of the last frame rendered
+ * with HOLO_OUT_LAYERS: masks (device, f64 [num_planes][ny][nx], overwritten) = 1
+ * where the plane's sum over channels of |layer| (f64 of the fp32 layer) is the
+ * strict maximum over planes (the first on ties), else 0; untouched pixels are 0
+ * in every plane. */
+int holo_plane_masks(holo_ctx* ctx, double* masks);
+
 /* OptimizerConfig (optimizer.hpp:17-31). */
 typedef struct {
     double lr_positions, lr_rotations, lr_log_scales, lr_amplitudes, lr_phases, lr_opacities, lr_plane_logits;

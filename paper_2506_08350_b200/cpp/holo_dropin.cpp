@@ -1295,22 +1295,14 @@ FocalStackTarget make_target_from_scene(const GaussianScene& oracle, const Camer
     t.camera = cam;
     t.images = std::move(f.intensities);
     const int L = cfg.num_planes;
-    t.masks.assign(L, IntensityImage(cfg.nx, cfg.ny, 1));
-    // the plane whose rasterised amplitude dominates (pipeline.cpp:106-124)
-    for (int y = 0; y < cfg.ny; ++y)
-        for (int x = 0; x < cfg.nx; ++x) {
-            int best = -1;
-            double best_amp = 0.0;
-            for (int l = 0; l < L; ++l) {
-                double amp = 0.0;
-                for (int ch = 0; ch < f.raster.layers[l].c; ++ch) amp += std::abs(f.raster.layers[l].at(ch, y, x));
-                if (amp > best_amp) {
-                    best_amp = amp;
-                    best = l;
-                }
-            }
-            if (best >= 0) t.masks[best].at(0, y, x) = 1.0;
-        }
+    // the masks (pipeline.cpp:106-124) from the frame's layers still resident on the
+    // device (holo_plane_masks), not from the 800 MB of widened host copies
+    const size_t P = static_cast<size_t>(cfg.nx) * cfg.ny;
+    t.masks = make_parallel<IntensityImage>(L, cfg.nx, cfg.ny, 1, 0.0);
+    DevMem dm(sizeof(double) * L * P);
+    check(holo_plane_masks(ctx(), static_cast<double*>(dm.p)));
+    for (int l = 0; l < L; ++l)
+        d2h(t.masks[l].data.data(), static_cast<const double*>(dm.p) + static_cast<size_t>(l) * P, sizeof(double) * P);
     return t;
 }
 

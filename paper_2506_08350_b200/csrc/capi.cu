@@ -1839,6 +1839,20 @@ int holo_ssim(holo_ctx* ctx, const double* x, const double* y, int L, int C, int
     });
 }
 
+int holo_plane_masks(holo_ctx* ctx, double* masks) {
+    return guarded([&] {
+        require(ctx && masks, HOLO_ERR_USAGE, "null argument");
+        require(ctx->f_L > 0 && ctx->f_C > 0 && (ctx->f_outputs & HOLO_OUT_LAYERS), HOLO_ERR_USAGE,
+                "plane masks need a frame rendered with HOLO_OUT_LAYERS");
+        require(ctx->f_plane_begin == 0 && ctx->f_plane_end == ctx->f_L, HOLO_ERR_USAGE,
+                "plane masks need every plane of the frame");
+        HC_CUDA(cudaSetDevice(ctx->device));
+        const size_t P = static_cast<size_t>(ctx->f_W) * ctx->f_H;
+        const auto* layers = static_cast<const cx<float>*>(ctx->buffer("layers", 1));
+        plane_masks(ctx, layers, ctx->f_L, ctx->f_C, P, masks);
+    });
+}
+
 int holo_adaptive_update(holo_ctx* ctx, double* params, const double* grads, double* m, double* v, double* n,
                          double* prev_grad, size_t count, double lr, long long step,
                          const holo_optimizer_config* cfg) {

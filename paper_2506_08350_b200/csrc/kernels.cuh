@@ -141,6 +141,8 @@ void bucket_emit(holo_ctx* ctx, const PreOut& pre, size_t N, int L, int plane_be
 // entries) are found and sorted without a host round trip; d_nlist[0..1] count them
 void sort_large_buckets(holo_ctx* ctx, const unsigned* bstart, long long B, unsigned capacity,
                         const unsigned long long* zkey, int* egidx, unsigned* d_nlist);
+// make_target_from_scene's per-plane masks [L][P] (f64 0/1) from layers [L][C][P]
+void plane_masks(holo_ctx* ctx, const cx<float>* layers, int L, int C, size_t P, double* masks);
 void entry_depths(holo_ctx* ctx, const int* egidx, const double* zc, double* edepth, const unsigned* d_E,
                   unsigned capacity);
 // host[0..2] = misc[0..2] (flags, num_valid, max bucket), host[4] = *total (E); host is pinned

@@ -8,6 +8,7 @@
 // -- is that of the full scene (rasterizer.cpp:221-224).  The subset is formed on
 // the device from the uploaded scene: a flag per Gaussian, an exclusive scan, and a
 // stable scatter of the seven f64 arrays.
+#include <algorithm>
 #include "kernels.cuh"
 
 namespace holo_cuda {
@@ -79,6 +80,40 @@ size_t scene_keep_planes(holo_ctx* ctx, const double* const src[7], double* cons
     HC_CUDA(cudaMemcpyAsync(&count, offs + n, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
     HC_CUDA(cudaStreamSynchronize(ctx->stream));
     return count;
+}
+
+namespace {
+// make_target_from_scene's masks (pipeline.cpp:106-124): pixel p belongs to the
+// plane whose rasterised amplitude sum_c |layer_c(p)| (f64, of the fp32 layer
+// widened exactly as the drop-in returns it) is the strict maximum, the first
+// such plane on ties; untouched pixels (all sums 0) stay unmasked.
+__global__ void k_plane_masks(const cx<float>* __restrict__ layers, int L, int C, size_t P,
+                              double* __restrict__ masks) {
+    for (size_t p = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; p < P;
+         p += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        int best = -1;
+        double best_amp = 0.0;
+        for (int l = 0; l < L; ++l) {
+            double amp = 0.0;
+            for (int c = 0; c < C; ++c) {
+                const cx<float> v = layers[(static_cast<size_t>(l) * C + c) * P + p];
+                amp += hypot(static_cast<double>(v.x), static_cast<double>(v.y));
+            }
+            if (amp > best_amp) {
+                best_amp = amp;
+                best = l;
+            }
+        }
+        for (int l = 0; l < L; ++l) masks[static_cast<size_t>(l) * P + p] = l == best ? 1.0 : 0.0;
+    }
+}
+}  // namespace
+
+void plane_masks(holo_ctx* ctx, const cx<float>* layers, int L, int C, size_t P, double* masks) {
+    if (P == 0 || L == 0) return;
+    const unsigned grid = static_cast<unsigned>(std::min<size_t>((P + 255) / 256, 8 * 148));
+    k_plane_masks<<<grid, 256, 0, ctx->stream>>>(layers, L, C, P, masks);
+    HC_LAUNCHED(ctx);
 }
 
 }  // namespace holo_cuda

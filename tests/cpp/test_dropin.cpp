@@ -154,6 +154,50 @@ TEST_CASE("pipeline forward produces consistently shaped stages") {
     CHECK(std::sqrt(num / den) < 1e-5);
 }
 
+TEST_CASE("make_target_from_scene masks follow the dominant rasterised plane") {
+    // the device masks (holo_plane_masks) against pipeline.cpp:106-124 evaluated on
+    // the host over the returned (widened) layers of the same scene
+    const WaveConfig cfg = desk(48, 3);
+    const CameraView cam = front(cfg);
+    GaussianScene s;
+    s.num_planes = 3;
+    s.resize(40);
+    for (int i = 0; i < 40; ++i) {
+        s.positions[3 * i] = 0.0009 * ((i * 7) % 19 - 9);
+        s.positions[3 * i + 1] = 0.0009 * ((i * 11) % 17 - 8);
+        s.positions[3 * i + 2] = 0.3 + 0.002 * (i % 5);
+        s.opacity_logits[i] = 0.2 * (i % 4);
+        s.plane_logits[3 * i + (i % 3)] = 1.0;
+        for (int d = 0; d < 3; ++d) {
+            s.log_scales[3 * i + d] = std::log(0.002 + 0.0005 * (i % 3));
+            s.amplitudes[3 * i + d] = 0.3 + 0.1 * ((i + d) % 5);
+            s.phases[3 * i + d] = 0.4 * d + 0.1 * i;
+        }
+    }
+    const PipelineOptions opt{};
+    const FocalStackTarget t = make_target_from_scene(s, cam, cfg, opt);
+    const PipelineForward f = pipeline_forward(s, cam, cfg, opt);
+    REQUIRE(t.masks.size() == 3);
+    int masked = 0;
+    for (int y = 0; y < cfg.ny; ++y)
+        for (int x = 0; x < cfg.nx; ++x) {
+            int best = -1;
+            double best_amp = 0.0;
+            for (int l = 0; l < 3; ++l) {
+                double amp = 0.0;
+                for (int ch = 0; ch < f.raster.layers[l].c; ++ch) amp += std::abs(f.raster.layers[l].at(ch, y, x));
+                if (amp > best_amp) {
+                    best_amp = amp;
+                    best = l;
+                }
+            }
+            for (int l = 0; l < 3; ++l) CHECK(t.masks[l].at(0, y, x) == (l == best ? 1.0 : 0.0));
+            masked += best >= 0;
+        }
+    CHECK(masked > 100);
+    CHECK(masked < cfg.nx * cfg.ny);
+}
+
 TEST_CASE("f64 operators meet the reference tolerances") {
     WaveConfig cfg = desk(64, 1);
     ComplexField u(64, 64, 3, cfg.pitch);
