@@ -122,9 +122,26 @@ __device__ __forceinline__ void project_one(const PreArgs& a, const PreOut& o, s
 
     // ---- plane assignment (compute_rho, rasterizer.cpp:81-99; ste_assign scene.cpp:132-152)
     const double* lg = lg_b + static_cast<size_t>(t) * L;
+    // The reference's strict-'>' scan from plane 0 yields the first index of the
+    // largest non-NaN logit, or 0 when logit 0 is NaN (NaNs never win).  The same
+    // result is formed here reading the planes in an order rotated by the thread
+    // index, so that a warp's reads of its 32 staged rows (L doubles apart) fall in
+    // distinct shared-memory banks instead of L-way conflicting ones.
     int best = 0;
-    for (int l = 1; l < L; ++l)
-        if (lg[l] > lg[best]) best = l;
+    {
+        int bl = -1;
+        double bv = 0.0;
+        int l = L > 0 ? t % L : 0;
+        for (int k = 0; k < L; ++k) {
+            const double v = lg[l];
+            if (!isnan(v) && (bl < 0 || v > bv || (v == bv && l < bl))) {
+                bv = v;
+                bl = l;
+            }
+            if (++l == L) l = 0;
+        }
+        best = (bl < 0 || isnan(lg[0])) ? 0 : bl;
+    }
     o.plane[i] = best;
     unsigned long long mask = 0;
     int nplanes = 0;

@@ -608,3 +608,32 @@ def test_plane_subset_shards_render_the_same_layers(gpu_ctx):
         gpu_ctx.render_begin(cam, cfg, None, None, pb, pe, sub_part.data_ptr(), 0)
         torch.cuda.synchronize()
         assert torch.equal(full_part, sub_part)
+
+def test_plane_assignment_follows_the_strict_scan(gpu_ctx):
+    """The device's hard plane (ste_assign's argmax, scene.cpp:132-152) equals the
+    reference's strict-'>' scan from plane 0 -- first index of the largest logit,
+    NaNs never win, a NaN logit 0 keeps plane 0, -0.0 ties +0.0 -- for Gaussians in
+    full shared-memory slices and in the tail slice (read from global memory)."""
+    cfg = desk_config(32, 5)
+    n = 150
+    rng = np.random.default_rng(11)
+    s = random_scene(n, cfg, 12)
+    lg = rng.integers(-2, 3, size=(n, 5)).astype(np.float64)  # many exact ties
+    lg[::7, 0] = np.nan
+    lg[3::11, 2] = np.nan
+    lg[5::13] = np.nan
+    lg[6::17, 1] = -0.0
+    lg[6::17, 3] = 0.0
+    lg[8::19, 4] = np.inf
+    lg[9::23, 0] = -np.inf
+    s.plane_logits = lg
+    r = api.raster_forward(s, front_camera(cfg), cfg, ctx=gpu_ctx)
+
+    def scan(row):
+        best = 0
+        for l in range(1, len(row)):
+            if row[l] > row[best]:
+                best = l
+        return best
+
+    assert list(r.projected["plane"]) == [scan(row) for row in lg]
